@@ -1,0 +1,784 @@
+// engine.cu -- host side of libaura_b200.so: the C-ABI declared in
+// include/aura_b200.h, device memory layout, filter preparation on the GPU,
+// per-block CUDA graphs and the measurement entry points.
+//
+// Reference interfaces replaced (under /root/reference/proj/include/aura):
+//   aura_b200_convolver_create  Convolver::Convolver      convolver.hpp:67-94
+//   aura_b200_auralizer_create  Auralizer::Auralizer      auralizer.hpp:27-41
+//   aura_b200_process           Convolver::process        convolver.hpp:111-123
+//                               Auralizer::process        auralizer.hpp:61-87
+//   aura_b200_reset             Convolver/Auralizer::reset convolver.hpp:133-142,
+//                                                          auralizer.hpp:95-99
+//   aura_b200_feedback_estimate Auralizer::feedback_estimate auralizer.hpp:56-58
+//   aura_b200_filter_spectrum   PartitionedFilterSet::spectrum engine.hpp:210-219
+//   aura_b200_device_count      list_backends             backend.hpp:186-193
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#if defined(__x86_64__)
+#include <immintrin.h>
+#endif
+
+#include "../../include/aura_b200.h"
+#include "kernels.cuh"
+
+using namespace aura_b200;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Fail {
+  int code;
+  std::string msg;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw Fail{code, msg}; }
+
+void ck(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return;
+  cudaGetLastError();
+  if (e == cudaErrorMemoryAllocation)
+    fail(AURA_B200_E_OUT_OF_MEMORY, std::string(what) + ": " + cudaGetErrorString(e));
+  fail(AURA_B200_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define CK(x) ck((x), #x)
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return AURA_B200_OK;
+  } catch (const Fail& e) {
+    g_err = e.msg;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "host allocation failed";
+    return AURA_B200_E_OUT_OF_MEMORY;
+  }
+}
+
+bool is_pow2(size_t v) { return v && !(v & (v - 1)); }
+int ilog2(size_t v) {
+  int r = 0;
+  while ((size_t(1) << r) < v) ++r;
+  return r;
+}
+
+// engine.hpp:74-94 (validate_config), same codes and precedence. MIMO (an
+// extension) lifts only the C_in in {1, C_out} rule.
+void validate(const aura_b200_config* c, bool mimo) {
+  if (!c) fail(AURA_B200_E_INVALID_ARGUMENT, "config is null");
+  if (c->sample_rate_hz == 0) fail(AURA_B200_E_ZERO_SAMPLE_RATE, "sample rate must be positive");
+  if (!is_pow2(c->block_size) || c->block_size < 16 || c->block_size > 8192)
+    fail(AURA_B200_E_NON_POWER_OF_TWO_BLOCK,
+         "block size must be a power of two in [16, 8192], got " + std::to_string(c->block_size));
+  if (c->fft_size != 2 * c->block_size)
+    fail(AURA_B200_E_FFT_SIZE_MISMATCH, "fft size must be 2 * block size");
+  if (c->outputs == 0 || c->inputs == 0 ||
+      (!mimo && c->inputs != 1 && c->inputs != c->outputs))
+    fail(AURA_B200_E_BAD_CHANNEL_COMBINATION,
+         "input channels must be 1 or equal to output channels");
+}
+
+constexpr int kSMs = 148;
+
+template <class T>
+T* dalloc(size_t count, std::vector<void*>& owned) {
+  void* p = nullptr;
+  if (count == 0) count = 1;
+  CK(cudaMalloc(&p, count * sizeof(T)));
+  owned.push_back(p);
+  return static_cast<T*>(p);
+}
+
+}  // namespace
+
+enum Phase { PH_INPUT = 0, PH_MAC_SYN, PH_TAIL_SYN, PH_MAC_AFC, PH_TAIL_AFC, PH_COUNT };
+static const char* kPhaseNames[PH_COUNT] = {"k_input", "k_mac_synth", "k_tail_synth",
+                                            "k_mac_afc", "k_tail_afc"};
+
+struct aura_b200_engine {
+  int device = 0;
+  bool aur = false;
+  int mode = 0;
+  size_t N = 0, Q = 1, L = 1, P = 0, K = 0, KF = 0, n_h = 0, n_hf = 0;
+  int Qx = 1;  // FDL channels
+  int LT = 1, PT = 1;
+  uint64_t blocks = 0;
+  cudaStream_t stream = nullptr;
+  std::vector<void*> dmem;
+  float4* W0 = nullptr;  // initial canceller spectra (reset of NLMS)
+  size_t w_elems = 0;
+  float* h_in = nullptr;   // mapped pinned
+  float* h_out = nullptr;  // mapped pinned
+  uint32_t* h_done = nullptr;
+  float* d_in_pool = nullptr;
+  size_t pool_blocks = 0;
+  float* d_out = nullptr;
+  BlockArgs args{};
+  BlockArgs dev_args{};
+  cudaGraphExec_t g_host = nullptr, g_dev = nullptr;
+  size_t smem_input = 0, smem_tail = 0;
+
+  ~aura_b200_engine() {
+    cudaSetDevice(device);
+    if (stream) cudaStreamSynchronize(stream);
+    if (g_host) cudaGraphExecDestroy(g_host);
+    if (g_dev) cudaGraphExecDestroy(g_dev);
+    for (void* p : dmem) cudaFree(p);
+    if (h_in) cudaFreeHost(h_in);
+    if (h_out) cudaFreeHost(h_out);
+    if (h_done) cudaFreeHost(h_done);
+    if (stream) cudaStreamDestroy(stream);
+  }
+
+  void launch_phase(int ph, const BlockArgs& a, cudaStream_t s) {
+    switch (ph) {
+      case PH_INPUT: {
+        const int grid = Qx + (a.nlms ? (int)P : 0);
+        k_input<<<grid, 256, smem_input, s>>>(a);
+        break;
+      }
+      case PH_MAC_SYN: {
+        dim3 grid(a.syn_chunks, (unsigned)(L / LT), a.syn_tiles);
+        const bool el = mode == AURA_B200_ELEMENTWISE;
+#define MAC_CASE(lt)                                                         \
+  case lt:                                                                   \
+    if (el) k_mac_synth<lt, true><<<grid, kMacThreads, 0, s>>>(a);           \
+    else k_mac_synth<lt, false><<<grid, kMacThreads, 0, s>>>(a);             \
+    break;
+        switch (LT) { MAC_CASE(1) MAC_CASE(2) MAC_CASE(4) MAC_CASE(8) }
+#undef MAC_CASE
+        break;
+      }
+      case PH_TAIL_SYN:
+        k_tail_synth<<<(unsigned)L, kTailThreads, smem_tail, s>>>(a);
+        break;
+      case PH_MAC_AFC: {
+        dim3 grid(a.afc_chunks, 1, a.afc_tiles);
+        switch (PT) {
+          case 1: k_mac_afc<1><<<grid, kMacThreads, 0, s>>>(a); break;
+          case 2: k_mac_afc<2><<<grid, kMacThreads, 0, s>>>(a); break;
+          case 4: k_mac_afc<4><<<grid, kMacThreads, 0, s>>>(a); break;
+          default: k_mac_afc<8><<<grid, kMacThreads, 0, s>>>(a); break;
+        }
+        break;
+      }
+      case PH_TAIL_AFC:
+        k_tail_afc<<<(unsigned)P, kTailThreads, smem_tail, s>>>(a);
+        break;
+    }
+  }
+
+  int n_phases() const { return aur ? PH_COUNT : PH_TAIL_SYN + 1; }
+
+  void launch_block(const BlockArgs& a, cudaStream_t s) {
+    for (int ph = 0; ph < n_phases(); ++ph) launch_phase(ph, a, s);
+  }
+
+  cudaGraphExec_t capture(const BlockArgs& a) {
+    cudaGraph_t g;
+    CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+    launch_block(a, stream);
+    CK(cudaStreamEndCapture(stream, &g));
+    cudaGraphExec_t ex;
+    CK(cudaGraphInstantiate(&ex, g, 0));
+    cudaGraphDestroy(g);
+    return ex;
+  }
+
+  double phase_bytes(int ph) const {
+    const double row = 8.0 * (double)N;  // one packed partition
+    const double T = mode == AURA_B200_MIMO ? (double)(Q * K) : (double)K;
+    switch (ph) {
+      case PH_INPUT: return 4.0 * N * Qx + row * Qx;
+      case PH_MAC_SYN: return row * ((double)L * T + (double)Qx * K);
+      case PH_TAIL_SYN:
+        return row * (double)args.syn_chunks * L + 4.0 * N * L + (aur ? row * L : 0.0);
+      case PH_MAC_AFC:
+        return row * ((double)P * L * KF * (1.0 + (args.nlms ? 1.0 : 0.0)) + (double)L * KF);
+      case PH_TAIL_AFC: return row * (double)args.afc_chunks * P + 4.0 * N * P;
+    }
+    return 0.0;
+  }
+};
+
+namespace {
+
+void setup_tables(aura_b200_engine* e, BlockArgs& a) {
+  const size_t N = e->N;
+  std::vector<float2> tw(N / 2), split(N);
+  for (size_t j = 0; j < N / 2; ++j) {
+    const double ang = -2.0 * M_PI * (double)j / (double)N;
+    tw[j] = make_float2((float)std::cos(ang), (float)std::sin(ang));
+  }
+  for (size_t k = 0; k < N; ++k) {
+    const double ang = -M_PI * (double)k / (double)N;
+    split[k] = make_float2((float)std::cos(ang), (float)std::sin(ang));
+  }
+  float2* dtw = dalloc<float2>(N / 2, e->dmem);
+  float2* dsp = dalloc<float2>(N, e->dmem);
+  CK(cudaMemcpy(dtw, tw.data(), sizeof(float2) * tw.size(), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dsp, split.data(), sizeof(float2) * split.size(), cudaMemcpyHostToDevice));
+  a.tw = dtw;
+  a.split = dsp;
+}
+
+// GPU make_partitioned_filters (convolver.hpp:19-46): rows of n_h taps are
+// uploaded in bounded batches and transformed in place into dst at the
+// packed offsets row_off[r] (float4 units).
+void partition_rows(aura_b200_engine* e, const BlockArgs& a,
+                    const float* const* rows, size_t n_rows, size_t n_h,
+                    size_t K, float4* dst, const std::vector<size_t>& row_off) {
+  const size_t N = e->N;
+  const size_t budget = size_t(256) << 20;  // bytes of staged taps per batch
+  size_t batch = std::max<size_t>(1, budget / (n_h * sizeof(float)));
+  batch = std::min<size_t>(batch, 65535);
+  float* d_taps = nullptr;
+  size_t* d_off = nullptr;
+  CK(cudaMalloc(&d_taps, std::min(batch, n_rows) * n_h * sizeof(float)));
+  CK(cudaMalloc(&d_off, std::min(batch, n_rows) * sizeof(size_t)));
+  const size_t smem = 16 * N;
+  CK(cudaFuncSetAttribute(k_partition, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  for (size_t r0 = 0; r0 < n_rows; r0 += batch) {
+    const size_t nr = std::min(batch, n_rows - r0);
+    for (size_t r = 0; r < nr; ++r)
+      CK(cudaMemcpyAsync(d_taps + r * n_h, rows[r0 + r], n_h * sizeof(float),
+                         cudaMemcpyHostToDevice, e->stream));
+    CK(cudaMemcpyAsync(d_off, row_off.data() + r0, nr * sizeof(size_t),
+                       cudaMemcpyHostToDevice, e->stream));
+    dim3 grid((unsigned)K, (unsigned)nr);
+    k_partition<<<grid, 256, smem, e->stream>>>(d_taps, n_h, (int)nr, (int)K, (int)N,
+                                                 ilog2(N), a.tw, a.split, dst, d_off);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(e->stream));
+  }
+  cudaFree(d_taps);
+  cudaFree(d_off);
+}
+
+int pick_tile(size_t L) {
+  for (int t : {8, 4, 2})
+    if (L % t == 0) return t;
+  return 1;
+}
+
+void plan_split(aura_b200_engine* e, BlockArgs& a) {
+  const int NF = a.NF;
+  a.syn_nft = std::min(NF, kMacThreads);
+  a.syn_tiles = NF / a.syn_nft;
+  const int KP = kMacThreads / a.syn_nft;
+  const long T = e->mode == AURA_B200_MIMO ? (long)(e->Q * e->K) : (long)e->K;
+  const long per_chunk = (long)(e->L / e->LT) * a.syn_tiles;
+  const long target = (long)kSMs * 4;
+  long chunks = (target + per_chunk - 1) / per_chunk;
+  chunks = std::min(chunks, std::max(1L, (T + 2 * KP - 1) / (2 * KP)));
+  chunks = std::max(1L, std::min(chunks, T));
+  a.syn_tc = (int)((T + chunks - 1) / chunks);
+  a.syn_chunks = (int)((T + a.syn_tc - 1) / a.syn_tc);
+  if (e->aur) {
+    a.afc_nft = std::min(NF, kMacThreads);
+    a.afc_tiles = NF / a.afc_nft;
+    const int KPa = kMacThreads / a.afc_nft;
+    const long U = (long)(e->L * e->KF);
+    long ch = (target + a.afc_tiles - 1) / a.afc_tiles;
+    ch = std::min(ch, std::max(1L, (U + 2 * KPa - 1) / (2 * KPa)));
+    ch = std::max(1L, std::min(ch, U));
+    a.afc_uc = (int)((U + ch - 1) / ch);
+    a.afc_chunks = (int)((U + a.afc_uc - 1) / a.afc_uc);
+  }
+}
+
+void common_init(aura_b200_engine* e, int device) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    fail(AURA_B200_E_BACKEND_UNAVAILABLE, "accelerator backend is not available: no CUDA device");
+  }
+  if (device < 0 || device >= n) fail(AURA_B200_E_INVALID_ARGUMENT, "device index out of range");
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10)
+    fail(AURA_B200_E_BACKEND_UNAVAILABLE,
+         std::string("accelerator backend needs an sm_100 (B200) device, found ") + prop.name);
+  e->device = device;
+  CK(cudaSetDevice(device));
+  CK(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+}
+
+void finish_init(aura_b200_engine* e) {
+  BlockArgs& a = e->args;
+  const size_t N = e->N;
+  // state + I/O
+  a.st = dalloc<DevState>(1, e->dmem);
+  CK(cudaMemset(a.st, 0, sizeof(DevState)));
+  const size_t in_ch = (size_t)e->Qx;
+  CK(cudaHostAlloc(&e->h_in, in_ch * N * sizeof(float), cudaHostAllocMapped | cudaHostAllocPortable));
+  CK(cudaHostAlloc(&e->h_out, e->L * N * sizeof(float), cudaHostAllocMapped | cudaHostAllocPortable));
+  CK(cudaHostAlloc(&e->h_done, 64, cudaHostAllocMapped | cudaHostAllocPortable));
+  std::memset(e->h_in, 0, in_ch * N * sizeof(float));
+  std::memset(e->h_out, 0, e->L * N * sizeof(float));
+  std::memset(e->h_done, 0, 64);
+  float* din;
+  float* dout;
+  uint32_t* ddone;
+  CK(cudaHostGetDevicePointer((void**)&din, e->h_in, 0));
+  CK(cudaHostGetDevicePointer((void**)&dout, e->h_out, 0));
+  CK(cudaHostGetDevicePointer((void**)&ddone, e->h_done, 0));
+  a.in = din;
+  a.out = dout;
+  a.done = ddone;
+  // dynamic shared memory
+  e->smem_input = 16 * N;
+  e->smem_tail = sizeof(float4) * kTailThreads + 24 * N;
+  CK(cudaFuncSetAttribute(k_input, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem_input));
+  CK(cudaFuncSetAttribute(k_tail_synth, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem_tail));
+  CK(cudaFuncSetAttribute(k_tail_afc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem_tail));
+  // device-resident I/O variant for measurement
+  e->pool_blocks = 64;
+  e->d_in_pool = dalloc<float>(e->pool_blocks * in_ch * N, e->dmem);
+  CK(cudaMemset(e->d_in_pool, 0, e->pool_blocks * in_ch * N * sizeof(float)));
+  e->d_out = dalloc<float>(e->L * N, e->dmem);
+  e->g_host = e->capture(a);
+  e->dev_args = a;
+  e->dev_args.out = e->d_out;
+  e->dev_args.in = e->d_in_pool;
+  e->g_dev = nullptr;  // built lazily (pool indexing needs the per-block pointer)
+  CK(cudaStreamSynchronize(e->stream));
+}
+
+void reset_state(aura_b200_engine* e) {
+  BlockArgs& a = e->args;
+  const size_t N = e->N, NF = N / 2;
+  cudaStream_t s = e->stream;
+  CK(cudaStreamSynchronize(s));
+  CK(cudaMemsetAsync(a.st, 0, sizeof(DevState), s));
+  CK(cudaMemsetAsync(a.prev_in, 0, sizeof(float) * e->Qx * N, s));
+  CK(cudaMemsetAsync(a.X, 0, sizeof(float4) * (size_t)e->Qx * e->K * NF, s));
+  if (e->aur) {
+    CK(cudaMemsetAsync(a.prev_spk, 0, sizeof(float) * e->L * N, s));
+    CK(cudaMemsetAsync(a.XA, 0, sizeof(float4) * e->L * (e->KF + 1) * NF, s));
+    CK(cudaMemsetAsync(a.fhat, 0, sizeof(float) * e->P * N, s));
+    CK(cudaMemsetAsync(a.pw, 0, sizeof(float2) * N, s));
+    CK(cudaMemsetAsync(a.pw_part, 0, sizeof(float2) * e->L * N, s));
+    if (a.nlms)
+      CK(cudaMemcpyAsync(a.W, e->W0, sizeof(float4) * e->w_elems, cudaMemcpyDeviceToDevice, s));
+  }
+  CK(cudaStreamSynchronize(s));
+  *e->h_done = 0;
+  e->blocks = 0;
+}
+
+void alloc_synth(aura_b200_engine* e, BlockArgs& a) {
+  const size_t N = e->N, NF = N / 2;
+  a.N = (int)N;
+  a.logN = ilog2(N);
+  a.NF = (int)NF;
+  a.Q = (int)e->Q;
+  a.L = (int)e->L;
+  a.K = (int)e->K;
+  a.mode = e->mode;
+  const size_t T = e->mode == AURA_B200_MIMO ? e->Q * e->K : e->K;
+  a.H = dalloc<float4>(e->L * T * NF, e->dmem);
+  a.X = dalloc<float4>((size_t)e->Qx * e->K * NF, e->dmem);
+  a.prev_in = dalloc<float>((size_t)e->Qx * N, e->dmem);
+  CK(cudaMemset(a.X, 0, sizeof(float4) * (size_t)e->Qx * e->K * NF));
+  CK(cudaMemset(a.prev_in, 0, sizeof(float) * e->Qx * N));
+}
+
+void upload_synth(aura_b200_engine* e, BlockArgs& a, const float* const* rows,
+                  size_t n_rows, size_t n_h) {
+  const size_t NF = e->N / 2;
+  std::vector<size_t> off(n_rows);
+  for (size_t r = 0; r < n_rows; ++r) {
+    size_t l = r, q = 0;
+    if (e->mode == AURA_B200_MIMO) { q = r / e->L; l = r % e->L; }
+    off[r] = ((l * (e->mode == AURA_B200_MIMO ? e->Q : 1) + q) * e->K) * NF;
+  }
+  partition_rows(e, a, rows, n_rows, n_h, e->K, const_cast<float4*>(a.H), off);
+}
+
+void check_rows(const float* const* rows, size_t n_rows) {
+  if (!rows) fail(AURA_B200_E_EMPTY_FILTER, "need at least one filter");
+  for (size_t r = 0; r < n_rows; ++r)
+    if (!rows[r]) fail(AURA_B200_E_INVALID_ARGUMENT, "null filter row");
+}
+
+}  // namespace
+
+// ====================================================================== ABI
+
+extern "C" {
+
+int aura_b200_abi_version(void) { return AURA_B200_ABI_VERSION; }
+const char* aura_b200_last_error(void) { return g_err.c_str(); }
+
+int aura_b200_device_count(int* out) {
+  return guarded([&] {
+    int n = 0, usable = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+      cudaGetLastError();
+      n = 0;
+    }
+    for (int d = 0; d < n; ++d) {
+      cudaDeviceProp p;
+      if (cudaGetDeviceProperties(&p, d) == cudaSuccess && p.major == 10) ++usable;
+    }
+    *out = usable;
+  });
+}
+
+int aura_b200_device_name(int device, char* buf, size_t cap) {
+  return guarded([&] {
+    cudaDeviceProp p;
+    CK(cudaGetDeviceProperties(&p, device));
+    std::snprintf(buf, cap, "%s (sm_%d%d, %d SMs)", p.name, p.major, p.minor, p.multiProcessorCount);
+  });
+}
+
+int aura_b200_convolver_create(const aura_b200_config* cfg, int mode,
+                               const float* const* filters, size_t n_rows,
+                               size_t n_h, int device, aura_b200_engine** out) {
+  return guarded([&] {
+    if (!out) fail(AURA_B200_E_INVALID_ARGUMENT, "out is null");
+    *out = nullptr;
+    if (mode < 0 || mode > 2) fail(AURA_B200_E_INVALID_ARGUMENT, "unknown channel mode");
+    validate(cfg, mode == AURA_B200_MIMO);
+    // convolver.hpp:22-30 (make_partitioned_filters runs before the mode checks)
+    if (n_rows == 0 || !filters) fail(AURA_B200_E_EMPTY_FILTER, "need at least one filter");
+    if (n_h == 0) fail(AURA_B200_E_EMPTY_FILTER, "filters must have at least one tap");
+    check_rows(filters, n_rows);
+    // convolver.hpp:84-93
+    if (mode == AURA_B200_BROADCAST && cfg->inputs != 1)
+      fail(AURA_B200_E_MODE_CHANNEL_MISMATCH, "broadcast mode requires one input channel");
+    if (mode == AURA_B200_ELEMENTWISE && cfg->inputs != cfg->outputs)
+      fail(AURA_B200_E_MODE_CHANNEL_MISMATCH,
+           "elementwise mode requires input channels == output channels");
+    const size_t want = mode == AURA_B200_MIMO ? cfg->inputs * cfg->outputs : cfg->outputs;
+    if (n_rows != want)
+      fail(AURA_B200_E_MODE_CHANNEL_MISMATCH, "filter count must equal the configured output channels");
+    std::unique_ptr<aura_b200_engine> e(new aura_b200_engine());
+    common_init(e.get(), device);
+    e->mode = mode;
+    e->N = cfg->block_size;
+    e->Q = mode == AURA_B200_ELEMENTWISE ? 1 : cfg->inputs;
+    e->L = cfg->outputs;
+    e->Qx = mode == AURA_B200_ELEMENTWISE ? (int)cfg->outputs : (int)cfg->inputs;
+    e->K = (n_h + e->N - 1) / e->N;
+    e->n_h = n_h;
+    e->LT = pick_tile(e->L);
+    BlockArgs& a = e->args;
+    setup_tables(e.get(), a);
+    alloc_synth(e.get(), a);
+    upload_synth(e.get(), a, filters, n_rows, n_h);
+    a.is_aur = 0;
+    a.nlms = 0;
+    a.P = 0;
+    plan_split(e.get(), a);
+    a.part_syn = dalloc<float4>((size_t)a.syn_chunks * e->L * a.NF, e->dmem);
+    finish_init(e.get());
+    *out = e.release();
+  });
+}
+
+int aura_b200_auralizer_create(const aura_b200_config* cfg,
+                               const float* const* synth, size_t n_synth_rows,
+                               size_t n_h, const float* const* fc,
+                               size_t n_fc_rows, size_t n_hf, float input_gain,
+                               const aura_b200_afc* afc, int device,
+                               aura_b200_engine** out) {
+  return guarded([&] {
+    if (!out) fail(AURA_B200_E_INVALID_ARGUMENT, "out is null");
+    *out = nullptr;
+    validate(cfg, true);
+    const size_t Q = cfg->inputs, L = cfg->outputs;
+    // auralizer.hpp:102-115 (single input in the reference; Q > 1 is the
+    // Appendix-B MIMO extension), then both convolvers' checks.
+    if (n_synth_rows != n_fc_rows)
+      fail(AURA_B200_E_CHANNEL_COUNT_MISMATCH,
+           "synthesis and feedback-cancellation filter sets must have the same channel count");
+    if (n_synth_rows == 0 || !synth || !fc) fail(AURA_B200_E_EMPTY_FILTER, "need at least one filter");
+    if (n_h == 0 || n_hf == 0) fail(AURA_B200_E_EMPTY_FILTER, "filters must have at least one tap");
+    check_rows(synth, n_synth_rows);
+    check_rows(fc, n_fc_rows);
+    if (n_synth_rows != Q * L)
+      fail(AURA_B200_E_MODE_CHANNEL_MISMATCH, "filter count must equal inputs x output channels");
+    if (Q > 8) fail(AURA_B200_E_INVALID_ARGUMENT, "at most 8 microphones/inputs are supported");
+    const float mu = afc ? afc->mu : 0.0f;
+    if (afc && (!(mu >= 0.0f) || !(afc->lambda >= 0.0f && afc->lambda <= 1.0f) ||
+                !(afc->delta > 0.0f) || !std::isfinite(mu)))
+      fail(AURA_B200_E_INVALID_ARGUMENT, "afc needs mu >= 0, 0 <= lambda <= 1, delta > 0");
+    std::unique_ptr<aura_b200_engine> e(new aura_b200_engine());
+    common_init(e.get(), device);
+    e->aur = true;
+    e->mode = Q == 1 ? AURA_B200_BROADCAST : AURA_B200_MIMO;
+    e->N = cfg->block_size;
+    e->Q = Q;
+    e->L = L;
+    e->P = Q;
+    e->Qx = (int)Q;
+    e->K = (n_h + e->N - 1) / e->N;
+    e->KF = (n_hf + e->N - 1) / e->N;
+    e->n_h = n_h;
+    e->n_hf = n_hf;
+    e->LT = pick_tile(L);
+    e->PT = Q == 1 ? 1 : Q == 2 ? 2 : Q <= 4 ? 4 : 8;
+    BlockArgs& a = e->args;
+    setup_tables(e.get(), a);
+    alloc_synth(e.get(), a);
+    upload_synth(e.get(), a, synth, n_synth_rows, n_h);
+    const size_t N = e->N, NF = N / 2;
+    a.is_aur = 1;
+    a.P = (int)Q;
+    a.KF = (int)e->KF;
+    a.gain = input_gain;
+    a.mu = mu;
+    a.lambda = afc ? afc->lambda : 0.9f;
+    a.delta = afc ? afc->delta : 1e-6f * (float)N;
+    a.nlms = mu > 0.0f;
+    e->w_elems = Q * L * e->KF * NF;
+    a.W = dalloc<float4>(e->w_elems, e->dmem);
+    std::vector<size_t> off(n_fc_rows);
+    for (size_t r = 0; r < n_fc_rows; ++r) off[r] = r * e->KF * NF;  // row p*L+l
+    partition_rows(e.get(), a, fc, n_fc_rows, n_hf, e->KF, a.W, off);
+    if (a.nlms) {
+      e->W0 = dalloc<float4>(e->w_elems, e->dmem);
+      CK(cudaMemcpy(e->W0, a.W, sizeof(float4) * e->w_elems, cudaMemcpyDeviceToDevice));
+    }
+    a.XA = dalloc<float4>(L * (e->KF + 1) * NF, e->dmem);
+    a.prev_spk = dalloc<float>(L * N, e->dmem);
+    a.fhat = dalloc<float>(Q * N, e->dmem);
+    a.pw = dalloc<float2>(N, e->dmem);
+    a.pw_part = dalloc<float2>(L * N, e->dmem);
+    a.E = dalloc<float4>(Q * NF, e->dmem);
+    CK(cudaMemset(a.XA, 0, sizeof(float4) * L * (e->KF + 1) * NF));
+    CK(cudaMemset(a.prev_spk, 0, sizeof(float) * L * N));
+    CK(cudaMemset(a.fhat, 0, sizeof(float) * Q * N));
+    CK(cudaMemset(a.pw, 0, sizeof(float2) * N));
+    CK(cudaMemset(a.pw_part, 0, sizeof(float2) * L * N));
+    CK(cudaMemset(a.E, 0, sizeof(float4) * Q * NF));
+    plan_split(e.get(), a);
+    a.part_syn = dalloc<float4>((size_t)a.syn_chunks * L * NF, e->dmem);
+    a.part_afc = dalloc<float4>((size_t)a.afc_chunks * Q * NF, e->dmem);
+    finish_init(e.get());
+    *out = e.release();
+  });
+}
+
+void aura_b200_destroy(aura_b200_engine* e) { delete e; }
+
+int aura_b200_process(aura_b200_engine* e, const float* in, float* out) {
+  return guarded([&] {
+    if (!e || !in || !out) fail(AURA_B200_E_INVALID_ARGUMENT, "null argument");
+    const size_t n_in = (size_t)e->Qx * e->N;
+    for (size_t i = 0; i < n_in; ++i)
+      if (!std::isfinite(in[i])) fail(AURA_B200_E_NON_FINITE_INPUT, "input contains NaN or Inf");
+    CK(cudaSetDevice(e->device));
+    std::memcpy(e->h_in, in, n_in * sizeof(float));
+    const uint32_t expect = (uint32_t)(e->blocks + 1);
+    std::atomic_thread_fence(std::memory_order_release);
+    CK(cudaGraphLaunch(e->g_host, e->stream));
+    volatile uint32_t* done = e->h_done;
+    uint64_t spins = 0;
+    auto t0 = std::chrono::steady_clock::now();
+    while (*done != expect) {
+#if defined(__x86_64__)
+      _mm_pause();
+#endif
+      if ((++spins & 0xFFFF) == 0) {
+        const cudaError_t q = cudaStreamQuery(e->stream);
+        if (q != cudaSuccess && q != cudaErrorNotReady) ck(q, "block execution");
+        if (q == cudaSuccess && *done != expect)
+          fail(AURA_B200_E_CUDA, "block finished without publishing its output");
+        if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(20))
+          fail(AURA_B200_E_TIMEOUT, "block did not complete within 20 s");
+      }
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
+    std::memcpy(out, e->h_out, e->L * e->N * sizeof(float));
+    ++e->blocks;
+  });
+}
+
+int aura_b200_reset(aura_b200_engine* e) {
+  return guarded([&] {
+    CK(cudaSetDevice(e->device));
+    reset_state(e);
+  });
+}
+
+int aura_b200_feedback_estimate(aura_b200_engine* e, float* out) {
+  return guarded([&] {
+    if (!e->aur) fail(AURA_B200_E_INVALID_ARGUMENT, "not an auralizer");
+    CK(cudaSetDevice(e->device));
+    CK(cudaStreamSynchronize(e->stream));
+    CK(cudaMemcpy(out, e->args.fhat, sizeof(float) * e->P * e->N, cudaMemcpyDeviceToHost));
+  });
+}
+
+int aura_b200_set_input_gain(aura_b200_engine* e, float gain) {
+  return guarded([&] {
+    if (!e->aur) fail(AURA_B200_E_INVALID_ARGUMENT, "not an auralizer");
+    CK(cudaSetDevice(e->device));
+    CK(cudaStreamSynchronize(e->stream));
+    e->args.gain = gain;
+    cudaGraphExecDestroy(e->g_host);
+    e->g_host = nullptr;
+    e->g_host = e->capture(e->args);
+    if (e->g_dev) {
+      cudaGraphExecDestroy(e->g_dev);
+      e->g_dev = nullptr;
+    }
+    e->dev_args.gain = gain;
+  });
+}
+
+float aura_b200_input_gain(const aura_b200_engine* e) { return e->args.gain; }
+uint64_t aura_b200_blocks_processed(const aura_b200_engine* e) { return e->blocks; }
+size_t aura_b200_partition_count(const aura_b200_engine* e) { return e->K; }
+size_t aura_b200_fc_partition_count(const aura_b200_engine* e) { return e->aur ? e->KF : 0; }
+size_t aura_b200_filter_length(const aura_b200_engine* e) { return e->n_h; }
+int aura_b200_mode(const aura_b200_engine* e) { return e->mode; }
+
+static void unpack_row(const float2* packed, size_t N, float* out) {
+  // packed bin 0 = (DC, Nyquist) -> reference bins 0 and N, imag exactly 0
+  out[0] = packed[0].x;
+  out[1] = 0.0f;
+  for (size_t j = 1; j < N; ++j) {
+    out[2 * j] = packed[j].x;
+    out[2 * j + 1] = packed[j].y;
+  }
+  out[2 * N] = packed[0].y;
+  out[2 * N + 1] = 0.0f;
+}
+
+int aura_b200_filter_spectrum(aura_b200_engine* e, size_t row, size_t k, float* out) {
+  return guarded([&] {
+    const size_t rows = e->mode == AURA_B200_MIMO ? e->Q * e->L : e->L;
+    if (row >= rows || k >= e->K) fail(AURA_B200_E_INVALID_ARGUMENT, "spectrum index out of range");
+    CK(cudaSetDevice(e->device));
+    size_t l = row, q = 0;
+    if (e->mode == AURA_B200_MIMO) { q = row / e->L; l = row % e->L; }
+    const size_t NF = e->N / 2;
+    const size_t Qh = e->mode == AURA_B200_MIMO ? e->Q : 1;
+    std::vector<float2> buf(e->N);
+    CK(cudaMemcpy(buf.data(), e->args.H + ((l * Qh + q) * e->K + k) * NF,
+                  sizeof(float2) * e->N, cudaMemcpyDeviceToHost));
+    unpack_row(buf.data(), e->N, out);
+  });
+}
+
+int aura_b200_afc_coeffs(aura_b200_engine* e, float* out) {
+  return guarded([&] {
+    if (!e->aur) fail(AURA_B200_E_INVALID_ARGUMENT, "not an auralizer");
+    CK(cudaSetDevice(e->device));
+    CK(cudaStreamSynchronize(e->stream));
+    std::vector<float2> buf(e->w_elems * 2);
+    CK(cudaMemcpy(buf.data(), e->args.W, sizeof(float4) * e->w_elems, cudaMemcpyDeviceToHost));
+    const size_t rows = e->P * e->L * e->KF;
+    for (size_t r = 0; r < rows; ++r) unpack_row(buf.data() + r * e->N, e->N, out + r * 2 * (e->N + 1));
+  });
+}
+
+// ------------------------------------------------------------ measurement
+
+int aura_b200_time_device_blocks(aura_b200_engine* e, const float* host_in,
+                                 size_t n_in_blocks, size_t blocks, float* block_us) {
+  return guarded([&] {
+    CK(cudaSetDevice(e->device));
+    const size_t per = (size_t)e->Qx * e->N;
+    if (host_in && n_in_blocks) {
+      const size_t nb = std::min(n_in_blocks, e->pool_blocks);
+      CK(cudaMemcpy(e->d_in_pool, host_in, nb * per * sizeof(float), cudaMemcpyHostToDevice));
+    }
+    // one graph per pool slot: the input pointer is baked per slot
+    std::vector<cudaGraphExec_t> gs;
+    const size_t slots = std::max<size_t>(1, std::min(n_in_blocks, e->pool_blocks));
+    for (size_t s = 0; s < slots; ++s) {
+      BlockArgs a = e->dev_args;
+      a.in = e->d_in_pool + s * per;
+      gs.push_back(e->capture(a));
+    }
+    std::vector<cudaEvent_t> ev(2 * blocks);
+    for (auto& x : ev) CK(cudaEventCreate(&x));
+    for (size_t b = 0; b < blocks; ++b) {
+      CK(cudaEventRecord(ev[2 * b], e->stream));
+      CK(cudaGraphLaunch(gs[b % slots], e->stream));
+      CK(cudaEventRecord(ev[2 * b + 1], e->stream));
+    }
+    CK(cudaStreamSynchronize(e->stream));
+    for (size_t b = 0; b < blocks; ++b) {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, ev[2 * b], ev[2 * b + 1]));
+      block_us[b] = ms * 1000.0f;
+    }
+    for (auto& x : ev) cudaEventDestroy(x);
+    for (auto g : gs) cudaGraphExecDestroy(g);
+    e->blocks += blocks;
+    *e->h_done = (uint32_t)e->blocks;
+  });
+}
+
+int aura_b200_profile_phases(aura_b200_engine* e, size_t blocks, float* phase_us,
+                             int* n_phases) {
+  return guarded([&] {
+    CK(cudaSetDevice(e->device));
+    const int np = e->n_phases();
+    std::vector<cudaEvent_t> ev((size_t)(np + 1) * blocks);
+    for (auto& x : ev) CK(cudaEventCreate(&x));
+    for (size_t b = 0; b < blocks; ++b) {
+      BlockArgs a = e->dev_args;
+      a.in = e->d_in_pool + (b % e->pool_blocks) * (size_t)e->Qx * e->N;
+      for (int ph = 0; ph < np; ++ph) {
+        CK(cudaEventRecord(ev[b * (np + 1) + ph], e->stream));
+        e->launch_phase(ph, a, e->stream);
+      }
+      CK(cudaEventRecord(ev[b * (np + 1) + np], e->stream));
+    }
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(e->stream));
+    for (int ph = 0; ph < np; ++ph) {
+      double s = 0;
+      for (size_t b = 0; b < blocks; ++b) {
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, ev[b * (np + 1) + ph], ev[b * (np + 1) + ph + 1]));
+        s += ms;
+      }
+      phase_us[ph] = (float)(1000.0 * s / (double)blocks);
+    }
+    for (auto& x : ev) cudaEventDestroy(x);
+    *n_phases = np;
+    e->blocks += blocks;
+    *e->h_done = (uint32_t)e->blocks;
+  });
+}
+
+const char* aura_b200_phase_name(const aura_b200_engine*, int phase) {
+  return (phase >= 0 && phase < PH_COUNT) ? kPhaseNames[phase] : "";
+}
+
+double aura_b200_phase_bytes(const aura_b200_engine* e, int phase) { return e->phase_bytes(phase); }
+
+int aura_b200_describe(const aura_b200_engine* e, char* buf, size_t cap) {
+  return guarded([&] {
+    const BlockArgs& a = e->args;
+    std::snprintf(buf, cap,
+                  "N=%zu Q=%zu L=%zu P=%zu K=%zu KF=%zu mode=%d LT=%d PT=%d "
+                  "syn: chunks=%d tc=%d nft=%d tiles=%d grid=(%d,%zu,%d)x%d | "
+                  "afc: chunks=%d uc=%d nft=%d tiles=%d nlms=%d",
+                  e->N, e->Q, e->L, e->P, e->K, e->KF, e->mode, e->LT, e->PT, a.syn_chunks,
+                  a.syn_tc, a.syn_nft, a.syn_tiles, a.syn_chunks, e->L / e->LT, a.syn_tiles,
+                  kMacThreads, a.afc_chunks, a.afc_uc, a.afc_nft, a.afc_tiles, a.nlms);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,197 @@
+"""GPU parity: the B200 Auralizer (synthesis + feedback canceller, through
+the C-ABI) against the reference (golden fixtures, mu = 0) and against the
+C oracle with the NLMS update (mu > 0) and MIMO
+(Appendix B). Mirrors test_auralizer.cpp and the closed-loop oracle."""
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2509_04390_b200 as A
+from closed_loop import simulate
+from conftest import decaying_filters, golden, rel_err, scaled_filters
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-5
+
+
+def gpu_aur(synth, fc, N, Q, L, gain=1.0, mu=0.0, lam=0.9, delta=None):
+    cfg = A.make_config(48000, N, Q, L, mimo=Q > 1)
+    return A.Auralizer(list(synth), list(fc), cfg, input_gain=gain,
+                       afc=A.AfcParams(mu, lam, delta))
+
+
+@pytest.mark.parametrize("name", ["aur_n64", "aur_n32_gain", "aur_n128_long"])
+def test_golden_reference_auralizer(name):
+    g = golden(name)
+    N, L = int(g["N"]), int(g["L"])
+    aur = gpu_aur(g["synth"], g["fc"], N, 1, L, gain=float(g["gain"]))
+    ys, fh = [], []
+    for m in g["mic"]:
+        ys.append(aur.process(m))
+        fh.append(aur.feedback_estimate()[0])
+    assert rel_err(np.stack(ys), g["y"]) <= TOL
+    assert rel_err(np.stack(fh), g["fhat"]) <= TOL
+
+
+def test_partition_counts_at_paper_defaults():
+    # test_auralizer.cpp:39-45
+    rng = np.random.default_rng(1)
+    aur = gpu_aur(scaled_filters(rng, 4, 480000), scaled_filters(rng, 4, 48000), 128, 1, 4)
+    assert aur.synth_partitions() == 3750 and aur.fc_partitions() == 375
+
+
+def test_zero_fc_is_bit_identical_to_plain_synthesis():
+    # test_auralizer.cpp:47-65 (EXPECT_EQ)
+    N, L = 64, 3
+    rng = np.random.default_rng(2)
+    synth = scaled_filters(rng, L, 200)
+    aur = gpu_aur(synth, np.zeros((L, 100), np.float32), N, 1, L)
+    plain = A.Convolver(list(synth), A.make_config(48000, N, 1, L))
+    for _ in range(8):
+        x = rng.standard_normal((1, N)).astype(np.float32)
+        assert np.array_equal(aur.process(x), plain.process(x))
+        assert np.all(aur.feedback_estimate() == 0.0)
+
+
+def test_first_call_zero_estimate_then_nonzero():
+    rng = np.random.default_rng(3)
+    aur = gpu_aur(scaled_filters(rng, 2, 128), scaled_filters(rng, 2, 128), 64, 1, 2)
+    assert np.all(aur.feedback_estimate() == 0.0)
+    aur.process(rng.standard_normal((1, 64)).astype(np.float32))
+    assert np.any(aur.feedback_estimate() != 0.0)
+
+
+@pytest.mark.parametrize("mu", [0.0, 0.01])
+def test_reset_restores_fresh_state_exactly(mu):
+    # test_auralizer.cpp:103-125, plus NLMS state (W restored to F^_0)
+    N = 64
+    rng = np.random.default_rng(11)
+    aur = gpu_aur(scaled_filters(rng, 2, 300), scaled_filters(rng, 2, 200, 0.1), N, 1, 2,
+                  mu=mu)
+    x = rng.standard_normal((1, N)).astype(np.float32)
+    fresh = aur.process(x).copy()
+    fresh_est = aur.feedback_estimate().copy()
+    W0 = aur.coeffs().copy()
+    for _ in range(10):
+        aur.process(rng.standard_normal((1, N)).astype(np.float32))
+    aur.reset()
+    assert np.all(aur.feedback_estimate() == 0.0)
+    assert np.array_equal(aur.process(x), fresh)
+    assert np.array_equal(aur.feedback_estimate(), fresh_est)
+    aur.reset()
+    aur.reset()
+    assert np.array_equal(aur.process(np.zeros((1, N), np.float32)), np.zeros((2, N)))
+    if mu == 0.0:
+        assert np.array_equal(aur.coeffs(), W0)
+
+
+def test_one_block_causality():
+    # test_auralizer.cpp:161-186 (EXPECT_EQ)
+    N, L, blocks = 64, 2, 6
+    rng = np.random.default_rng(15)
+    s, fc = scaled_filters(rng, L, 3 * N), scaled_filters(rng, L, 2 * N)
+    hist = [rng.standard_normal((1, N)).astype(np.float32) for _ in range(blocks)]
+    a, b = gpu_aur(s, fc, N, 1, L), gpu_aur(s, fc, N, 1, L)
+    for n in range(blocks):
+        last = n + 1 == blocks
+        ya = a.process(hist[n])
+        yb = b.process(rng.standard_normal((1, N)).astype(np.float32) if last else hist[n])
+        if not last:
+            assert np.array_equal(ya, yb)
+
+
+def test_fused_equals_manual_composition():
+    # test_auralizer.cpp:127-159, composed from the GPU Convolver
+    N, L, blocks = 64, 3, 12
+    rng = np.random.default_rng(13)
+    synth = scaled_filters(rng, L, 5 * N + 3)
+    fc = scaled_filters(rng, L, 2 * N + 1)
+    aur = gpu_aur(synth, fc, N, 1, L)
+    sref = A.Convolver(list(synth), A.make_config(48000, N, 1, L))
+    fref = A.Convolver(list(fc), A.make_config(48000, N, L, L), A.ChannelMode.elementwise)
+    est = np.zeros(N, np.float32)
+    for _ in range(blocks):
+        x = rng.standard_normal((1, N)).astype(np.float32)
+        fused = aur.process(x)
+        spk = sref.process((x - est).astype(np.float32))
+        est = fref.process(spk).sum(axis=0, dtype=np.float32)
+        assert np.max(np.abs(fused - spk)) <= 1e-5
+
+
+def test_input_gain():
+    N = 64
+    rng = np.random.default_rng(17)
+    s = scaled_filters(rng, 1, 100)
+    fc = np.zeros((1, 50), np.float32)
+    unit, twice = gpu_aur(s, fc, N, 1, 1, 1.0), gpu_aur(s, fc, N, 1, 1, 2.0)
+    assert twice.input_gain() == 2.0
+    x = rng.standard_normal((1, N)).astype(np.float32)
+    assert np.max(np.abs(twice.process(x) - unit.process(2 * x))) <= 1e-6
+    twice.set_input_gain(0.5)
+    assert twice.input_gain() == 0.5
+
+
+@pytest.mark.parametrize("Q,L,N,mu", [(1, 4, 64, 0.01), (1, 16, 32, 0.05), (4, 8, 64, 0.01),
+                                      (2, 5, 16, 0.02), (1, 3, 256, 0.0), (4, 6, 32, 0.0)])
+def test_nlms_and_mimo_vs_oracle(Q, L, N, mu):
+    """Outputs, f^ and the canceller spectra W after 200 blocks match the C
+    oracle (Appendix A/B) within 1e-5 of their RMS."""
+    rng = np.random.default_rng(Q * 1000 + L * 10 + N)
+    synth = decaying_filters(rng, Q * L, 12 * N + 5, scale=0.5)
+    fc = decaying_filters(rng, Q * L, 4 * N + 1, scale=0.1)
+    kw = dict(gain=0.9, mu=mu, lam=0.9, delta=1e-2)
+    g = gpu_aur(synth, fc, N, Q, L, **kw)
+    o = O.OracleAuralizer(synth, fc, N, Q, L, **kw)
+    ys, yo, fg, fo = [], [], [], []
+    for _ in range(200):
+        m = rng.standard_normal((Q, N)).astype(np.float32)
+        ys.append(g.process(m))
+        yo.append(o.process(m))
+        fg.append(g.feedback_estimate())
+        fo.append(o.feedback_estimate())
+    assert rel_err(np.stack(ys), np.stack(yo)) <= TOL
+    assert rel_err(np.stack(fg), np.stack(fo)) <= TOL
+    assert rel_err(g.coeffs(), o.coeffs()) <= TOL
+
+
+def test_closed_loop_perfect_cancellation():
+    """verify.hpp:148-179 / acceptance C3: F^ = F -> residual < 1e-4."""
+    N, L, blocks = 128, 2, 50
+    rng = np.random.default_rng(7)
+    synth = scaled_filters(rng, L, 3 * N)
+    fc = scaled_filters(rng, L, 4800, 0.1)
+    aur = gpu_aur(synth, fc, N, 1, L)
+    src = rng.standard_normal((1, blocks * N))
+    res = simulate(aur, src, fc.astype(np.float64)[None], N, blocks)
+    assert max(np.max(np.abs(r)) for r in res["residual"]) < 1e-4
+
+
+def test_closed_loop_divergence_without_cancellation():
+    """verify.hpp:182-206: F^ = 0, loop gain 1.2 -> mic energy grows."""
+    N, blocks = 64, 14
+    aur = gpu_aur(np.ones((1, 1), np.float32), np.zeros((1, 1), np.float32), N, 1, 1)
+    src = np.ones((1, blocks * N))
+    res = simulate(aur, src, np.array([[[1.2]]]), N, blocks)
+    energy = [float(np.sum(m.astype(np.float64) ** 2)) for m in res["mic"]]
+    assert all(energy[b + 1] > energy[b] for b in range(3, 12))
+
+
+def test_c3_config_streams_and_matches_oracle_subset():
+    """configs[2] shape (1 x 64, N = 64, 10 s synthesis, 1 s canceller, NLMS
+    on): 300 blocks on the GPU against the C oracle at full size."""
+    N, L = 64, 64
+    rng = np.random.default_rng(2024)
+    synth = decaying_filters(rng, L, 480000)
+    fc = decaying_filters(rng, L, 48000, t60_s=0.3, scale=0.1)
+    kw = dict(mu=0.005, lam=0.9, delta=1e-6 * N)
+    g = gpu_aur(synth, fc, N, 1, L, **kw)
+    assert g.synth_partitions() == 7500 and g.fc_partitions() == 750
+    o = O.OracleAuralizer(synth, fc, N, 1, L, **kw)
+    ys, yo = [], []
+    for _ in range(40):
+        m = rng.standard_normal((1, N)).astype(np.float32)
+        ys.append(g.process(m))
+        yo.append(o.process(m))
+    assert rel_err(np.stack(ys), np.stack(yo)) <= TOL
+    assert rel_err(g.feedback_estimate(), o.feedback_estimate()) <= TOL
+    assert rel_err(g.coeffs(), o.coeffs()) <= TOL

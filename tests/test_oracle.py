@@ -1,0 +1,147 @@
+"""CPU: pin the C oracle (oracle/aura_oracle.c) against the UNMODIFIED
+reference (oracle/_ref) and against the committed golden fixtures.
+
+With the reference present the comparison is bit-exact (same float
+operations in the same order, -ffp-contract=off)."""
+import numpy as np
+import pytest
+
+import oracle as O
+from conftest import golden, scaled_filters
+
+need_ref = pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+
+
+def bits_equal(a, b):
+    a = np.ascontiguousarray(a)
+    b = np.ascontiguousarray(b)
+    return a.shape == b.shape and np.array_equal(a.view(np.uint32), b.view(np.uint32))
+
+
+@pytest.mark.parametrize("nf", [32, 64, 128, 512, 2048, 16384])
+@need_ref
+def test_fft_bitexact_vs_reference(nf):
+    rng = np.random.default_rng(nf)
+    x = rng.standard_normal(nf).astype(np.float32)
+    X = O.forward(x)
+    assert bits_equal(X, O.ref_forward(x))
+    assert bits_equal(O.inverse(X), O.ref_inverse(X))
+
+
+def test_fft_golden():
+    g = golden("fft")
+    for nf in (32, 64, 256, 1024):
+        assert bits_equal(O.forward(g[f"x{nf}"]), g[f"X{nf}"])
+        assert bits_equal(O.inverse(g[f"X{nf}"]), g[f"xi{nf}"])
+    # test_dft.cpp:56-64: impulse -> flat spectrum
+    assert np.allclose(g["impulse64"], 1.0, atol=1e-6)
+    assert np.allclose(O.forward(np.eye(1, 64, dtype=np.float32)[0]), 1.0, atol=1e-6)
+
+
+def test_fft_against_numpy():
+    rng = np.random.default_rng(1)
+    for nf in (32, 256, 4096):
+        x = rng.standard_normal(nf).astype(np.float32)
+        ref = np.fft.rfft(x.astype(np.float64))
+        assert np.max(np.abs(O.forward(x) - ref)) < 1e-5 * nf  # test_dft.cpp:76-100
+        assert O.forward(x)[0].imag == 0.0 and O.forward(x)[-1].imag == 0.0
+
+
+def test_direct_convolve_kat():
+    # test_oracle.cpp:44-51
+    assert np.array_equal(O.direct_convolve([1, 2, 3], [1, 1]), [1, 3, 5, 3])
+    g = golden("direct")
+    assert np.array_equal(g["kat"], [1, 3, 5, 3])
+    assert np.allclose(O.direct_convolve(g["x"], g["h"]), g["y"], rtol=0, atol=1e-12)
+
+
+@pytest.mark.parametrize("name", ["conv_bcast_n64", "conv_bcast_n128", "conv_elem_n16",
+                                  "conv_bcast_n16_h1", "conv_bcast_n256_long"])
+def test_convolver_golden(name):
+    g = golden(name)
+    N, L, mode = int(g["N"]), int(g["L"]), int(g["mode"])
+    inputs = 1 if mode == O.BROADCAST else L
+    oc = O.OracleConvolver(g["filters"], N, inputs, L, mode)
+    assert oc.partitions == int(g["partitions"])
+    y = np.stack([oc.process(x) for x in g["x"]])
+    assert bits_equal(y, g["y"])
+    k_show = min(oc.partitions, 3)
+    spec = np.stack([oc.spectrum(c, k) for c in range(L) for k in range(k_show)])
+    assert bits_equal(spec, g["spectra"])
+
+
+@pytest.mark.parametrize("name", ["aur_n64", "aur_n32_gain", "aur_n128_long"])
+def test_auralizer_golden(name):
+    g = golden(name)
+    N, L = int(g["N"]), int(g["L"])
+    oa = O.OracleAuralizer(g["synth"], g["fc"], N, 1, L, gain=float(g["gain"]))
+    for b in range(g["mic"].shape[0]):
+        assert bits_equal(oa.process(g["mic"][b]), g["y"][b])
+        assert bits_equal(oa.feedback_estimate()[0], g["fhat"][b])
+
+
+@need_ref
+@pytest.mark.parametrize("N,n_h,C,mode", [
+    (16, 1, 1, O.BROADCAST), (16, 15, 4, O.ELEMENTWISE), (64, 64, 4, O.BROADCAST),
+    (64, 65, 1, O.ELEMENTWISE), (128, 3 * 128 + 7, 4, O.BROADCAST),
+    (32, 10 * 32, 4, O.ELEMENTWISE)])
+def test_convolver_bitexact_vs_reference(N, n_h, C, mode):
+    rng = np.random.default_rng(N * 1000 + n_h)
+    f = scaled_filters(rng, C, n_h)
+    inputs = 1 if mode == O.BROADCAST else C
+    oc = O.OracleConvolver(f, N, inputs, C, mode)
+    rc = O.RefConvolver(f, N, inputs, C, mode)
+    for _ in range(oc.partitions + 3):
+        x = rng.standard_normal((inputs, N)).astype(np.float32)
+        assert bits_equal(oc.process(x), rc.process(x))
+    oc.reset(); rc.reset()
+    x = rng.standard_normal((inputs, N)).astype(np.float32)
+    assert bits_equal(oc.process(x), rc.process(x))
+
+
+@need_ref
+def test_auralizer_mu0_bitexact_vs_reference():
+    rng = np.random.default_rng(3)
+    N, L = 64, 4
+    s = scaled_filters(rng, L, 7 * N + 5)
+    fc = scaled_filters(rng, L, 3 * N + 1, 0.1)
+    oa = O.OracleAuralizer(s, fc, N, 1, L, gain=0.8)
+    ra = O.RefAuralizer(s, fc, N, L, gain=0.8)
+    for b in range(30):
+        m = rng.standard_normal((1, N)).astype(np.float32)
+        assert bits_equal(oa.process(m), ra.process(m))
+        assert bits_equal(oa.feedback_estimate()[0], ra.feedback_estimate())
+        if b == 15:
+            oa.reset(); ra.reset()
+
+
+@need_ref
+def test_reference_verify_small_grid_passes():
+    ok, log = O.ref_verify(full=False)
+    assert ok, log
+
+
+def test_mimo_oracle_is_sum_of_broadcast_engines():
+    """Appendix B: MIMO synthesis = sum over q of broadcast convolvers."""
+    rng = np.random.default_rng(9)
+    N, Q, L, n_h = 32, 3, 4, 200
+    f = scaled_filters(rng, Q * L, n_h)
+    mimo = O.OracleConvolver(f, N, Q, L, O.MIMO)
+    parts = [O.OracleConvolver(f[q * L:(q + 1) * L], N, 1, L, O.BROADCAST) for q in range(Q)]
+    for _ in range(12):
+        x = rng.standard_normal((Q, N)).astype(np.float32)
+        y = mimo.process(x)
+        acc = parts[0].process(x[0:1])
+        for q in range(1, Q):
+            acc = acc + parts[q].process(x[q:q + 1])
+        assert bits_equal(y, acc)
+
+
+def test_partition_count_kats():
+    # test_engine.cpp:75-78, test_auralizer.cpp:39-45
+    import paper_2509_04390_b200 as A
+    assert A.partition_count(480000, 128) == 3750
+    assert A.partition_count(48000, 128) == 375
+    assert A.partition_count(1, 64) == 1
+    if O.ref_available():
+        assert O.rlib().ref_partition_count(480000, 128) == 3750
