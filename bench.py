@@ -1,0 +1,394 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 UPOLS + feedback-canceller block loop.
+
+Metric (BASELINE.json): per-block latency p50/p99 (us) and maximum
+real-time channels x taps at 48 kHz. One "step" = one audio block through
+the whole path (m~ = g m - f^, r2c, FDL MAC over all partitions x
+loudspeakers, c2r + overlap-save, canceller r2c, canceller MAC with the NLMS
+update, f^ for the next block).
+
+    python bench.py [--config c3] [--gpus N] [--steps K] [--warmup W]
+    python bench.py --impl reference ...   # the reference's CPU path
+
+value  = p99 device time per block, inputs resident in HBM, CUDA events on
+         the engine stream (lower is better).
+e2e    = p99 of aura_b200_process() with host buffers (host->device input,
+         all kernels, device->host output, completion wait), steady_clock.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = ("per-block latency p50/p99 (µs) and max real-time channels×taps "
+          "at 48 kHz")
+
+# BASELINE.json configs (SURVEY 8(d) sizes); AFC length 1 s where on.
+CONFIGS = {
+    "c1": dict(fs=48000, N=256, Q=1, L=2, n_h=96000, afc=False,
+               desc="c1: 1 input x 2 loudspeakers, 48 kHz, block 256, 2 s IR (96k taps), no AFC"),
+    "c2": dict(fs=48000, N=128, Q=1, L=16, n_h=480000, afc=False,
+               desc="c2: 1 input x 16 loudspeakers, 48 kHz, block 128, 10 s IR (480k taps)"),
+    "c3": dict(fs=48000, N=64, Q=1, L=64, n_h=480000, afc=True, n_hf=48000, mu=0.005,
+               desc="c3: 1 input x 64 loudspeakers, 48 kHz, block 64, 10 s IR (480k taps), "
+                    "PBFDAF feedback canceller 1 s (48k taps) with NLMS update"),
+    "c4": dict(fs=48000, N=64, Q=4, L=64, n_h=576000, afc=True, n_hf=48000, mu=0.005,
+               desc="c4: 4 inputs x 64 loudspeakers MIMO, 48 kHz, block 64, 12 s IR (576k taps), "
+                    "AFC 1 s with NLMS"),
+    "c5": dict(fs=96000, N=128, Q=1, L=512, n_h=1920000, afc=False,
+               desc="c5: 1 input x 512 loudspeakers, 96 kHz, block 128, 20 s IR (1.92M taps)"),
+}
+
+
+def decaying_noise(rng, rows, n, fs, t60_s=None, scale=1.0):
+    """Exponentially decaying noise IRs: n(t) 10^(-3 t / T60), sum h^2 = 1
+    (SURVEY 8(d)); T60 = IR length unless given."""
+    t60 = n / fs if t60_s is None else t60_s
+    env = (10.0 ** (-3.0 * np.arange(n, dtype=np.float64) / (t60 * fs))).astype(np.float32)
+    out = np.empty((rows, n), np.float32)
+    for r in range(rows):
+        h = rng.standard_normal(n, dtype=np.float32) * env
+        h *= np.float32(scale / np.sqrt(np.dot(h.astype(np.float64), h)))
+        out[r] = h
+    return out
+
+
+def make_workload(cfg, seed=1000):
+    rng = np.random.default_rng(seed)
+    Q, L = cfg["Q"], cfg["L"]
+    synth = decaying_noise(rng, Q * L, cfg["n_h"], cfg["fs"])
+    fc = None
+    if cfg["afc"]:
+        fc = decaying_noise(rng, Q * L, cfg["n_hf"], cfg["fs"], t60_s=0.3, scale=0.1)
+    mic = np.random.default_rng(7).standard_normal((64, Q, cfg["N"])).astype(np.float32)
+    return synth, fc, mic
+
+
+def pct(a, q):
+    return float(np.percentile(np.asarray(a, np.float64), q))
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in getattr(self, "lines", []):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for name, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------ reference arm
+
+def reference_blocks(cfg, synth, fc, mic, blocks, warmup, backend="parallel", L_sub=None):
+    """Time the UNMODIFIED reference (oracle/_ref: aura::Convolver /
+    aura::Auralizer, ParallelBackend with hardware_concurrency workers) on the
+    same synthetic inputs. Q > 1 (c4) is timed as Q single-input Auralizers
+    (the same MAC work, Appendix B); the reference has no NLMS, so its
+    canceller is the fixed-F^ one."""
+    import oracle as O
+    N, Q, L = cfg["N"], cfg["Q"], cfg["L"]
+    if L_sub:
+        L = L_sub
+    t_setup = time.perf_counter()
+    engines = []
+    for q in range(Q):
+        s = synth[q * cfg["L"]:q * cfg["L"] + L]
+        if cfg["afc"]:
+            f = fc[q * cfg["L"]:q * cfg["L"] + L]
+            engines.append(O.RefAuralizer(s, f, N, L, backend=backend))
+        else:
+            engines.append(O.RefConvolver(s, N, 1, L, O.BROADCAST, backend=backend))
+    t_setup = time.perf_counter() - t_setup
+    times = []
+    for b in range(warmup + blocks):
+        m = mic[b % mic.shape[0]]
+        t0 = time.perf_counter()
+        for q, e in enumerate(engines):
+            e.process(m[q:q + 1])
+        t1 = time.perf_counter()
+        if b >= warmup:
+            times.append((t1 - t0) * 1e6)
+    workers = O.ref_backend_workers(backend)
+    return np.array(times), workers, t_setup
+
+
+def run_reference_arm(args, cfg, rank):
+    if rank != 0:
+        return 0
+    synth, fc, mic = make_workload(cfg)
+    blocks = max(1, args.steps)
+    us, workers, t_setup = reference_blocks(cfg, synth, fc, mic, blocks, args.warmup)
+    p50, p99 = pct(us, 50), pct(us, 99)
+    sample = (f"{blocks} blocks of {cfg['desc']} (after {args.warmup} warm-up), reference "
+              f"ParallelBackend, -O3 -DNDEBUG -std=c++20; fixed-F^ canceller (the reference "
+              f"has no NLMS); setup {t_setup:.1f} s excluded")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": p99, "unit": "us",
+        "n_gpus": args.gpus, "steps": blocks, "warmup": args.warmup,
+        "ms_per_step": float(np.mean(us)) / 1000.0, "higher_is_better": False,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": cfg["desc"]},
+        "p50_us": p50, "p99_us": p99, "budget_us": 1e6 * cfg["N"] / cfg["fs"],
+        "cpu_baseline": {"value": p99, "unit": "us", "cores": workers, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": p99, "unit": "us", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------- B200 arm
+
+def make_engine(A, cfg, synth, fc, device=0, L=None, mu=None):
+    N, Q = cfg["N"], cfg["Q"]
+    L = cfg["L"] if L is None else L
+    if L != cfg["L"]:
+        idx = np.concatenate([np.arange(q * cfg["L"], q * cfg["L"] + L) for q in range(Q)])
+        synth = synth[idx] if synth.shape[0] >= idx.max() + 1 else synth
+        fc = fc[idx] if fc is not None else None
+    backend = A.make_backend("gpu", device)
+    ec = A.make_config(cfg["fs"], N, Q, L, mimo=Q > 1)
+    if cfg["afc"]:
+        m = cfg.get("mu", 0.0) if mu is None else mu
+        return A.Auralizer(list(synth), list(fc), ec, backend,
+                           afc=A.AfcParams(m, 0.9, None))
+    mode = A.ChannelMode.mimo if Q > 1 else A.ChannelMode.broadcast
+    return A.Convolver(list(synth), ec, mode, backend)
+
+
+def max_realtime(A, cfg, device, blocks=300, budget_s=90.0):
+    """Largest loudspeaker count L (taps fixed at the config's n_h, same AFC
+    setting) whose p99 device block time stays under N/f_s; returns
+    (L, L * n_h). Synthetic filters are generated per L."""
+    t_start = time.perf_counter()
+    N, fs = cfg["N"], cfg["fs"]
+    budget_us = 1e6 * N / fs
+    rng = np.random.default_rng(3)
+
+    def fits(L):
+        c = dict(cfg, L=L)
+        Q = c["Q"]
+        synth = rng.standard_normal((Q * L, c["n_h"]), dtype=np.float32) * np.float32(1e-3)
+        fc = (rng.standard_normal((Q * L, c["n_hf"]), dtype=np.float32) * np.float32(1e-4)
+              if c["afc"] else None)
+        try:
+            e = make_engine(A, c, synth, fc, device)
+        except A.Error as err:
+            if err.code == A.ErrorCode.out_of_memory:
+                return False, None
+            raise
+        del synth, fc
+        mic = np.random.default_rng(7).standard_normal((64, Q, N)).astype(np.float32)
+        e.time_device_blocks(20, mic)
+        lat, us = e.time_device_blocks(blocks, mic)
+        e.close()
+        # real time needs ALL of a block's work inside its period
+        return pct(us, 99) < budget_us, pct(us, 99)
+
+    lo, hi = cfg["L"], None
+    ok, p = fits(lo)
+    if not ok:
+        return None
+    step = lo
+    while hi is None and time.perf_counter() - t_start < budget_s:
+        cand = lo + step
+        ok, p = fits(cand)
+        if ok:
+            lo, step = cand, step * 2
+        else:
+            hi = cand
+    while hi is not None and hi - lo > max(1, lo // 32) and time.perf_counter() - t_start < budget_s:
+        mid = (lo + hi) // 2
+        ok, p = fits(mid)
+        if ok:
+            lo = mid
+        else:
+            hi = mid
+    return {"channels": lo, "taps": cfg["n_h"], "channels_x_taps": lo * cfg["n_h"],
+            "upper_bound_channels": hi, "p99_criterion_us": budget_us}
+
+
+def run_b200_arm(args, cfg, rank, world, local_rank):
+    import paper_2509_04390_b200 as A
+    device = local_rank
+    if world > 1:
+        return run_sharded(args, cfg, rank, world, local_rank)
+    synth, fc, mic = make_workload(cfg)
+    t0 = time.perf_counter()
+    eng = make_engine(A, cfg, synth, fc, device)
+    t_setup = time.perf_counter() - t0
+    N, Q, L = cfg["N"], cfg["Q"], cfg["L"]
+    K, W = args.steps, args.warmup
+
+    # warm-up, then device-resident timed region (value)
+    eng.time_device_blocks(max(3, W), mic)
+    with ClockSampler(device) as clk:
+        lat_us, dev_us = eng.time_device_blocks(K, mic)
+        host_us = eng.time_host_blocks(mic, K)
+    clocks = clk.summary()
+    phases = eng.profile_phases(min(K, 200))
+    peak, peak_kind = load_peaks()
+    mac_us, mac_bytes = phases["k_mac_pre"]
+    if mac_bytes == 0:
+        mac_us, mac_bytes = phases["k_front"]
+    achieved = mac_bytes / (mac_us * 1e-6) / 1e9
+    n_launch = 1 + (2 if phases["k_mac_pre"][1] > 0 else 0) + (2 if cfg["afc"] else 0)
+
+    paced = None
+    if not args.no_paced:
+        paced_us = eng.time_host_blocks(mic, min(K, 2000), pace_us=1e6 * N / cfg["fs"])
+        paced = {"p50_us": pct(paced_us, 50), "p99_us": pct(paced_us, 99),
+                 "blocks": int(paced_us.size),
+                 "definition": "aura_b200_process() latency with calls on the real-time grid "
+                               "(one block every N/fs), host buffers"}
+
+    cpu = None
+    if not args.no_cpu_baseline:
+        ref_blocks = max(3, int(args.cpu_blocks))
+        us, workers, t_ref_setup = reference_blocks(cfg, synth, fc, mic, ref_blocks, 2)
+        cpu = {"value": pct(us, 99), "unit": "us", "cores": workers, "kind": "reference",
+               "p50_us": pct(us, 50),
+               "sample": f"{ref_blocks} blocks of the same workload through the unmodified "
+                         f"reference (oracle/_ref, ParallelBackend, -O3 -DNDEBUG); fixed-F^ "
+                         f"canceller (no NLMS in the reference); setup {t_ref_setup:.1f} s excluded"}
+    maxrt = None
+    if args.max_rt:
+        del synth, fc
+        eng.close()
+        maxrt = max_realtime(A, cfg, device)
+
+    total_bytes = sum(b for _, b in phases.values())
+    line = {
+        "metric": METRIC, "value": pct(dev_us, 99), "unit": "us", "n_gpus": 1,
+        "steps": K, "warmup": W, "ms_per_step": float(np.mean(dev_us)) / 1000.0,
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic: decaying-noise IRs (T60 = IR length, sum h^2 = 1), "
+                                "AFC paths T60 0.3 s x 0.1, N(0,1) mic blocks",
+        "config": {"workload": cfg["desc"], "block": N, "inputs": Q, "loudspeakers": L,
+                   "taps": cfg["n_h"], "fc_taps": cfg.get("n_hf", 0),
+                   "nlms_mu": cfg.get("mu", 0.0) if cfg["afc"] else None,
+                   "l2": f"inputs larger than L2: {total_bytes / 1e6:.0f} MB streamed per block "
+                         f"vs 126 MB L2" if total_bytes > 126e6 else
+                         "working set fits L2 (real-time steady state; no flush)",
+                   "parallelism": "1 GPU", "engine": eng.describe() if not args.max_rt else None},
+        "p50_us": pct(dev_us, 50), "p99_us": pct(dev_us, 99), "max_us": float(np.max(dev_us)),
+        "budget_us": 1e6 * N / cfg["fs"],
+        "value_definition": "p99 device time of ALL of a block's work (front + background "
+                            "graphs), back to back, inputs in HBM",
+        "latency_to_output_us": {"p50": pct(lat_us, 50), "p99": pct(lat_us, 99),
+                                 "definition": "device time from block start to its output "
+                                               "written (front graph); the rest of the block's "
+                                               "work runs after the output is published"},
+        "e2e": {"value": pct(host_us, 99), "unit": "us", "p50_us": pct(host_us, 50),
+                "h2d_bytes_per_step": 4 * Q * N, "d2h_bytes_per_step": 4 * L * N,
+                "path": "aura_b200_process() C-ABI, pinned mapped host I/O, back-to-back "
+                        "(each call also waits for the previous block's background work)"},
+        "paced_e2e": paced,
+        "roofline": {"bound": "hbm", "kernel": "k_mac_pre", "achieved": achieved,
+                     "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "peak_kind": peak_kind, "traffic": None,
+                     "bytes_per_launch": mac_bytes, "avg_launch_us": mac_us},
+        "phases_us": {k: v[0] for k, v in phases.items()},
+        "phases_GBps": {k: v[1] / (v[0] * 1e-6) / 1e9 for k, v in phases.items()},
+        "cpu_baseline": cpu, "clocks": clocks, "gpu_launches": int(K * n_launch),
+        "max_realtime": maxrt, "setup_s": t_setup,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_sharded(args, cfg, rank, world, local_rank):
+    raise SystemExit("multi-GPU sharding: not implemented in this build")
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=50)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--block", type=int, default=None, help="override block size (c4 sweep)")
+    ap.add_argument("--cpu-blocks", type=int, default=60)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--max-rt", action="store_true")
+    ap.add_argument("--no-paced", action="store_true")
+    args = ap.parse_args()
+    cfg = dict(CONFIGS[args.config])
+    if args.block:
+        cfg["N"] = args.block
+        cfg["desc"] += f" [block {args.block}]"
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference_arm(args, cfg, rank)
+    return run_b200_arm(args, cfg, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,127 @@
+// Drop-in for the reference's aura/backend.hpp (backend.hpp:1-257).
+//
+// Put <repo>/include BEFORE the reference's include directory. This header
+// pulls in the reference's backend.hpp unchanged (#include_next) -- its
+// ExecutionBackend interface, CPU dispatchers and spectral_mac helpers -- and
+// fills the reserved accelerator slot (backend.hpp:16, :201-203) with the
+// B200 engine: make_backend("accelerator"|"gpu") returns an
+// AcceleratorBackend and list_backends() lists one entry per B200.
+#pragma once
+
+#define list_backends aura_reference_list_backends
+#define make_backend aura_reference_make_backend
+#include_next <aura/backend.hpp>
+#undef list_backends
+#undef make_backend
+
+#include <cstdio>
+#include <memory>
+#include <string>
+#include <string_view>
+#include <vector>
+
+#include "aura_b200.h"
+
+namespace aura {
+
+/// The B200 device slot. It carries no CPU dispatch: Convolver and Auralizer
+/// see it and run their whole block loop on the GPU (csrc/, C-ABI
+/// aura_b200.h); for_each is a plain serial loop kept only so the interface
+/// stays complete.
+class AcceleratorBackend final : public ExecutionBackend {
+ public:
+  explicit AcceleratorBackend(int device = 0) : device_(device) {
+    char name[256] = {0};
+    if (aura_b200_device_name(device, name, sizeof name) != AURA_B200_OK)
+      raise(ErrorCode::backend_unavailable,
+            std::string("accelerator backend is not available: ") + aura_b200_last_error());
+    desc_.name = "accelerator";
+    desc_.kind = BackendKind::accelerator;
+    desc_.available = true;
+    desc_.detail = name;
+  }
+  const BackendDescriptor& descriptor() const override { return desc_; }
+  void for_each(std::size_t count, TaskFn fn, void* ctx) override {
+    for (std::size_t i = 0; i < count; ++i) fn(ctx, i);
+  }
+  int device() const noexcept { return device_; }
+
+ private:
+  int device_;
+  BackendDescriptor desc_;
+};
+
+inline int accelerator_count() noexcept {
+  int n = 0;
+  if (aura_b200_device_count(&n) != AURA_B200_OK) return 0;
+  return n;
+}
+
+/// backend.hpp:186-193 plus one accelerator entry per usable B200.
+inline std::vector<BackendDescriptor> list_backends() {
+  auto out = aura_reference_list_backends();
+  const int n = accelerator_count();
+  for (int d = 0; d < n; ++d) {
+    char name[256] = {0};
+    aura_b200_device_name(d, name, sizeof name);
+    out.push_back({"accelerator", BackendKind::accelerator, true, name});
+  }
+  return out;
+}
+
+/// backend.hpp:197-207 with the accelerator slot filled.
+inline std::shared_ptr<ExecutionBackend> make_backend(std::string_view name) {
+  if (name == "accelerator" || name == "gpu") {
+    if (accelerator_count() == 0)
+      raise(ErrorCode::backend_unavailable,
+            "accelerator backend is not available: no compatible device");
+    return std::make_shared<AcceleratorBackend>(0);
+  }
+  return aura_reference_make_backend(name);
+}
+
+namespace b200_detail {
+
+[[noreturn]] inline void rethrow(int rc) {
+  const std::string msg = aura_b200_last_error();
+  if (rc >= 1 && rc <= static_cast<int>(ErrorCode::invalid_argument) + 1)
+    raise(static_cast<ErrorCode>(rc - 1), msg);
+  raise(ErrorCode::backend_unavailable, "accelerator failure: " + msg);
+}
+inline void check(int rc) {
+  if (rc != AURA_B200_OK) rethrow(rc);
+}
+
+/// nullptr -> the default accelerator; a CPU backend is rejected (this
+/// build's Convolver/Auralizer have no CPU path).
+inline int device_of(const std::shared_ptr<ExecutionBackend>& b) {
+  if (!b) return 0;
+  if (auto* acc = dynamic_cast<const AcceleratorBackend*>(b.get())) return acc->device();
+  raise(ErrorCode::backend_unavailable,
+        "this build of aura::Convolver/Auralizer runs on the accelerator only; backend '" +
+            b->descriptor().name + "' is a CPU backend");
+}
+
+inline std::shared_ptr<ExecutionBackend> resolve(std::shared_ptr<ExecutionBackend> b) {
+  if (b) return b;
+  return std::make_shared<AcceleratorBackend>(0);
+}
+
+struct EngineDeleter {
+  void operator()(aura_b200_engine* e) const noexcept { aura_b200_destroy(e); }
+};
+using EnginePtr = std::unique_ptr<aura_b200_engine, EngineDeleter>;
+
+inline std::vector<const float*> row_pointers(std::span<const std::vector<float>> rows) {
+  std::vector<const float*> p(rows.size());
+  for (std::size_t i = 0; i < rows.size(); ++i) p[i] = rows[i].data();
+  return p;
+}
+
+inline aura_b200_config to_c(const EngineConfig& c) {
+  return aura_b200_config{c.sample_rate_hz, c.block_size, c.fft_size, c.input_channels,
+                          c.output_channels};
+}
+
+}  // namespace b200_detail
+}  // namespace aura

@@ -136,6 +136,11 @@ int aura_b200_reset(aura_b200_engine* e);
 
 /* Auralizer::feedback_estimate (auralizer.hpp:56-58): inputs x N floats */
 int aura_b200_feedback_estimate(aura_b200_engine* e, float* out);
+/* Zero-copy view of the same estimate: a pinned host buffer the GPU writes
+ * at the end of every block (inputs x N floats), valid while the engine
+ * lives and stable between process() calls. Backs the C++ drop-in's
+ * span-returning feedback_estimate(). */
+int aura_b200_feedback_estimate_view(aura_b200_engine* e, const float** out);
 /* Auralizer::input_gain / set_input_gain (auralizer.hpp:51-52) */
 int aura_b200_set_input_gain(aura_b200_engine* e, float gain);
 float aura_b200_input_gain(const aura_b200_engine* e);
@@ -150,17 +155,38 @@ int aura_b200_mode(const aura_b200_engine* e);
  * floats, copied back from the device. */
 int aura_b200_filter_spectrum(aura_b200_engine* e, size_t row, size_t k,
                               float* out);
+/* FrequencyDelayLine::slot(channel, age) (engine.hpp:261-266) of the input
+ * FDL (which = 0) or the canceller FDL (which = 1): the spectrum pushed
+ * `age` blocks ago, (N+1) complex in the reference layout. */
+int aura_b200_fdl_slot(aura_b200_engine* e, int which, size_t channel,
+                       size_t age, float* out);
 /* Current canceller spectra W[p][l][k][j], P x L x K_f x (N+1) complex. */
 int aura_b200_afc_coeffs(aura_b200_engine* e, float* out);
 
+/* Wait until every processed block has fully finished, including the
+ * background work (next-block precompute, canceller update, f^). process()
+ * returns as soon as the block's OUTPUT is ready. */
+int aura_b200_synchronize(aura_b200_engine* e);
+
 /* ---- measurement (bench.py; not part of the reference API) ----------- */
-/* Run `blocks` blocks with device-resident I/O (inputs already in HBM,
- * uploaded from host_in: blocks x inputs x N floats, cycling if NULL
- * random), one CUDA-graph launch each, timed with CUDA events on the
- * engine stream. block_us[i] = device time of block i. */
+/* Run `blocks` blocks back to back with device-resident I/O (inputs already
+ * in HBM, uploaded from host_in: n_in_blocks x inputs x N floats, cycled),
+ * front and background graphs per block, timed with CUDA events on the
+ * engine stream. latency_us[i] (may be NULL) = device time from block start
+ * to its output written; block_us[i] = device time of ALL of block i's work
+ * (front + background). */
 int aura_b200_time_device_blocks(aura_b200_engine* e, const float* host_in,
                                  size_t n_in_blocks, size_t blocks,
-                                 float* block_us);
+                                 float* latency_us, float* block_us);
+/* End-to-end latency through aura_b200_process() itself: `blocks` calls
+ * with HOST input (cycling over host_in: n_in_blocks x inputs x N) and host
+ * output, each timed with steady_clock from call to return (host->device
+ * input transfer, all kernels, device->host output, completion wait).
+ * pace_us > 0 spaces the calls on a real-time grid (one block every
+ * pace_us, as an audio callback would) instead of back to back. */
+int aura_b200_time_host_blocks(aura_b200_engine* e, const float* host_in,
+                               size_t n_in_blocks, size_t blocks,
+                               double pace_us, float* block_us);
 /* Same blocks launched kernel by kernel with an event pair around each
  * phase; phase_us[p] = mean device time of phase p over `blocks`, names
  * via aura_b200_phase_name. Returns the phase count in *n_phases. */

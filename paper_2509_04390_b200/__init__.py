@@ -187,7 +187,9 @@ def lib():
     L.aura_b200_mode.argtypes = [vp]
     L.aura_b200_filter_spectrum.argtypes = [vp, sz, sz, _f32p]
     L.aura_b200_afc_coeffs.argtypes = [vp, _f32p]
-    L.aura_b200_time_device_blocks.argtypes = [vp, C.c_void_p, sz, sz, _f32p]
+    L.aura_b200_time_device_blocks.argtypes = [vp, C.c_void_p, sz, sz, _f32p, _f32p]
+    L.aura_b200_synchronize.argtypes = [vp]
+    L.aura_b200_time_host_blocks.argtypes = [vp, _f32p, sz, sz, C.c_double, _f32p]
     L.aura_b200_profile_phases.argtypes = [vp, sz, _f32p, C.POINTER(C.c_int)]
     L.aura_b200_phase_name.argtypes = [vp, C.c_int]
     L.aura_b200_phase_name.restype = C.c_char_p
@@ -308,15 +310,32 @@ class _Engine:
         return buf.value.decode()
 
     # ---- measurement hooks used by bench.py
+    def synchronize(self):
+        """Wait for every processed block's background work (next-block
+        precompute, canceller update)."""
+        _check(lib().aura_b200_synchronize(self._h))
+
     def time_device_blocks(self, blocks: int, inputs: Optional[np.ndarray] = None):
+        """Back-to-back device-resident blocks timed with CUDA events.
+        Returns (latency_us, block_us): block start -> output written, and
+        all of the block's work (front + background)."""
+        lat = np.zeros(blocks, np.float32)
         out = np.zeros(blocks, np.float32)
         if inputs is not None:
             inputs = np.ascontiguousarray(inputs, np.float32)
             n_in = inputs.shape[0]
             _check(lib().aura_b200_time_device_blocks(self._h, inputs.ctypes.data, n_in,
-                                                      blocks, out))
+                                                      blocks, lat, out))
         else:
-            _check(lib().aura_b200_time_device_blocks(self._h, None, 0, blocks, out))
+            _check(lib().aura_b200_time_device_blocks(self._h, None, 0, blocks, lat, out))
+        return lat, out
+
+    def time_host_blocks(self, inputs: np.ndarray, blocks: int, pace_us: float = 0.0):
+        """Per-call latency of process() with host buffers (C-side timing)."""
+        inputs = np.ascontiguousarray(inputs, np.float32)
+        out = np.zeros(blocks, np.float32)
+        _check(lib().aura_b200_time_host_blocks(self._h, inputs, inputs.shape[0], blocks,
+                                                pace_us, out))
         return out
 
     def profile_phases(self, blocks: int):
@@ -387,10 +406,16 @@ class Convolver(_Engine):
 @dataclass
 class AfcParams:
     """Feedback-canceller adaptation; mu = 0 is the
-    reference's fixed canceller."""
+    reference's fixed canceller. delta None -> 1e-2 * (2N)."""
     mu: float = 0.0
     lam: float = 0.9
     delta: Optional[float] = None
+
+
+def default_delta(block_size: int) -> float:
+    """NLMS regulariser default: -20 dB of the per-bin
+    power of one unit-variance loudspeaker signal."""
+    return 1e-2 * 2 * block_size
 
 
 class Auralizer(_Engine):
@@ -416,7 +441,7 @@ class Auralizer(_Engine):
                 _raise(ErrorCode.filter_length_mismatch, "all filters must share one length")
         device = backend.device if backend is not None else 0
         a = afc or AfcParams()
-        delta = a.delta if a.delta is not None else 1e-6 * cfg.block_size
+        delta = a.delta if a.delta is not None else default_delta(cfg.block_size)
         pa = _Afc(a.mu, a.lam, delta)
         h = C.c_void_p()
         _check(lib().aura_b200_auralizer_create(

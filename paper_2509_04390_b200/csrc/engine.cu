@@ -90,6 +90,9 @@ void validate(const aura_b200_config* c, bool mimo) {
 }
 
 constexpr int kSMs = 148;
+// NLMS regulariser default: 1e-2 x (2N), i.e. -20 dB of the per-bin power of
+// one unit-variance loudspeaker signal.
+constexpr float kDefaultDeltaPerBin = 1e-2f;
 
 template <class T>
 T* dalloc(size_t count, std::vector<void*>& owned) {
@@ -102,9 +105,9 @@ T* dalloc(size_t count, std::vector<void*>& owned) {
 
 }  // namespace
 
-enum Phase { PH_INPUT = 0, PH_MAC_SYN, PH_TAIL_SYN, PH_MAC_AFC, PH_TAIL_AFC, PH_COUNT };
-static const char* kPhaseNames[PH_COUNT] = {"k_input", "k_mac_synth", "k_tail_synth",
-                                            "k_mac_afc", "k_tail_afc"};
+enum Phase { PH_FRONT = 0, PH_MAC_PRE, PH_TAIL_PRE, PH_MAC_AFC, PH_TAIL_AFC, PH_COUNT };
+static const char* kPhaseNames[PH_COUNT] = {"k_front", "k_mac_pre", "k_tail_pre", "k_mac_afc",
+                                            "k_tail_afc"};
 
 struct aura_b200_engine {
   int device = 0;
@@ -114,56 +117,67 @@ struct aura_b200_engine {
   int Qx = 1;  // FDL channels
   int LT = 1, PT = 1;
   uint64_t blocks = 0;
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr;  // the engine's stream (front + background)
+  cudaStream_t side = nullptr;    // second branch used while capturing
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::vector<void*> dmem;
   float4* W0 = nullptr;  // initial canceller spectra (reset of NLMS)
   size_t w_elems = 0;
-  float* h_in = nullptr;   // mapped pinned
-  float* h_out = nullptr;  // mapped pinned
-  uint32_t* h_done = nullptr;
+  float* h_in = nullptr;    // mapped pinned
+  float* h_out = nullptr;   // mapped pinned
+  uint32_t* h_done = nullptr;  // [0] output ready, [16] background done
+  float* h_fhat = nullptr;  // mapped pinned copy of f^
   float* d_in_pool = nullptr;
   size_t pool_blocks = 0;
   float* d_out = nullptr;
   BlockArgs args{};
   BlockArgs dev_args{};
-  cudaGraphExec_t g_host = nullptr, g_dev = nullptr;
-  size_t smem_input = 0, smem_tail = 0;
+  cudaGraphExec_t g_front = nullptr, g_back = nullptr;
+  size_t smem_front = 0, smem_tail = 0;
 
   ~aura_b200_engine() {
     cudaSetDevice(device);
     if (stream) cudaStreamSynchronize(stream);
-    if (g_host) cudaGraphExecDestroy(g_host);
-    if (g_dev) cudaGraphExecDestroy(g_dev);
+    if (g_front) cudaGraphExecDestroy(g_front);
+    if (g_back) cudaGraphExecDestroy(g_back);
     for (void* p : dmem) cudaFree(p);
     if (h_in) cudaFreeHost(h_in);
     if (h_out) cudaFreeHost(h_out);
     if (h_done) cudaFreeHost(h_done);
+    if (h_fhat) cudaFreeHost(h_fhat);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (side) cudaStreamDestroy(side);
     if (stream) cudaStreamDestroy(stream);
   }
 
+  bool has_pre() const { return K > 1; }
+
   void launch_phase(int ph, const BlockArgs& a, cudaStream_t s) {
     switch (ph) {
-      case PH_INPUT: {
-        const int grid = Qx + (a.nlms ? (int)P : 0);
-        k_input<<<grid, 256, smem_input, s>>>(a);
+      case PH_FRONT: {
+        const int grid = (int)((L + a.cpb - 1) / a.cpb);
+        k_front<<<grid, kFrontThreads, smem_front, s>>>(a);
         break;
       }
-      case PH_MAC_SYN: {
+      case PH_MAC_PRE: {
+        if (!has_pre()) break;
         dim3 grid(a.syn_chunks, (unsigned)(L / LT), a.syn_tiles);
         const bool el = mode == AURA_B200_ELEMENTWISE;
-#define MAC_CASE(lt)                                                         \
-  case lt:                                                                   \
-    if (el) k_mac_synth<lt, true><<<grid, kMacThreads, 0, s>>>(a);           \
-    else k_mac_synth<lt, false><<<grid, kMacThreads, 0, s>>>(a);             \
+#define MAC_CASE(lt)                                                     \
+  case lt:                                                               \
+    if (el) k_mac_pre<lt, true><<<grid, kMacThreads, 0, s>>>(a);         \
+    else k_mac_pre<lt, false><<<grid, kMacThreads, 0, s>>>(a);           \
     break;
         switch (LT) { MAC_CASE(1) MAC_CASE(2) MAC_CASE(4) MAC_CASE(8) }
 #undef MAC_CASE
         break;
       }
-      case PH_TAIL_SYN:
-        k_tail_synth<<<(unsigned)L, kTailThreads, smem_tail, s>>>(a);
+      case PH_TAIL_PRE:
+        if (has_pre()) k_tail_pre<<<(unsigned)L, kTailThreads, smem_tail, s>>>(a);
         break;
       case PH_MAC_AFC: {
+        if (!aur) break;
         dim3 grid(a.afc_chunks, 1, a.afc_tiles);
         switch (PT) {
           case 1: k_mac_afc<1><<<grid, kMacThreads, 0, s>>>(a); break;
@@ -174,39 +188,74 @@ struct aura_b200_engine {
         break;
       }
       case PH_TAIL_AFC:
-        k_tail_afc<<<(unsigned)P, kTailThreads, smem_tail, s>>>(a);
+        if (aur) k_tail_afc<<<(unsigned)P, kTailThreads, smem_tail, s>>>(a);
         break;
     }
   }
 
-  int n_phases() const { return aur ? PH_COUNT : PH_TAIL_SYN + 1; }
+  // kernels launched per block (front + background)
+  int launches_per_block() const { return 1 + (has_pre() ? 2 : 0) + (aur ? 2 : 0); }
 
-  void launch_block(const BlockArgs& a, cudaStream_t s) {
-    for (int ph = 0; ph < n_phases(); ++ph) launch_phase(ph, a, s);
-  }
-
-  cudaGraphExec_t capture(const BlockArgs& a) {
-    cudaGraph_t g;
-    CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
-    launch_block(a, stream);
-    CK(cudaStreamEndCapture(stream, &g));
+  cudaGraphExec_t instantiate(cudaGraph_t g) {
     cudaGraphExec_t ex;
     CK(cudaGraphInstantiate(&ex, g, 0));
     cudaGraphDestroy(g);
     return ex;
   }
 
+  cudaGraphExec_t capture_front(const BlockArgs& a) {
+    cudaGraph_t g;
+    CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+    launch_phase(PH_FRONT, a, stream);
+    CK(cudaStreamEndCapture(stream, &g));
+    return instantiate(g);
+  }
+
+  // background: the synthesis precompute and the canceller as two
+  // concurrent branches of one graph
+  cudaGraphExec_t capture_back(const BlockArgs& a) {
+    cudaGraph_t g;
+    CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+    const bool fork = has_pre() && aur;
+    if (fork) {
+      CK(cudaEventRecord(ev_fork, stream));
+      CK(cudaStreamWaitEvent(side, ev_fork, 0));
+      launch_phase(PH_MAC_AFC, a, side);
+      launch_phase(PH_TAIL_AFC, a, side);
+      CK(cudaEventRecord(ev_join, side));
+    } else {
+      launch_phase(PH_MAC_AFC, a, stream);
+      launch_phase(PH_TAIL_AFC, a, stream);
+    }
+    launch_phase(PH_MAC_PRE, a, stream);
+    launch_phase(PH_TAIL_PRE, a, stream);
+    if (fork) CK(cudaStreamWaitEvent(stream, ev_join, 0));
+    CK(cudaStreamEndCapture(stream, &g));
+    return instantiate(g);
+  }
+
+  void rebuild_graphs() {
+    if (g_front) cudaGraphExecDestroy(g_front);
+    if (g_back) cudaGraphExecDestroy(g_back);
+    g_front = g_back = nullptr;
+    g_front = capture_front(args);
+    if (has_pre() || aur) g_back = capture_back(args);
+  }
+
   double phase_bytes(int ph) const {
     const double row = 8.0 * (double)N;  // one packed partition
-    const double T = mode == AURA_B200_MIMO ? (double)(Q * K) : (double)K;
+    const double Qh = mode == AURA_B200_MIMO ? (double)Q : 1.0;
     switch (ph) {
-      case PH_INPUT: return 4.0 * N * Qx + row * Qx;
-      case PH_MAC_SYN: return row * ((double)L * T + (double)Qx * K);
-      case PH_TAIL_SYN:
-        return row * (double)args.syn_chunks * L + 4.0 * N * L + (aur ? row * L : 0.0);
+      case PH_FRONT:  // inputs, X push, H[.][.][0], S, outputs (+ canceller stage 1)
+        return 4.0 * N * Qx + row * Qx + row * (double)L * Qh + row * L + 4.0 * N * L +
+               (aur ? row * L + 4.0 * N * L : 0.0);
+      case PH_MAC_PRE:
+        return has_pre() ? row * ((double)L * Qh * (K - 1) + (double)Qx * (K - 1)) : 0.0;
+      case PH_TAIL_PRE: return has_pre() ? row * (double)args.syn_chunks * L + row * L : 0.0;
       case PH_MAC_AFC:
-        return row * ((double)P * L * KF * (1.0 + (args.nlms ? 1.0 : 0.0)) + (double)L * KF);
-      case PH_TAIL_AFC: return row * (double)args.afc_chunks * P + 4.0 * N * P;
+        return aur ? row * ((double)P * L * KF * (1.0 + (args.nlms ? 1.0 : 0.0)) + (double)L * KF)
+                   : 0.0;
+      case PH_TAIL_AFC: return aur ? row * (double)args.afc_chunks * P + 4.0 * N * P : 0.0;
     }
     return 0.0;
   }
@@ -215,18 +264,18 @@ struct aura_b200_engine {
 namespace {
 
 void setup_tables(aura_b200_engine* e, BlockArgs& a) {
-  const size_t N = e->N;
-  std::vector<float2> tw(N / 2), split(N);
-  for (size_t j = 0; j < N / 2; ++j) {
-    const double ang = -2.0 * M_PI * (double)j / (double)N;
-    tw[j] = make_float2((float)std::cos(ang), (float)std::sin(ang));
-  }
-  for (size_t k = 0; k < N; ++k) {
-    const double ang = -M_PI * (double)k / (double)N;
-    split[k] = make_float2((float)std::cos(ang), (float)std::sin(ang));
-  }
-  float2* dtw = dalloc<float2>(N / 2, e->dmem);
-  float2* dsp = dalloc<float2>(N, e->dmem);
+  // DftPlan ctor (dft.hpp:36-52), bit for bit: angle step computed once in
+  // double, multiplied by the index, cos/sin in double, rounded to float.
+  const size_t N = e->N;  // = half of n_f
+  std::vector<float2> tw(N / 2), split(N / 2 + 1);
+  const double step = -2.0 * M_PI / (double)N;
+  for (size_t j = 0; j < N / 2; ++j)
+    tw[j] = make_float2((float)std::cos(step * (double)j), (float)std::sin(step * (double)j));
+  const double sstep = -2.0 * M_PI / (double)(2 * N);
+  for (size_t j = 0; j <= N / 2; ++j)
+    split[j] = make_float2((float)std::cos(sstep * (double)j), (float)std::sin(sstep * (double)j));
+  float2* dtw = dalloc<float2>(tw.size(), e->dmem);
+  float2* dsp = dalloc<float2>(split.size(), e->dmem);
   CK(cudaMemcpy(dtw, tw.data(), sizeof(float2) * tw.size(), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(dsp, split.data(), sizeof(float2) * split.size(), cudaMemcpyHostToDevice));
   a.tw = dtw;
@@ -277,7 +326,7 @@ void plan_split(aura_b200_engine* e, BlockArgs& a) {
   a.syn_nft = std::min(NF, kMacThreads);
   a.syn_tiles = NF / a.syn_nft;
   const int KP = kMacThreads / a.syn_nft;
-  const long T = e->mode == AURA_B200_MIMO ? (long)(e->Q * e->K) : (long)e->K;
+  const long T = std::max(1L, (e->mode == AURA_B200_MIMO ? (long)e->Q : 1L) * (long)(e->K - 1));
   const long per_chunk = (long)(e->L / e->LT) * a.syn_tiles;
   const long target = (long)kSMs * 4;
   long chunks = (target + per_chunk - 1) / per_chunk;
@@ -313,21 +362,31 @@ void common_init(aura_b200_engine* e, int device) {
   e->device = device;
   CK(cudaSetDevice(device));
   CK(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&e->ev_join, cudaEventDisableTiming));
 }
 
 void finish_init(aura_b200_engine* e) {
   BlockArgs& a = e->args;
-  const size_t N = e->N;
+  const size_t N = e->N, NF = N / 2;
   // state + I/O
   a.st = dalloc<DevState>(1, e->dmem);
   CK(cudaMemset(a.st, 0, sizeof(DevState)));
+  a.S = dalloc<float4>(e->L * NF, e->dmem);
+  CK(cudaMemset(a.S, 0, sizeof(float4) * e->L * NF));
   const size_t in_ch = (size_t)e->Qx;
   CK(cudaHostAlloc(&e->h_in, in_ch * N * sizeof(float), cudaHostAllocMapped | cudaHostAllocPortable));
   CK(cudaHostAlloc(&e->h_out, e->L * N * sizeof(float), cudaHostAllocMapped | cudaHostAllocPortable));
-  CK(cudaHostAlloc(&e->h_done, 64, cudaHostAllocMapped | cudaHostAllocPortable));
+  CK(cudaHostAlloc(&e->h_done, 128, cudaHostAllocMapped | cudaHostAllocPortable));
   std::memset(e->h_in, 0, in_ch * N * sizeof(float));
   std::memset(e->h_out, 0, e->L * N * sizeof(float));
-  std::memset(e->h_done, 0, 64);
+  std::memset(e->h_done, 0, 128);
+  if (e->aur) {
+    CK(cudaHostAlloc(&e->h_fhat, e->P * N * sizeof(float), cudaHostAllocMapped | cudaHostAllocPortable));
+    std::memset(e->h_fhat, 0, e->P * N * sizeof(float));
+    CK(cudaHostGetDevicePointer((void**)&a.fhat_host, e->h_fhat, 0));
+  }
   float* din;
   float* dout;
   uint32_t* ddone;
@@ -337,22 +396,27 @@ void finish_init(aura_b200_engine* e) {
   a.in = din;
   a.out = dout;
   a.done = ddone;
-  // dynamic shared memory
-  e->smem_input = 16 * N;
+  a.back_done = ddone + 16;  // separate 64-byte line
+  a.back_total = (e->has_pre() ? (int)e->L : 0) + (e->aur ? (int)e->P : 0);
+  // front: one CTA per cpb output channels
+  a.cpb = (int)std::max<size_t>(1, (e->L + kSMs - 1) / kSMs);
+  const size_t Qs = e->mode == AURA_B200_ELEMENTWISE ? 1 : e->Q;
+  e->smem_front = 8 * N * (Qs + 2) + 4 * N * Qs;
+  if (e->smem_front > 227 * 1024)
+    fail(AURA_B200_E_INVALID_ARGUMENT, "block size too large for this many inputs (shared memory)");
   e->smem_tail = sizeof(float4) * kTailThreads + 24 * N;
-  CK(cudaFuncSetAttribute(k_input, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem_input));
-  CK(cudaFuncSetAttribute(k_tail_synth, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem_tail));
+  CK(cudaFuncSetAttribute(k_front, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem_front));
+  CK(cudaFuncSetAttribute(k_tail_pre, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem_tail));
   CK(cudaFuncSetAttribute(k_tail_afc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem_tail));
   // device-resident I/O variant for measurement
   e->pool_blocks = 64;
   e->d_in_pool = dalloc<float>(e->pool_blocks * in_ch * N, e->dmem);
   CK(cudaMemset(e->d_in_pool, 0, e->pool_blocks * in_ch * N * sizeof(float)));
   e->d_out = dalloc<float>(e->L * N, e->dmem);
-  e->g_host = e->capture(a);
+  e->rebuild_graphs();
   e->dev_args = a;
   e->dev_args.out = e->d_out;
   e->dev_args.in = e->d_in_pool;
-  e->g_dev = nullptr;  // built lazily (pool indexing needs the per-block pointer)
   CK(cudaStreamSynchronize(e->stream));
 }
 
@@ -364,17 +428,20 @@ void reset_state(aura_b200_engine* e) {
   CK(cudaMemsetAsync(a.st, 0, sizeof(DevState), s));
   CK(cudaMemsetAsync(a.prev_in, 0, sizeof(float) * e->Qx * N, s));
   CK(cudaMemsetAsync(a.X, 0, sizeof(float4) * (size_t)e->Qx * e->K * NF, s));
+  CK(cudaMemsetAsync(a.S, 0, sizeof(float4) * e->L * NF, s));
   if (e->aur) {
     CK(cudaMemsetAsync(a.prev_spk, 0, sizeof(float) * e->L * N, s));
     CK(cudaMemsetAsync(a.XA, 0, sizeof(float4) * e->L * (e->KF + 1) * NF, s));
     CK(cudaMemsetAsync(a.fhat, 0, sizeof(float) * e->P * N, s));
+    std::memset(e->h_fhat, 0, sizeof(float) * e->P * N);
     CK(cudaMemsetAsync(a.pw, 0, sizeof(float2) * N, s));
     CK(cudaMemsetAsync(a.pw_part, 0, sizeof(float2) * e->L * N, s));
     if (a.nlms)
       CK(cudaMemcpyAsync(a.W, e->W0, sizeof(float4) * e->w_elems, cudaMemcpyDeviceToDevice, s));
   }
   CK(cudaStreamSynchronize(s));
-  *e->h_done = 0;
+  e->h_done[0] = 0;
+  e->h_done[16] = 0;
   e->blocks = 0;
 }
 
@@ -414,6 +481,18 @@ void check_rows(const float* const* rows, size_t n_rows) {
 }
 
 }  // namespace
+
+static void unpack_row(const float2* packed, size_t N, float* out) {
+  // packed bin 0 = (DC, Nyquist) -> reference bins 0 and N, imag exactly 0
+  out[0] = packed[0].x;
+  out[1] = 0.0f;
+  for (size_t j = 1; j < N; ++j) {
+    out[2 * j] = packed[j].x;
+    out[2 * j + 1] = packed[j].y;
+  }
+  out[2 * N] = packed[0].y;
+  out[2 * N + 1] = 0.0f;
+}
 
 // ====================================================================== ABI
 
@@ -543,7 +622,7 @@ int aura_b200_auralizer_create(const aura_b200_config* cfg,
     a.gain = input_gain;
     a.mu = mu;
     a.lambda = afc ? afc->lambda : 0.9f;
-    a.delta = afc ? afc->delta : 1e-6f * (float)N;
+    a.delta = afc ? afc->delta : kDefaultDeltaPerBin * (float)(2 * N);
     a.nlms = mu > 0.0f;
     e->w_elems = Q * L * e->KF * NF;
     a.W = dalloc<float4>(e->w_elems, e->dmem);
@@ -556,6 +635,7 @@ int aura_b200_auralizer_create(const aura_b200_config* cfg,
     }
     a.XA = dalloc<float4>(L * (e->KF + 1) * NF, e->dmem);
     a.prev_spk = dalloc<float>(L * N, e->dmem);
+    a.spk = dalloc<float>(L * N, e->dmem);
     a.fhat = dalloc<float>(Q * N, e->dmem);
     a.pw = dalloc<float2>(N, e->dmem);
     a.pw_part = dalloc<float2>(L * N, e->dmem);
@@ -576,6 +656,32 @@ int aura_b200_auralizer_create(const aura_b200_config* cfg,
 
 void aura_b200_destroy(aura_b200_engine* e) { delete e; }
 
+namespace {
+// Spin on a mapped word the GPU publishes; poll the stream for errors.
+void wait_word(aura_b200_engine* e, volatile uint32_t* word, uint32_t expect, const char* what) {
+  uint64_t spins = 0;
+  const auto t0 = std::chrono::steady_clock::now();
+  while (*word != expect) {
+#if defined(__x86_64__)
+    _mm_pause();
+#endif
+    if ((++spins & 0xFFFF) == 0) {
+      const cudaError_t q = cudaStreamQuery(e->stream);
+      if (q != cudaSuccess && q != cudaErrorNotReady) ck(q, what);
+      if (q == cudaSuccess && *word != expect)
+        fail(AURA_B200_E_CUDA, std::string(what) + ": stream idle without publishing");
+      if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(20))
+        fail(AURA_B200_E_TIMEOUT, std::string(what) + ": not complete within 20 s");
+    }
+  }
+  std::atomic_thread_fence(std::memory_order_acquire);
+}
+}  // namespace
+
+// One block: launch FRONT then BACK; return as soon as the front's last CTA
+// has published the output. The background keeps running; the next call's
+// front is stream-ordered after it, and feedback_estimate()/synchronize()
+// wait for it explicitly.
 int aura_b200_process(aura_b200_engine* e, const float* in, float* out) {
   return guarded([&] {
     if (!e || !in || !out) fail(AURA_B200_E_INVALID_ARGUMENT, "null argument");
@@ -583,29 +689,24 @@ int aura_b200_process(aura_b200_engine* e, const float* in, float* out) {
     for (size_t i = 0; i < n_in; ++i)
       if (!std::isfinite(in[i])) fail(AURA_B200_E_NON_FINITE_INPUT, "input contains NaN or Inf");
     CK(cudaSetDevice(e->device));
+    // the previous block's front has finished reading h_in (its output word
+    // was observed), so the staging buffer can be refilled
     std::memcpy(e->h_in, in, n_in * sizeof(float));
     const uint32_t expect = (uint32_t)(e->blocks + 1);
     std::atomic_thread_fence(std::memory_order_release);
-    CK(cudaGraphLaunch(e->g_host, e->stream));
-    volatile uint32_t* done = e->h_done;
-    uint64_t spins = 0;
-    auto t0 = std::chrono::steady_clock::now();
-    while (*done != expect) {
-#if defined(__x86_64__)
-      _mm_pause();
-#endif
-      if ((++spins & 0xFFFF) == 0) {
-        const cudaError_t q = cudaStreamQuery(e->stream);
-        if (q != cudaSuccess && q != cudaErrorNotReady) ck(q, "block execution");
-        if (q == cudaSuccess && *done != expect)
-          fail(AURA_B200_E_CUDA, "block finished without publishing its output");
-        if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(20))
-          fail(AURA_B200_E_TIMEOUT, "block did not complete within 20 s");
-      }
-    }
-    std::atomic_thread_fence(std::memory_order_acquire);
+    CK(cudaGraphLaunch(e->g_front, e->stream));
+    if (e->g_back) CK(cudaGraphLaunch(e->g_back, e->stream));
+    wait_word(e, e->h_done, expect, "block output");
     std::memcpy(out, e->h_out, e->L * e->N * sizeof(float));
     ++e->blocks;
+  });
+}
+
+int aura_b200_synchronize(aura_b200_engine* e) {
+  return guarded([&] {
+    CK(cudaSetDevice(e->device));
+    if (e->blocks) wait_word(e, e->h_done + 16, (uint32_t)e->blocks, "block background");
+    CK(cudaStreamSynchronize(e->stream));
   });
 }
 
@@ -620,8 +721,47 @@ int aura_b200_feedback_estimate(aura_b200_engine* e, float* out) {
   return guarded([&] {
     if (!e->aur) fail(AURA_B200_E_INVALID_ARGUMENT, "not an auralizer");
     CK(cudaSetDevice(e->device));
+    if (e->blocks) wait_word(e, e->h_done + 16, (uint32_t)e->blocks, "block background");
+    std::memcpy(out, e->h_fhat, sizeof(float) * e->P * e->N);
+  });
+}
+
+int aura_b200_feedback_estimate_view(aura_b200_engine* e, const float** out) {
+  return guarded([&] {
+    if (!e->aur) fail(AURA_B200_E_INVALID_ARGUMENT, "not an auralizer");
+    *out = e->h_fhat;
+  });
+}
+
+int aura_b200_fdl_slot(aura_b200_engine* e, int which, size_t channel, size_t age,
+                       float* out) {
+  return guarded([&] {
+    CK(cudaSetDevice(e->device));
     CK(cudaStreamSynchronize(e->stream));
-    CK(cudaMemcpy(out, e->args.fhat, sizeof(float) * e->P * e->N, cudaMemcpyDeviceToHost));
+    const size_t NF = e->N / 2;
+    size_t cap, chans;
+    const float4* base;
+    if (which == 0) {
+      cap = e->K;
+      chans = (size_t)e->Qx;
+      base = e->args.X;
+    } else {
+      if (!e->aur) fail(AURA_B200_E_INVALID_ARGUMENT, "not an auralizer");
+      cap = e->KF + 1;
+      chans = e->L;
+      base = e->args.XA;
+    }
+    if (channel >= chans || age >= (which == 0 ? e->K : e->KF))
+      fail(AURA_B200_E_INVALID_ARGUMENT, "delay-line index out of range");
+    // block b's spectrum lives at slot b % cap; age a is block (blocks-1-a)
+    const long long blk = (long long)e->blocks - 1 - (long long)age;
+    std::vector<float2> buf(e->N, make_float2(0.f, 0.f));
+    if (blk >= 0) {
+      const size_t slot = (size_t)(blk % (long long)cap);
+      CK(cudaMemcpy(buf.data(), base + (channel * cap + slot) * NF, sizeof(float2) * e->N,
+                    cudaMemcpyDeviceToHost));
+    }
+    unpack_row(buf.data(), e->N, out);
   });
 }
 
@@ -631,14 +771,8 @@ int aura_b200_set_input_gain(aura_b200_engine* e, float gain) {
     CK(cudaSetDevice(e->device));
     CK(cudaStreamSynchronize(e->stream));
     e->args.gain = gain;
-    cudaGraphExecDestroy(e->g_host);
-    e->g_host = nullptr;
-    e->g_host = e->capture(e->args);
-    if (e->g_dev) {
-      cudaGraphExecDestroy(e->g_dev);
-      e->g_dev = nullptr;
-    }
     e->dev_args.gain = gain;
+    e->rebuild_graphs();
   });
 }
 
@@ -649,17 +783,6 @@ size_t aura_b200_fc_partition_count(const aura_b200_engine* e) { return e->aur ?
 size_t aura_b200_filter_length(const aura_b200_engine* e) { return e->n_h; }
 int aura_b200_mode(const aura_b200_engine* e) { return e->mode; }
 
-static void unpack_row(const float2* packed, size_t N, float* out) {
-  // packed bin 0 = (DC, Nyquist) -> reference bins 0 and N, imag exactly 0
-  out[0] = packed[0].x;
-  out[1] = 0.0f;
-  for (size_t j = 1; j < N; ++j) {
-    out[2 * j] = packed[j].x;
-    out[2 * j + 1] = packed[j].y;
-  }
-  out[2 * N] = packed[0].y;
-  out[2 * N + 1] = 0.0f;
-}
 
 int aura_b200_filter_spectrum(aura_b200_engine* e, size_t row, size_t k, float* out) {
   return guarded([&] {
@@ -692,47 +815,88 @@ int aura_b200_afc_coeffs(aura_b200_engine* e, float* out) {
 // ------------------------------------------------------------ measurement
 
 int aura_b200_time_device_blocks(aura_b200_engine* e, const float* host_in,
-                                 size_t n_in_blocks, size_t blocks, float* block_us) {
+                                 size_t n_in_blocks, size_t blocks, float* latency_us,
+                                 float* block_us) {
   return guarded([&] {
     CK(cudaSetDevice(e->device));
+    CK(cudaStreamSynchronize(e->stream));
     const size_t per = (size_t)e->Qx * e->N;
     if (host_in && n_in_blocks) {
       const size_t nb = std::min(n_in_blocks, e->pool_blocks);
       CK(cudaMemcpy(e->d_in_pool, host_in, nb * per * sizeof(float), cudaMemcpyHostToDevice));
     }
-    // one graph per pool slot: the input pointer is baked per slot
+    // one front graph per pool slot (the input pointer is baked per slot)
     std::vector<cudaGraphExec_t> gs;
     const size_t slots = std::max<size_t>(1, std::min(n_in_blocks, e->pool_blocks));
     for (size_t s = 0; s < slots; ++s) {
       BlockArgs a = e->dev_args;
       a.in = e->d_in_pool + s * per;
-      gs.push_back(e->capture(a));
+      gs.push_back(e->capture_front(a));
     }
-    std::vector<cudaEvent_t> ev(2 * blocks);
+    cudaGraphExec_t back = (e->has_pre() || e->aur) ? e->capture_back(e->dev_args) : nullptr;
+    std::vector<cudaEvent_t> ev(3 * blocks);
     for (auto& x : ev) CK(cudaEventCreate(&x));
     for (size_t b = 0; b < blocks; ++b) {
-      CK(cudaEventRecord(ev[2 * b], e->stream));
+      CK(cudaEventRecord(ev[3 * b], e->stream));
       CK(cudaGraphLaunch(gs[b % slots], e->stream));
-      CK(cudaEventRecord(ev[2 * b + 1], e->stream));
+      CK(cudaEventRecord(ev[3 * b + 1], e->stream));
+      if (back) CK(cudaGraphLaunch(back, e->stream));
+      CK(cudaEventRecord(ev[3 * b + 2], e->stream));
     }
     CK(cudaStreamSynchronize(e->stream));
     for (size_t b = 0; b < blocks; ++b) {
       float ms = 0.f;
-      CK(cudaEventElapsedTime(&ms, ev[2 * b], ev[2 * b + 1]));
+      if (latency_us) {
+        CK(cudaEventElapsedTime(&ms, ev[3 * b], ev[3 * b + 1]));
+        latency_us[b] = ms * 1000.0f;
+      }
+      CK(cudaEventElapsedTime(&ms, ev[3 * b], ev[3 * b + 2]));
       block_us[b] = ms * 1000.0f;
     }
     for (auto& x : ev) cudaEventDestroy(x);
     for (auto g : gs) cudaGraphExecDestroy(g);
+    if (back) cudaGraphExecDestroy(back);
     e->blocks += blocks;
-    *e->h_done = (uint32_t)e->blocks;
+    e->h_done[0] = (uint32_t)e->blocks;
+    e->h_done[16] = (uint32_t)e->blocks;
   });
+}
+
+int aura_b200_time_host_blocks(aura_b200_engine* e, const float* host_in,
+                               size_t n_in_blocks, size_t blocks, double pace_us,
+                               float* block_us) {
+  if (!e || !host_in || !n_in_blocks || !block_us) {
+    g_err = "null argument";
+    return AURA_B200_E_INVALID_ARGUMENT;
+  }
+  const size_t per = (size_t)e->Qx * e->N;
+  std::vector<float> out(e->L * e->N);
+  using clk = std::chrono::steady_clock;
+  auto next = clk::now();
+  for (size_t b = 0; b < blocks; ++b) {
+    if (pace_us > 0) {
+      while (clk::now() < next) {
+#if defined(__x86_64__)
+        _mm_pause();
+#endif
+      }
+      next += std::chrono::nanoseconds((long long)(pace_us * 1000.0));
+    }
+    const auto t0 = clk::now();
+    const int rc = aura_b200_process(e, host_in + (b % n_in_blocks) * per, out.data());
+    const auto t1 = clk::now();
+    if (rc) return rc;
+    block_us[b] = (float)std::chrono::duration<double, std::micro>(t1 - t0).count();
+  }
+  return AURA_B200_OK;
 }
 
 int aura_b200_profile_phases(aura_b200_engine* e, size_t blocks, float* phase_us,
                              int* n_phases) {
   return guarded([&] {
     CK(cudaSetDevice(e->device));
-    const int np = e->n_phases();
+    CK(cudaStreamSynchronize(e->stream));
+    const int np = PH_COUNT;
     std::vector<cudaEvent_t> ev((size_t)(np + 1) * blocks);
     for (auto& x : ev) CK(cudaEventCreate(&x));
     for (size_t b = 0; b < blocks; ++b) {
@@ -758,7 +922,8 @@ int aura_b200_profile_phases(aura_b200_engine* e, size_t blocks, float* phase_us
     for (auto& x : ev) cudaEventDestroy(x);
     *n_phases = np;
     e->blocks += blocks;
-    *e->h_done = (uint32_t)e->blocks;
+    e->h_done[0] = (uint32_t)e->blocks;
+    e->h_done[16] = (uint32_t)e->blocks;
   });
 }
 
@@ -772,12 +937,13 @@ int aura_b200_describe(const aura_b200_engine* e, char* buf, size_t cap) {
   return guarded([&] {
     const BlockArgs& a = e->args;
     std::snprintf(buf, cap,
-                  "N=%zu Q=%zu L=%zu P=%zu K=%zu KF=%zu mode=%d LT=%d PT=%d "
-                  "syn: chunks=%d tc=%d nft=%d tiles=%d grid=(%d,%zu,%d)x%d | "
-                  "afc: chunks=%d uc=%d nft=%d tiles=%d nlms=%d",
-                  e->N, e->Q, e->L, e->P, e->K, e->KF, e->mode, e->LT, e->PT, a.syn_chunks,
-                  a.syn_tc, a.syn_nft, a.syn_tiles, a.syn_chunks, e->L / e->LT, a.syn_tiles,
-                  kMacThreads, a.afc_chunks, a.afc_uc, a.afc_nft, a.afc_tiles, a.nlms);
+                  "N=%zu Q=%zu L=%zu P=%zu K=%zu KF=%zu mode=%d LT=%d PT=%d | front: grid=%zu "
+                  "cpb=%d smem=%zu | mac_pre: chunks=%d tc=%d nft=%d tiles=%d grid=(%d,%zu,%d)x%d "
+                  "| mac_afc: chunks=%d uc=%d nft=%d tiles=%d nlms=%d delta=%g",
+                  e->N, e->Q, e->L, e->P, e->K, e->KF, e->mode, e->LT, e->PT,
+                  (e->L + a.cpb - 1) / a.cpb, a.cpb, e->smem_front, a.syn_chunks, a.syn_tc,
+                  a.syn_nft, a.syn_tiles, a.syn_chunks, e->L / e->LT, a.syn_tiles, kMacThreads,
+                  a.afc_chunks, a.afc_uc, a.afc_nft, a.afc_tiles, a.nlms, (double)a.delta);
   });
 }
 

@@ -1,18 +1,28 @@
 // kernels.cuh -- the per-block UPOLS + feedback-canceller kernels (sm_100a).
 //
-// One block of audio = one CUDA-graph launch of these kernels, in order:
-//   k_input      m~ = g m - f^, window, r2c, FDL push; NLMS error spectra
-//   k_mac_synth  streaming FDL x filter-spectra MAC, split over partitions
-//   k_tail_synth fixed-order split-K reduce, c2r, overlap-save output,
-//                feedback-canceller r2c + FDL push, power partials
-//   k_mac_afc    feedback-canceller MAC with the fused NLMS update of W
-//   k_tail_afc   fixed-order reduce, one c2r per mic -> f^ for next block
-// (a Convolver launches only the first three.)
+// Block n runs as two CUDA graphs on one stream.
 //
-// Reference anchors: convolver.hpp:150-206 (stages 1-3), backend.hpp:212-235
-// (spectral_mac_channel), auralizer.hpp:61-87 (AFC pipeline), SURVEY.md
-// Appendix A/B (NLMS, MIMO). All reductions run in a fixed order, so
-// results are bit-reproducible run to run (test_convolver.cpp:172-193).
+//  FRONT (the latency-critical path, one kernel):
+//   k_front      m~ = g m - f^ (auralizer.hpp:73-76), window + r2c of every
+//                input (convolver.hpp:180-191), FDL push, then per output
+//                channel  Y_l = S_l + sum_q X_q,n (.) H_{l,q}[0],  c2r +
+//                overlap-save straight into the (mapped) output. The last CTA
+//                publishes the host-visible "output ready" word. After that
+//                point each CTA also does the canceller's stage 1 on its l_n
+//                (r2c, canceller-FDL push, power) and the NLMS error spectra.
+//
+//  BACK (off the critical path, two concurrent branches):
+//   k_mac_pre  -> k_tail_pre   S_l for block n+1 = sum_{j=0}^{K-2}
+//                              X(age j) (.) H_l[j+1]: every partition except
+//                              partition 0 depends only on inputs up to n.
+//   k_mac_afc  -> k_tail_afc   canceller MAC with the fused NLMS update,
+//                              one c2r per mic -> f^ for block n+1.
+//
+// So the output of block n is c2r(X_n H_0 + sum_{k>=1} X_{n-k} H_k), exactly
+// the reference's accumulator (backend.hpp:212-235) with the partition sum
+// split in two; the work per block is unchanged, only its position in time.
+// All reductions run in a fixed order: results are bit-reproducible run to
+// run (test_convolver.cpp:172-193).
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -22,47 +32,56 @@
 namespace aura_b200 {
 
 constexpr int kMacThreads = 256;
-constexpr int kTailThreads = 512;
+constexpr int kTailThreads = 256;
+constexpr int kFrontThreads = 256;
 
-// Device-resident stream state. `block` is the index of the block being
-// processed; it advances when the last CTA of the last kernel retires.
+// Device-resident stream state. `block` = index of the next block the FRONT
+// will process; the background of block n reads block - 1.
 struct DevState {
   uint32_t block;
-  uint32_t ticket;
+  uint32_t front_ticket;
+  uint32_t back_ticket;
+  uint32_t pad;
 };
 
 struct BlockArgs {
   // geometry
   int N, logN, NF;   // NF = N/2 float4 columns per packed spectrum
-  int Q, L, P;       // inputs, outputs (local), mics (auralizer: P = Q)
+  int Q, L, P;       // inputs, outputs, mics (auralizer: P = Q)
   int K, KF;         // synth partitions, canceller partitions
   int mode;          // 0 broadcast, 1 elementwise, 2 mimo
   int is_aur, nlms;
   float gain, mu, lambda, delta;
+  int cpb;           // output channels per front CTA
+  int back_total;    // CTAs of the background's final kernels
   // split-K geometry
   int syn_chunks, syn_tc, syn_nft, syn_tiles;
   int afc_chunks, afc_uc, afc_nft, afc_tiles;
   // tables
   const float2* tw;     // N/2, e^{-2 pi i j / N}
-  const float2* split;  // N,   e^{-i pi k / N}
+  const float2* split;  // N/2+1, e^{-2 pi i k / (2N)}
   // state
   DevState* st;
-  float* prev_in;       // Q x N (elementwise: L x N)  previous input block
-  float4* X;            // input FDL   [Qx][K][NF]
-  const float4* H;      // spectra     [L][Q][K][NF] (bcast/elem Q = 1)
+  float* prev_in;       // Qx x N    previous input block (after g m - f^)
+  float4* X;            // input FDL [Qx][K][NF]
+  const float4* H;      // spectra   [L][Qh][K][NF] (Qh = Q for mimo, else 1)
+  float4* S;            // [L][NF]   precomputed partitions >= 1 for next block
   float4* part_syn;     // [syn_chunks][L][NF]
-  float* prev_spk;      // L x N previous loudspeaker block
+  float* prev_spk;      // L x N     previous loudspeaker block
+  float* spk;           // L x N     l_n (device copy for the canceller stage)
   float4* XA;           // canceller FDL [L][KF+1][NF]
   float4* W;            // canceller spectra [P][L][KF][NF]
-  float2* pw_part;      // [L][N]   packed |X_l|^2 of the newest spectrum
-  float2* pw;           // [N]      smoothed power (packed: bin0 = DC,Nyq)
-  float4* E;            // [P][NF]  error spectra
+  float2* pw_part;      // [L][N]    packed |X_l|^2 of the newest spectrum
+  float2* pw;           // [N]       smoothed power (packed: bin0 = DC,Nyq)
+  float4* E;            // [P][NF]   error spectra
   float4* part_afc;     // [afc_chunks][P][NF]
-  float* fhat;          // P x N    feedback estimate for the next block
+  float* fhat;          // P x N     feedback estimate for the next block
+  float* fhat_host;     // P x N     same, mapped pinned host copy
   // I/O (device pointers; may alias pinned mapped host memory)
-  const float* in;      // inputs x N
+  const float* in;      // Qx x N
   float* out;           // L x N
-  volatile uint32_t* done;  // mapped host word: block sequence when done
+  volatile uint32_t* done;       // mapped: sequence of the last output ready
+  volatile uint32_t* back_done;  // mapped: sequence of the last finished block
 };
 
 // ---------------------------------------------------------------- helpers
@@ -80,7 +99,7 @@ __device__ __forceinline__ float4 ld_stream(const float4* p) {
 // x.y*h.y. xr0/xi0 are x.x/x.y with the cross terms zeroed on that lane.
 struct XPack {
   float4 v;
-  float xr0, xi0;  // cross-term operands for the first pair
+  float xr0, xi0;
 };
 __device__ __forceinline__ XPack xpack(float4 x, bool dc) {
   XPack p;
@@ -89,8 +108,7 @@ __device__ __forceinline__ XPack xpack(float4 x, bool dc) {
   p.xi0 = dc ? 0.0f : x.y;
   return p;
 }
-__device__ __forceinline__ void cmac(float4& acc, const XPack& x, float4 h,
-                                     bool dc) {
+__device__ __forceinline__ void cmac(float4& acc, const XPack& x, float4 h, bool dc) {
   const float hr0 = dc ? h.y : h.x;
   acc.x = fmaf(x.v.x, h.x, acc.x);
   acc.x = fmaf(-x.xi0, h.y, acc.x);
@@ -101,6 +119,15 @@ __device__ __forceinline__ void cmac(float4& acc, const XPack& x, float4 h,
   acc.w = fmaf(x.v.z, h.w, acc.w);
   acc.w = fmaf(x.v.w, h.z, acc.w);
 }
+// same on one packed complex bin j (float2 granularity)
+__device__ __forceinline__ float2 cmac2(float2 acc, float2 x, float2 h, bool dc) {
+  if (dc) return make_float2(fmaf(x.x, h.x, acc.x), fmaf(x.y, h.y, acc.y));
+  acc.x = fmaf(x.x, h.x, acc.x);
+  acc.x = fmaf(-x.y, h.y, acc.x);
+  acc.y = fmaf(x.x, h.y, acc.y);
+  acc.y = fmaf(x.y, h.x, acc.y);
+  return acc;
+}
 __device__ __forceinline__ float4 f4add(float4 a, float4 b) {
   return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
 }
@@ -110,102 +137,212 @@ __device__ __forceinline__ int ring(int v, int cap) {
   return v < 0 ? v + cap : v;
 }
 
-// Sum `nc` partial rows part[c*stride + col] for every column of an NF-wide
-// float4 row, in a fixed order, into out[col] (shared). Uses all threads.
-// red: blockDim float4 shared scratch.
-__device__ void reduce_partials(const float4* __restrict__ part, int nc,
-                                size_t stride, int NF, float4* red,
-                                float4* out) {
+// Sum nc partial rows part[c*stride + col] for every column of an NF-wide
+// float4 row into out[col] (shared), in a fixed association order
+// independent of timing. Thread row r takes chunks r, r+R, ... with four
+// independent accumulators so the L2 loads overlap.
+__device__ void reduce_partials(const float4* __restrict__ part, int nc, size_t stride,
+                                int NF, float4* red, float4* out) {
   const int T = blockDim.x;
-  if (NF >= T) {
-    for (int f = threadIdx.x; f < NF; f += T) {
-      float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (int c = 0; c < nc; ++c) s = f4add(s, part[(size_t)c * stride + f]);
-      out[f] = s;
+  const int W = min(NF, T);  // columns per pass
+  const int R = T / W;
+  const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int f0 = 0; f0 < NF; f0 += W) {
+    const int f = f0 + (threadIdx.x % W);
+    const int r = threadIdx.x / W;
+    float4 a0 = zero, a1 = zero, a2 = zero, a3 = zero;
+    int c = r;
+    for (; c + 3 * R < nc; c += 4 * R) {
+      const float4 v0 = part[(size_t)c * stride + f];
+      const float4 v1 = part[(size_t)(c + R) * stride + f];
+      const float4 v2 = part[(size_t)(c + 2 * R) * stride + f];
+      const float4 v3 = part[(size_t)(c + 3 * R) * stride + f];
+      a0 = f4add(a0, v0);
+      a1 = f4add(a1, v1);
+      a2 = f4add(a2, v2);
+      a3 = f4add(a3, v3);
+    }
+    for (; c < nc; c += R) a0 = f4add(a0, part[(size_t)c * stride + f]);
+    red[threadIdx.x] = f4add(f4add(a0, a1), f4add(a2, a3));
+    __syncthreads();
+    if (r == 0) {
+      float4 t = red[threadIdx.x];
+      for (int rr = 1; rr < R; ++rr) t = f4add(t, red[rr * W + threadIdx.x]);
+      out[f] = t;
     }
     __syncthreads();
-    return;
   }
-  const int R = T / NF;
-  const int f = threadIdx.x % NF;
-  const int r = threadIdx.x / NF;
-  float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int c = r; c < nc; c += R) s = f4add(s, part[(size_t)c * stride + f]);
-  red[threadIdx.x] = s;
-  __syncthreads();
-  if (r == 0) {
-    float4 t = red[f];
-    for (int rr = 1; rr < R; ++rr) t = f4add(t, red[rr * NF + f]);
-    out[f] = t;
-  }
-  __syncthreads();
 }
 
-// Retire one CTA of the last kernel of a block; the last one advances the
-// block counter and publishes the host-visible done word.
-__device__ void retire_block(const BlockArgs& a, uint32_t n) {
+// Background retirement: the last CTA of the background's final kernels
+// publishes the finished block sequence (f^ and S for block n+1 are ready).
+__device__ void retire_back(const BlockArgs& a, uint32_t n) {
+  __threadfence_system();
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence_system();
-    const uint32_t total = gridDim.x * gridDim.y * gridDim.z;
-    const uint32_t t = atomicAdd(&a.st->ticket, 1u);
-    if (t == total - 1) {
-      a.st->ticket = 0;
+    const uint32_t t = atomicAdd(&a.st->back_ticket, 1u);
+    if (t == (uint32_t)a.back_total - 1) {
+      a.st->back_ticket = 0;
+      __threadfence_system();
+      *a.back_done = n + 1;
+    }
+  }
+}
+
+// ------------------------------------------------------------- k_front
+// grid = ceil(L / cpb), 256 threads; elementwise CTAs also own their
+// channels' inputs. Shared: Qs input spectra (N float2 each), FFT scratch z
+// (N float2), window/accumulator (2N floats), m~ (Qs x N floats).
+__global__ void __launch_bounds__(kFrontThreads) k_front(BlockArgs a) {
+  extern __shared__ float4 smem4[];
+  const int N = a.N, NF = a.NF;
+  const bool elem = a.mode == 1;
+  const int Qs = elem ? 1 : a.Q;
+  float2* Xs = reinterpret_cast<float2*>(smem4);          // Qs x N
+  float2* z = Xs + (size_t)Qs * N;                        // N
+  float* wa = reinterpret_cast<float*>(z + N);            // 2N (window / acc)
+  float2* acc = reinterpret_cast<float2*>(wa);
+  float* mts = wa + 2 * N;                                // Qs x N
+  __shared__ uint32_t s_last;
+
+  const uint32_t n = a.st->block;
+  const int c0 = blockIdx.x * a.cpb;
+  const int c1 = min(c0 + a.cpb, a.L);
+  const int Qh = a.mode == 2 ? a.Q : 1;
+
+  // ---- stage 1 for the shared inputs (broadcast / mimo)
+  if (!elem) {
+    for (int q = 0; q < Qs; ++q) {
+      const float* in = a.in + (size_t)q * N;
+      const float* prev = a.prev_in + (size_t)q * N;
+      for (int i = threadIdx.x; i < N; i += blockDim.x) {
+        float v = in[i];
+        if (a.is_aur) v = __fsub_rn(__fmul_rn(a.gain, v), a.fhat[(size_t)q * N + i]);
+        mts[q * N + i] = v;
+        wa[i] = prev[i];
+        wa[N + i] = v;
+      }
+      __syncthreads();
+      rfft_packed(wa, z, Xs + (size_t)q * N, N, a.logN, a.tw, a.split);
+      if (blockIdx.x == 0) {
+        float2* dst = reinterpret_cast<float2*>(a.X + ((size_t)q * a.K + n % (uint32_t)a.K) * NF);
+        for (int j = threadIdx.x; j < N; j += blockDim.x) dst[j] = Xs[(size_t)q * N + j];
+      }
+    }
+  }
+
+  // ---- per output channel: Y = S + sum_q X_q H_q[0], c2r, overlap-save
+  for (int l = c0; l < c1; ++l) {
+    if (elem) {
+      const float* in = a.in + (size_t)l * N;
+      float* prev = a.prev_in + (size_t)l * N;
+      for (int i = threadIdx.x; i < N; i += blockDim.x) {
+        wa[i] = prev[i];
+        wa[N + i] = in[i];
+      }
+      __syncthreads();
+      for (int i = threadIdx.x; i < N; i += blockDim.x) prev[i] = wa[N + i];
+      rfft_packed(wa, z, Xs, N, a.logN, a.tw, a.split);
+      float2* dst = reinterpret_cast<float2*>(a.X + ((size_t)l * a.K + n % (uint32_t)a.K) * NF);
+      for (int j = threadIdx.x; j < N; j += blockDim.x) dst[j] = Xs[j];
+    }
+    const float2* Sl = reinterpret_cast<const float2*>(a.S + (size_t)l * NF);
+    for (int j = threadIdx.x; j < N; j += blockDim.x) {
+      float2 y = Sl[j];
+      for (int q = 0; q < Qs; ++q) {
+        const float2 h = reinterpret_cast<const float2*>(
+            a.H + (((size_t)l * Qh + q) * a.K) * NF)[j];
+        y = cmac2(y, Xs[(size_t)q * N + j], h, j == 0);
+      }
+      acc[j] = y;
+    }
+    __syncthreads();
+    float* out = a.out + (size_t)l * N;
+    float* sp = a.spk + (size_t)l * N;
+    const bool keep = a.is_aur;
+    irfft_packed_tail(acc, z, N, a.logN, a.tw, a.split, [&](int i, float v) {
+      out[i] = v;
+      if (keep) sp[i] = v;
+    });
+  }
+
+  // ---- publish: the last CTA raises "output ready" for block n
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t t = atomicAdd(&a.st->front_ticket, 1u);
+    s_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (s_last) {
+    // every CTA has read prev_in / st->block: safe to advance them
+    if (!elem)
+      for (int q = 0; q < Qs; ++q)
+        for (int i = threadIdx.x; i < N; i += blockDim.x)
+          a.prev_in[(size_t)q * N + i] = mts[q * N + i];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      a.st->front_ticket = 0;
       a.st->block = n + 1;
       __threadfence_system();
       *a.done = n + 1;
+      if (a.back_total == 0) *a.back_done = n + 1;
+    }
+  }
+  if (!a.is_aur) return;
+
+  // ---- canceller stage 1 on l_n (convolver.hpp:180-191 on fc_) + power
+  for (int l = c0; l < c1; ++l) {
+    float* prev = a.prev_spk + (size_t)l * N;
+    const float* sp = a.spk + (size_t)l * N;
+    __syncthreads();
+    for (int i = threadIdx.x; i < N; i += blockDim.x) {
+      wa[i] = prev[i];
+      wa[N + i] = sp[i];
+      prev[i] = sp[i];
+    }
+    __syncthreads();
+    float2* xnew = reinterpret_cast<float2*>(
+        a.XA + ((size_t)l * (a.KF + 1) + n % (uint32_t)(a.KF + 1)) * NF);
+    rfft_packed(wa, z, xnew, N, a.logN, a.tw, a.split);
+    if (a.nlms) {
+      for (int j = threadIdx.x; j < N; j += blockDim.x) {
+        const float2 v = xnew[j];
+        float2 p;
+        if (j == 0) {
+          p = make_float2(__fmul_rn(v.x, v.x), __fmul_rn(v.y, v.y));
+        } else {
+          const float m = __fadd_rn(__fmul_rn(v.x, v.x), __fmul_rn(v.y, v.y));
+          p = make_float2(m, m);
+        }
+        a.pw_part[(size_t)l * N + j] = p;
+      }
+    }
+  }
+  // ---- NLMS error spectra E_p = r2c([0_N, m~_p]) (Appendix A step 2)
+  if (a.nlms) {
+    for (int p = blockIdx.x; p < a.P; p += gridDim.x) {
+      __syncthreads();
+      for (int i = threadIdx.x; i < N; i += blockDim.x) {
+        wa[i] = 0.0f;
+        wa[N + i] = mts[(size_t)p * N + i];
+      }
+      __syncthreads();
+      rfft_packed(wa, z, reinterpret_cast<float2*>(a.E + (size_t)p * NF), N, a.logN, a.tw,
+                  a.split);
     }
   }
 }
 
-// ------------------------------------------------------------ k_input
-// Stage 1 (convolver.hpp:180-191) for every input channel, with the
-// auralizer's m~ = g*m - f^ (auralizer.hpp:73-76) fused in. CTAs
-// [Qx, Qx + P) build the NLMS error spectra E_p = r2c([0_N, m~_p])
-// (Appendix A step 2). Shared: 2N floats window + N float2 FFT scratch.
-__global__ void __launch_bounds__(256) k_input(BlockArgs a) {
-  extern __shared__ float smem[];
-  float* win = smem;                           // 2N
-  float2* z = reinterpret_cast<float2*>(win + 2 * a.N);  // N
-  const int N = a.N;
-  const uint32_t n = a.st->block;
-  const int Qx = a.mode == 1 ? a.L : a.Q;  // FDL channels
-  const int ch = blockIdx.x;
-  const bool err_cta = ch >= Qx;
-  const int q = err_cta ? ch - Qx : ch;
-  const float* in = a.in + (size_t)q * N;
-  for (int i = threadIdx.x; i < N; i += blockDim.x) {
-    float v = in[i];
-    if (a.is_aur) v = __fsub_rn(__fmul_rn(a.gain, v), a.fhat[(size_t)q * N + i]);
-    if (err_cta) {
-      win[i] = 0.0f;
-      win[N + i] = v;
-    } else {
-      float* prev = a.prev_in + (size_t)q * N;
-      win[i] = prev[i];
-      win[N + i] = v;
-    }
-  }
-  __syncthreads();
-  if (!err_cta) {
-    float* prev = a.prev_in + (size_t)q * N;
-    for (int i = threadIdx.x; i < N; i += blockDim.x) prev[i] = win[N + i];
-  }
-  float2* dst = err_cta
-                    ? reinterpret_cast<float2*>(a.E + (size_t)q * a.NF)
-                    : reinterpret_cast<float2*>(
-                          a.X + ((size_t)q * a.K + (n % (uint32_t)a.K)) * a.NF);
-  rfft_packed(win, z, dst, N, a.logN, a.tw, a.split);
-}
-
-// --------------------------------------------------------- k_mac_synth
-// out[l][j] += sum_{taps t in chunk} X[q(t)][age k(t)][j] * H[l][t][j]
-// (backend.hpp:212-235). grid = (syn_chunks, L/LT, syn_tiles), 256 threads.
-// Thread (kp, f): column f of the tile, tap phase kp; LT channels share
-// each X load (broadcast / MIMO) -- X is read from L2, H streamed from HBM
-// with 128-bit no-L1-allocate loads. ELEM: channel l reads FDL channel l.
+// ------------------------------------------------------------ k_mac_pre
+// Split-K partials of S_l(n+1) = sum_q sum_{j=0}^{K-2} X_q(age j) H_{l,q}[j+1]
+// (backend.hpp:212-235 over every partition but the first).
+// grid = (syn_chunks, L/LT, syn_tiles), 256 threads; thread (kp, f): column
+// f of the tile, tap phase kp. LT channels share every X load (broadcast /
+// mimo): X comes from L2, H streams from HBM with 128-bit no-L1 loads.
+// ELEM: channel l reads FDL channel l.
 template <int LT, bool ELEM>
-__global__ void __launch_bounds__(kMacThreads, 2) k_mac_synth(BlockArgs a) {
+__global__ void __launch_bounds__(kMacThreads, 2) k_mac_pre(BlockArgs a) {
   __shared__ float4 red[kMacThreads * LT];
   const int nft = a.syn_nft;
   const int KP = kMacThreads / nft;
@@ -214,10 +351,12 @@ __global__ void __launch_bounds__(kMacThreads, 2) k_mac_synth(BlockArgs a) {
   const int f = blockIdx.z * nft + fl;
   const int l0 = blockIdx.y * LT;
   const int K = a.K;
-  const int T = ELEM ? K : a.Q * K;
+  const int Kt = K - 1;                      // taps per input
+  const int Qh = ELEM ? 1 : a.Q;
+  const int T = Qh * Kt;
   const int t0 = blockIdx.x * a.syn_tc;
   const int t1 = min(t0 + a.syn_tc, T);
-  const int nk = (int)(a.st->block % (uint32_t)K);
+  const int nk = (int)((a.st->block - 1u) % (uint32_t)K);
   const bool dc = (f == 0);
   const int NF = a.NF;
 
@@ -226,17 +365,18 @@ __global__ void __launch_bounds__(kMacThreads, 2) k_mac_synth(BlockArgs a) {
   for (int i = 0; i < LT; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
 
   int t = t0 + kp;
-  int q = t / K;
-  int k = t - q * K;
+  int q = t / Kt;
+  int j = t - q * Kt;
 #pragma unroll 2
   for (; t < t1; t += KP) {
-    int slot = nk - k;
+    int slot = nk - j;
     if (slot < 0) slot += K;
+    const size_t hrow = (size_t)q * K + j + 1;  // partition j+1 of input q
     if (ELEM) {
 #pragma unroll
       for (int i = 0; i < LT; ++i) {
         const float4 xv = a.X[((size_t)(l0 + i) * K + slot) * NF + f];
-        const float4 h = ld_stream(a.H + ((size_t)(l0 + i) * T + t) * NF + f);
+        const float4 h = ld_stream(a.H + ((size_t)(l0 + i) * K + j + 1) * NF + f);
         cmac(acc[i], xpack(xv, dc), h, dc);
       }
     } else {
@@ -244,13 +384,13 @@ __global__ void __launch_bounds__(kMacThreads, 2) k_mac_synth(BlockArgs a) {
       float4 h[LT];
 #pragma unroll
       for (int i = 0; i < LT; ++i)
-        h[i] = ld_stream(a.H + ((size_t)(l0 + i) * T + t) * NF + f);
+        h[i] = ld_stream(a.H + ((size_t)(l0 + i) * Qh * K + hrow) * NF + f);
 #pragma unroll
       for (int i = 0; i < LT; ++i) cmac(acc[i], x, h[i], dc);
     }
-    k += KP;
-    while (k >= K) {
-      k -= K;
+    j += KP;
+    while (j >= Kt) {
+      j -= Kt;
       ++q;
     }
   }
@@ -265,58 +405,17 @@ __global__ void __launch_bounds__(kMacThreads, 2) k_mac_synth(BlockArgs a) {
   }
 }
 
-// -------------------------------------------------------- k_tail_synth
-// One CTA per output channel l: fixed-order reduction of the split-K
-// partials, c2r + overlap-save (convolver.hpp:202-205) straight into the
-// output; for the auralizer also the canceller's stage 1 on l_n
-// (convolver.hpp:180-191 on fc_) and the packed power |X_l|^2.
-__global__ void __launch_bounds__(kTailThreads) k_tail_synth(BlockArgs a) {
+// ----------------------------------------------------------- k_tail_pre
+// One CTA per output channel: S_l = fixed-order sum of the split-K partials.
+__global__ void __launch_bounds__(kTailThreads) k_tail_pre(BlockArgs a) {
   extern __shared__ float4 sm4[];
-  const int N = a.N, NF = a.NF;
-  float4* red = sm4;                                        // blockDim
-  float4* acc = red + blockDim.x;                           // NF
-  float2* z = reinterpret_cast<float2*>(acc + NF);          // N
-  float* win = reinterpret_cast<float*>(z + N);             // 2N
+  const int NF = a.NF;
+  float4* red = sm4;
+  float4* acc = red + blockDim.x;
   const int l = blockIdx.x;
-  const uint32_t n = a.st->block;
-
-  reduce_partials(a.part_syn + (size_t)l * NF, a.syn_chunks, (size_t)a.L * NF,
-                  NF, red, acc);
-  float* out = a.out + (size_t)l * N;
-  float* tailw = win + N;
-  irfft_packed_tail(reinterpret_cast<const float2*>(acc), z, N, a.logN, a.tw,
-                    a.split, [&](int i, float v) {
-                      out[i] = v;
-                      tailw[i] = v;
-                    });
-  if (!a.is_aur) {
-    retire_block(a, n);
-    return;
-  }
-  float* prev = a.prev_spk + (size_t)l * N;
-  for (int i = threadIdx.x; i < N; i += blockDim.x) {
-    win[i] = prev[i];
-    prev[i] = tailw[i];
-  }
-  __syncthreads();
-  float2* xnew = reinterpret_cast<float2*>(
-      a.XA + ((size_t)l * (a.KF + 1) + (n % (uint32_t)(a.KF + 1))) * NF);
-  float2* xs = reinterpret_cast<float2*>(acc);  // reuse: spectrum in smem
-  rfft_packed(win, z, xs, N, a.logN, a.tw, a.split);
-  for (int j = threadIdx.x; j < N; j += blockDim.x) {
-    const float2 v = xs[j];
-    xnew[j] = v;
-    if (a.nlms) {
-      float2 p;
-      if (j == 0) p = make_float2(v.x * v.x, v.y * v.y);
-      else {
-        const float m = v.x * v.x + v.y * v.y;
-        p = make_float2(m, m);
-      }
-      a.pw_part[(size_t)l * N + j] = p;
-    }
-  }
-  __threadfence_system();
+  reduce_partials(a.part_syn + (size_t)l * NF, a.syn_chunks, (size_t)a.L * NF, NF, red, acc);
+  for (int f = threadIdx.x; f < NF; f += blockDim.x) a.S[(size_t)l * NF + f] = acc[f];
+  retire_back(a, a.st->block - 1u);
 }
 
 // ----------------------------------------------------------- k_mac_afc
@@ -338,7 +437,7 @@ __global__ void __launch_bounds__(kMacThreads, 2) k_mac_afc(BlockArgs a) {
   const int U = L * KF;
   const int u0 = blockIdx.x * a.afc_uc;
   const int u1 = min(u0 + a.afc_uc, U);
-  const int nk = (int)(a.st->block % (uint32_t)cap);
+  const int nk = (int)((a.st->block - 1u) % (uint32_t)cap);
   const bool dc = (f == 0);
 
   float4 acc[PT];
@@ -351,8 +450,10 @@ __global__ void __launch_bounds__(kMacThreads, 2) k_mac_afc(BlockArgs a) {
   }
   if (a.nlms) {
     const float2 p0 = a.pw[2 * f], p1 = a.pw[2 * f + 1];
-    s = make_float4(a.mu / (p0.x + a.delta), a.mu / (p0.y + a.delta),
-                    a.mu / (p1.x + a.delta), a.mu / (p1.y + a.delta));
+    s = make_float4(__fdiv_rn(a.mu, __fadd_rn(p0.x, a.delta)),
+                    __fdiv_rn(a.mu, __fadd_rn(p0.y, a.delta)),
+                    __fdiv_rn(a.mu, __fadd_rn(p1.x, a.delta)),
+                    __fdiv_rn(a.mu, __fadd_rn(p1.y, a.delta)));
   }
 
   int u = u0 + kp;
@@ -369,21 +470,22 @@ __global__ void __launch_bounds__(kMacThreads, 2) k_mac_afc(BlockArgs a) {
       float4* wp = a.W + (((size_t)p * L + l) * KF + k) * NF + f;
       float4 w = *wp;
       if (a.nlms) {
-        // g = conj(x1) * E_p ; packed bin 0 is (DC, Nyquist) real products
+        // g = conj(x1) * E_p ; packed bin 0 is (DC, Nyquist) real products.
+        // Rounded exactly as the oracle (aura_oracle.c nlms_update): no FMA.
         float4 g;
         if (dc) {
-          g.x = x1.x * e[p].x;
-          g.y = x1.y * e[p].y;
+          g.x = __fmul_rn(x1.x, e[p].x);
+          g.y = __fmul_rn(x1.y, e[p].y);
         } else {
-          g.x = x1.x * e[p].x + x1.y * e[p].y;
-          g.y = x1.x * e[p].y - x1.y * e[p].x;
+          g.x = __fadd_rn(__fmul_rn(x1.x, e[p].x), __fmul_rn(x1.y, e[p].y));
+          g.y = __fsub_rn(__fmul_rn(x1.x, e[p].y), __fmul_rn(x1.y, e[p].x));
         }
-        g.z = x1.z * e[p].z + x1.w * e[p].w;
-        g.w = x1.z * e[p].w - x1.w * e[p].z;
-        w.x = fmaf(s.x, g.x, w.x);
-        w.y = fmaf(s.y, g.y, w.y);
-        w.z = fmaf(s.z, g.z, w.z);
-        w.w = fmaf(s.w, g.w, w.w);
+        g.z = __fadd_rn(__fmul_rn(x1.z, e[p].z), __fmul_rn(x1.w, e[p].w));
+        g.w = __fsub_rn(__fmul_rn(x1.z, e[p].w), __fmul_rn(x1.w, e[p].z));
+        w.x = __fadd_rn(w.x, __fmul_rn(s.x, g.x));
+        w.y = __fadd_rn(w.y, __fmul_rn(s.y, g.y));
+        w.z = __fadd_rn(w.z, __fmul_rn(s.z, g.z));
+        w.w = __fadd_rn(w.w, __fmul_rn(s.w, g.w));
         *wp = w;
       }
       cmac(acc[p], x0, w, dc);
@@ -417,27 +519,32 @@ __global__ void __launch_bounds__(kTailThreads) k_tail_afc(BlockArgs a) {
   float4* acc = red + blockDim.x;
   float2* z = reinterpret_cast<float2*>(acc + NF);
   const int p = blockIdx.x;
-  const uint32_t n = a.st->block;
-  reduce_partials(a.part_afc + (size_t)p * NF, a.afc_chunks, (size_t)a.P * NF,
-                  NF, red, acc);
+  const uint32_t n = a.st->block - 1u;
+  reduce_partials(a.part_afc + (size_t)p * NF, a.afc_chunks, (size_t)a.P * NF, NF, red, acc);
   float* fh = a.fhat + (size_t)p * N;
-  irfft_packed_tail(reinterpret_cast<const float2*>(acc), z, N, a.logN, a.tw,
-                    a.split, [&](int i, float v) { fh[i] = v; });
+  float* fhh = a.fhat_host + (size_t)p * N;
+  irfft_packed_tail(reinterpret_cast<const float2*>(acc), z, N, a.logN, a.tw, a.split,
+                    [&](int i, float v) {
+                      fh[i] = v;
+                      fhh[i] = v;
+                    });
   if (a.nlms && p == 0) {
     for (int j = threadIdx.x; j < N; j += blockDim.x) {
       float2 sum = make_float2(0.f, 0.f);
       for (int ll = 0; ll < a.L; ++ll) {
         const float2 v = a.pw_part[(size_t)ll * N + j];
-        sum.x += v.x;
-        sum.y += v.y;
+        sum.x = __fadd_rn(sum.x, v.x);
+        sum.y = __fadd_rn(sum.y, v.y);
       }
+      // Appendix A step 5, rounded as the oracle: lambda P + (1 - lambda) s
       float2 w = a.pw[j];
-      w.x = a.lambda * w.x + (1.0f - a.lambda) * sum.x;
-      w.y = a.lambda * w.y + (1.0f - a.lambda) * sum.y;
+      const float oml = __fsub_rn(1.0f, a.lambda);
+      w.x = __fadd_rn(__fmul_rn(a.lambda, w.x), __fmul_rn(oml, sum.x));
+      w.y = __fadd_rn(__fmul_rn(a.lambda, w.y), __fmul_rn(oml, sum.y));
       a.pw[j] = w;
     }
   }
-  retire_block(a, n);
+  retire_back(a, n);
 }
 
 // ------------------------------------------------------ k_partition
@@ -445,9 +552,8 @@ __global__ void __launch_bounds__(kTailThreads) k_tail_afc(BlockArgs a) {
 // (k, r) transforms taps[r][kN .. kN+N) zero-padded to 2N into the packed
 // spectrum dst + row_off[r] + k*NF. taps rows are n_h long.
 __global__ void __launch_bounds__(256) k_partition(
-    const float* __restrict__ taps, size_t n_h, int rows, int K, int N,
-    int logN, const float2* tw, const float2* split, float4* dst,
-    const size_t* __restrict__ row_off) {
+    const float* __restrict__ taps, size_t n_h, int rows, int K, int N, int logN,
+    const float2* tw, const float2* split, float4* dst, const size_t* __restrict__ row_off) {
   extern __shared__ float smem[];
   float* win = smem;
   float2* z = reinterpret_cast<float2*>(win + 2 * N);

@@ -178,17 +178,18 @@ def test_closed_loop_divergence_without_cancellation():
 
 def test_c3_config_streams_and_matches_oracle_subset():
     """configs[2] shape (1 x 64, N = 64, 10 s synthesis, 1 s canceller, NLMS
-    on): 300 blocks on the GPU against the C oracle at full size."""
+    on): 200 blocks on the GPU against the C oracle at full size; outputs,
+    f^ and the canceller spectra W within 1e-5 of their RMS."""
     N, L = 64, 64
     rng = np.random.default_rng(2024)
     synth = decaying_filters(rng, L, 480000)
     fc = decaying_filters(rng, L, 48000, t60_s=0.3, scale=0.1)
-    kw = dict(mu=0.005, lam=0.9, delta=1e-6 * N)
+    kw = dict(mu=0.005, lam=0.9)  # default regulariser 1e-2 * 2N
     g = gpu_aur(synth, fc, N, 1, L, **kw)
     assert g.synth_partitions() == 7500 and g.fc_partitions() == 750
     o = O.OracleAuralizer(synth, fc, N, 1, L, **kw)
     ys, yo = [], []
-    for _ in range(40):
+    for _ in range(200):
         m = rng.standard_normal((1, N)).astype(np.float32)
         ys.append(g.process(m))
         yo.append(o.process(m))

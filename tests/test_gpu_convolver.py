@@ -32,7 +32,8 @@ def test_golden_reference_outputs(name):
     assert rel_err(y, g["y"]) <= TOL
     k_show = min(conv.partition_count(), 3)
     spec = np.stack([conv.spectrum(c, k) for c in range(L) for k in range(k_show)])
-    assert np.max(np.abs(spec - g["spectra"])) <= 1e-6 * max(1.0, np.max(np.abs(g["spectra"])))
+    # the device r2c performs the reference's float operations: bit-identical
+    assert np.array_equal(spec, g["spectra"])
     assert np.all(spec[:, 0].imag == 0) and np.all(spec[:, -1].imag == 0)
 
 
