@@ -290,12 +290,15 @@ def run_b200_arm(args, cfg, rank, world, local_rank):
         host_us = eng.time_host_blocks(mic, K)
     clocks = clk.summary()
     phases = eng.profile_phases(min(K, 200))
+    trace = eng.trace_blocks(32)
+    timeline = {k: {"start_us": float(np.median(v[:, 0])), "end_us": float(np.median(v[:, 1]))}
+                for k, v in trace.items()}
     peak, peak_kind = load_peaks()
-    mac_us, mac_bytes = phases["k_mac_pre"]
-    if mac_bytes == 0:
-        mac_us, mac_bytes = phases["k_front"]
+    mac_name = "k_mac_pre" if phases["k_mac_pre"][1] > 0 else "k_front"
+    mac_bytes = phases[mac_name][1]
+    mac_us = eng.time_phase(mac_name, 20)
     achieved = mac_bytes / (mac_us * 1e-6) / 1e9
-    n_launch = 1 + (2 if phases["k_mac_pre"][1] > 0 else 0) + (2 if cfg["afc"] else 0)
+    n_launch = eng.launches_per_block()
 
     paced = None
     if not args.no_paced:
@@ -347,12 +350,13 @@ def run_b200_arm(args, cfg, rank, world, local_rank):
                 "path": "aura_b200_process() C-ABI, pinned mapped host I/O, back-to-back "
                         "(each call also waits for the previous block's background work)"},
         "paced_e2e": paced,
-        "roofline": {"bound": "hbm", "kernel": "k_mac_pre", "achieved": achieved,
+        "roofline": {"bound": "hbm", "kernel": mac_name, "achieved": achieved,
                      "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "peak_kind": peak_kind, "traffic": None,
                      "bytes_per_launch": mac_bytes, "avg_launch_us": mac_us},
-        "phases_us": {k: v[0] for k, v in phases.items()},
-        "phases_GBps": {k: v[1] / (v[0] * 1e-6) / 1e9 for k, v in phases.items()},
+        "phases_us_serial": {k: v[0] for k, v in phases.items()},
+        "timeline_us": timeline,
+        "phase_bytes": {k: v[1] for k, v in phases.items()},
         "cpu_baseline": cpu, "clocks": clocks, "gpu_launches": int(K * n_launch),
         "max_realtime": maxrt, "setup_s": t_setup,
     }

@@ -196,6 +196,9 @@ def lib():
     L.aura_b200_phase_bytes.argtypes = [vp, C.c_int]
     L.aura_b200_phase_bytes.restype = C.c_double
     L.aura_b200_describe.argtypes = [vp, C.c_char_p, sz]
+    L.aura_b200_launches_per_block.argtypes = [vp]
+    L.aura_b200_time_phase.argtypes = [vp, C.c_int, sz, C.POINTER(C.c_float)]
+    L.aura_b200_trace_blocks.argtypes = [vp, sz, np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")]
     _lib = L
     return L
 
@@ -304,6 +307,31 @@ class _Engine:
     def reset(self):
         _check(lib().aura_b200_reset(self._h))
 
+    TRACE_KERNELS = ("k_front", "k_mac_pre", "k_tail_pre", "k_back_head", "k_mac_afc",
+                     "k_tail_afc")
+
+    def trace_blocks(self, blocks: int = 32):
+        """Per-kernel [start, end] (us from the block's front start) of
+        back-to-back blocks, from %globaltimer stamps inside the kernels."""
+        blocks = min(blocks, 64)
+        out = np.zeros(blocks * 8 * 2, np.float64)
+        _check(lib().aura_b200_trace_blocks(self._h, blocks, out))
+        out = out.reshape(blocks, 8, 2)
+        return {name: out[:, k, :] for k, name in enumerate(self.TRACE_KERNELS)
+                if np.all(out[:, k, 0] >= 0)}
+
+    PHASES = {"k_front": 0, "k_mac_pre": 1, "k_tail_pre": 2}
+
+    def time_phase(self, name: str, reps: int = 20) -> float:
+        """Mean device time (us) of back-to-back launches of one idempotent
+        phase kernel, CUDA events on the engine stream."""
+        v = C.c_float(0)
+        _check(lib().aura_b200_time_phase(self._h, self.PHASES[name], reps, C.byref(v)))
+        return float(v.value)
+
+    def launches_per_block(self) -> int:
+        return int(lib().aura_b200_launches_per_block(self._h))
+
     def describe(self) -> str:
         buf = C.create_string_buffer(1024)
         _check(lib().aura_b200_describe(self._h, buf, 1024))
@@ -339,7 +367,7 @@ class _Engine:
         return out
 
     def profile_phases(self, blocks: int):
-        us = np.zeros(8, np.float32)
+        us = np.zeros(16, np.float32)
         n = C.c_int(0)
         _check(lib().aura_b200_profile_phases(self._h, blocks, us, C.byref(n)))
         return {lib().aura_b200_phase_name(self._h, i).decode():

@@ -105,9 +105,12 @@ T* dalloc(size_t count, std::vector<void*>& owned) {
 
 }  // namespace
 
-enum Phase { PH_FRONT = 0, PH_MAC_PRE, PH_TAIL_PRE, PH_MAC_AFC, PH_TAIL_AFC, PH_COUNT };
-static const char* kPhaseNames[PH_COUNT] = {"k_front", "k_mac_pre", "k_tail_pre", "k_mac_afc",
-                                            "k_tail_afc"};
+enum Phase {
+  PH_FRONT = 0, PH_MAC_PRE, PH_TAIL_PRE, PH_BACK_HEAD, PH_MAC_AFC, PH_TAIL_AFC, PH_ADVANCE,
+  PH_COUNT
+};
+static const char* kPhaseNames[PH_COUNT] = {"k_front", "k_mac_pre", "k_tail_pre", "k_back_head",
+                                            "k_mac_afc", "k_tail_afc", "k_advance"};
 
 struct aura_b200_engine {
   int device = 0;
@@ -120,40 +123,74 @@ struct aura_b200_engine {
   cudaStream_t stream = nullptr;  // the engine's stream (front + background)
   cudaStream_t side = nullptr;    // second branch used while capturing
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_front = nullptr, ev_back = nullptr;  // completion, per block
   std::vector<void*> dmem;
   float4* W0 = nullptr;  // initial canceller spectra (reset of NLMS)
   size_t w_elems = 0;
   float* h_in = nullptr;    // mapped pinned
   float* h_out = nullptr;   // mapped pinned
-  uint32_t* h_done = nullptr;  // [0] output ready, [16] background done
   float* h_fhat = nullptr;  // mapped pinned copy of f^
   float* d_in_pool = nullptr;
   size_t pool_blocks = 0;
   float* d_out = nullptr;
   BlockArgs args{};
   BlockArgs dev_args{};
-  cudaGraphExec_t g_front = nullptr, g_back = nullptr;
-  size_t smem_front = 0, smem_tail = 0;
+  struct BlockGraph {
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t ex = nullptr;
+    cudaGraphNode_t out_node = nullptr;  // external event-record node (output ready)
+    void destroy() {
+      if (ex) cudaGraphExecDestroy(ex);
+      if (g) cudaGraphDestroy(g);
+      ex = nullptr;
+      g = nullptr;
+    }
+  };
+  BlockGraph g_block;
+  int prio_high = 0;  // stream priority of the canceller branch
+  size_t smem_front = 0, smem_tail = 0, smem_head = 0;
 
   ~aura_b200_engine() {
     cudaSetDevice(device);
     if (stream) cudaStreamSynchronize(stream);
-    if (g_front) cudaGraphExecDestroy(g_front);
-    if (g_back) cudaGraphExecDestroy(g_back);
+    g_block.destroy();
     for (void* p : dmem) cudaFree(p);
     if (h_in) cudaFreeHost(h_in);
     if (h_out) cudaFreeHost(h_out);
-    if (h_done) cudaFreeHost(h_done);
     if (h_fhat) cudaFreeHost(h_fhat);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
+    if (ev_front) cudaEventDestroy(ev_front);
+    if (ev_back) cudaEventDestroy(ev_back);
     if (side) cudaStreamDestroy(side);
     if (stream) cudaStreamDestroy(stream);
   }
 
   bool has_pre() const { return K > 1; }
+  bool has_head() const { return aur || mode != AURA_B200_ELEMENTWISE; }
+
+  // cudaLaunchKernelEx with an explicit scheduling priority (captured into
+  // the graph's kernel nodes): the canceller branch runs at high priority so
+  // its CTAs interleave with the synthesis precompute instead of queueing
+  // behind it.
+  template <typename Kern>
+  void launch(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t s, int prio,
+              const BlockArgs& a) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributePriority;
+    at[0].val.priority = prio;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, kern, a));
+  }
 
   void launch_phase(int ph, const BlockArgs& a, cudaStream_t s) {
+    const int hp = prio_high;
     switch (ph) {
       case PH_FRONT: {
         const int grid = (int)((L + a.cpb - 1) / a.cpb);
@@ -174,27 +211,40 @@ struct aura_b200_engine {
         break;
       }
       case PH_TAIL_PRE:
-        if (has_pre()) k_tail_pre<<<(unsigned)L, kTailThreads, smem_tail, s>>>(a);
+        if (has_pre()) k_tail_pre<<<(unsigned)(kRedCluster * L), kTailThreads, smem_tail, s>>>(a);
+        break;
+      case PH_BACK_HEAD:
+        if (has_head())
+          launch(k_back_head, dim3((unsigned)(aur ? L + (a.nlms ? P : 0) : 1)), dim3(kFrontThreads),
+                 smem_head, s, hp, a);
         break;
       case PH_MAC_AFC: {
         if (!aur) break;
         dim3 grid(a.afc_chunks, 1, a.afc_tiles);
         switch (PT) {
-          case 1: k_mac_afc<1><<<grid, kMacThreads, 0, s>>>(a); break;
-          case 2: k_mac_afc<2><<<grid, kMacThreads, 0, s>>>(a); break;
-          case 4: k_mac_afc<4><<<grid, kMacThreads, 0, s>>>(a); break;
-          default: k_mac_afc<8><<<grid, kMacThreads, 0, s>>>(a); break;
+          case 1: launch(k_mac_afc<1>, grid, dim3(kMacThreads), 0, s, hp, a); break;
+          case 2: launch(k_mac_afc<2>, grid, dim3(kMacThreads), 0, s, hp, a); break;
+          case 4: launch(k_mac_afc<4>, grid, dim3(kMacThreads), 0, s, hp, a); break;
+          default: launch(k_mac_afc<8>, grid, dim3(kMacThreads), 0, s, hp, a); break;
         }
         break;
       }
       case PH_TAIL_AFC:
-        if (aur) k_tail_afc<<<(unsigned)P, kTailThreads, smem_tail, s>>>(a);
+        if (aur)
+          launch(k_tail_afc, dim3((unsigned)(kRedCluster * P)), dim3(kTailThreads), smem_tail, s, hp,
+                 a);
+        break;
+      case PH_ADVANCE:
+        if (a.advance_total == 0) k_advance<<<1, 1, 0, s>>>(a.st);
         break;
     }
   }
 
   // kernels launched per block (front + background)
-  int launches_per_block() const { return 1 + (has_pre() ? 2 : 0) + (aur ? 2 : 0); }
+  int launches_per_block() const {
+    return 1 + (args.advance_total == 0 ? 1 : 0) + (has_pre() ? 2 : 0) + (has_head() ? 1 : 0) +
+           (aur ? 2 : 0);
+  }
 
   cudaGraphExec_t instantiate(cudaGraph_t g) {
     cudaGraphExec_t ex;
@@ -203,52 +253,51 @@ struct aura_b200_engine {
     return ex;
   }
 
-  cudaGraphExec_t capture_front(const BlockArgs& a) {
-    cudaGraph_t g;
+  // One graph per block: k_front, an external event node the host waits on
+  // (output ready), then the background as two concurrent branches --
+  // canceller (high priority) and synthesis precompute.
+  BlockGraph capture_block(const BlockArgs& a, cudaEvent_t out_event) {
+    BlockGraph bg;
     CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
     launch_phase(PH_FRONT, a, stream);
-    CK(cudaStreamEndCapture(stream, &g));
-    return instantiate(g);
-  }
-
-  // background: the synthesis precompute and the canceller as two
-  // concurrent branches of one graph
-  cudaGraphExec_t capture_back(const BlockArgs& a) {
-    cudaGraph_t g;
-    CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
-    const bool fork = has_pre() && aur;
-    if (fork) {
-      CK(cudaEventRecord(ev_fork, stream));
-      CK(cudaStreamWaitEvent(side, ev_fork, 0));
-      launch_phase(PH_MAC_AFC, a, side);
-      launch_phase(PH_TAIL_AFC, a, side);
-      CK(cudaEventRecord(ev_join, side));
-    } else {
-      launch_phase(PH_MAC_AFC, a, stream);
-      launch_phase(PH_TAIL_AFC, a, stream);
-    }
+    if (out_event) CK(cudaEventRecordWithFlags(out_event, stream, cudaEventRecordExternal));
+    CK(cudaEventRecord(ev_fork, stream));
+    CK(cudaStreamWaitEvent(side, ev_fork, 0));
+    launch_phase(PH_BACK_HEAD, a, side);
+    launch_phase(PH_MAC_AFC, a, side);
+    launch_phase(PH_TAIL_AFC, a, side);
+    CK(cudaEventRecord(ev_join, side));
     launch_phase(PH_MAC_PRE, a, stream);
     launch_phase(PH_TAIL_PRE, a, stream);
-    if (fork) CK(cudaStreamWaitEvent(stream, ev_join, 0));
-    CK(cudaStreamEndCapture(stream, &g));
-    return instantiate(g);
+    CK(cudaStreamWaitEvent(stream, ev_join, 0));
+    if (a.advance_total == 0) launch_phase(PH_ADVANCE, a, stream);
+    CK(cudaStreamEndCapture(stream, &bg.g));
+    if (out_event) {
+      size_t n = 0;
+      CK(cudaGraphGetNodes(bg.g, nullptr, &n));
+      std::vector<cudaGraphNode_t> nodes(n);
+      CK(cudaGraphGetNodes(bg.g, nodes.data(), &n));
+      for (auto nd : nodes) {
+        cudaGraphNodeType t;
+        CK(cudaGraphNodeGetType(nd, &t));
+        if (t == cudaGraphNodeTypeEventRecord) bg.out_node = nd;
+      }
+    }
+    CK(cudaGraphInstantiate(&bg.ex, bg.g, 0));
+    return bg;
   }
 
   void rebuild_graphs() {
-    if (g_front) cudaGraphExecDestroy(g_front);
-    if (g_back) cudaGraphExecDestroy(g_back);
-    g_front = g_back = nullptr;
-    g_front = capture_front(args);
-    if (has_pre() || aur) g_back = capture_back(args);
+    g_block.destroy();
+    g_block = capture_block(args, ev_front);
   }
 
   double phase_bytes(int ph) const {
     const double row = 8.0 * (double)N;  // one packed partition
     const double Qh = mode == AURA_B200_MIMO ? (double)Q : 1.0;
     switch (ph) {
-      case PH_FRONT:  // inputs, X push, H[.][.][0], S, outputs (+ canceller stage 1)
-        return 4.0 * N * Qx + row * Qx + row * (double)L * Qh + row * L + 4.0 * N * L +
-               (aur ? row * L + 4.0 * N * L : 0.0);
+      case PH_FRONT:  // inputs, X push, H[.][.][0], S, outputs
+        return 4.0 * N * Qx + row * Qx + row * (double)L * Qh + row * L + 4.0 * N * L;
       case PH_MAC_PRE:
         return has_pre() ? row * ((double)L * Qh * (K - 1) + (double)Qx * (K - 1)) : 0.0;
       case PH_TAIL_PRE: return has_pre() ? row * (double)args.syn_chunks * L + row * L : 0.0;
@@ -256,6 +305,7 @@ struct aura_b200_engine {
         return aur ? row * ((double)P * L * KF * (1.0 + (args.nlms ? 1.0 : 0.0)) + (double)L * KF)
                    : 0.0;
       case PH_TAIL_AFC: return aur ? row * (double)args.afc_chunks * P + 4.0 * N * P : 0.0;
+      case PH_BACK_HEAD: return aur ? (row + 8.0 * N) * L + row * P : 4.0 * N * Qx;
     }
     return 0.0;
   }
@@ -362,9 +412,14 @@ void common_init(aura_b200_engine* e, int device) {
   e->device = device;
   CK(cudaSetDevice(device));
   CK(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
-  CK(cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking));
+  int least = 0, greatest = 0;
+  CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+  e->prio_high = greatest;
+  CK(cudaStreamCreateWithPriority(&e->side, cudaStreamNonBlocking, greatest));
   CK(cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&e->ev_join, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&e->ev_front, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&e->ev_back, cudaEventDisableTiming));
 }
 
 void finish_init(aura_b200_engine* e) {
@@ -378,10 +433,8 @@ void finish_init(aura_b200_engine* e) {
   const size_t in_ch = (size_t)e->Qx;
   CK(cudaHostAlloc(&e->h_in, in_ch * N * sizeof(float), cudaHostAllocMapped | cudaHostAllocPortable));
   CK(cudaHostAlloc(&e->h_out, e->L * N * sizeof(float), cudaHostAllocMapped | cudaHostAllocPortable));
-  CK(cudaHostAlloc(&e->h_done, 128, cudaHostAllocMapped | cudaHostAllocPortable));
   std::memset(e->h_in, 0, in_ch * N * sizeof(float));
   std::memset(e->h_out, 0, e->L * N * sizeof(float));
-  std::memset(e->h_done, 0, 128);
   if (e->aur) {
     CK(cudaHostAlloc(&e->h_fhat, e->P * N * sizeof(float), cudaHostAllocMapped | cudaHostAllocPortable));
     std::memset(e->h_fhat, 0, e->P * N * sizeof(float));
@@ -389,23 +442,31 @@ void finish_init(aura_b200_engine* e) {
   }
   float* din;
   float* dout;
-  uint32_t* ddone;
   CK(cudaHostGetDevicePointer((void**)&din, e->h_in, 0));
   CK(cudaHostGetDevicePointer((void**)&dout, e->h_out, 0));
-  CK(cudaHostGetDevicePointer((void**)&ddone, e->h_done, 0));
   a.in = din;
   a.out = dout;
-  a.done = ddone;
-  a.back_done = ddone + 16;  // separate 64-byte line
-  a.back_total = (e->has_pre() ? (int)e->L : 0) + (e->aur ? (int)e->P : 0);
+  a.cur_mt = dalloc<float>(std::max<size_t>(1, e->Q) * N, e->dmem);
+  CK(cudaMemset(a.cur_mt, 0, sizeof(float) * std::max<size_t>(1, e->Q) * N));
+  // contiguous copy of every row's partition 0 for the front kernel
+  {
+    const size_t Qh = e->mode == AURA_B200_MIMO ? e->Q : 1;
+    float4* h0 = dalloc<float4>(e->L * Qh * NF, e->dmem);
+    CK(cudaMemcpy2D(h0, NF * sizeof(float4), a.H, e->K * NF * sizeof(float4), NF * sizeof(float4),
+                    e->L * Qh, cudaMemcpyDeviceToDevice));
+    a.H0 = h0;
+  }
+  a.advance_total = (int)((e->has_pre() ? kRedCluster * e->L : 0) + (e->aur ? kRedCluster * e->P : 0));
   // front: one CTA per cpb output channels
   a.cpb = (int)std::max<size_t>(1, (e->L + kSMs - 1) / kSMs);
   const size_t Qs = e->mode == AURA_B200_ELEMENTWISE ? 1 : e->Q;
-  e->smem_front = 8 * N * (Qs + 2) + 4 * N * Qs;
+  e->smem_front = 8 * N * (Qs + 2);
+  e->smem_head = 16 * N;
   if (e->smem_front > 227 * 1024)
     fail(AURA_B200_E_INVALID_ARGUMENT, "block size too large for this many inputs (shared memory)");
   e->smem_tail = sizeof(float4) * kTailThreads + 24 * N;
   CK(cudaFuncSetAttribute(k_front, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem_front));
+  CK(cudaFuncSetAttribute(k_back_head, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem_head));
   CK(cudaFuncSetAttribute(k_tail_pre, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem_tail));
   CK(cudaFuncSetAttribute(k_tail_afc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem_tail));
   // device-resident I/O variant for measurement
@@ -440,8 +501,6 @@ void reset_state(aura_b200_engine* e) {
       CK(cudaMemcpyAsync(a.W, e->W0, sizeof(float4) * e->w_elems, cudaMemcpyDeviceToDevice, s));
   }
   CK(cudaStreamSynchronize(s));
-  e->h_done[0] = 0;
-  e->h_done[16] = 0;
   e->blocks = 0;
 }
 
@@ -657,31 +716,30 @@ int aura_b200_auralizer_create(const aura_b200_config* cfg,
 void aura_b200_destroy(aura_b200_engine* e) { delete e; }
 
 namespace {
-// Spin on a mapped word the GPU publishes; poll the stream for errors.
-void wait_word(aura_b200_engine* e, volatile uint32_t* word, uint32_t expect, const char* what) {
+// Spin until `ev` (recorded on the engine stream) has completed; kernel
+// completion makes the block's mapped-memory writes visible to the host.
+void wait_event(aura_b200_engine* e, cudaEvent_t ev, const char* what) {
   uint64_t spins = 0;
   const auto t0 = std::chrono::steady_clock::now();
-  while (*word != expect) {
+  for (;;) {
+    const cudaError_t q = cudaEventQuery(ev);
+    if (q == cudaSuccess) break;
+    if (q != cudaErrorNotReady) ck(q, what);
 #if defined(__x86_64__)
     _mm_pause();
 #endif
-    if ((++spins & 0xFFFF) == 0) {
-      const cudaError_t q = cudaStreamQuery(e->stream);
-      if (q != cudaSuccess && q != cudaErrorNotReady) ck(q, what);
-      if (q == cudaSuccess && *word != expect)
-        fail(AURA_B200_E_CUDA, std::string(what) + ": stream idle without publishing");
-      if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(20))
-        fail(AURA_B200_E_TIMEOUT, std::string(what) + ": not complete within 20 s");
-    }
+    if ((++spins & 0xFFF) == 0 &&
+        std::chrono::steady_clock::now() - t0 > std::chrono::seconds(20))
+      fail(AURA_B200_E_TIMEOUT, std::string(what) + ": not complete within 20 s");
   }
   std::atomic_thread_fence(std::memory_order_acquire);
 }
 }  // namespace
 
-// One block: launch FRONT then BACK; return as soon as the front's last CTA
-// has published the output. The background keeps running; the next call's
-// front is stream-ordered after it, and feedback_estimate()/synchronize()
-// wait for it explicitly.
+// One block: launch FRONT then BACK; return as soon as the front has
+// written the output. The background keeps running; the next call's front
+// is stream-ordered after it, and feedback_estimate()/synchronize() wait
+// for it explicitly.
 int aura_b200_process(aura_b200_engine* e, const float* in, float* out) {
   return guarded([&] {
     if (!e || !in || !out) fail(AURA_B200_E_INVALID_ARGUMENT, "null argument");
@@ -689,14 +747,12 @@ int aura_b200_process(aura_b200_engine* e, const float* in, float* out) {
     for (size_t i = 0; i < n_in; ++i)
       if (!std::isfinite(in[i])) fail(AURA_B200_E_NON_FINITE_INPUT, "input contains NaN or Inf");
     CK(cudaSetDevice(e->device));
-    // the previous block's front has finished reading h_in (its output word
-    // was observed), so the staging buffer can be refilled
+    // the previous block's front has completed, so the staging buffer is free
     std::memcpy(e->h_in, in, n_in * sizeof(float));
-    const uint32_t expect = (uint32_t)(e->blocks + 1);
     std::atomic_thread_fence(std::memory_order_release);
-    CK(cudaGraphLaunch(e->g_front, e->stream));
-    if (e->g_back) CK(cudaGraphLaunch(e->g_back, e->stream));
-    wait_word(e, e->h_done, expect, "block output");
+    CK(cudaGraphLaunch(e->g_block.ex, e->stream));  // records ev_front after k_front
+    CK(cudaEventRecord(e->ev_back, e->stream));
+    wait_event(e, e->ev_front, "block output");
     std::memcpy(out, e->h_out, e->L * e->N * sizeof(float));
     ++e->blocks;
   });
@@ -705,7 +761,7 @@ int aura_b200_process(aura_b200_engine* e, const float* in, float* out) {
 int aura_b200_synchronize(aura_b200_engine* e) {
   return guarded([&] {
     CK(cudaSetDevice(e->device));
-    if (e->blocks) wait_word(e, e->h_done + 16, (uint32_t)e->blocks, "block background");
+    if (e->blocks) wait_event(e, e->ev_back, "block background");
     CK(cudaStreamSynchronize(e->stream));
   });
 }
@@ -721,7 +777,8 @@ int aura_b200_feedback_estimate(aura_b200_engine* e, float* out) {
   return guarded([&] {
     if (!e->aur) fail(AURA_B200_E_INVALID_ARGUMENT, "not an auralizer");
     CK(cudaSetDevice(e->device));
-    if (e->blocks) wait_word(e, e->h_done + 16, (uint32_t)e->blocks, "block background");
+    if (e->blocks) wait_event(e, e->ev_back, "block background");
+    CK(cudaStreamSynchronize(e->stream));
     std::memcpy(out, e->h_fhat, sizeof(float) * e->P * e->N);
   });
 }
@@ -825,22 +882,24 @@ int aura_b200_time_device_blocks(aura_b200_engine* e, const float* host_in,
       const size_t nb = std::min(n_in_blocks, e->pool_blocks);
       CK(cudaMemcpy(e->d_in_pool, host_in, nb * per * sizeof(float), cudaMemcpyHostToDevice));
     }
-    // one front graph per pool slot (the input pointer is baked per slot)
-    std::vector<cudaGraphExec_t> gs;
+    // one block graph per pool slot (the input pointer is baked per slot);
+    // its output-event node is re-pointed at a fresh timing event per block
+    std::vector<aura_b200_engine::BlockGraph> gs;
     const size_t slots = std::max<size_t>(1, std::min(n_in_blocks, e->pool_blocks));
+    cudaEvent_t proto;
+    CK(cudaEventCreate(&proto));
     for (size_t s = 0; s < slots; ++s) {
       BlockArgs a = e->dev_args;
       a.in = e->d_in_pool + s * per;
-      gs.push_back(e->capture_front(a));
+      gs.push_back(e->capture_block(a, proto));
     }
-    cudaGraphExec_t back = (e->has_pre() || e->aur) ? e->capture_back(e->dev_args) : nullptr;
     std::vector<cudaEvent_t> ev(3 * blocks);
     for (auto& x : ev) CK(cudaEventCreate(&x));
     for (size_t b = 0; b < blocks; ++b) {
+      auto& g = gs[b % slots];
+      CK(cudaGraphExecEventRecordNodeSetEvent(g.ex, g.out_node, ev[3 * b + 1]));
       CK(cudaEventRecord(ev[3 * b], e->stream));
-      CK(cudaGraphLaunch(gs[b % slots], e->stream));
-      CK(cudaEventRecord(ev[3 * b + 1], e->stream));
-      if (back) CK(cudaGraphLaunch(back, e->stream));
+      CK(cudaGraphLaunch(g.ex, e->stream));
       CK(cudaEventRecord(ev[3 * b + 2], e->stream));
     }
     CK(cudaStreamSynchronize(e->stream));
@@ -854,11 +913,9 @@ int aura_b200_time_device_blocks(aura_b200_engine* e, const float* host_in,
       block_us[b] = ms * 1000.0f;
     }
     for (auto& x : ev) cudaEventDestroy(x);
-    for (auto g : gs) cudaGraphExecDestroy(g);
-    if (back) cudaGraphExecDestroy(back);
+    for (auto& g : gs) g.destroy();
+    cudaEventDestroy(proto);
     e->blocks += blocks;
-    e->h_done[0] = (uint32_t)e->blocks;
-    e->h_done[16] = (uint32_t)e->blocks;
   });
 }
 
@@ -922,8 +979,70 @@ int aura_b200_profile_phases(aura_b200_engine* e, size_t blocks, float* phase_us
     for (auto& x : ev) cudaEventDestroy(x);
     *n_phases = np;
     e->blocks += blocks;
-    e->h_done[0] = (uint32_t)e->blocks;
-    e->h_done[16] = (uint32_t)e->blocks;
+  });
+}
+
+int aura_b200_time_phase(aura_b200_engine* e, int phase, size_t reps, float* avg_us) {
+  return guarded([&] {
+    if (phase != PH_MAC_PRE && phase != PH_FRONT && phase != PH_TAIL_PRE)
+      fail(AURA_B200_E_INVALID_ARGUMENT, "only idempotent phases can be re-launched");
+    CK(cudaSetDevice(e->device));
+    CK(cudaStreamSynchronize(e->stream));
+    BlockArgs a = e->dev_args;
+    e->launch_phase(phase, a, e->stream);  // warm
+    cudaEvent_t t0, t1;
+    CK(cudaEventCreate(&t0));
+    CK(cudaEventCreate(&t1));
+    CK(cudaEventRecord(t0, e->stream));
+    for (size_t r = 0; r < reps; ++r) e->launch_phase(phase, a, e->stream);
+    CK(cudaEventRecord(t1, e->stream));
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(e->stream));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, t0, t1));
+    cudaEventDestroy(t0);
+    cudaEventDestroy(t1);
+    *avg_us = 1000.0f * ms / (float)reps;
+  });
+}
+
+int aura_b200_trace_blocks(aura_b200_engine* e, size_t blocks, double* out) {
+  return guarded([&] {
+    CK(cudaSetDevice(e->device));
+    CK(cudaStreamSynchronize(e->stream));
+    blocks = std::min<size_t>(blocks, kTraceBlocks);
+    const size_t words = (size_t)kTraceBlocks * kTraceKernels * 2;
+    std::vector<unsigned long long> init(words);
+    for (size_t i = 0; i < words; i += 2) {
+      init[i] = ~0ull;
+      init[i + 1] = 0ull;
+    }
+    unsigned long long* dtr = nullptr;
+    CK(cudaMalloc(&dtr, words * sizeof(unsigned long long)));
+    CK(cudaMemcpy(dtr, init.data(), words * sizeof(unsigned long long), cudaMemcpyHostToDevice));
+    BlockArgs a = e->dev_args;
+    a.trace = dtr;
+    auto g = e->capture_block(a, nullptr);
+    const uint64_t first = e->blocks;
+    for (size_t i = 0; i < blocks; ++i) CK(cudaGraphLaunch(g.ex, e->stream));
+    CK(cudaStreamSynchronize(e->stream));
+    std::vector<unsigned long long> tr(words);
+    CK(cudaMemcpy(tr.data(), dtr, words * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    cudaFree(dtr);
+    g.destroy();
+    // out[i][k][2]: start/end in microseconds relative to block i's front start
+    for (size_t i = 0; i < blocks; ++i) {
+      const size_t slot = (first + i) % kTraceBlocks;
+      const unsigned long long t0 = tr[(slot * kTraceKernels + TR_FRONT) * 2];
+      for (int k = 0; k < kTraceKernels; ++k) {
+        const unsigned long long s0 = tr[(slot * kTraceKernels + k) * 2];
+        const unsigned long long s1 = tr[(slot * kTraceKernels + k) * 2 + 1];
+        const bool ran = s0 != ~0ull;
+        out[(i * kTraceKernels + k) * 2] = ran ? (double)(long long)(s0 - t0) * 1e-3 : -1.0;
+        out[(i * kTraceKernels + k) * 2 + 1] = ran ? (double)(long long)(s1 - t0) * 1e-3 : -1.0;
+      }
+    }
+    e->blocks += blocks;
   });
 }
 
@@ -932,6 +1051,7 @@ const char* aura_b200_phase_name(const aura_b200_engine*, int phase) {
 }
 
 double aura_b200_phase_bytes(const aura_b200_engine* e, int phase) { return e->phase_bytes(phase); }
+int aura_b200_launches_per_block(const aura_b200_engine* e) { return e->launches_per_block(); }
 
 int aura_b200_describe(const aura_b200_engine* e, char* buf, size_t cap) {
   return guarded([&] {

@@ -1,31 +1,37 @@
 // kernels.cuh -- the per-block UPOLS + feedback-canceller kernels (sm_100a).
 //
-// Block n runs as two CUDA graphs on one stream.
+// Block n runs as two CUDA graphs on one stream; completion is observed by
+// the host through stream events (no system-scope fences inside kernels).
 //
 //  FRONT (the latency-critical path, one kernel):
-//   k_front      m~ = g m - f^ (auralizer.hpp:73-76), window + r2c of every
-//                input (convolver.hpp:180-191), FDL push, then per output
-//                channel  Y_l = S_l + sum_q X_q,n (.) H_{l,q}[0],  c2r +
-//                overlap-save straight into the (mapped) output. The last CTA
-//                publishes the host-visible "output ready" word. After that
-//                point each CTA also does the canceller's stage 1 on its l_n
-//                (r2c, canceller-FDL push, power) and the NLMS error spectra.
+//   k_front       m~ = g m - f^ (auralizer.hpp:73-76), window + r2c of every
+//                 input (convolver.hpp:180-191), FDL push, then per output
+//                 channel  Y_l = S_l + sum_q X_q,n (.) H_{l,q}[0],  c2r +
+//                 overlap-save straight into the (mapped) output buffer.
 //
-//  BACK (off the critical path, two concurrent branches):
-//   k_mac_pre  -> k_tail_pre   S_l for block n+1 = sum_{j=0}^{K-2}
-//                              X(age j) (.) H_l[j+1]: every partition except
-//                              partition 0 depends only on inputs up to n.
-//   k_mac_afc  -> k_tail_afc   canceller MAC with the fused NLMS update,
-//                              one c2r per mic -> f^ for block n+1.
+//  BACK (off the critical path; two concurrent branches, then k_advance):
+//   branch 1: k_mac_pre -> k_tail_pre
+//                 S_l for block n+1 = sum_{j=0}^{K-2} X(age j) (.) H_l[j+1]:
+//                 every partition but the first depends only on inputs <= n.
+//   branch 2: k_back_head -> k_mac_afc -> k_tail_afc
+//                 canceller stage 1 on l_n (r2c, FDL push, power), NLMS error
+//                 spectra, canceller MAC with the fused NLMS update, one c2r
+//                 per mic -> f^ for block n+1.
+//   The last CTA of the two branch tails advances the block counter
+//   (k_advance only when a block has no tail kernels).
 //
 // So the output of block n is c2r(X_n H_0 + sum_{k>=1} X_{n-k} H_k), exactly
 // the reference's accumulator (backend.hpp:212-235) with the partition sum
 // split in two; the work per block is unchanged, only its position in time.
-// All reductions run in a fixed order: results are bit-reproducible run to
-// run (test_convolver.cpp:172-193).
+// All reductions run in a fixed order -- split-K partials are combined by
+// 8-CTA thread-block clusters through distributed shared memory in rank
+// order -- so results are bit-reproducible run to run
+// (test_convolver.cpp:172-193).
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+
+#include <cooperative_groups.h>
 
 #include "fft.cuh"
 
@@ -34,15 +40,22 @@ namespace aura_b200 {
 constexpr int kMacThreads = 256;
 constexpr int kTailThreads = 256;
 constexpr int kFrontThreads = 256;
+constexpr int kRedCluster = 8;  // CTAs per split-K reduction cluster
 
-// Device-resident stream state. `block` = index of the next block the FRONT
-// will process; the background of block n reads block - 1.
+// Device-resident stream state: index of the block in flight. Every kernel
+// of block n (front and background) reads it; the last CTA of the
+// background's tail kernels (ticket) moves it to n + 1.
 struct DevState {
   uint32_t block;
-  uint32_t front_ticket;
-  uint32_t back_ticket;
-  uint32_t pad;
+  uint32_t ticket;
+  uint32_t pad[2];
 };
+
+// Optional timeline trace (%globaltimer, ns): per traced block slot and
+// kernel, the earliest CTA start and the latest CTA end.
+constexpr int kTraceBlocks = 64;
+constexpr int kTraceKernels = 8;
+enum TraceId { TR_FRONT = 0, TR_MAC_PRE, TR_TAIL_PRE, TR_BACK_HEAD, TR_MAC_AFC, TR_TAIL_AFC };
 
 struct BlockArgs {
   // geometry
@@ -53,7 +66,8 @@ struct BlockArgs {
   int is_aur, nlms;
   float gain, mu, lambda, delta;
   int cpb;           // output channels per front CTA
-  int back_total;    // CTAs of the background's final kernels
+  int advance_total; // CTAs of the tail kernels that retire the block (ticket)
+  unsigned long long* trace;  // [kTraceBlocks][kTraceKernels][2] or null
   // split-K geometry
   int syn_chunks, syn_tc, syn_nft, syn_tiles;
   int afc_chunks, afc_uc, afc_nft, afc_tiles;
@@ -63,8 +77,10 @@ struct BlockArgs {
   // state
   DevState* st;
   float* prev_in;       // Qx x N    previous input block (after g m - f^)
+  float* cur_mt;        // Q x N     this block's m~ (front -> background)
   float4* X;            // input FDL [Qx][K][NF]
   const float4* H;      // spectra   [L][Qh][K][NF] (Qh = Q for mimo, else 1)
+  const float4* H0;     // partition 0 of every row, contiguous [L][Qh][NF]
   float4* S;            // [L][NF]   precomputed partitions >= 1 for next block
   float4* part_syn;     // [syn_chunks][L][NF]
   float* prev_spk;      // L x N     previous loudspeaker block
@@ -80,8 +96,6 @@ struct BlockArgs {
   // I/O (device pointers; may alias pinned mapped host memory)
   const float* in;      // Qx x N
   float* out;           // L x N
-  volatile uint32_t* done;       // mapped: sequence of the last output ready
-  volatile uint32_t* back_done;  // mapped: sequence of the last finished block
 };
 
 // ---------------------------------------------------------------- helpers
@@ -174,25 +188,62 @@ __device__ void reduce_partials(const float4* __restrict__ part, int nc, size_t 
   }
 }
 
-// Background retirement: the last CTA of the background's final kernels
-// publishes the finished block sequence (f^ and S for block n+1 are ready).
-__device__ void retire_back(const BlockArgs& a, uint32_t n) {
-  __threadfence_system();
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void trace_begin(const BlockArgs& a, int id, uint32_t n) {
+  if (a.trace && threadIdx.x == 0)
+    atomicMin(&a.trace[((n % kTraceBlocks) * kTraceKernels + id) * 2], globaltimer());
+}
+__device__ __forceinline__ void trace_end(const BlockArgs& a, int id, uint32_t n) {
+  if (a.trace) {
+    __syncthreads();
+    if (threadIdx.x == 0)
+      atomicMax(&a.trace[((n % kTraceBlocks) * kTraceKernels + id) * 2 + 1], globaltimer());
+  }
+}
+// Last CTA of the background's tail kernels advances the block counter.
+// Device scope suffices: every reader of st->block for block n has read it
+// before its CTA reached this point, and the next block's front is
+// stream-ordered after the whole background graph.
+__device__ void retire_block(const BlockArgs& a, uint32_t n) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    const uint32_t t = atomicAdd(&a.st->back_ticket, 1u);
-    if (t == (uint32_t)a.back_total - 1) {
-      a.st->back_ticket = 0;
-      __threadfence_system();
-      *a.back_done = n + 1;
+    if (atomicAdd(&a.st->ticket, 1u) == (uint32_t)a.advance_total - 1) {
+      a.st->ticket = 0;
+      a.st->block = n + 1;
     }
   }
+}
+
+// Split-K reduction by one 8-CTA cluster: CTA `rank` sums chunks rank,
+// rank+8, ... into its shared `mine`; after a cluster barrier rank 0 adds
+// the eight vectors in rank order through distributed shared memory into
+// `out`. Deterministic; every CTA of the cluster must call it.
+__device__ void cluster_reduce(const float4* __restrict__ part, int nc, size_t stride, int NF,
+                               float4* red, float4* mine, float4* out) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = (int)cluster.block_rank();
+  const int mine_nc = nc > rank ? (nc - rank + kRedCluster - 1) / kRedCluster : 0;
+  reduce_partials(part + (size_t)rank * stride, mine_nc, stride * kRedCluster, NF, red, mine);
+  cluster.sync();
+  if (rank == 0) {
+    for (int f = threadIdx.x; f < NF; f += blockDim.x) {
+      float4 t = mine[f];
+      for (int r = 1; r < kRedCluster; ++r) t = f4add(t, cluster.map_shared_rank(mine, r)[f]);
+      out[f] = t;
+    }
+  }
+  cluster.sync();
 }
 
 // ------------------------------------------------------------- k_front
 // grid = ceil(L / cpb), 256 threads; elementwise CTAs also own their
 // channels' inputs. Shared: Qs input spectra (N float2 each), FFT scratch z
-// (N float2), window/accumulator (2N floats), m~ (Qs x N floats).
+// (N float2), window/accumulator (2N floats).
 __global__ void __launch_bounds__(kFrontThreads) k_front(BlockArgs a) {
   extern __shared__ float4 smem4[];
   const int N = a.N, NF = a.NF;
@@ -202,10 +253,9 @@ __global__ void __launch_bounds__(kFrontThreads) k_front(BlockArgs a) {
   float2* z = Xs + (size_t)Qs * N;                        // N
   float* wa = reinterpret_cast<float*>(z + N);            // 2N (window / acc)
   float2* acc = reinterpret_cast<float2*>(wa);
-  float* mts = wa + 2 * N;                                // Qs x N
-  __shared__ uint32_t s_last;
 
   const uint32_t n = a.st->block;
+  trace_begin(a, TR_FRONT, n);
   const int c0 = blockIdx.x * a.cpb;
   const int c1 = min(c0 + a.cpb, a.L);
   const int Qh = a.mode == 2 ? a.Q : 1;
@@ -218,7 +268,7 @@ __global__ void __launch_bounds__(kFrontThreads) k_front(BlockArgs a) {
       for (int i = threadIdx.x; i < N; i += blockDim.x) {
         float v = in[i];
         if (a.is_aur) v = __fsub_rn(__fmul_rn(a.gain, v), a.fhat[(size_t)q * N + i]);
-        mts[q * N + i] = v;
+        if (blockIdx.x == 0) a.cur_mt[(size_t)q * N + i] = v;
         wa[i] = prev[i];
         wa[N + i] = v;
       }
@@ -250,8 +300,7 @@ __global__ void __launch_bounds__(kFrontThreads) k_front(BlockArgs a) {
     for (int j = threadIdx.x; j < N; j += blockDim.x) {
       float2 y = Sl[j];
       for (int q = 0; q < Qs; ++q) {
-        const float2 h = reinterpret_cast<const float2*>(
-            a.H + (((size_t)l * Qh + q) * a.K) * NF)[j];
+        const float2 h = reinterpret_cast<const float2*>(a.H0 + ((size_t)l * Qh + q) * NF)[j];
         y = cmac2(y, Xs[(size_t)q * N + j], h, j == 0);
       }
       acc[j] = y;
@@ -265,43 +314,40 @@ __global__ void __launch_bounds__(kFrontThreads) k_front(BlockArgs a) {
       if (keep) sp[i] = v;
     });
   }
+  trace_end(a, TR_FRONT, n);
+}
 
-  // ---- publish: the last CTA raises "output ready" for block n
-  __threadfence_system();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const uint32_t t = atomicAdd(&a.st->front_ticket, 1u);
-    s_last = (t == gridDim.x - 1);
+// ---------------------------------------------------------- k_back_head
+// Background of block n, canceller branch head. CTA l < L (auralizer):
+// canceller stage 1 on l_n (convolver.hpp:180-191 on fc_) and the packed
+// power |X_l|^2; CTAs [Lb, Lb + P): NLMS error spectra E_p = r2c([0_N,
+// m~_p]) (Appendix A step 2). CTA 0 also moves this block's m~ into the
+// input window history (broadcast / mimo).
+__global__ void __launch_bounds__(kFrontThreads) k_back_head(BlockArgs a) {
+  extern __shared__ float4 smem4[];
+  const int N = a.N, NF = a.NF;
+  float2* z = reinterpret_cast<float2*>(smem4);  // N
+  float* wa = reinterpret_cast<float*>(z + N);   // 2N
+  const uint32_t n = a.st->block;
+  trace_begin(a, TR_BACK_HEAD, n);
+  const int Lb = a.is_aur ? a.L : 1;
+  const int b = blockIdx.x;
+  if (b == 0 && a.mode != 1)
+    for (int i = threadIdx.x; i < a.Q * N; i += blockDim.x) a.prev_in[i] = a.cur_mt[i];
+  if (!a.is_aur) {
+    trace_end(a, TR_BACK_HEAD, n);
+    return;
   }
-  __syncthreads();
-  if (s_last) {
-    // every CTA has read prev_in / st->block: safe to advance them
-    if (!elem)
-      for (int q = 0; q < Qs; ++q)
-        for (int i = threadIdx.x; i < N; i += blockDim.x)
-          a.prev_in[(size_t)q * N + i] = mts[q * N + i];
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      a.st->front_ticket = 0;
-      a.st->block = n + 1;
-      __threadfence_system();
-      *a.done = n + 1;
-      if (a.back_total == 0) *a.back_done = n + 1;
-    }
-  }
-  if (!a.is_aur) return;
-
-  // ---- canceller stage 1 on l_n (convolver.hpp:180-191 on fc_) + power
-  for (int l = c0; l < c1; ++l) {
+  if (b < Lb) {
+    const int l = b;
     float* prev = a.prev_spk + (size_t)l * N;
     const float* sp = a.spk + (size_t)l * N;
-    __syncthreads();
     for (int i = threadIdx.x; i < N; i += blockDim.x) {
       wa[i] = prev[i];
       wa[N + i] = sp[i];
-      prev[i] = sp[i];
     }
     __syncthreads();
+    for (int i = threadIdx.x; i < N; i += blockDim.x) prev[i] = wa[N + i];
     float2* xnew = reinterpret_cast<float2*>(
         a.XA + ((size_t)l * (a.KF + 1) + n % (uint32_t)(a.KF + 1)) * NF);
     rfft_packed(wa, z, xnew, N, a.logN, a.tw, a.split);
@@ -318,21 +364,21 @@ __global__ void __launch_bounds__(kFrontThreads) k_front(BlockArgs a) {
         a.pw_part[(size_t)l * N + j] = p;
       }
     }
-  }
-  // ---- NLMS error spectra E_p = r2c([0_N, m~_p]) (Appendix A step 2)
-  if (a.nlms) {
-    for (int p = blockIdx.x; p < a.P; p += gridDim.x) {
-      __syncthreads();
-      for (int i = threadIdx.x; i < N; i += blockDim.x) {
-        wa[i] = 0.0f;
-        wa[N + i] = mts[(size_t)p * N + i];
-      }
-      __syncthreads();
-      rfft_packed(wa, z, reinterpret_cast<float2*>(a.E + (size_t)p * NF), N, a.logN, a.tw,
-                  a.split);
+  } else {
+    const int p = b - Lb;
+    for (int i = threadIdx.x; i < N; i += blockDim.x) {
+      wa[i] = 0.0f;
+      wa[N + i] = a.cur_mt[(size_t)p * N + i];
     }
+    __syncthreads();
+    rfft_packed(wa, z, reinterpret_cast<float2*>(a.E + (size_t)p * NF), N, a.logN, a.tw,
+                a.split);
   }
+  trace_end(a, TR_BACK_HEAD, n);
 }
+
+// ------------------------------------------------------------ k_advance
+__global__ void k_advance(DevState* st) { st->block += 1u; }  // blocks without tails
 
 // ------------------------------------------------------------ k_mac_pre
 // Split-K partials of S_l(n+1) = sum_q sum_{j=0}^{K-2} X_q(age j) H_{l,q}[j+1]
@@ -356,7 +402,9 @@ __global__ void __launch_bounds__(kMacThreads, 2) k_mac_pre(BlockArgs a) {
   const int T = Qh * Kt;
   const int t0 = blockIdx.x * a.syn_tc;
   const int t1 = min(t0 + a.syn_tc, T);
-  const int nk = (int)((a.st->block - 1u) % (uint32_t)K);
+  const uint32_t n = a.st->block;
+  trace_begin(a, TR_MAC_PRE, n);
+  const int nk = (int)(n % (uint32_t)K);
   const bool dc = (f == 0);
   const int NF = a.NF;
 
@@ -403,19 +451,27 @@ __global__ void __launch_bounds__(kMacThreads, 2) k_mac_pre(BlockArgs a) {
     for (int p = 1; p < KP; ++p) s = f4add(s, red[(p * LT + i) * nft + c]);
     a.part_syn[((size_t)blockIdx.x * a.L + l0 + i) * NF + blockIdx.z * nft + c] = s;
   }
+  trace_end(a, TR_MAC_PRE, n);
 }
 
 // ----------------------------------------------------------- k_tail_pre
-// One CTA per output channel: S_l = fixed-order sum of the split-K partials.
-__global__ void __launch_bounds__(kTailThreads) k_tail_pre(BlockArgs a) {
+// One 8-CTA cluster per output channel: S_l = fixed-order sum of the split-K
+// partials (cluster_reduce). grid = 8 L.
+__global__ void __cluster_dims__(kRedCluster, 1, 1) __launch_bounds__(kTailThreads)
+    k_tail_pre(BlockArgs a) {
   extern __shared__ float4 sm4[];
   const int NF = a.NF;
-  float4* red = sm4;
-  float4* acc = red + blockDim.x;
-  const int l = blockIdx.x;
-  reduce_partials(a.part_syn + (size_t)l * NF, a.syn_chunks, (size_t)a.L * NF, NF, red, acc);
-  for (int f = threadIdx.x; f < NF; f += blockDim.x) a.S[(size_t)l * NF + f] = acc[f];
-  retire_back(a, a.st->block - 1u);
+  float4* red = sm4;                 // blockDim
+  float4* mine = red + blockDim.x;   // NF
+  float4* acc = mine + NF;           // NF
+  const int l = blockIdx.x / kRedCluster;
+  const uint32_t n = a.st->block;
+  trace_begin(a, TR_TAIL_PRE, n);
+  cluster_reduce(a.part_syn + (size_t)l * NF, a.syn_chunks, (size_t)a.L * NF, NF, red, mine, acc);
+  if (blockIdx.x % kRedCluster == 0)
+    for (int f = threadIdx.x; f < NF; f += blockDim.x) a.S[(size_t)l * NF + f] = acc[f];
+  trace_end(a, TR_TAIL_PRE, n);
+  retire_block(a, n);
 }
 
 // ----------------------------------------------------------- k_mac_afc
@@ -437,7 +493,9 @@ __global__ void __launch_bounds__(kMacThreads, 2) k_mac_afc(BlockArgs a) {
   const int U = L * KF;
   const int u0 = blockIdx.x * a.afc_uc;
   const int u1 = min(u0 + a.afc_uc, U);
-  const int nk = (int)((a.st->block - 1u) % (uint32_t)cap);
+  const uint32_t n = a.st->block;
+  trace_begin(a, TR_MAC_AFC, n);
+  const int nk = (int)(n % (uint32_t)cap);
   const bool dc = (f == 0);
 
   float4 acc[PT];
@@ -505,33 +563,52 @@ __global__ void __launch_bounds__(kMacThreads, 2) k_mac_afc(BlockArgs a) {
     for (int r = 1; r < KP; ++r) t = f4add(t, red[(r * PT + p) * nft + c]);
     a.part_afc[((size_t)blockIdx.x * P + p) * NF + blockIdx.z * nft + c] = t;
   }
+  trace_end(a, TR_MAC_AFC, n);
 }
 
 // ---------------------------------------------------------- k_tail_afc
-// One CTA per mic p: fixed-order reduce over chunks (the sum over l and k is
-// done in the frequency domain -- one c2r per mic instead of the
-// reference's L, auralizer.hpp:81-86), c2r -> f^_p for the next block.
-// CTA 0 also advances the NLMS power (Appendix A step 5).
-__global__ void __launch_bounds__(kTailThreads) k_tail_afc(BlockArgs a) {
+// One 8-CTA cluster per mic p: fixed-order reduce over chunks (the sum over
+// l and k is done in the frequency domain -- one c2r per mic instead of the
+// reference's L, auralizer.hpp:81-86), c2r -> f^_p for the next block, on
+// rank 0. Rank 1 of mic 0's cluster advances the NLMS power (Appendix A
+// step 5). grid = 8 P.
+__global__ void __cluster_dims__(kRedCluster, 1, 1) __launch_bounds__(kTailThreads)
+    k_tail_afc(BlockArgs a) {
   extern __shared__ float4 sm4[];
   const int N = a.N, NF = a.NF;
   float4* red = sm4;
-  float4* acc = red + blockDim.x;
+  float4* mine = red + blockDim.x;
+  float4* acc = mine + NF;
   float2* z = reinterpret_cast<float2*>(acc + NF);
-  const int p = blockIdx.x;
-  const uint32_t n = a.st->block - 1u;
-  reduce_partials(a.part_afc + (size_t)p * NF, a.afc_chunks, (size_t)a.P * NF, NF, red, acc);
-  float* fh = a.fhat + (size_t)p * N;
-  float* fhh = a.fhat_host + (size_t)p * N;
-  irfft_packed_tail(reinterpret_cast<const float2*>(acc), z, N, a.logN, a.tw, a.split,
-                    [&](int i, float v) {
-                      fh[i] = v;
-                      fhh[i] = v;
-                    });
-  if (a.nlms && p == 0) {
+  const int p = blockIdx.x / kRedCluster;
+  const int rank = blockIdx.x % kRedCluster;
+  const uint32_t n = a.st->block;
+  trace_begin(a, TR_TAIL_AFC, n);
+  cluster_reduce(a.part_afc + (size_t)p * NF, a.afc_chunks, (size_t)a.P * NF, NF, red, mine, acc);
+  if (rank == 0) {
+    float* fh = a.fhat + (size_t)p * N;
+    float* fhh = a.fhat_host + (size_t)p * N;
+    irfft_packed_tail(reinterpret_cast<const float2*>(acc), z, N, a.logN, a.tw, a.split,
+                      [&](int i, float v) {
+                        fh[i] = v;
+                        fhh[i] = v;
+                      });
+  } else if (rank == 1 && p == 0 && a.nlms) {
     for (int j = threadIdx.x; j < N; j += blockDim.x) {
+      // sum over l in ascending order (as the oracle); loads batched by 8
       float2 sum = make_float2(0.f, 0.f);
-      for (int ll = 0; ll < a.L; ++ll) {
+      int ll = 0;
+      for (; ll + 8 <= a.L; ll += 8) {
+        float2 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = a.pw_part[(size_t)(ll + u) * N + j];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          sum.x = __fadd_rn(sum.x, v[u].x);
+          sum.y = __fadd_rn(sum.y, v[u].y);
+        }
+      }
+      for (; ll < a.L; ++ll) {
         const float2 v = a.pw_part[(size_t)ll * N + j];
         sum.x = __fadd_rn(sum.x, v.x);
         sum.y = __fadd_rn(sum.y, v.y);
@@ -544,7 +621,8 @@ __global__ void __launch_bounds__(kTailThreads) k_tail_afc(BlockArgs a) {
       a.pw[j] = w;
     }
   }
-  retire_back(a, n);
+  trace_end(a, TR_TAIL_AFC, n);
+  retire_block(a, n);
 }
 
 // ------------------------------------------------------ k_partition
