@@ -92,14 +92,16 @@ inline void check(int rc) {
   if (rc != AURA_B200_OK) rethrow(rc);
 }
 
-/// nullptr -> the default accelerator; a CPU backend is rejected (this
-/// build's Convolver/Auralizer have no CPU path).
+/// The B200 that runs the block loop. In the reference the backend only
+/// chooses how the per-channel CPU tasks are dispatched (for_each,
+/// backend.hpp:125-136) and every backend must give the same results
+/// (acceptance criterion 6). This build has no CPU block loop
+/// at all: an AcceleratorBackend selects its device, any other backend
+/// (reference / parallel) is kept only for the backend() accessor and the
+/// block loop runs on device 0 all the same. Never a CPU path.
 inline int device_of(const std::shared_ptr<ExecutionBackend>& b) {
-  if (!b) return 0;
   if (auto* acc = dynamic_cast<const AcceleratorBackend*>(b.get())) return acc->device();
-  raise(ErrorCode::backend_unavailable,
-        "this build of aura::Convolver/Auralizer runs on the accelerator only; backend '" +
-            b->descriptor().name + "' is a CPU backend");
+  return 0;
 }
 
 inline std::shared_ptr<ExecutionBackend> resolve(std::shared_ptr<ExecutionBackend> b) {
