@@ -168,6 +168,28 @@ int aura_b200_afc_coeffs(aura_b200_engine* e, float* out);
  * returns as soon as the block's OUTPUT is ready. */
 int aura_b200_synchronize(aura_b200_engine* e);
 
+/* ---- multi-GPU loudspeaker sharding ---------------- */
+/* An auralizer whose L loudspeakers are split over G engines (one per GPU,
+ * one process per GPU): each engine is created with its contiguous slice of
+ * loudspeaker rows (synth q*L_g + l, fc p*L_g + l) and the SAME mic input.
+ * The canceller output and the NLMS power sum over all loudspeakers, so the
+ * shards exchange P*N + 2N floats per block over NVLink (k_afc_finish: P2P
+ * stores + system-scope flags, fixed rank-order sum, identical on every
+ * shard). Convolvers need no exchange: their shards are independent.
+ * Protocol: every rank calls shard_export, the G handles are all-gathered
+ * by the host (torch.distributed is the plumbing), every rank calls
+ * shard_connect; then all ranks process the same block sequence. reset()
+ * must be called on every shard between two host barriers. */
+#define AURA_B200_SHARD_HANDLE_BYTES 64
+/* Allocate the exchange buffer; writes its CUDA IPC handle (64 bytes). */
+int aura_b200_shard_export(aura_b200_engine* e, int world, int rank, void* handle);
+/* handles: world x 64 bytes in rank order (own entry ignored). */
+int aura_b200_shard_connect(aura_b200_engine* e, const void* handles);
+/* Same wiring for G engines living in ONE process (virtual shards on one
+ * GPU, or several GPUs of one process through P2P); engine g is rank g. */
+int aura_b200_shard_connect_local(aura_b200_engine* const* engines, int world);
+int aura_b200_shard_info(const aura_b200_engine* e, int* world, int* rank);
+
 /* ---- measurement (bench.py; not part of the reference API) ----------- */
 /* Run `blocks` blocks back to back with device-resident I/O (inputs already
  * in HBM, uploaded from host_in: n_in_blocks x inputs x N floats, cycled),

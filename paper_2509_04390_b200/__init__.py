@@ -308,7 +308,7 @@ class _Engine:
         _check(lib().aura_b200_reset(self._h))
 
     TRACE_KERNELS = ("k_front", "k_mac_pre", "k_tail_pre", "k_back_head", "k_mac_afc",
-                     "k_tail_afc")
+                     "k_tail_afc", "k_afc_finish")
 
     def trace_blocks(self, blocks: int = 32):
         """Per-kernel [start, end] (us from the block's front start) of

@@ -106,11 +106,12 @@ T* dalloc(size_t count, std::vector<void*>& owned) {
 }  // namespace
 
 enum Phase {
-  PH_FRONT = 0, PH_MAC_PRE, PH_TAIL_PRE, PH_BACK_HEAD, PH_MAC_AFC, PH_TAIL_AFC, PH_ADVANCE,
-  PH_COUNT
+  PH_FRONT = 0, PH_MAC_PRE, PH_TAIL_PRE, PH_BACK_HEAD, PH_MAC_AFC, PH_TAIL_AFC, PH_AFC_FINISH,
+  PH_ADVANCE, PH_COUNT
 };
-static const char* kPhaseNames[PH_COUNT] = {"k_front", "k_mac_pre", "k_tail_pre", "k_back_head",
-                                            "k_mac_afc", "k_tail_afc", "k_advance"};
+static const char* kPhaseNames[PH_COUNT] = {"k_front",   "k_mac_pre",  "k_tail_pre",
+                                            "k_back_head", "k_mac_afc", "k_tail_afc",
+                                            "k_afc_finish", "k_advance"};
 
 struct aura_b200_engine {
   int device = 0;
@@ -148,6 +149,12 @@ struct aura_b200_engine {
   };
   BlockGraph g_block;
   int prio_high = 0;  // stream priority of the canceller branch
+  // sharding: shard grank of G; xbuf = own exchange buffer
+  int G = 1, grank = 0;
+  char* xbuf = nullptr;
+  size_t xbuf_bytes = 0;
+  std::vector<void*> ipc_opened;  // peer buffers opened through CUDA IPC
+  unsigned* h_status = nullptr;   // mapped pinned; set by k_afc_finish on timeout
   size_t smem_front = 0, smem_tail = 0, smem_head = 0;
 
   ~aura_b200_engine() {
@@ -158,6 +165,8 @@ struct aura_b200_engine {
     if (h_in) cudaFreeHost(h_in);
     if (h_out) cudaFreeHost(h_out);
     if (h_fhat) cudaFreeHost(h_fhat);
+    if (h_status) cudaFreeHost(h_status);
+    for (void* p : ipc_opened) cudaIpcCloseMemHandle(p);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     if (ev_front) cudaEventDestroy(ev_front);
@@ -168,6 +177,7 @@ struct aura_b200_engine {
 
   bool has_pre() const { return K > 1; }
   bool has_head() const { return aur || mode != AURA_B200_ELEMENTWISE; }
+  bool sharded() const { return aur && G > 1; }
 
   // cudaLaunchKernelEx with an explicit scheduling priority (captured into
   // the graph's kernel nodes): the canceller branch runs at high priority so
@@ -234,6 +244,9 @@ struct aura_b200_engine {
           launch(k_tail_afc, dim3((unsigned)(kRedCluster * P)), dim3(kTailThreads), smem_tail, s, hp,
                  a);
         break;
+      case PH_AFC_FINISH:
+        if (sharded()) launch(k_afc_finish, dim3(1), dim3(kTailThreads), 0, s, hp, a);
+        break;
       case PH_ADVANCE:
         if (a.advance_total == 0) k_advance<<<1, 1, 0, s>>>(a.st);
         break;
@@ -243,7 +256,7 @@ struct aura_b200_engine {
   // kernels launched per block (front + background)
   int launches_per_block() const {
     return 1 + (args.advance_total == 0 ? 1 : 0) + (has_pre() ? 2 : 0) + (has_head() ? 1 : 0) +
-           (aur ? 2 : 0);
+           (aur ? 2 : 0) + (sharded() ? 1 : 0);
   }
 
   cudaGraphExec_t instantiate(cudaGraph_t g) {
@@ -266,6 +279,7 @@ struct aura_b200_engine {
     launch_phase(PH_BACK_HEAD, a, side);
     launch_phase(PH_MAC_AFC, a, side);
     launch_phase(PH_TAIL_AFC, a, side);
+    launch_phase(PH_AFC_FINISH, a, side);
     CK(cudaEventRecord(ev_join, side));
     launch_phase(PH_MAC_PRE, a, stream);
     launch_phase(PH_TAIL_PRE, a, stream);
@@ -305,6 +319,8 @@ struct aura_b200_engine {
         return aur ? row * ((double)P * L * KF * (1.0 + (args.nlms ? 1.0 : 0.0)) + (double)L * KF)
                    : 0.0;
       case PH_TAIL_AFC: return aur ? row * (double)args.afc_chunks * P + 4.0 * N * P : 0.0;
+      case PH_AFC_FINISH:  // push P*N + 2N floats to G shards, read G slots
+        return sharded() ? 2.0 * G * 4.0 * (double)(P * N + 2 * N) : 0.0;
       case PH_BACK_HEAD: return aur ? (row + 8.0 * N) * L + row * P : 4.0 * N * Qx;
     }
     return 0.0;
@@ -422,6 +438,14 @@ void common_init(aura_b200_engine* e, int device) {
   CK(cudaEventCreateWithFlags(&e->ev_back, cudaEventDisableTiming));
 }
 
+// CTAs that tick the block ticket (retire_block): every tail CTA, or with
+// sharding the single k_afc_finish CTA in place of the canceller tails.
+void set_advance_total(aura_b200_engine* e) {
+  BlockArgs& a = e->args;
+  a.advance_total = (int)((e->has_pre() ? kRedCluster * e->L : 0) +
+                          (e->aur ? (e->sharded() ? 1 : kRedCluster * e->P) : 0));
+}
+
 void finish_init(aura_b200_engine* e) {
   BlockArgs& a = e->args;
   const size_t N = e->N, NF = N / 2;
@@ -435,6 +459,11 @@ void finish_init(aura_b200_engine* e) {
   CK(cudaHostAlloc(&e->h_out, e->L * N * sizeof(float), cudaHostAllocMapped | cudaHostAllocPortable));
   std::memset(e->h_in, 0, in_ch * N * sizeof(float));
   std::memset(e->h_out, 0, e->L * N * sizeof(float));
+  CK(cudaHostAlloc(&e->h_status, sizeof(unsigned), cudaHostAllocMapped | cudaHostAllocPortable));
+  *e->h_status = 0;
+  CK(cudaHostGetDevicePointer((void**)&a.status_host, e->h_status, 0));
+  a.G = 1;
+  a.grank = 0;
   if (e->aur) {
     CK(cudaHostAlloc(&e->h_fhat, e->P * N * sizeof(float), cudaHostAllocMapped | cudaHostAllocPortable));
     std::memset(e->h_fhat, 0, e->P * N * sizeof(float));
@@ -456,7 +485,7 @@ void finish_init(aura_b200_engine* e) {
                     e->L * Qh, cudaMemcpyDeviceToDevice));
     a.H0 = h0;
   }
-  a.advance_total = (int)((e->has_pre() ? kRedCluster * e->L : 0) + (e->aur ? kRedCluster * e->P : 0));
+  set_advance_total(e);
   // front: one CTA per cpb output channels
   a.cpb = (int)std::max<size_t>(1, (e->L + kSMs - 1) / kSMs);
   const size_t Qs = e->mode == AURA_B200_ELEMENTWISE ? 1 : e->Q;
@@ -499,6 +528,9 @@ void reset_state(aura_b200_engine* e) {
     CK(cudaMemsetAsync(a.pw_part, 0, sizeof(float2) * e->L * N, s));
     if (a.nlms)
       CK(cudaMemcpyAsync(a.W, e->W0, sizeof(float4) * e->w_elems, cudaMemcpyDeviceToDevice, s));
+    // sharded: the caller resets every shard between two barriers (no block
+    // in flight anywhere), so zeroing the own flags restarts the sequence
+    if (e->xbuf) CK(cudaMemsetAsync(e->xbuf, 0, e->xbuf_bytes, s));
   }
   CK(cudaStreamSynchronize(s));
   e->blocks = 0;
@@ -747,6 +779,8 @@ int aura_b200_process(aura_b200_engine* e, const float* in, float* out) {
     for (size_t i = 0; i < n_in; ++i)
       if (!std::isfinite(in[i])) fail(AURA_B200_E_NON_FINITE_INPUT, "input contains NaN or Inf");
     CK(cudaSetDevice(e->device));
+    if (e->h_status && *reinterpret_cast<volatile unsigned*>(e->h_status))
+      fail(AURA_B200_E_TIMEOUT, "a shard peer missed the canceller exchange deadline");
     // the previous block's front has completed, so the staging buffer is free
     std::memcpy(e->h_in, in, n_in * sizeof(float));
     std::atomic_thread_fence(std::memory_order_release);
@@ -866,6 +900,111 @@ int aura_b200_afc_coeffs(aura_b200_engine* e, float* out) {
     CK(cudaMemcpy(buf.data(), e->args.W, sizeof(float4) * e->w_elems, cudaMemcpyDeviceToHost));
     const size_t rows = e->P * e->L * e->KF;
     for (size_t r = 0; r < rows; ++r) unpack_row(buf.data() + r * e->N, e->N, out + r * 2 * (e->N + 1));
+  });
+}
+
+// ----------------------------------------------------------- sharding
+namespace {
+
+void shard_alloc(aura_b200_engine* e, int world, int rank) {
+  if (!e->aur)
+    fail(AURA_B200_E_INVALID_ARGUMENT,
+         "only a feedback canceller exchanges data between shards (convolver shards are independent)");
+  if (world < 2 || world > kMaxShards || rank < 0 || rank >= world)
+    fail(AURA_B200_E_INVALID_ARGUMENT, "shard world must be 2..8 and 0 <= rank < world");
+  if (e->xbuf) fail(AURA_B200_E_INVALID_ARGUMENT, "engine is already sharded");
+  if (e->blocks) fail(AURA_B200_E_INVALID_ARGUMENT, "shard before the first block");
+  CK(cudaSetDevice(e->device));
+  const size_t S = e->P * e->N + 2 * e->N;
+  e->xbuf_bytes = kXFlagBytes + 2 * (size_t)world * S * sizeof(float);
+  e->xbuf = reinterpret_cast<char*>(dalloc<float>(e->xbuf_bytes / sizeof(float), e->dmem));
+  CK(cudaMemset(e->xbuf, 0, e->xbuf_bytes));
+  e->args.xmine = dalloc<float>(S, e->dmem);
+  CK(cudaMemset(e->args.xmine, 0, S * sizeof(float)));
+  e->G = world;
+  e->grank = rank;
+}
+
+void shard_finalize(aura_b200_engine* e, char* const* peers) {
+  CK(cudaSetDevice(e->device));
+  BlockArgs& a = e->args;
+  a.G = e->G;
+  a.grank = e->grank;
+  for (int g = 0; g < kMaxShards; ++g) a.xpeer[g] = g < e->G ? peers[g] : nullptr;
+  set_advance_total(e);
+  CK(cudaStreamSynchronize(e->stream));
+  e->rebuild_graphs();
+  BlockArgs d = a;
+  d.out = e->d_out;
+  d.in = e->d_in_pool;
+  e->dev_args = d;
+}
+
+}  // namespace
+
+int aura_b200_shard_export(aura_b200_engine* e, int world, int rank, void* handle) {
+  return guarded([&] {
+    if (!e || !handle) fail(AURA_B200_E_INVALID_ARGUMENT, "null argument");
+    shard_alloc(e, world, rank);
+    cudaIpcMemHandle_t h;
+    CK(cudaIpcGetMemHandle(&h, e->xbuf));
+    static_assert(sizeof(h) == AURA_B200_SHARD_HANDLE_BYTES, "IPC handle size");
+    std::memcpy(handle, &h, sizeof h);
+  });
+}
+
+int aura_b200_shard_connect(aura_b200_engine* e, const void* handles) {
+  return guarded([&] {
+    if (!e || !handles) fail(AURA_B200_E_INVALID_ARGUMENT, "null argument");
+    if (!e->xbuf) fail(AURA_B200_E_INVALID_ARGUMENT, "call aura_b200_shard_export first");
+    CK(cudaSetDevice(e->device));
+    std::vector<char*> peers(e->G, nullptr);
+    for (int g = 0; g < e->G; ++g) {
+      if (g == e->grank) {
+        peers[g] = e->xbuf;
+        continue;
+      }
+      cudaIpcMemHandle_t h;
+      std::memcpy(&h, static_cast<const char*>(handles) + (size_t)g * sizeof h, sizeof h);
+      void* p = nullptr;
+      CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+      e->ipc_opened.push_back(p);
+      peers[g] = static_cast<char*>(p);
+    }
+    shard_finalize(e, peers.data());
+  });
+}
+
+int aura_b200_shard_connect_local(aura_b200_engine* const* engines, int world) {
+  return guarded([&] {
+    if (!engines) fail(AURA_B200_E_INVALID_ARGUMENT, "null argument");
+    for (int g = 0; g < world; ++g)
+      if (!engines[g]) fail(AURA_B200_E_INVALID_ARGUMENT, "null engine");
+    for (int g = 0; g < world; ++g) shard_alloc(engines[g], world, g);
+    // engines on different devices of one process reach each other by P2P
+    for (int g = 0; g < world; ++g)
+      for (int h = 0; h < world; ++h) {
+        const int dg = engines[g]->device, dh = engines[h]->device;
+        if (dg == dh) continue;
+        int ok = 0;
+        CK(cudaDeviceCanAccessPeer(&ok, dg, dh));
+        if (!ok) fail(AURA_B200_E_BACKEND_UNAVAILABLE, "devices cannot access each other (no P2P)");
+        CK(cudaSetDevice(dg));
+        const cudaError_t r = cudaDeviceEnablePeerAccess(dh, 0);
+        if (r != cudaErrorPeerAccessAlreadyEnabled) ck(r, "cudaDeviceEnablePeerAccess");
+        cudaGetLastError();
+      }
+    std::vector<char*> peers(world);
+    for (int g = 0; g < world; ++g) peers[g] = engines[g]->xbuf;
+    for (int g = 0; g < world; ++g) shard_finalize(engines[g], peers.data());
+  });
+}
+
+int aura_b200_shard_info(const aura_b200_engine* e, int* world, int* rank) {
+  return guarded([&] {
+    if (!e || !world || !rank) fail(AURA_B200_E_INVALID_ARGUMENT, "null argument");
+    *world = e->G;
+    *rank = e->grank;
   });
 }
 

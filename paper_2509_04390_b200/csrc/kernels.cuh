@@ -55,7 +55,18 @@ struct DevState {
 // kernel, the earliest CTA start and the latest CTA end.
 constexpr int kTraceBlocks = 64;
 constexpr int kTraceKernels = 8;
-enum TraceId { TR_FRONT = 0, TR_MAC_PRE, TR_TAIL_PRE, TR_BACK_HEAD, TR_MAC_AFC, TR_TAIL_AFC };
+enum TraceId {
+  TR_FRONT = 0, TR_MAC_PRE, TR_TAIL_PRE, TR_BACK_HEAD, TR_MAC_AFC, TR_TAIL_AFC, TR_AFC_FINISH
+};
+
+// Loudspeaker-channel sharding: at most kMaxShards engines
+// (one per GPU, or virtual shards on one GPU) exchange their canceller
+// partials every block. Each engine owns an exchange buffer: kMaxShards
+// uint32 flags (flag g = 1 + last block whose partial shard g delivered),
+// padded to kXFlagBytes, then slots[2 parities][G][P*N + 2N] floats.
+constexpr int kMaxShards = 8;
+constexpr size_t kXFlagBytes = 256;
+constexpr unsigned long long kShardTimeoutNs = 5ull * 1000 * 1000 * 1000;
 
 struct BlockArgs {
   // geometry
@@ -93,6 +104,11 @@ struct BlockArgs {
   float4* part_afc;     // [afc_chunks][P][NF]
   float* fhat;          // P x N     feedback estimate for the next block
   float* fhat_host;     // P x N     same, mapped pinned host copy
+  // sharding (G > 1): this engine is shard `grank` of G
+  int G, grank;
+  float* xmine;                 // [P*N + 2N] this shard's partial f^ and power sum
+  char* xpeer[kMaxShards];      // every shard's exchange buffer (xpeer[grank] = own)
+  unsigned* status_host;        // mapped; nonzero when a peer missed the deadline
   // I/O (device pointers; may alias pinned mapped host memory)
   const float* in;      // Qx x N
   float* out;           // L x N
@@ -585,13 +601,15 @@ __global__ void __cluster_dims__(kRedCluster, 1, 1) __launch_bounds__(kTailThrea
   const uint32_t n = a.st->block;
   trace_begin(a, TR_TAIL_AFC, n);
   cluster_reduce(a.part_afc + (size_t)p * NF, a.afc_chunks, (size_t)a.P * NF, NF, red, mine, acc);
+  const bool sharded = a.G > 1;
   if (rank == 0) {
-    float* fh = a.fhat + (size_t)p * N;
+    // sharded: this shard's partial f^_p (c2r is linear), summed by k_afc_finish
+    float* fh = sharded ? a.xmine + (size_t)p * N : a.fhat + (size_t)p * N;
     float* fhh = a.fhat_host + (size_t)p * N;
     irfft_packed_tail(reinterpret_cast<const float2*>(acc), z, N, a.logN, a.tw, a.split,
                       [&](int i, float v) {
                         fh[i] = v;
-                        fhh[i] = v;
+                        if (!sharded) fhh[i] = v;
                       });
   } else if (rank == 1 && p == 0 && a.nlms) {
     for (int j = threadIdx.x; j < N; j += blockDim.x) {
@@ -613,6 +631,10 @@ __global__ void __cluster_dims__(kRedCluster, 1, 1) __launch_bounds__(kTailThrea
         sum.x = __fadd_rn(sum.x, v.x);
         sum.y = __fadd_rn(sum.y, v.y);
       }
+      if (sharded) {  // partial power of this shard's loudspeakers
+        reinterpret_cast<float2*>(a.xmine + (size_t)a.P * N)[j] = sum;
+        continue;
+      }
       // Appendix A step 5, rounded as the oracle: lambda P + (1 - lambda) s
       float2 w = a.pw[j];
       const float oml = __fsub_rn(1.0f, a.lambda);
@@ -622,6 +644,82 @@ __global__ void __cluster_dims__(kRedCluster, 1, 1) __launch_bounds__(kTailThrea
     }
   }
   trace_end(a, TR_TAIL_AFC, n);
+  if (!sharded) retire_block(a, n);
+}
+
+__device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// ------------------------------------------------------- k_afc_finish
+// Sharded canceller (G > 1), one CTA per shard and block: push this shard's
+// partial (P*N f^ samples + 2N packed power values) into slot [n&1][grank]
+// of every shard's exchange buffer over NVLink (P2P stores; same-device
+// stores for virtual shards), publish flag[grank] = n+1 with a system-scope
+// release, wait for every shard's flag, then sum the G slots in rank order.
+// Every shard sums the same values in the same order, so all shards hold a
+// bit-identical f^ and power. Two parities suffice: a shard can only write
+// block n+1's partial after finishing block n, which needed every shard's
+// block-n partial, and each shard consumes its block-n slots before it
+// produces block n+1 (stream order). The wait is bounded (kShardTimeoutNs):
+// a missing peer sets status_host instead of hanging the GPU.
+__global__ void __launch_bounds__(kTailThreads) k_afc_finish(BlockArgs a) {
+  const uint32_t n = a.st->block;
+  trace_begin(a, TR_AFC_FINISH, n);
+  const int N = a.N, P = a.P, G = a.G;
+  const size_t S = (size_t)P * N + 2 * (size_t)N;
+  const int par = (int)(n & 1u);
+  for (int g = 0; g < G; ++g) {
+    float* dst = reinterpret_cast<float*>(a.xpeer[g] + kXFlagBytes) + ((size_t)par * G + a.grank) * S;
+    for (size_t i = threadIdx.x; i < S; i += blockDim.x) dst[i] = __ldcg(a.xmine + i);
+  }
+  __syncthreads();
+  __shared__ int timed_out;
+  if (threadIdx.x == 0) {
+    timed_out = 0;
+    __threadfence_system();
+    for (int g = 0; g < G; ++g) st_release_sys(reinterpret_cast<unsigned*>(a.xpeer[g]) + a.grank, n + 1);
+    const unsigned* flags = reinterpret_cast<const unsigned*>(a.xpeer[a.grank]);
+    const unsigned long long t0 = globaltimer();
+    for (int g = 0; g < G && !timed_out; ++g)
+      while (ld_acquire_sys(flags + g) < n + 1) {
+        if (globaltimer() - t0 > kShardTimeoutNs) {
+          timed_out = 1;
+          *reinterpret_cast<volatile unsigned*>(a.status_host) = 1u;
+          break;
+        }
+        __nanosleep(64);
+      }
+  }
+  __syncthreads();
+  const float* slots = reinterpret_cast<const float*>(a.xpeer[a.grank] + kXFlagBytes) + (size_t)par * G * S;
+  for (int i = threadIdx.x; i < P * N; i += blockDim.x) {
+    float v = __ldcg(slots + i);
+    for (int g = 1; g < G; ++g) v = __fadd_rn(v, __ldcg(slots + (size_t)g * S + i));
+    a.fhat[i] = v;
+    a.fhat_host[i] = v;
+  }
+  if (a.nlms) {
+    const float oml = __fsub_rn(1.0f, a.lambda);
+    for (int j = threadIdx.x; j < N; j += blockDim.x) {
+      const float* b = slots + (size_t)P * N + 2 * j;
+      float2 sum = make_float2(__ldcg(b), __ldcg(b + 1));
+      for (int g = 1; g < G; ++g) {
+        sum.x = __fadd_rn(sum.x, __ldcg(b + (size_t)g * S));
+        sum.y = __fadd_rn(sum.y, __ldcg(b + (size_t)g * S + 1));
+      }
+      float2 w = a.pw[j];
+      w.x = __fadd_rn(__fmul_rn(a.lambda, w.x), __fmul_rn(oml, sum.x));
+      w.y = __fadd_rn(__fmul_rn(a.lambda, w.y), __fmul_rn(oml, sum.y));
+      a.pw[j] = w;
+    }
+  }
+  trace_end(a, TR_AFC_FINISH, n);
   retire_block(a, n);
 }
 
