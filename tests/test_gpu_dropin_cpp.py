@@ -21,6 +21,18 @@ BIN = os.path.join(ROOT, "tests", "cpp", "_bin")
 # Reference tests whose assertion contradicts the drop-in by design; every
 # entry says why. Everything else must pass.
 EXCLUDED = {
+    # Compares the fused Auralizer with a manual composition of two
+    # Convolvers to 1e-5 ABSOLUTE inside a feedback loop whose gain is > 1
+    # (3 unit-energy canceller filters). It holds in the reference only
+    # because both paths run the identical fp32 code: the reference's own
+    # fp32 output is 2-4e-5 away from the exact (float64) result on this
+    # configuration (tests/test_oracle.py::
+    # test_fused_vs_manual_pin_is_bit_identity_not_accuracy). Our fused path
+    # sums the canceller in the frequency domain (one c2r, not L), so the
+    # two fp32 orders differ at 1e-7 and the loop grows that to ~1e-5. The
+    # same property with a stable loop is tested in
+    # tests/test_gpu_auralizer.py::test_fused_equals_manual_composition.
+    "test_auralizer::Auralizer.FusedPathEqualsManualComposition",
 }
 
 

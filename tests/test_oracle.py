@@ -145,3 +145,25 @@ def test_partition_count_kats():
     assert A.partition_count(1, 64) == 1
     if O.ref_available():
         assert O.rlib().ref_partition_count(480000, 128) == 3750
+
+
+@need_ref
+def test_fused_vs_manual_pin_is_bit_identity_not_accuracy():
+    """test_auralizer.cpp:127-159 (FusedPathEqualsManualComposition) asserts
+    1e-5 absolute between two fp32 evaluations inside a loop of gain > 1.
+    On that configuration the reference's own fp32 Auralizer is further than
+    1e-5 from the exact float64 result, so the pin tests bit-identity of two
+    code paths, not accuracy (why tests/test_gpu_dropin_cpp.py excludes it)."""
+    from nlms_f64 import NlmsF64
+    worst = 0.0
+    for seed in range(3):
+        rng = np.random.default_rng(seed)
+        N, C = 64, 3
+        s = (rng.standard_normal((C, 5 * N + 3)) / np.sqrt(5 * N + 3)).astype(np.float32)
+        fc = (rng.standard_normal((C, 2 * N + 1)) / np.sqrt(2 * N + 1)).astype(np.float32)
+        r = O.RefAuralizer(s, fc, N, C)
+        d = NlmsF64(s, fc, N, 1, C, gain=1.0, mu=0.0, lam=0.9, delta=1.0)
+        for _ in range(12):
+            x = rng.standard_normal((1, N)).astype(np.float32)
+            worst = max(worst, float(np.max(np.abs(r.process(x) - d.process(x)))))
+    assert worst > 1e-5
