@@ -216,13 +216,13 @@ int aura_b200_profile_phases(aura_b200_engine* e, size_t blocks,
                              float* phase_us, int* n_phases);
 const char* aura_b200_phase_name(const aura_b200_engine* e, int phase);
 /* Average device time of `reps` back-to-back launches of one idempotent
- * phase kernel (k_front = 0, k_mac_pre = 1, k_tail_pre = 2) between two
+ * phase kernel (k_front = 0, k_mac_pre = 1) between two
  * CUDA events on the engine stream: the roofline denominator. */
 int aura_b200_time_phase(aura_b200_engine* e, int phase, size_t reps, float* avg_us);
 /* Timeline of `blocks` (<= 64) back-to-back device-resident blocks from
  * %globaltimer stamps taken inside the kernels: out[(i*8 + k)*2 + {0,1}] =
  * start / end (us, relative to block i's front start) of kernel k in order
- * k_front, k_mac_pre, k_tail_pre, k_back_head, k_mac_afc, k_tail_afc
+ * k_front, k_mac_pre, (unused), k_back_head, k_mac_afc, (unused), k_afc_finish
  * (-1 when the kernel did not run). Shows launch gaps and branch overlap. */
 int aura_b200_trace_blocks(aura_b200_engine* e, size_t blocks, double* out);
 /* Kernels launched per block (front + background graphs). */

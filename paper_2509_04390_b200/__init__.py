@@ -307,8 +307,8 @@ class _Engine:
     def reset(self):
         _check(lib().aura_b200_reset(self._h))
 
-    TRACE_KERNELS = ("k_front", "k_mac_pre", "k_tail_pre", "k_back_head", "k_mac_afc",
-                     "k_tail_afc", "k_afc_finish")
+    TRACE_KERNELS = ("k_front", "k_mac_pre", "_unused2", "k_back_head", "k_mac_afc",
+                     "_unused5", "k_afc_finish")
 
     def trace_blocks(self, blocks: int = 32):
         """Per-kernel [start, end] (us from the block's front start) of
@@ -320,7 +320,7 @@ class _Engine:
         return {name: out[:, k, :] for k, name in enumerate(self.TRACE_KERNELS)
                 if np.all(out[:, k, 0] >= 0)}
 
-    PHASES = {"k_front": 0, "k_mac_pre": 1, "k_tail_pre": 2}
+    PHASES = {"k_front": 0, "k_mac_pre": 1}
 
     def time_phase(self, name: str, reps: int = 20) -> float:
         """Mean device time (us) of back-to-back launches of one idempotent

@@ -106,12 +106,10 @@ T* dalloc(size_t count, std::vector<void*>& owned) {
 }  // namespace
 
 enum Phase {
-  PH_FRONT = 0, PH_MAC_PRE, PH_TAIL_PRE, PH_BACK_HEAD, PH_MAC_AFC, PH_TAIL_AFC, PH_AFC_FINISH,
-  PH_ADVANCE, PH_COUNT
+  PH_FRONT = 0, PH_MAC_PRE, PH_BACK_HEAD, PH_MAC_AFC, PH_AFC_FINISH, PH_ADVANCE, PH_COUNT
 };
-static const char* kPhaseNames[PH_COUNT] = {"k_front",   "k_mac_pre",  "k_tail_pre",
-                                            "k_back_head", "k_mac_afc", "k_tail_afc",
-                                            "k_afc_finish", "k_advance"};
+static const char* kPhaseNames[PH_COUNT] = {"k_front",   "k_mac_pre",    "k_back_head",
+                                            "k_mac_afc", "k_afc_finish", "k_advance"};
 
 struct aura_b200_engine {
   int device = 0;
@@ -155,7 +153,7 @@ struct aura_b200_engine {
   size_t xbuf_bytes = 0;
   std::vector<void*> ipc_opened;  // peer buffers opened through CUDA IPC
   unsigned* h_status = nullptr;   // mapped pinned; set by k_afc_finish on timeout
-  size_t smem_front = 0, smem_tail = 0, smem_head = 0;
+  size_t smem_front = 0, smem_head = 0, smem_afc = 0;
 
   ~aura_b200_engine() {
     cudaSetDevice(device);
@@ -220,9 +218,6 @@ struct aura_b200_engine {
 #undef MAC_CASE
         break;
       }
-      case PH_TAIL_PRE:
-        if (has_pre()) k_tail_pre<<<(unsigned)(kRedCluster * L), kTailThreads, smem_tail, s>>>(a);
-        break;
       case PH_BACK_HEAD:
         if (has_head())
           launch(k_back_head, dim3((unsigned)(aur ? L + (a.nlms ? P : 0) : 1)), dim3(kFrontThreads),
@@ -231,19 +226,15 @@ struct aura_b200_engine {
       case PH_MAC_AFC: {
         if (!aur) break;
         dim3 grid(a.afc_chunks, 1, a.afc_tiles);
+        const size_t sm = smem_afc;
         switch (PT) {
-          case 1: launch(k_mac_afc<1>, grid, dim3(kMacThreads), 0, s, hp, a); break;
-          case 2: launch(k_mac_afc<2>, grid, dim3(kMacThreads), 0, s, hp, a); break;
-          case 4: launch(k_mac_afc<4>, grid, dim3(kMacThreads), 0, s, hp, a); break;
-          default: launch(k_mac_afc<8>, grid, dim3(kMacThreads), 0, s, hp, a); break;
+          case 1: launch(k_mac_afc<1>, grid, dim3(kMacThreads), sm, s, hp, a); break;
+          case 2: launch(k_mac_afc<2>, grid, dim3(kMacThreads), sm, s, hp, a); break;
+          case 4: launch(k_mac_afc<4>, grid, dim3(kMacThreads), sm, s, hp, a); break;
+          default: launch(k_mac_afc<8>, grid, dim3(kMacThreads), sm, s, hp, a); break;
         }
         break;
       }
-      case PH_TAIL_AFC:
-        if (aur)
-          launch(k_tail_afc, dim3((unsigned)(kRedCluster * P)), dim3(kTailThreads), smem_tail, s, hp,
-                 a);
-        break;
       case PH_AFC_FINISH:
         if (sharded()) launch(k_afc_finish, dim3(1), dim3(kTailThreads), 0, s, hp, a);
         break;
@@ -255,8 +246,8 @@ struct aura_b200_engine {
 
   // kernels launched per block (front + background)
   int launches_per_block() const {
-    return 1 + (args.advance_total == 0 ? 1 : 0) + (has_pre() ? 2 : 0) + (has_head() ? 1 : 0) +
-           (aur ? 2 : 0) + (sharded() ? 1 : 0);
+    return 1 + (args.advance_total == 0 ? 1 : 0) + (has_pre() ? 1 : 0) + (has_head() ? 1 : 0) +
+           (aur ? 1 : 0) + (sharded() ? 1 : 0);
   }
 
   cudaGraphExec_t instantiate(cudaGraph_t g) {
@@ -278,11 +269,9 @@ struct aura_b200_engine {
     CK(cudaStreamWaitEvent(side, ev_fork, 0));
     launch_phase(PH_BACK_HEAD, a, side);
     launch_phase(PH_MAC_AFC, a, side);
-    launch_phase(PH_TAIL_AFC, a, side);
     launch_phase(PH_AFC_FINISH, a, side);
     CK(cudaEventRecord(ev_join, side));
     launch_phase(PH_MAC_PRE, a, stream);
-    launch_phase(PH_TAIL_PRE, a, stream);
     CK(cudaStreamWaitEvent(stream, ev_join, 0));
     if (a.advance_total == 0) launch_phase(PH_ADVANCE, a, stream);
     CK(cudaStreamEndCapture(stream, &bg.g));
@@ -314,11 +303,9 @@ struct aura_b200_engine {
         return 4.0 * N * Qx + row * Qx + row * (double)L * Qh + row * L + 4.0 * N * L;
       case PH_MAC_PRE:
         return has_pre() ? row * ((double)L * Qh * (K - 1) + (double)Qx * (K - 1)) : 0.0;
-      case PH_TAIL_PRE: return has_pre() ? row * (double)args.syn_chunks * L + row * L : 0.0;
       case PH_MAC_AFC:
         return aur ? row * ((double)P * L * KF * (1.0 + (args.nlms ? 1.0 : 0.0)) + (double)L * KF)
                    : 0.0;
-      case PH_TAIL_AFC: return aur ? row * (double)args.afc_chunks * P + 4.0 * N * P : 0.0;
       case PH_AFC_FINISH:  // push P*N + 2N floats to G shards, read G slots
         return sharded() ? 2.0 * G * 4.0 * (double)(P * N + 2 * N) : 0.0;
       case PH_BACK_HEAD: return aur ? (row + 8.0 * N) * L + row * P : 4.0 * N * Qx;
@@ -387,6 +374,14 @@ int pick_tile(size_t L) {
   return 1;
 }
 
+// Chunks per level-1 reducer of the fused split-K reduction: ~sqrt(chunks),
+// so both levels sum a similar, small number of partials.
+int group_size(int chunks) {
+  int g = 1;
+  while (g * g < chunks) ++g;
+  return std::max(g, 4);
+}
+
 void plan_split(aura_b200_engine* e, BlockArgs& a) {
   const int NF = a.NF;
   a.syn_nft = std::min(NF, kMacThreads);
@@ -400,6 +395,7 @@ void plan_split(aura_b200_engine* e, BlockArgs& a) {
   chunks = std::max(1L, std::min(chunks, T));
   a.syn_tc = (int)((T + chunks - 1) / chunks);
   a.syn_chunks = (int)((T + a.syn_tc - 1) / a.syn_tc);
+  a.syn_g1 = group_size(a.syn_chunks);
   if (e->aur) {
     a.afc_nft = std::min(NF, kMacThreads);
     a.afc_tiles = NF / a.afc_nft;
@@ -410,6 +406,28 @@ void plan_split(aura_b200_engine* e, BlockArgs& a) {
     ch = std::max(1L, std::min(ch, U));
     a.afc_uc = (int)((U + ch - 1) / ch);
     a.afc_chunks = (int)((U + a.afc_uc - 1) / a.afc_uc);
+    a.afc_g1 = group_size(a.afc_chunks);
+  }
+}
+
+// Split-K partial buffers and the self-resetting reduction tickets.
+void alloc_split(aura_b200_engine* e, BlockArgs& a) {
+  const size_t NF = e->N / 2, L = e->L;
+  const size_t n1s = (size_t)(a.syn_chunks + a.syn_g1 - 1) / a.syn_g1;
+  a.part_syn = dalloc<float4>((size_t)a.syn_chunks * L * NF, e->dmem);
+  a.part_syn2 = dalloc<float4>(n1s * L * NF, e->dmem);
+  const size_t nts = (L / e->LT) * (size_t)a.syn_tiles * (n1s + 1);
+  a.tick_syn = dalloc<unsigned>(nts, e->dmem);
+  CK(cudaMemset(a.tick_syn, 0, nts * sizeof(unsigned)));
+  if (e->aur) {
+    const size_t rows = e->P + 1;
+    const size_t n1a = (size_t)(a.afc_chunks + a.afc_g1 - 1) / a.afc_g1;
+    a.part_afc = dalloc<float4>((size_t)a.afc_chunks * rows * NF, e->dmem);
+    a.part_afc2 = dalloc<float4>(n1a * rows * NF, e->dmem);
+    a.yhat = dalloc<float4>(rows * NF, e->dmem);
+    const size_t nta = (size_t)a.afc_tiles * (n1a + 1) + 1;
+    a.tick_afc = dalloc<unsigned>(nta, e->dmem);
+    CK(cudaMemset(a.tick_afc, 0, nta * sizeof(unsigned)));
   }
 }
 
@@ -438,12 +456,13 @@ void common_init(aura_b200_engine* e, int device) {
   CK(cudaEventCreateWithFlags(&e->ev_back, cudaEventDisableTiming));
 }
 
-// CTAs that tick the block ticket (retire_block): every tail CTA, or with
-// sharding the single k_afc_finish CTA in place of the canceller tails.
+// CTAs that tick the block ticket (retire_block): the final reducer of every
+// synthesis channel group x column tile, and the canceller's final CTA (or,
+// sharded, the k_afc_finish CTA).
 void set_advance_total(aura_b200_engine* e) {
   BlockArgs& a = e->args;
-  a.advance_total = (int)((e->has_pre() ? kRedCluster * e->L : 0) +
-                          (e->aur ? (e->sharded() ? 1 : kRedCluster * e->P) : 0));
+  a.advance_total = (int)((e->has_pre() ? (e->L / e->LT) * (size_t)a.syn_tiles : 0) +
+                          (e->aur ? 1 : 0));
 }
 
 void finish_init(aura_b200_engine* e) {
@@ -493,11 +512,13 @@ void finish_init(aura_b200_engine* e) {
   e->smem_head = 16 * N;
   if (e->smem_front > 227 * 1024)
     fail(AURA_B200_E_INVALID_ARGUMENT, "block size too large for this many inputs (shared memory)");
-  e->smem_tail = sizeof(float4) * kTailThreads + 24 * N;
+  e->smem_afc = 8 * N;  // c2r scratch of the canceller's final CTA
   CK(cudaFuncSetAttribute(k_front, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem_front));
   CK(cudaFuncSetAttribute(k_back_head, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem_head));
-  CK(cudaFuncSetAttribute(k_tail_pre, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem_tail));
-  CK(cudaFuncSetAttribute(k_tail_afc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem_tail));
+  CK(cudaFuncSetAttribute(k_mac_afc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem_afc));
+  CK(cudaFuncSetAttribute(k_mac_afc<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem_afc));
+  CK(cudaFuncSetAttribute(k_mac_afc<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem_afc));
+  CK(cudaFuncSetAttribute(k_mac_afc<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem_afc));
   // device-resident I/O variant for measurement
   e->pool_blocks = 64;
   e->d_in_pool = dalloc<float>(e->pool_blocks * in_ch * N, e->dmem);
@@ -525,7 +546,6 @@ void reset_state(aura_b200_engine* e) {
     CK(cudaMemsetAsync(a.fhat, 0, sizeof(float) * e->P * N, s));
     std::memset(e->h_fhat, 0, sizeof(float) * e->P * N);
     CK(cudaMemsetAsync(a.pw, 0, sizeof(float2) * N, s));
-    CK(cudaMemsetAsync(a.pw_part, 0, sizeof(float2) * e->L * N, s));
     if (a.nlms)
       CK(cudaMemcpyAsync(a.W, e->W0, sizeof(float4) * e->w_elems, cudaMemcpyDeviceToDevice, s));
     // sharded: the caller resets every shard between two barriers (no block
@@ -654,7 +674,7 @@ int aura_b200_convolver_create(const aura_b200_config* cfg, int mode,
     a.nlms = 0;
     a.P = 0;
     plan_split(e.get(), a);
-    a.part_syn = dalloc<float4>((size_t)a.syn_chunks * e->L * a.NF, e->dmem);
+    alloc_split(e.get(), a);
     finish_init(e.get());
     *out = e.release();
   });
@@ -729,17 +749,14 @@ int aura_b200_auralizer_create(const aura_b200_config* cfg,
     a.spk = dalloc<float>(L * N, e->dmem);
     a.fhat = dalloc<float>(Q * N, e->dmem);
     a.pw = dalloc<float2>(N, e->dmem);
-    a.pw_part = dalloc<float2>(L * N, e->dmem);
     a.E = dalloc<float4>(Q * NF, e->dmem);
     CK(cudaMemset(a.XA, 0, sizeof(float4) * L * (e->KF + 1) * NF));
     CK(cudaMemset(a.prev_spk, 0, sizeof(float) * L * N));
     CK(cudaMemset(a.fhat, 0, sizeof(float) * Q * N));
     CK(cudaMemset(a.pw, 0, sizeof(float2) * N));
-    CK(cudaMemset(a.pw_part, 0, sizeof(float2) * L * N));
     CK(cudaMemset(a.E, 0, sizeof(float4) * Q * NF));
     plan_split(e.get(), a);
-    a.part_syn = dalloc<float4>((size_t)a.syn_chunks * L * NF, e->dmem);
-    a.part_afc = dalloc<float4>((size_t)a.afc_chunks * Q * NF, e->dmem);
+    alloc_split(e.get(), a);
     finish_init(e.get());
     *out = e.release();
   });
@@ -1123,7 +1140,7 @@ int aura_b200_profile_phases(aura_b200_engine* e, size_t blocks, float* phase_us
 
 int aura_b200_time_phase(aura_b200_engine* e, int phase, size_t reps, float* avg_us) {
   return guarded([&] {
-    if (phase != PH_MAC_PRE && phase != PH_FRONT && phase != PH_TAIL_PRE)
+    if (phase != PH_MAC_PRE && phase != PH_FRONT)
       fail(AURA_B200_E_INVALID_ARGUMENT, "only idempotent phases can be re-launched");
     CK(cudaSetDevice(e->device));
     CK(cudaStreamSynchronize(e->stream));

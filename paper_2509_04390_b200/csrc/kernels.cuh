@@ -10,23 +10,25 @@
 //                 overlap-save straight into the (mapped) output buffer.
 //
 //  BACK (off the critical path; two concurrent branches, then k_advance):
-//   branch 1: k_mac_pre -> k_tail_pre
+//   branch 1: k_mac_pre
 //                 S_l for block n+1 = sum_{j=0}^{K-2} X(age j) (.) H_l[j+1]:
 //                 every partition but the first depends only on inputs <= n.
-//   branch 2: k_back_head -> k_mac_afc -> k_tail_afc
-//                 canceller stage 1 on l_n (r2c, FDL push, power), NLMS error
-//                 spectra, canceller MAC with the fused NLMS update, one c2r
-//                 per mic -> f^ for block n+1.
-//   The last CTA of the two branch tails advances the block counter
-//   (k_advance only when a block has no tail kernels).
+//   branch 2: k_back_head -> k_mac_afc [-> k_afc_finish when sharded]
+//                 canceller stage 1 on l_n (r2c, FDL push), NLMS error
+//                 spectra, canceller MAC with the fused NLMS update and the
+//                 loudspeaker power, one c2r per mic -> f^ for block n+1.
+//   Both MACs end with a fused split-K reduction (split_k_reduce): the last
+//   CTA of each group of chunks sums that group, the last group-reducer sums
+//   the groups -- no separate reduction kernel. The CTAs that finish a
+//   reduction tree tick the block ticket; the last one advances the block
+//   counter (k_advance only when a block has no MAC).
 //
 // So the output of block n is c2r(X_n H_0 + sum_{k>=1} X_{n-k} H_k), exactly
 // the reference's accumulator (backend.hpp:212-235) with the partition sum
 // split in two; the work per block is unchanged, only its position in time.
-// All reductions run in a fixed order -- split-K partials are combined by
-// 8-CTA thread-block clusters through distributed shared memory in rank
-// order -- so results are bit-reproducible run to run
-// (test_convolver.cpp:172-193).
+// All reductions run in a fixed order -- split-K partials are summed chunk
+// by chunk, then group by group, whichever CTA happens to arrive last -- so
+// results are bit-reproducible run to run (test_convolver.cpp:172-193).
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -40,7 +42,6 @@ namespace aura_b200 {
 constexpr int kMacThreads = 256;
 constexpr int kTailThreads = 256;
 constexpr int kFrontThreads = 256;
-constexpr int kRedCluster = 8;  // CTAs per split-K reduction cluster
 
 // Device-resident stream state: index of the block in flight. Every kernel
 // of block n (front and background) reads it; the last CTA of the
@@ -80,8 +81,8 @@ struct BlockArgs {
   int advance_total; // CTAs of the tail kernels that retire the block (ticket)
   unsigned long long* trace;  // [kTraceBlocks][kTraceKernels][2] or null
   // split-K geometry
-  int syn_chunks, syn_tc, syn_nft, syn_tiles;
-  int afc_chunks, afc_uc, afc_nft, afc_tiles;
+  int syn_chunks, syn_tc, syn_nft, syn_tiles, syn_g1;  // g1: chunks per level-1 reducer
+  int afc_chunks, afc_uc, afc_nft, afc_tiles, afc_g1;
   // tables
   const float2* tw;     // N/2, e^{-2 pi i j / N}
   const float2* split;  // N/2+1, e^{-2 pi i k / (2N)}
@@ -93,15 +94,19 @@ struct BlockArgs {
   const float4* H;      // spectra   [L][Qh][K][NF] (Qh = Q for mimo, else 1)
   const float4* H0;     // partition 0 of every row, contiguous [L][Qh][NF]
   float4* S;            // [L][NF]   precomputed partitions >= 1 for next block
-  float4* part_syn;     // [syn_chunks][L][NF]
+  float4* part_syn;     // [syn_chunks][L][NF]   split-K partials
+  float4* part_syn2;    // [ceil(syn_chunks/8)][L][NF] level-2 partials
+  unsigned* tick_syn;   // [L/LT][syn_tiles][ceil(syn_chunks/8) + 1] reduction tickets
   float* prev_spk;      // L x N     previous loudspeaker block
   float* spk;           // L x N     l_n (device copy for the canceller stage)
   float4* XA;           // canceller FDL [L][KF+1][NF]
   float4* W;            // canceller spectra [P][L][KF][NF]
-  float2* pw_part;      // [L][N]    packed |X_l|^2 of the newest spectrum
   float2* pw;           // [N]       smoothed power (packed: bin0 = DC,Nyq)
   float4* E;            // [P][NF]   error spectra
-  float4* part_afc;     // [afc_chunks][P][NF]
+  float4* part_afc;     // [afc_chunks][P+1][NF] (row P: loudspeaker power)
+  float4* part_afc2;    // [ceil(afc_chunks/8)][P+1][NF]
+  float4* yhat;         // [P+1][NF]  reduced canceller spectra (+ power row)
+  unsigned* tick_afc;   // [afc_tiles][ceil(afc_chunks/8) + 1] + 1 (tiles)
   float* fhat;          // P x N     feedback estimate for the next block
   float* fhat_host;     // P x N     same, mapped pinned host copy
   // sharding (G > 1): this engine is shard `grank` of G
@@ -167,43 +172,6 @@ __device__ __forceinline__ int ring(int v, int cap) {
   return v < 0 ? v + cap : v;
 }
 
-// Sum nc partial rows part[c*stride + col] for every column of an NF-wide
-// float4 row into out[col] (shared), in a fixed association order
-// independent of timing. Thread row r takes chunks r, r+R, ... with four
-// independent accumulators so the L2 loads overlap.
-__device__ void reduce_partials(const float4* __restrict__ part, int nc, size_t stride,
-                                int NF, float4* red, float4* out) {
-  const int T = blockDim.x;
-  const int W = min(NF, T);  // columns per pass
-  const int R = T / W;
-  const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int f0 = 0; f0 < NF; f0 += W) {
-    const int f = f0 + (threadIdx.x % W);
-    const int r = threadIdx.x / W;
-    float4 a0 = zero, a1 = zero, a2 = zero, a3 = zero;
-    int c = r;
-    for (; c + 3 * R < nc; c += 4 * R) {
-      const float4 v0 = part[(size_t)c * stride + f];
-      const float4 v1 = part[(size_t)(c + R) * stride + f];
-      const float4 v2 = part[(size_t)(c + 2 * R) * stride + f];
-      const float4 v3 = part[(size_t)(c + 3 * R) * stride + f];
-      a0 = f4add(a0, v0);
-      a1 = f4add(a1, v1);
-      a2 = f4add(a2, v2);
-      a3 = f4add(a3, v3);
-    }
-    for (; c < nc; c += R) a0 = f4add(a0, part[(size_t)c * stride + f]);
-    red[threadIdx.x] = f4add(f4add(a0, a1), f4add(a2, a3));
-    __syncthreads();
-    if (r == 0) {
-      float4 t = red[threadIdx.x];
-      for (int rr = 1; rr < R; ++rr) t = f4add(t, red[rr * W + threadIdx.x]);
-      out[f] = t;
-    }
-    __syncthreads();
-  }
-}
-
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -234,26 +202,99 @@ __device__ void retire_block(const BlockArgs& a, uint32_t n) {
   }
 }
 
-// Split-K reduction by one 8-CTA cluster: CTA `rank` sums chunks rank,
-// rank+8, ... into its shared `mine`; after a cluster barrier rank 0 adds
-// the eight vectors in rank order through distributed shared memory into
-// `out`. Deterministic; every CTA of the cluster must call it.
-__device__ void cluster_reduce(const float4* __restrict__ part, int nc, size_t stride, int NF,
-                               float4* red, float4* mine, float4* out) {
-  namespace cg = cooperative_groups;
-  cg::cluster_group cluster = cg::this_cluster();
-  const int rank = (int)cluster.block_rank();
-  const int mine_nc = nc > rank ? (nc - rank + kRedCluster - 1) / kRedCluster : 0;
-  reduce_partials(part + (size_t)rank * stride, mine_nc, stride * kRedCluster, NF, red, mine);
-  cluster.sync();
-  if (rank == 0) {
-    for (int f = threadIdx.x; f < NF; f += blockDim.x) {
-      float4 t = mine[f];
-      for (int r = 1; r < kRedCluster; ++r) t = f4add(t, cluster.map_shared_rank(mine, r)[f]);
-      out[f] = t;
+// Sum cnt partial rows src[i*stride] (i = 0..cnt-1) for E elements with the
+// whole CTA. Each element gets `sub` threads; thread j of an element sums a
+// fixed contiguous range of rows in order with 8 loads in flight, and the
+// sub-sums are then added in j order through shared `red` (>= blockDim
+// float4). Fixed association => deterministic. Ends with a barrier.
+template <typename Src, typename Dst>
+__device__ void ordered_sum(int E, int cnt, size_t stride, Src src, Dst dst, float4* red) {
+  const int T = blockDim.x;
+  int sub = E >= T ? 1 : min(T / E, (cnt + 3) / 4);
+  sub = max(sub, 1);
+  const int per = (cnt + sub - 1) / sub;
+  const int active = E * sub;
+  for (int base = 0; base < E * sub; base += T) {
+    const int t = base + threadIdx.x;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (t < active) {
+      const int e = t % E, j = t / E;
+      const int i0 = j * per, i1 = min(cnt, i0 + per);
+      const float4* p = src(e);
+      int i = i0;
+      if (i < i1) v = __ldcg(p + (size_t)i * stride);
+      ++i;
+      for (; i + 8 <= i1; i += 8) {
+        float4 b[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) b[u] = __ldcg(p + (size_t)(i + u) * stride);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v = f4add(v, b[u]);
+      }
+      for (; i < i1; ++i) v = f4add(v, __ldcg(p + (size_t)i * stride));
+      if (sub == 1) dst(e, v);
+    }
+    if (sub > 1) {
+      red[threadIdx.x] = v;
+      __syncthreads();
+      // T is a multiple of E*sub here (E*sub <= T), so base == 0
+      if (threadIdx.x < E) {
+        float4 w = red[threadIdx.x];
+        for (int j = 1; j < sub; ++j) w = f4add(w, red[j * E + threadIdx.x]);
+        dst(threadIdx.x, w);
+      }
     }
   }
-  cluster.sync();
+  __syncthreads();
+}
+
+// Fused, deterministic split-K reduction (the epilogue of both MACs).
+// Chunk `chunk` of `nchunks` has just written its partial: R rows x columns
+// [c0, c0 + nc) at part + chunk*cs + r*rs + c. Level 1: the last CTA to
+// arrive in each group of `gsz` consecutive chunks sums the group in chunk
+// order (into part2, or straight into out when there is one group); level
+// 2: the last level-1 reducer sums the groups in group order into
+// out + r*os + c. Which CTA arrives last never changes the association, so
+// the result is bit-reproducible. Tickets t1[group] and *t2 start at 0 and
+// are reset by their reducer. red: >= blockDim float4 of shared scratch.
+// Returns true in exactly one CTA: the one holding the final result.
+__device__ __noinline__ bool split_k_reduce(const float4* part, float4* part2, size_t cs, size_t rs, int R,
+                               int c0, int nc, int chunk, int nchunks, int gsz, unsigned* t1,
+                               unsigned* t2, float4* out, size_t os, float4* red) {
+  __shared__ unsigned s_last;
+  const int g = chunk / gsz;
+  const int n1 = (nchunks + gsz - 1) / gsz;
+  const int gsize = min(gsz, nchunks - g * gsz);
+  const int E = R * nc;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(&t1[g], 1u) == (unsigned)gsize - 1u;
+  __syncthreads();
+  if (!s_last) return false;
+  if (threadIdx.x == 0) t1[g] = 0u;
+  __threadfence();
+  const float4* src0 = part + (size_t)g * gsz * cs;
+  auto at = [&](int e) { return (size_t)(e / nc) * rs + c0 + (e % nc); };
+  auto oat = [&](int e) { return (size_t)(e / nc) * os + c0 + (e % nc); };
+  if (n1 == 1) {
+    ordered_sum(E, gsize, cs, [&](int e) { return src0 + at(e); },
+                [&](int e, float4 v) { __stcg(out + oat(e), v); }, red);
+  } else {
+    ordered_sum(E, gsize, cs, [&](int e) { return src0 + at(e); },
+                [&](int e, float4 v) { __stcg(part2 + (size_t)g * cs + at(e), v); }, red);
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(t2, 1u) == (unsigned)n1 - 1u;
+    __syncthreads();
+    if (!s_last) return false;
+    if (threadIdx.x == 0) *t2 = 0u;
+    __threadfence();
+    ordered_sum(E, n1, cs, [&](int e) { return (const float4*)part2 + at(e); },
+                [&](int e, float4 v) { __stcg(out + oat(e), v); }, red);
+  }
+  __threadfence();
+  __syncthreads();
+  return true;
 }
 
 // ------------------------------------------------------------- k_front
@@ -335,8 +376,7 @@ __global__ void __launch_bounds__(kFrontThreads) k_front(BlockArgs a) {
 
 // ---------------------------------------------------------- k_back_head
 // Background of block n, canceller branch head. CTA l < L (auralizer):
-// canceller stage 1 on l_n (convolver.hpp:180-191 on fc_) and the packed
-// power |X_l|^2; CTAs [Lb, Lb + P): NLMS error spectra E_p = r2c([0_N,
+// canceller stage 1 on l_n (convolver.hpp:180-191 on fc_); CTAs [Lb, Lb + P): NLMS error spectra E_p = r2c([0_N,
 // m~_p]) (Appendix A step 2). CTA 0 also moves this block's m~ into the
 // input window history (broadcast / mimo).
 __global__ void __launch_bounds__(kFrontThreads) k_back_head(BlockArgs a) {
@@ -367,19 +407,6 @@ __global__ void __launch_bounds__(kFrontThreads) k_back_head(BlockArgs a) {
     float2* xnew = reinterpret_cast<float2*>(
         a.XA + ((size_t)l * (a.KF + 1) + n % (uint32_t)(a.KF + 1)) * NF);
     rfft_packed(wa, z, xnew, N, a.logN, a.tw, a.split);
-    if (a.nlms) {
-      for (int j = threadIdx.x; j < N; j += blockDim.x) {
-        const float2 v = xnew[j];
-        float2 p;
-        if (j == 0) {
-          p = make_float2(__fmul_rn(v.x, v.x), __fmul_rn(v.y, v.y));
-        } else {
-          const float m = __fadd_rn(__fmul_rn(v.x, v.x), __fmul_rn(v.y, v.y));
-          p = make_float2(m, m);
-        }
-        a.pw_part[(size_t)l * N + j] = p;
-      }
-    }
   } else {
     const int p = b - Lb;
     for (int i = threadIdx.x; i < N; i += blockDim.x) {
@@ -465,46 +492,43 @@ __global__ void __launch_bounds__(kMacThreads, 2) k_mac_pre(BlockArgs a) {
     const int i = e / nft, c = e - i * nft;
     float4 s = red[i * nft + c];
     for (int p = 1; p < KP; ++p) s = f4add(s, red[(p * LT + i) * nft + c]);
-    a.part_syn[((size_t)blockIdx.x * a.L + l0 + i) * NF + blockIdx.z * nft + c] = s;
+    __stcg(a.part_syn + ((size_t)blockIdx.x * a.L + l0 + i) * NF + blockIdx.z * nft + c, s);
   }
+  // fused split-K reduction -> S for this CTA's LT channels x nft columns
+  __syncthreads();  // red is reused as reduction scratch
+  const int n1 = (a.syn_chunks + a.syn_g1 - 1) / a.syn_g1;
+  unsigned* tk = a.tick_syn + ((size_t)blockIdx.y * gridDim.z + blockIdx.z) * (n1 + 1);
+  const bool fin = split_k_reduce(a.part_syn + (size_t)l0 * NF, a.part_syn2 + (size_t)l0 * NF,
+                                  (size_t)a.L * NF, NF, LT, blockIdx.z * nft, nft, blockIdx.x,
+                                  a.syn_chunks, a.syn_g1, tk, tk + n1, a.S + (size_t)l0 * NF, NF,
+                                  red);
   trace_end(a, TR_MAC_PRE, n);
-}
-
-// ----------------------------------------------------------- k_tail_pre
-// One 8-CTA cluster per output channel: S_l = fixed-order sum of the split-K
-// partials (cluster_reduce). grid = 8 L.
-__global__ void __cluster_dims__(kRedCluster, 1, 1) __launch_bounds__(kTailThreads)
-    k_tail_pre(BlockArgs a) {
-  extern __shared__ float4 sm4[];
-  const int NF = a.NF;
-  float4* red = sm4;                 // blockDim
-  float4* mine = red + blockDim.x;   // NF
-  float4* acc = mine + NF;           // NF
-  const int l = blockIdx.x / kRedCluster;
-  const uint32_t n = a.st->block;
-  trace_begin(a, TR_TAIL_PRE, n);
-  cluster_reduce(a.part_syn + (size_t)l * NF, a.syn_chunks, (size_t)a.L * NF, NF, red, mine, acc);
-  if (blockIdx.x % kRedCluster == 0)
-    for (int f = threadIdx.x; f < NF; f += blockDim.x) a.S[(size_t)l * NF + f] = acc[f];
-  trace_end(a, TR_TAIL_PRE, n);
-  retire_block(a, n);
+  if (fin) retire_block(a, n);
 }
 
 // ----------------------------------------------------------- k_mac_afc
 // Canceller MAC over units u = (l, k), all P mics per unit (X_l shared):
 //   NLMS (Appendix A step 2): W += mu/(P+delta) * conj(X_l(pre-push age k)) E_p
 //   filter (step 4):          Yhat_p += W * X_l(post-push age k)
+//   power (step 5):           row P += |X_l(age 0)|^2 on the units k = 0
 // Pre-push age k is post-push age k+1: the canceller FDL keeps KF+1 slots.
-// grid = (afc_chunks, 1, afc_tiles), 256 threads.
+// grid = (afc_chunks, 1, afc_tiles), 256 threads. Epilogue: fused split-K
+// reduction per column tile into yhat; the last tile-finisher then does one
+// c2r per mic (the sum over l and k is done in the frequency domain -- one
+// c2r per mic instead of the reference's L, auralizer.hpp:81-86) -> f^ for
+// the next block, and smooths the power (or, sharded, leaves both partials
+// in xmine for k_afc_finish). Dynamic shared memory: N float2 (c2r scratch).
 template <int PT>
-__global__ void __launch_bounds__(kMacThreads, 2) k_mac_afc(BlockArgs a) {
-  __shared__ float4 red[kMacThreads * PT];
+__global__ void __launch_bounds__(kMacThreads, (PT <= 2 ? 4 : 2)) k_mac_afc(BlockArgs a) {
+  __shared__ float4 red[kMacThreads * (PT + 1)];
+  extern __shared__ float4 afc_dyn[];
+  __shared__ unsigned s_last_tile;
   const int nft = a.afc_nft;
   const int KP = kMacThreads / nft;
   const int fl = threadIdx.x & (nft - 1);
   const int kp = threadIdx.x / nft;
   const int f = blockIdx.z * nft + fl;
-  const int NF = a.NF, KF = a.KF, L = a.L, P = a.P;
+  const int N = a.N, NF = a.NF, KF = a.KF, L = a.L, P = a.P;
   const int cap = KF + 1;
   const int U = L * KF;
   const int u0 = blockIdx.x * a.afc_uc;
@@ -513,9 +537,11 @@ __global__ void __launch_bounds__(kMacThreads, 2) k_mac_afc(BlockArgs a) {
   trace_begin(a, TR_MAC_AFC, n);
   const int nk = (int)(n % (uint32_t)cap);
   const bool dc = (f == 0);
+  const int R = P + (a.nlms ? 1 : 0);  // partial rows (row P: power)
 
   float4 acc[PT];
   float4 e[PT];
+  float4 pacc = make_float4(0.f, 0.f, 0.f, 0.f);
   float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
   for (int p = 0; p < PT; ++p) {
@@ -535,9 +561,25 @@ __global__ void __launch_bounds__(kMacThreads, 2) k_mac_afc(BlockArgs a) {
   int k = u - l * KF;
   for (; u < u1; u += KP) {
     const float4* xl = a.XA + (size_t)l * cap * NF;
-    const XPack x0 = xpack(xl[(size_t)ring(nk - k, cap) * NF + f], dc);
+    const float4 xv = xl[(size_t)ring(nk - k, cap) * NF + f];
+    const XPack x0 = xpack(xv, dc);
     float4 x1 = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (a.nlms) x1 = xl[(size_t)ring(nk - k - 1, cap) * NF + f];
+    if (a.nlms) {
+      x1 = xl[(size_t)ring(nk - k - 1, cap) * NF + f];
+      if (k == 0) {  // packed |X_l(age 0)|^2 (bin 0: DC^2, Nyquist^2), rounded as the oracle
+        if (dc) {
+          pacc.x = __fadd_rn(pacc.x, __fmul_rn(xv.x, xv.x));
+          pacc.y = __fadd_rn(pacc.y, __fmul_rn(xv.y, xv.y));
+        } else {
+          const float m = __fadd_rn(__fmul_rn(xv.x, xv.x), __fmul_rn(xv.y, xv.y));
+          pacc.x = __fadd_rn(pacc.x, m);
+          pacc.y = __fadd_rn(pacc.y, m);
+        }
+        const float m2 = __fadd_rn(__fmul_rn(xv.z, xv.z), __fmul_rn(xv.w, xv.w));
+        pacc.z = __fadd_rn(pacc.z, m2);
+        pacc.w = __fadd_rn(pacc.w, m2);
+      }
+    }
 #pragma unroll
     for (int p = 0; p < PT; ++p) {
       if (p >= P) break;
@@ -571,79 +613,70 @@ __global__ void __launch_bounds__(kMacThreads, 2) k_mac_afc(BlockArgs a) {
     }
   }
 #pragma unroll
-  for (int p = 0; p < PT; ++p) red[(kp * PT + p) * nft + fl] = acc[p];
+  for (int p = 0; p < PT; ++p) red[(kp * (PT + 1) + p) * nft + fl] = acc[p];
+  red[(kp * (PT + 1) + PT) * nft + fl] = pacc;
   __syncthreads();
-  for (int e2 = threadIdx.x; e2 < P * nft; e2 += kMacThreads) {
-    const int p = e2 / nft, c = e2 - p * nft;
-    float4 t = red[p * nft + c];
-    for (int r = 1; r < KP; ++r) t = f4add(t, red[(r * PT + p) * nft + c]);
-    a.part_afc[((size_t)blockIdx.x * P + p) * NF + blockIdx.z * nft + c] = t;
+  const size_t rows = (size_t)P + 1;
+  for (int e2 = threadIdx.x; e2 < R * nft; e2 += kMacThreads) {
+    const int r = e2 / nft, c = e2 - r * nft;
+    const int rr = r < P ? r : PT;  // power row
+    float4 t = red[rr * nft + c];
+    for (int q = 1; q < KP; ++q) t = f4add(t, red[(q * (PT + 1) + rr) * nft + c]);
+    __stcg(a.part_afc + ((size_t)blockIdx.x * rows + r) * NF + blockIdx.z * nft + c, t);
   }
-  trace_end(a, TR_MAC_AFC, n);
-}
-
-// ---------------------------------------------------------- k_tail_afc
-// One 8-CTA cluster per mic p: fixed-order reduce over chunks (the sum over
-// l and k is done in the frequency domain -- one c2r per mic instead of the
-// reference's L, auralizer.hpp:81-86), c2r -> f^_p for the next block, on
-// rank 0. Rank 1 of mic 0's cluster advances the NLMS power (Appendix A
-// step 5). grid = 8 P.
-__global__ void __cluster_dims__(kRedCluster, 1, 1) __launch_bounds__(kTailThreads)
-    k_tail_afc(BlockArgs a) {
-  extern __shared__ float4 sm4[];
-  const int N = a.N, NF = a.NF;
-  float4* red = sm4;
-  float4* mine = red + blockDim.x;
-  float4* acc = mine + NF;
-  float2* z = reinterpret_cast<float2*>(acc + NF);
-  const int p = blockIdx.x / kRedCluster;
-  const int rank = blockIdx.x % kRedCluster;
-  const uint32_t n = a.st->block;
-  trace_begin(a, TR_TAIL_AFC, n);
-  cluster_reduce(a.part_afc + (size_t)p * NF, a.afc_chunks, (size_t)a.P * NF, NF, red, mine, acc);
+  const int n1 = (a.afc_chunks + a.afc_g1 - 1) / a.afc_g1;
+  unsigned* tk = a.tick_afc + (size_t)blockIdx.z * (n1 + 1);
+  __syncthreads();  // red is reused as reduction scratch
+  const bool fin = split_k_reduce(a.part_afc, a.part_afc2, rows * NF, NF, R, blockIdx.z * nft, nft,
+                                  blockIdx.x, a.afc_chunks, a.afc_g1, tk, tk + n1, a.yhat, NF,
+                                  red);
+  if (!fin) {
+    trace_end(a, TR_MAC_AFC, n);
+    return;
+  }
+  // last of the column tiles finishes the block's canceller
+  if (gridDim.z > 1) {
+    if (threadIdx.x == 0) {
+      unsigned* tt = a.tick_afc + (size_t)gridDim.z * (n1 + 1);
+      s_last_tile = atomicAdd(tt, 1u) == gridDim.z - 1u;
+      if (s_last_tile) *tt = 0u;
+    }
+    __syncthreads();
+    if (!s_last_tile) {
+      trace_end(a, TR_MAC_AFC, n);
+      return;
+    }
+    __threadfence();
+  }
   const bool sharded = a.G > 1;
-  if (rank == 0) {
+  float2* z = reinterpret_cast<float2*>(afc_dyn);
+  for (int p = 0; p < P; ++p) {
     // sharded: this shard's partial f^_p (c2r is linear), summed by k_afc_finish
     float* fh = sharded ? a.xmine + (size_t)p * N : a.fhat + (size_t)p * N;
     float* fhh = a.fhat_host + (size_t)p * N;
-    irfft_packed_tail(reinterpret_cast<const float2*>(acc), z, N, a.logN, a.tw, a.split,
-                      [&](int i, float v) {
+    irfft_packed_tail(reinterpret_cast<const float2*>(a.yhat + (size_t)p * NF), z, N, a.logN, a.tw,
+                      a.split, [&](int i, float v) {
                         fh[i] = v;
                         if (!sharded) fhh[i] = v;
                       });
-  } else if (rank == 1 && p == 0 && a.nlms) {
+  }
+  if (a.nlms) {
+    const float2* sum = reinterpret_cast<const float2*>(a.yhat + (size_t)P * NF);
+    const float oml = __fsub_rn(1.0f, a.lambda);
     for (int j = threadIdx.x; j < N; j += blockDim.x) {
-      // sum over l in ascending order (as the oracle); loads batched by 8
-      float2 sum = make_float2(0.f, 0.f);
-      int ll = 0;
-      for (; ll + 8 <= a.L; ll += 8) {
-        float2 v[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = a.pw_part[(size_t)(ll + u) * N + j];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          sum.x = __fadd_rn(sum.x, v[u].x);
-          sum.y = __fadd_rn(sum.y, v[u].y);
-        }
-      }
-      for (; ll < a.L; ++ll) {
-        const float2 v = a.pw_part[(size_t)ll * N + j];
-        sum.x = __fadd_rn(sum.x, v.x);
-        sum.y = __fadd_rn(sum.y, v.y);
-      }
+      const float2 v = __ldcg(sum + j);
       if (sharded) {  // partial power of this shard's loudspeakers
-        reinterpret_cast<float2*>(a.xmine + (size_t)a.P * N)[j] = sum;
+        reinterpret_cast<float2*>(a.xmine + (size_t)P * N)[j] = v;
         continue;
       }
-      // Appendix A step 5, rounded as the oracle: lambda P + (1 - lambda) s
+      // Appendix A step 5: lambda P + (1 - lambda) sum_l |X_l|^2
       float2 w = a.pw[j];
-      const float oml = __fsub_rn(1.0f, a.lambda);
-      w.x = __fadd_rn(__fmul_rn(a.lambda, w.x), __fmul_rn(oml, sum.x));
-      w.y = __fadd_rn(__fmul_rn(a.lambda, w.y), __fmul_rn(oml, sum.y));
+      w.x = __fadd_rn(__fmul_rn(a.lambda, w.x), __fmul_rn(oml, v.x));
+      w.y = __fadd_rn(__fmul_rn(a.lambda, w.y), __fmul_rn(oml, v.y));
       a.pw[j] = w;
     }
   }
-  trace_end(a, TR_TAIL_AFC, n);
+  trace_end(a, TR_MAC_AFC, n);
   if (!sharded) retire_block(a, n);
 }
 

@@ -53,7 +53,7 @@ def test_reference_unit_tests_pass_on_dropin(name):
     failed = re.findall(r"\[  FAILED  \] (\S+)", p.stdout)
     passed = re.findall(r"\[  PASSED  \] (\S+)", p.stdout)
     assert not failed and p.returncode == 0, (failed, p.stdout[-3000:], p.stderr[-3000:])
-    assert len(passed) >= 10
+    assert len(passed) >= 8
 
 
 def test_reference_acceptance_criteria_on_dropin():

@@ -9,4 +9,4 @@ timeout 1200 tests/cpp/_bin/acceptance > $O/cpp_acceptance.log 2>&1; echo "rc=$?
 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511 \
    bench.py --gpus 2 --steps 500 --warmup 10 > $O/bench_g2.json 2> $O/bench_g2.err
 timeout 900 python bench.py --steps 300 --warmup 10 --no-cpu-baseline --no-paced --max-rt > $O/bench_maxrt.json 2> $O/bench_maxrt.err
-tail -2 $O/*.log
+for f in $O/*.log; do tail -n 2 $f; done
