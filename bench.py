@@ -298,7 +298,7 @@ def run_b200_arm(args, cfg, rank, world, local_rank):
     timeline = {k: {"start_us": float(np.median(v[:, 0])), "end_us": float(np.median(v[:, 1]))}
                 for k, v in trace.items()}
     peak, peak_kind = load_peaks()
-    mac_name = "k_mac_pre" if phases["k_mac_pre"][1] > 0 else "k_front"
+    mac_name = "k_back" if phases["k_back"][1] > 0 else "k_front"
     mac_bytes = phases[mac_name][1]
     mac_us = eng.time_phase(mac_name, 20)
     achieved = mac_bytes / (mac_us * 1e-6) / 1e9
@@ -408,7 +408,7 @@ def run_sharded(args, cfg, rank, world, local_rank):
     dist.barrier()
     clocks = clk.summary()
     phases = local.profile_phases(min(K, 200))
-    mac_name = "k_mac_pre" if phases["k_mac_pre"][1] > 0 else "k_front"
+    mac_name = "k_back" if phases["k_back"][1] > 0 else "k_front"
     dist.barrier()
     mac_us = local.time_phase(mac_name, 20)
     mac_bytes = phases[mac_name][1]

@@ -225,6 +225,14 @@ int aura_b200_time_phase(aura_b200_engine* e, int phase, size_t reps, float* avg
  * k_front, k_mac_pre, (unused), k_back_head, k_mac_afc, (unused), k_afc_finish
  * (-1 when the kernel did not run). Shows launch gaps and branch overlap. */
 int aura_b200_trace_blocks(aura_b200_engine* e, size_t blocks, double* out);
+/* Diagnostics (not in the reference): per-segment / per-CTA timeline of the
+ * streaming kernel k_back for the last of `blocks` blocks, us from the
+ * kernel's first CTA start. out_segs: n_segs x {kind, tile, begin, end,
+ * cta, start_us, partial_us, end_us} (one row per work item); out_ctas:
+ * n_ctas x {start_us, first_data_us, exit_us}. Call with null outputs to get
+ * the sizes. */
+int aura_b200_trace_back(aura_b200_engine* e, size_t blocks, double* out_segs, size_t* n_segs,
+                         double* out_ctas, size_t* n_ctas);
 /* Kernels launched per block (front + background graphs). */
 int aura_b200_launches_per_block(const aura_b200_engine* e);
 /* Algorithmic bytes per block of each phase (SURVEY.md 8(d) formula). */

@@ -199,6 +199,7 @@ def lib():
     L.aura_b200_launches_per_block.argtypes = [vp]
     L.aura_b200_time_phase.argtypes = [vp, C.c_int, sz, C.POINTER(C.c_float)]
     L.aura_b200_trace_blocks.argtypes = [vp, sz, np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")]
+    L.aura_b200_trace_back.argtypes = [vp, sz, vp, C.POINTER(C.c_size_t), vp, C.POINTER(C.c_size_t)]
     _lib = L
     return L
 
@@ -307,8 +308,7 @@ class _Engine:
     def reset(self):
         _check(lib().aura_b200_reset(self._h))
 
-    TRACE_KERNELS = ("k_front", "k_mac_pre", "_unused2", "k_back_head", "k_mac_afc",
-                     "_unused5", "k_afc_finish")
+    TRACE_KERNELS = ("k_front", "k_back_head", "k_back", "k_reduce", "afc_done", "k_afc_finish")
 
     def trace_blocks(self, blocks: int = 32):
         """Per-kernel [start, end] (us from the block's front start) of
@@ -317,10 +317,24 @@ class _Engine:
         out = np.zeros(blocks * 8 * 2, np.float64)
         _check(lib().aura_b200_trace_blocks(self._h, blocks, out))
         out = out.reshape(blocks, 8, 2)
-        return {name: out[:, k, :] for k, name in enumerate(self.TRACE_KERNELS)
-                if np.all(out[:, k, 0] >= 0)}
+        res = {name: out[:, k, :] for k, name in enumerate(self.TRACE_KERNELS)
+               if np.all(out[:, k, 0] >= 0)}
+        if blocks > 1:  # front start -> next block's front start (back to back)
+            res["cycle"] = out[:-1, 7, :]
+        return res
 
-    PHASES = {"k_front": 0, "k_mac_pre": 1}
+    def trace_back(self, blocks: int = 8):
+        """Diagnostics: k_back's per-segment end times and per-CTA {start,
+        first data, exit} (us from the block's front start), last block."""
+        ns, nc = C.c_size_t(0), C.c_size_t(0)
+        _check(lib().aura_b200_trace_back(self._h, blocks, None, C.byref(ns), None, C.byref(nc)))
+        segs = np.zeros((ns.value, 8), np.float64)
+        ctas = np.zeros((nc.value, 3), np.float64)
+        _check(lib().aura_b200_trace_back(self._h, blocks, segs.ctypes.data, C.byref(ns),
+                                          ctas.ctypes.data, C.byref(nc)))
+        return segs, ctas
+
+    PHASES = {"k_front": 0, "k_back": 2}
 
     def time_phase(self, name: str, reps: int = 20) -> float:
         """Mean device time (us) of back-to-back launches of one idempotent

@@ -29,6 +29,8 @@
 
 #include "../../include/aura_b200.h"
 #include "kernels.cuh"
+#include "stream.cuh"
+#include <algorithm>
 
 using namespace aura_b200;
 
@@ -89,7 +91,6 @@ void validate(const aura_b200_config* c, bool mimo) {
          "input channels must be 1 or equal to output channels");
 }
 
-constexpr int kSMs = 148;
 // NLMS regulariser default: 1e-2 x (2N), i.e. -20 dB of the per-bin power of
 // one unit-variance loudspeaker signal.
 constexpr float kDefaultDeltaPerBin = 1e-2f;
@@ -105,23 +106,22 @@ T* dalloc(size_t count, std::vector<void*>& owned) {
 
 }  // namespace
 
-enum Phase {
-  PH_FRONT = 0, PH_MAC_PRE, PH_BACK_HEAD, PH_MAC_AFC, PH_AFC_FINISH, PH_ADVANCE, PH_COUNT
-};
-static const char* kPhaseNames[PH_COUNT] = {"k_front",   "k_mac_pre",    "k_back_head",
-                                            "k_mac_afc", "k_afc_finish", "k_advance"};
+enum Phase { PH_FRONT = 0, PH_BACK_HEAD, PH_BACK, PH_REDUCE, PH_AFC_FINISH, PH_ADVANCE, PH_COUNT };
+static const char* kPhaseNames[PH_COUNT] = {"k_front",  "k_back_head",  "k_back",
+                                            "k_reduce", "k_afc_finish", "k_advance"};
+
+using BackFn = void (*)(BlockArgs);
 
 struct aura_b200_engine {
   int device = 0;
+  int sms = 148;
   bool aur = false;
   int mode = 0;
   size_t N = 0, Q = 1, L = 1, P = 0, K = 0, KF = 0, n_h = 0, n_hf = 0;
   int Qx = 1;  // FDL channels
-  int LT = 1, PT = 1;
+  int LT = 1, PT = 0;
   uint64_t blocks = 0;
-  cudaStream_t stream = nullptr;  // the engine's stream (front + background)
-  cudaStream_t side = nullptr;    // second branch used while capturing
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaStream_t stream = nullptr;  // the engine's stream
   cudaEvent_t ev_front = nullptr, ev_back = nullptr;  // completion, per block
   std::vector<void*> dmem;
   float4* W0 = nullptr;  // initial canceller spectra (reset of NLMS)
@@ -146,14 +146,19 @@ struct aura_b200_engine {
     }
   };
   BlockGraph g_block;
-  int prio_high = 0;  // stream priority of the canceller branch
+  // streaming kernel k_back
+  BackFn back_fn = nullptr;
+  int back_ctas = 0;
+  size_t smem_back = 0, smem_reduce = 0;
+  size_t n_syn_segs = 0, n_afc_segs = 0;
+  std::vector<int4> h_chunks;  // host copy of the k_back work queue (diagnostics)
   // sharding: shard grank of G; xbuf = own exchange buffer
   int G = 1, grank = 0;
   char* xbuf = nullptr;
   size_t xbuf_bytes = 0;
   std::vector<void*> ipc_opened;  // peer buffers opened through CUDA IPC
   unsigned* h_status = nullptr;   // mapped pinned; set by k_afc_finish on timeout
-  size_t smem_front = 0, smem_head = 0, smem_afc = 0;
+  size_t smem_front = 0, smem_head = 0;
 
   ~aura_b200_engine() {
     cudaSetDevice(device);
@@ -165,115 +170,77 @@ struct aura_b200_engine {
     if (h_fhat) cudaFreeHost(h_fhat);
     if (h_status) cudaFreeHost(h_status);
     for (void* p : ipc_opened) cudaIpcCloseMemHandle(p);
-    if (ev_fork) cudaEventDestroy(ev_fork);
-    if (ev_join) cudaEventDestroy(ev_join);
     if (ev_front) cudaEventDestroy(ev_front);
     if (ev_back) cudaEventDestroy(ev_back);
-    if (side) cudaStreamDestroy(side);
     if (stream) cudaStreamDestroy(stream);
   }
 
-  bool has_pre() const { return K > 1; }
+  bool has_syn() const { return K > 1; }
+  bool has_back() const { return has_syn() || aur; }
   bool has_head() const { return aur || mode != AURA_B200_ELEMENTWISE; }
   bool sharded() const { return aur && G > 1; }
 
-  // cudaLaunchKernelEx with an explicit scheduling priority (captured into
-  // the graph's kernel nodes): the canceller branch runs at high priority so
-  // its CTAs interleave with the synthesis precompute instead of queueing
-  // behind it.
+  // k_back after k_back_head is a programmatic dependent launch: it starts
+  // while k_back_head runs and waits for it (griddepcontrol.wait) only where
+  // it reads k_back_head's outputs.
   template <typename Kern>
-  void launch(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t s, int prio,
-              const BlockArgs& a) {
+  void launch_pdl(Kern kern, unsigned grid, unsigned threads, size_t smem, bool pdl, const BlockArgs& a,
+                  cudaStream_t s) {
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = grid;
-    cfg.blockDim = block;
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(threads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributePriority;
-    at[0].val.priority = prio;
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl ? 1 : 0;
     CK(cudaLaunchKernelEx(&cfg, kern, a));
   }
 
   void launch_phase(int ph, const BlockArgs& a, cudaStream_t s) {
-    const int hp = prio_high;
     switch (ph) {
       case PH_FRONT: {
         const int grid = (int)((L + a.cpb - 1) / a.cpb);
         k_front<<<grid, kFrontThreads, smem_front, s>>>(a);
         break;
       }
-      case PH_MAC_PRE: {
-        if (!has_pre()) break;
-        dim3 grid(a.syn_chunks, (unsigned)(L / LT), a.syn_tiles);
-        const bool el = mode == AURA_B200_ELEMENTWISE;
-#define MAC_CASE(lt)                                                     \
-  case lt:                                                               \
-    if (el) k_mac_pre<lt, true><<<grid, kMacThreads, 0, s>>>(a);         \
-    else k_mac_pre<lt, false><<<grid, kMacThreads, 0, s>>>(a);           \
-    break;
-        switch (LT) { MAC_CASE(1) MAC_CASE(2) MAC_CASE(4) MAC_CASE(8) }
-#undef MAC_CASE
-        break;
-      }
       case PH_BACK_HEAD:
         if (has_head())
-          launch(k_back_head, dim3((unsigned)(aur ? L + (a.nlms ? P : 0) : 1)), dim3(kFrontThreads),
-                 smem_head, s, hp, a);
+          k_back_head<<<(unsigned)(aur ? L + (a.nlms ? P : 0) : 1), kFrontThreads, smem_head, s>>>(a);
         break;
-      case PH_MAC_AFC: {
-        if (!aur) break;
-        dim3 grid(a.afc_chunks, 1, a.afc_tiles);
-        const size_t sm = smem_afc;
-        switch (PT) {
-          case 1: launch(k_mac_afc<1>, grid, dim3(kMacThreads), sm, s, hp, a); break;
-          case 2: launch(k_mac_afc<2>, grid, dim3(kMacThreads), sm, s, hp, a); break;
-          case 4: launch(k_mac_afc<4>, grid, dim3(kMacThreads), sm, s, hp, a); break;
-          default: launch(k_mac_afc<8>, grid, dim3(kMacThreads), sm, s, hp, a); break;
-        }
+      case PH_BACK:
+        if (has_back()) launch_pdl(back_fn, (unsigned)back_ctas, kBackThreads, smem_back, has_head(), a, s);
         break;
-      }
+      case PH_REDUCE:
+        if (has_back())
+          launch_pdl(k_reduce, (unsigned)(a.red_syn_ctas + a.red_afc_ctas), kReduceThreads, smem_reduce,
+                     true, a, s);
+        break;
       case PH_AFC_FINISH:
-        if (sharded()) launch(k_afc_finish, dim3(1), dim3(kTailThreads), 0, s, hp, a);
+        if (sharded()) k_afc_finish<<<1, kTailThreads, 0, s>>>(a);
         break;
       case PH_ADVANCE:
-        if (a.advance_total == 0) k_advance<<<1, 1, 0, s>>>(a.st);
+        if (!has_back()) k_advance<<<1, 1, 0, s>>>(a.st);
         break;
     }
   }
 
-  // kernels launched per block (front + background)
+  // kernels launched per block
   int launches_per_block() const {
-    return 1 + (args.advance_total == 0 ? 1 : 0) + (has_pre() ? 1 : 0) + (has_head() ? 1 : 0) +
-           (aur ? 1 : 0) + (sharded() ? 1 : 0);
-  }
-
-  cudaGraphExec_t instantiate(cudaGraph_t g) {
-    cudaGraphExec_t ex;
-    CK(cudaGraphInstantiate(&ex, g, 0));
-    cudaGraphDestroy(g);
-    return ex;
+    return 1 + (has_head() ? 1 : 0) + (has_back() ? 2 : 0) + (sharded() ? 1 : 0) +
+           (has_back() ? 0 : 1);
   }
 
   // One graph per block: k_front, an external event node the host waits on
-  // (output ready), then the background as two concurrent branches --
-  // canceller (high priority) and synthesis precompute.
+  // (output ready), then k_back_head -> k_back (PDL) [-> k_afc_finish].
   BlockGraph capture_block(const BlockArgs& a, cudaEvent_t out_event) {
     BlockGraph bg;
     CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
     launch_phase(PH_FRONT, a, stream);
     if (out_event) CK(cudaEventRecordWithFlags(out_event, stream, cudaEventRecordExternal));
-    CK(cudaEventRecord(ev_fork, stream));
-    CK(cudaStreamWaitEvent(side, ev_fork, 0));
-    launch_phase(PH_BACK_HEAD, a, side);
-    launch_phase(PH_MAC_AFC, a, side);
-    launch_phase(PH_AFC_FINISH, a, side);
-    CK(cudaEventRecord(ev_join, side));
-    launch_phase(PH_MAC_PRE, a, stream);
-    CK(cudaStreamWaitEvent(stream, ev_join, 0));
-    if (a.advance_total == 0) launch_phase(PH_ADVANCE, a, stream);
+    for (int ph = PH_BACK_HEAD; ph < PH_COUNT; ++ph) launch_phase(ph, a, stream);
     CK(cudaStreamEndCapture(stream, &bg.g));
     if (out_event) {
       size_t n = 0;
@@ -295,17 +262,22 @@ struct aura_b200_engine {
     g_block = capture_block(args, ev_front);
   }
 
+  // algorithmic HBM bytes per block: 8N per packed partition
   double phase_bytes(int ph) const {
     const double row = 8.0 * (double)N;  // one packed partition
     const double Qh = mode == AURA_B200_MIMO ? (double)Q : 1.0;
     switch (ph) {
       case PH_FRONT:  // inputs, X push, H[.][.][0], S, outputs
         return 4.0 * N * Qx + row * Qx + row * (double)L * Qh + row * L + 4.0 * N * L;
-      case PH_MAC_PRE:
-        return has_pre() ? row * ((double)L * Qh * (K - 1) + (double)Qx * (K - 1)) : 0.0;
-      case PH_MAC_AFC:
-        return aur ? row * ((double)P * L * KF * (1.0 + (args.nlms ? 1.0 : 0.0)) + (double)L * KF)
-                   : 0.0;
+      case PH_BACK: {
+        double b = has_syn() ? row * ((double)L * Qh * (K - 1) + (double)Qx * (K - 1)) : 0.0;
+        if (aur) b += row * ((double)P * L * KF * (1.0 + (args.nlms ? 1.0 : 0.0)) + (double)L * KF);
+        return b;
+      }
+      case PH_REDUCE: {  // the split-K partials, read once
+        const double E = (double)LT * args.CT * 16.0;
+        return (double)n_syn_segs * E + (double)n_afc_segs * args.red_afc_rows * args.CT * 16.0;
+      }
       case PH_AFC_FINISH:  // push P*N + 2N floats to G shards, read G slots
         return sharded() ? 2.0 * G * 4.0 * (double)(P * N + 2 * N) : 0.0;
       case PH_BACK_HEAD: return aur ? (row + 8.0 * N) * L + row * P : 4.0 * N * Qx;
@@ -336,31 +308,37 @@ void setup_tables(aura_b200_engine* e, BlockArgs& a) {
 }
 
 // GPU make_partitioned_filters (convolver.hpp:19-46): rows of n_h taps are
-// uploaded in bounded batches and transformed in place into dst at the
-// packed offsets row_off[r] (float4 units).
-void partition_rows(aura_b200_engine* e, const BlockArgs& a,
-                    const float* const* rows, size_t n_rows, size_t n_h,
-                    size_t K, float4* dst, const std::vector<size_t>& row_off) {
+// uploaded in bounded batches, transformed and scattered into the device
+// layout described by `o`, base[r] and base0[r] (k_partition).
+void partition_rows(aura_b200_engine* e, const BlockArgs& a, const float* const* rows, size_t n_rows,
+                    size_t n_h, size_t K, PartOut o, const std::vector<long long>& base,
+                    const std::vector<long long>& base0) {
   const size_t N = e->N;
   const size_t budget = size_t(256) << 20;  // bytes of staged taps per batch
   size_t batch = std::max<size_t>(1, budget / (n_h * sizeof(float)));
   batch = std::min<size_t>(batch, 65535);
   float* d_taps = nullptr;
-  size_t* d_off = nullptr;
-  CK(cudaMalloc(&d_taps, std::min(batch, n_rows) * n_h * sizeof(float)));
-  CK(cudaMalloc(&d_off, std::min(batch, n_rows) * sizeof(size_t)));
-  const size_t smem = 16 * N;
+  long long* d_off = nullptr;
+  const size_t nb = std::min(batch, n_rows);
+  CK(cudaMalloc(&d_taps, nb * n_h * sizeof(float)));
+  CK(cudaMalloc(&d_off, 2 * nb * sizeof(long long)));
+  const size_t smem = 16 * N + 8 * (size_t)table_f2((int)N);
   CK(cudaFuncSetAttribute(k_partition, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  std::vector<long long> offs(2 * nb);
   for (size_t r0 = 0; r0 < n_rows; r0 += batch) {
     const size_t nr = std::min(batch, n_rows - r0);
     for (size_t r = 0; r < nr; ++r)
-      CK(cudaMemcpyAsync(d_taps + r * n_h, rows[r0 + r], n_h * sizeof(float),
-                         cudaMemcpyHostToDevice, e->stream));
-    CK(cudaMemcpyAsync(d_off, row_off.data() + r0, nr * sizeof(size_t),
-                       cudaMemcpyHostToDevice, e->stream));
+      CK(cudaMemcpyAsync(d_taps + r * n_h, rows[r0 + r], n_h * sizeof(float), cudaMemcpyHostToDevice,
+                         e->stream));
+    for (size_t r = 0; r < nr; ++r) {
+      offs[r] = base[r0 + r];
+      offs[nb + r] = base0.empty() ? 0 : base0[r0 + r];
+    }
+    CK(cudaMemcpyAsync(d_off, offs.data(), 2 * nb * sizeof(long long), cudaMemcpyHostToDevice,
+                       e->stream));
     dim3 grid((unsigned)K, (unsigned)nr);
-    k_partition<<<grid, 256, smem, e->stream>>>(d_taps, n_h, (int)nr, (int)K, (int)N,
-                                                 ilog2(N), a.tw, a.split, dst, d_off);
+    k_partition<<<grid, 256, smem, e->stream>>>(d_taps, n_h, (int)K, (int)N, ilog2(N), a.tw, a.split, o,
+                                                 d_off, d_off + nb);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(e->stream));
   }
@@ -374,61 +352,175 @@ int pick_tile(size_t L) {
   return 1;
 }
 
-// Chunks per level-1 reducer of the fused split-K reduction: ~sqrt(chunks),
-// so both levels sum a similar, small number of partials.
-int group_size(int chunks) {
-  int g = 1;
-  while (g * g < chunks) ++g;
-  return std::max(g, 4);
-}
-
-void plan_split(aura_b200_engine* e, BlockArgs& a) {
-  const int NF = a.NF;
-  a.syn_nft = std::min(NF, kMacThreads);
-  a.syn_tiles = NF / a.syn_nft;
-  const int KP = kMacThreads / a.syn_nft;
-  const long T = std::max(1L, (e->mode == AURA_B200_MIMO ? (long)e->Q : 1L) * (long)(e->K - 1));
-  const long per_chunk = (long)(e->L / e->LT) * a.syn_tiles;
-  const long target = (long)kSMs * 4;
-  long chunks = (target + per_chunk - 1) / per_chunk;
-  chunks = std::min(chunks, std::max(1L, (T + 2 * KP - 1) / (2 * KP)));
-  chunks = std::max(1L, std::min(chunks, T));
-  a.syn_tc = (int)((T + chunks - 1) / chunks);
-  a.syn_chunks = (int)((T + a.syn_tc - 1) / a.syn_tc);
-  a.syn_g1 = group_size(a.syn_chunks);
-  if (e->aur) {
-    a.afc_nft = std::min(NF, kMacThreads);
-    a.afc_tiles = NF / a.afc_nft;
-    const int KPa = kMacThreads / a.afc_nft;
-    const long U = (long)(e->L * e->KF);
-    long ch = (target + a.afc_tiles - 1) / a.afc_tiles;
-    ch = std::min(ch, std::max(1L, (U + 2 * KPa - 1) / (2 * KPa)));
-    ch = std::max(1L, std::min(ch, U));
-    a.afc_uc = (int)((U + ch - 1) / ch);
-    a.afc_chunks = (int)((U + a.afc_uc - 1) / a.afc_uc);
-    a.afc_g1 = group_size(a.afc_chunks);
+template <int LT>
+BackFn back_for(bool elem, int PT) {
+  if (elem) return k_back<LT, true, 0>;
+  switch (PT) {
+    case 0: return k_back<LT, false, 0>;
+    case 1: return k_back<LT, false, 1>;
+    case 2: return k_back<LT, false, 2>;
+    case 4: return k_back<LT, false, 4>;
+    default: return k_back<LT, false, 8>;
   }
 }
 
-// Split-K partial buffers and the self-resetting reduction tickets.
-void alloc_split(aura_b200_engine* e, BlockArgs& a) {
-  const size_t NF = e->N / 2, L = e->L;
-  const size_t n1s = (size_t)(a.syn_chunks + a.syn_g1 - 1) / a.syn_g1;
-  a.part_syn = dalloc<float4>((size_t)a.syn_chunks * L * NF, e->dmem);
-  a.part_syn2 = dalloc<float4>(n1s * L * NF, e->dmem);
-  const size_t nts = (L / e->LT) * (size_t)a.syn_tiles * (n1s + 1);
-  a.tick_syn = dalloc<unsigned>(nts, e->dmem);
-  CK(cudaMemset(a.tick_syn, 0, nts * sizeof(unsigned)));
-  if (e->aur) {
-    const size_t rows = e->P + 1;
-    const size_t n1a = (size_t)(a.afc_chunks + a.afc_g1 - 1) / a.afc_g1;
-    a.part_afc = dalloc<float4>((size_t)a.afc_chunks * rows * NF, e->dmem);
-    a.part_afc2 = dalloc<float4>(n1a * rows * NF, e->dmem);
-    a.yhat = dalloc<float4>(rows * NF, e->dmem);
-    const size_t nta = (size_t)a.afc_tiles * (n1a + 1) + 1;
-    a.tick_afc = dalloc<unsigned>(nta, e->dmem);
-    CK(cudaMemset(a.tick_afc, 0, nta * sizeof(unsigned)));
+// Plan k_back (stream.cuh): tiling, stage sizes, pipeline depth, and the
+// static work split. Three phases -- synthesis taps [0, TA) of every tile,
+// the canceller units, synthesis taps [TA, T) -- are each cut into
+// back_ctas equal contiguous pieces; CTA c runs piece c of each phase in
+// that order. Every (CTA, tile) piece is one split-K partial; a tile's
+// partials are numbered by tap position, which fixes the summation order.
+void plan_back(aura_b200_engine* e, BlockArgs& a) {
+  const int N = (int)e->N, NF = N / 2;
+  const int CT = std::min(NF, 32), CTn = NF / CT, PH = kConsumers / CT;
+  a.CT = CT;
+  a.CTn = CTn;
+  const bool elem = e->mode == AURA_B200_ELEMENTWISE;
+  const int LT = e->LT, XL = elem ? LT : 1;
+  const long long Kt = (long long)e->K - 1;
+  const long long Qh = e->mode == AURA_B200_MIMO ? (long long)e->Q : 1;
+  const long long T = Qh * Kt;
+  const int tiles = (int)(e->L / LT) * CTn;
+  a.n_syn_tiles = tiles;
+  const int P = e->aur ? (int)e->P : 0;
+  const long long U = e->aur ? (long long)e->L * e->KF : 0;
+  if (T > INT32_MAX / 2 || U > INT32_MAX / 2) fail(AURA_B200_E_INVALID_ARGUMENT, "filters too long");
+  // stage sizes: ~32 KB per stage, a whole number of tap phases
+  const int target_f4 = 32 * 1024 / 16;
+  const int syn_row = (LT + XL) * CT;
+  a.sp = PH * std::max(1, target_f4 / (PH * syn_row));
+  const int afc_row = (P + 1) * CT;
+  a.spa = PH * std::max(1, target_f4 / (PH * std::max(afc_row, 1)));
+  long long slot = 0;
+  if (T > 0) slot = std::max<long long>(slot, (long long)a.sp * syn_row);
+  if (U > 0)  // W rows, canceller FDL rows, then E_p and the power of the column tile
+    slot = std::max<long long>(slot, (long long)a.spa * P * CT + (long long)(a.spa + 1) * CT +
+                                         (long long)(P + 1) * CT);
+  a.slot_f4 = (int)slot;
+  const int rmax = std::max(LT, P + 1);
+  a.red_f4 = std::max({kConsumers, 64 * rmax, NF});
+  const size_t budget = 200 * 1024;
+  const size_t fixed = kBackBarrierBytes + (size_t)a.red_f4 * 16;
+  const size_t per = (size_t)a.slot_f4 * 16;
+  a.stages = per ? (int)std::min<size_t>(kMaxStages, (budget - fixed) / per) : 0;
+  if (e->has_back() && a.stages < 2)
+    fail(AURA_B200_E_INVALID_ARGUMENT, "block size / channel tile too large for the streaming kernel");
+  e->smem_back = fixed + (size_t)a.stages * per;
+  // footprint: keep the spectra in L2 across blocks when they fit
+  const double foot = 8.0 * N * ((double)e->L * Qh * e->K + (double)e->Qx * e->K +
+                                 (double)P * U + (double)(e->aur ? e->L * (e->KF + 1) : 0));
+  a.h_in_l2 = foot < 80e6 ? 1 : 0;
+  // grid: one CTA per SM, fewer for small work (>= ~96 KB per CTA). Sized
+  // and planned from the synthesis alone when there is one, so the
+  // synthesis association -- and the output bits -- are the same with or
+  // without a canceller (test_auralizer.cpp:47-65 pins EXPECT_EQ).
+  const double syn_b = (double)tiles * T * syn_row * 16.0;
+  const double afc_b = (double)CTn * U * (P * (e->args.nlms ? 2 : 1) + 1) * CT * 16.0;
+  const double drive = T > 0 ? syn_b : afc_b;
+  const int ctas = (int)std::min<double>(e->sms, std::max(1.0, std::ceil(drive / (96.0 * 1024))));
+  e->back_ctas = ctas;
+  // Work: every CTA first runs a static piece of each of three phases -- the
+  // first 15% of every synthesis tile's taps (covers k_back_head, which the
+  // canceller waits for), the canceller units, the next 70% of the taps --
+  // then claims small queue items (the last 15%) so the CTAs finish
+  // together whatever their share of HBM bandwidth.
+  const long long TA = T > 0 ? std::max<long long>(1, (long long)std::ceil(0.15 * T)) : 0;
+  const long long TB = T > 0 ? std::max<long long>(TA, (long long)std::ceil(0.85 * T)) : 0;
+  const long long CQ = 2LL * a.sp;  // taps per queue item
+  std::vector<int4> chunks;
+  std::vector<int> item_off(ctas + 1, 0);
+  std::vector<std::vector<std::pair<int, int>>> at(tiles + CTn);  // per tile: (b, item)
+  auto push = [&](int kind, int tile, long long b, long long e_) {
+    at[kind ? tiles + tile : tile].push_back({(int)b, (int)chunks.size()});
+    chunks.push_back(make_int4(kind | (tile << 1), (int)b, (int)e_, 0));
+  };
+  struct Ph { int kind; long long lo, hi; int ntile; };  // items [lo, hi) of every tile
+  const Ph phases[3] = {{0, 0, TA, tiles}, {1, 0, U, CTn}, {0, TA, TB, tiles}};
+  for (int c = 0; c < ctas; ++c) {
+    item_off[c] = (int)chunks.size();
+    for (const Ph& ph : phases) {
+      const long long span = ph.hi - ph.lo;
+      if (span <= 0) continue;
+      const long long n_items = span * ph.ntile;
+      long long i0 = n_items * c / ctas, i1 = n_items * (c + 1) / ctas;
+      while (i0 < i1) {
+        const int tile = (int)(i0 / span);
+        const long long b = ph.lo + (i0 - (long long)tile * span);
+        const long long e_ = std::min<long long>(ph.hi, b + (i1 - i0));
+        push(ph.kind, tile, b, e_);
+        i0 += e_ - b;
+      }
+    }
   }
+  item_off[ctas] = (int)chunks.size();
+  a.n_static = (int)chunks.size();
+  {  // queue: tile-interleaved, so every tile's last partial lands near the end
+
+    long long nq = T > TB ? (T - TB + CQ - 1) / CQ : 0;
+    for (long long j = 0; j < nq; ++j)
+      for (int t = 0; t < tiles; ++t) push(0, t, TB + j * CQ, std::min<long long>(T, TB + (j + 1) * CQ));
+  }
+  std::vector<int> cnt(tiles + CTn);
+  for (int t = 0; t < tiles + CTn; ++t) {
+    std::sort(at[t].begin(), at[t].end());
+    cnt[t] = (int)at[t].size();
+    for (int i = 0; i < cnt[t]; ++i) chunks[at[t][i].second].w = i;
+  }
+  std::vector<int4> tinfo(tiles + CTn);
+  int slot_syn = 0, slot_afc = 0, max_syn = 1, max_afc = 1;
+  for (int t = 0; t < tiles + CTn; ++t) {
+    int& sl = t < tiles ? slot_syn : slot_afc;
+    tinfo[t] = make_int4(sl, cnt[t], 0, 0);
+    sl += cnt[t];
+    (t < tiles ? max_syn : max_afc) = std::max(t < tiles ? max_syn : max_afc, cnt[t]);
+  }
+  a.n_chunks = (int)chunks.size();
+  int* doff = dalloc<int>(item_off.size(), e->dmem);
+  CK(cudaMemcpy(doff, item_off.data(), item_off.size() * sizeof(int), cudaMemcpyHostToDevice));
+  a.item_off = doff;
+  e->n_syn_segs = slot_syn;
+  e->n_afc_segs = slot_afc;
+  e->h_chunks = chunks;
+  int4* dch = dalloc<int4>(std::max<size_t>(1, chunks.size()), e->dmem);
+  int4* dti = dalloc<int4>(std::max<size_t>(1, tinfo.size()), e->dmem);
+  if (!chunks.empty())
+    CK(cudaMemcpy(dch, chunks.data(), chunks.size() * sizeof(int4), cudaMemcpyHostToDevice));
+  if (!tinfo.empty()) CK(cudaMemcpy(dti, tinfo.data(), tinfo.size() * sizeof(int4), cudaMemcpyHostToDevice));
+  a.chunks = dch;
+  a.tinfo = dti;
+  // k_reduce geometry: ~16 partials per thread, elements split over CTAs
+  a.LTr = LT;
+  auto cpt_for = [&](int E, int maxcnt) {
+    const int sub = std::min(16, std::max(1, (maxcnt + 15) / 16));
+    const int ne = std::max(1, kReduceThreads / sub);
+    return (E + ne - 1) / ne;
+  };
+  a.red_syn_cpt = tiles ? cpt_for(LT * CT, max_syn) : 1;
+  a.red_syn_ctas = T > 0 ? tiles * a.red_syn_cpt : 0;
+  a.red_afc_rows = P + (e->args.nlms ? 1 : 0);
+  a.red_afc_cpt = U > 0 ? cpt_for(a.red_afc_rows * CT, max_afc) : 1;
+  a.red_afc_ctas = U > 0 ? CTn * a.red_afc_cpt : 0;
+  e->smem_reduce = (size_t)kReduceThreads * 16 + (e->aur ? 8 * ((size_t)N + table_f2(N)) : 0);
+  CK(cudaFuncSetAttribute(k_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem_reduce));
+  // tickets: [0] canceller CTAs of k_reduce, [1] all k_reduce CTAs, [2] work queue
+  a.tick_queue = 2;
+  a.tick = dalloc<unsigned>(3, e->dmem);
+  CK(cudaMemset(a.tick, 0, 3 * sizeof(unsigned)));
+  a.part_syn = dalloc<float4>(std::max<size_t>(1, (size_t)slot_syn * LT * CT), e->dmem);
+  if (e->aur) {
+    const size_t R = (size_t)P + 1;
+    a.part_afc = dalloc<float4>(std::max<size_t>(1, (size_t)slot_afc * R * CT), e->dmem);
+    a.yhat = dalloc<float4>(R * NF, e->dmem);
+    CK(cudaMemset(a.yhat, 0, sizeof(float4) * R * NF));
+  }
+  switch (LT) {
+    case 1: e->back_fn = back_for<1>(elem, e->PT); break;
+    case 2: e->back_fn = back_for<2>(elem, e->PT); break;
+    case 4: e->back_fn = back_for<4>(elem, e->PT); break;
+    default: e->back_fn = back_for<8>(elem, e->PT); break;
+  }
+  if (e->has_back())
+    CK(cudaFuncSetAttribute(e->back_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem_back));
 }
 
 void common_init(aura_b200_engine* e, int device) {
@@ -444,26 +536,16 @@ void common_init(aura_b200_engine* e, int device) {
     fail(AURA_B200_E_BACKEND_UNAVAILABLE,
          std::string("accelerator backend needs an sm_100 (B200) device, found ") + prop.name);
   e->device = device;
+  e->sms = prop.multiProcessorCount;
   CK(cudaSetDevice(device));
   CK(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
-  int least = 0, greatest = 0;
-  CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
-  e->prio_high = greatest;
-  CK(cudaStreamCreateWithPriority(&e->side, cudaStreamNonBlocking, greatest));
-  CK(cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming));
-  CK(cudaEventCreateWithFlags(&e->ev_join, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&e->ev_front, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&e->ev_back, cudaEventDisableTiming));
 }
 
-// CTAs that tick the block ticket (retire_block): the final reducer of every
-// synthesis channel group x column tile, and the canceller's final CTA (or,
-// sharded, the k_afc_finish CTA).
-void set_advance_total(aura_b200_engine* e) {
-  BlockArgs& a = e->args;
-  a.advance_total = (int)((e->has_pre() ? (e->L / e->LT) * (size_t)a.syn_tiles : 0) +
-                          (e->aur ? 1 : 0));
-}
+// CTAs that tick the block ticket in retire_block: only the sharded
+// canceller's k_afc_finish (k_back retires a block itself).
+void set_advance_total(aura_b200_engine* e) { e->args.advance_total = e->sharded() ? 1 : 0; }
 
 void finish_init(aura_b200_engine* e) {
   BlockArgs& a = e->args;
@@ -496,29 +578,16 @@ void finish_init(aura_b200_engine* e) {
   a.out = dout;
   a.cur_mt = dalloc<float>(std::max<size_t>(1, e->Q) * N, e->dmem);
   CK(cudaMemset(a.cur_mt, 0, sizeof(float) * std::max<size_t>(1, e->Q) * N));
-  // contiguous copy of every row's partition 0 for the front kernel
-  {
-    const size_t Qh = e->mode == AURA_B200_MIMO ? e->Q : 1;
-    float4* h0 = dalloc<float4>(e->L * Qh * NF, e->dmem);
-    CK(cudaMemcpy2D(h0, NF * sizeof(float4), a.H, e->K * NF * sizeof(float4), NF * sizeof(float4),
-                    e->L * Qh, cudaMemcpyDeviceToDevice));
-    a.H0 = h0;
-  }
   set_advance_total(e);
   // front: one CTA per cpb output channels
-  a.cpb = (int)std::max<size_t>(1, (e->L + kSMs - 1) / kSMs);
+  a.cpb = (int)std::max<size_t>(1, (e->L + e->sms - 1) / e->sms);
   const size_t Qs = e->mode == AURA_B200_ELEMENTWISE ? 1 : e->Q;
-  e->smem_front = 8 * N * (Qs + 2);
-  e->smem_head = 16 * N;
+  e->smem_front = 8 * N * (Qs + 2) + 8 * (size_t)table_f2((int)N);
+  e->smem_head = 24 * N + 8 * (size_t)table_f2((int)N);
   if (e->smem_front > 227 * 1024)
     fail(AURA_B200_E_INVALID_ARGUMENT, "block size too large for this many inputs (shared memory)");
-  e->smem_afc = 8 * N;  // c2r scratch of the canceller's final CTA
   CK(cudaFuncSetAttribute(k_front, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem_front));
   CK(cudaFuncSetAttribute(k_back_head, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem_head));
-  CK(cudaFuncSetAttribute(k_mac_afc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem_afc));
-  CK(cudaFuncSetAttribute(k_mac_afc<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem_afc));
-  CK(cudaFuncSetAttribute(k_mac_afc<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem_afc));
-  CK(cudaFuncSetAttribute(k_mac_afc<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem_afc));
   // device-resident I/O variant for measurement
   e->pool_blocks = 64;
   e->d_in_pool = dalloc<float>(e->pool_blocks * in_ch * N, e->dmem);
@@ -565,24 +634,34 @@ void alloc_synth(aura_b200_engine* e, BlockArgs& a) {
   a.L = (int)e->L;
   a.K = (int)e->K;
   a.mode = e->mode;
-  const size_t T = e->mode == AURA_B200_MIMO ? e->Q * e->K : e->K;
-  a.H = dalloc<float4>(e->L * T * NF, e->dmem);
+  a.CT = (int)std::min<size_t>(NF, 32);
+  a.CTn = (int)(NF / a.CT);
+  const size_t Qh = e->mode == AURA_B200_MIMO ? e->Q : 1;
+  a.Ht = dalloc<float4>(std::max<size_t>(1, e->L * Qh * (e->K - 1) * NF), e->dmem);
+  a.H0 = dalloc<float4>(e->L * Qh * NF, e->dmem);
   a.X = dalloc<float4>((size_t)e->Qx * e->K * NF, e->dmem);
   a.prev_in = dalloc<float>((size_t)e->Qx * N, e->dmem);
   CK(cudaMemset(a.X, 0, sizeof(float4) * (size_t)e->Qx * e->K * NF));
   CK(cudaMemset(a.prev_in, 0, sizeof(float) * e->Qx * N));
 }
 
-void upload_synth(aura_b200_engine* e, BlockArgs& a, const float* const* rows,
-                  size_t n_rows, size_t n_h) {
-  const size_t NF = e->N / 2;
-  std::vector<size_t> off(n_rows);
+// Synthesis spectra: partition 0 -> H0 [L][Qh][NF]; partitions k >= 1 ->
+// Ht [L/LT][CTn][T][LT][CT], tap t = q (K-1) + k - 1 (kernels.cuh).
+void upload_synth(aura_b200_engine* e, BlockArgs& a, const float* const* rows, size_t n_rows,
+                  size_t n_h) {
+  const long long NF = (long long)e->N / 2, CT = a.CT, CTn = a.CTn, LT = e->LT;
+  const long long Qh = e->mode == AURA_B200_MIMO ? (long long)e->Q : 1;
+  const long long Kt = (long long)e->K - 1, T = Qh * Kt;
+  std::vector<long long> base(n_rows), base0(n_rows);
   for (size_t r = 0; r < n_rows; ++r) {
-    size_t l = r, q = 0;
-    if (e->mode == AURA_B200_MIMO) { q = r / e->L; l = r % e->L; }
-    off[r] = ((l * (e->mode == AURA_B200_MIMO ? e->Q : 1) + q) * e->K) * NF;
+    long long l = (long long)r, q = 0;
+    if (e->mode == AURA_B200_MIMO) { q = (long long)(r / e->L); l = (long long)(r % e->L); }
+    const long long g = l / LT, i = l % LT;
+    base[r] = ((g * CTn) * T + q * Kt - 1) * LT * CT + i * CT;
+    base0[r] = (l * Qh + q) * NF;
   }
-  partition_rows(e, a, rows, n_rows, n_h, e->K, const_cast<float4*>(a.H), off);
+  PartOut o{const_cast<float4*>(a.Ht), const_cast<float4*>(a.H0), LT * CT, T * LT * CT, (int)CT};
+  partition_rows(e, a, rows, n_rows, n_h, e->K, o, base, base0);
 }
 
 void check_rows(const float* const* rows, size_t n_rows) {
@@ -673,8 +752,8 @@ int aura_b200_convolver_create(const aura_b200_config* cfg, int mode,
     a.is_aur = 0;
     a.nlms = 0;
     a.P = 0;
-    plan_split(e.get(), a);
-    alloc_split(e.get(), a);
+    e->PT = 0;
+    plan_back(e.get(), a);
     finish_init(e.get());
     *out = e.release();
   });
@@ -737,9 +816,17 @@ int aura_b200_auralizer_create(const aura_b200_config* cfg,
     a.nlms = mu > 0.0f;
     e->w_elems = Q * L * e->KF * NF;
     a.W = dalloc<float4>(e->w_elems, e->dmem);
-    std::vector<size_t> off(n_fc_rows);
-    for (size_t r = 0; r < n_fc_rows; ++r) off[r] = r * e->KF * NF;  // row p*L+l
-    partition_rows(e.get(), a, fc, n_fc_rows, n_hf, e->KF, a.W, off);
+    {  // W [CTn][L*KF][P][CT], row p*L + l
+      const long long CT = a.CT, KF = (long long)e->KF, P = (long long)Q;
+      const long long U = (long long)L * KF;
+      std::vector<long long> base(n_fc_rows);
+      for (size_t r = 0; r < n_fc_rows; ++r) {
+        const long long p = (long long)(r / L), l = (long long)(r % L);
+        base[r] = (l * KF * P + p) * CT;
+      }
+      PartOut o{a.W, nullptr, P * CT, U * P * CT, (int)CT};
+      partition_rows(e.get(), a, fc, n_fc_rows, n_hf, e->KF, o, base, {});
+    }
     if (a.nlms) {
       e->W0 = dalloc<float4>(e->w_elems, e->dmem);
       CK(cudaMemcpy(e->W0, a.W, sizeof(float4) * e->w_elems, cudaMemcpyDeviceToDevice));
@@ -755,8 +842,7 @@ int aura_b200_auralizer_create(const aura_b200_config* cfg,
     CK(cudaMemset(a.fhat, 0, sizeof(float) * Q * N));
     CK(cudaMemset(a.pw, 0, sizeof(float2) * N));
     CK(cudaMemset(a.E, 0, sizeof(float4) * Q * NF));
-    plan_split(e.get(), a);
-    alloc_split(e.get(), a);
+    plan_back(e.get(), a);
     finish_init(e.get());
     *out = e.release();
   });
@@ -864,10 +950,12 @@ int aura_b200_fdl_slot(aura_b200_engine* e, int which, size_t channel, size_t ag
     // block b's spectrum lives at slot b % cap; age a is block (blocks-1-a)
     const long long blk = (long long)e->blocks - 1 - (long long)age;
     std::vector<float2> buf(e->N, make_float2(0.f, 0.f));
-    if (blk >= 0) {
+    if (blk >= 0) {  // tiled [ch][CTn][cap][CT]
       const size_t slot = (size_t)(blk % (long long)cap);
-      CK(cudaMemcpy(buf.data(), base + (channel * cap + slot) * NF, sizeof(float2) * e->N,
-                    cudaMemcpyDeviceToHost));
+      const size_t CT = e->args.CT, CTn = e->args.CTn;
+      for (size_t c = 0; c < CTn; ++c)
+        CK(cudaMemcpy(buf.data() + 2 * c * CT, base + ((channel * CTn + c) * cap + slot) * CT,
+                      sizeof(float4) * CT, cudaMemcpyDeviceToHost));
     }
     unpack_row(buf.data(), e->N, out);
   });
@@ -902,8 +990,16 @@ int aura_b200_filter_spectrum(aura_b200_engine* e, size_t row, size_t k, float* 
     const size_t NF = e->N / 2;
     const size_t Qh = e->mode == AURA_B200_MIMO ? e->Q : 1;
     std::vector<float2> buf(e->N);
-    CK(cudaMemcpy(buf.data(), e->args.H + ((l * Qh + q) * e->K + k) * NF,
-                  sizeof(float2) * e->N, cudaMemcpyDeviceToHost));
+    if (k == 0) {
+      CK(cudaMemcpy(buf.data(), e->args.H0 + (l * Qh + q) * NF, sizeof(float2) * e->N,
+                    cudaMemcpyDeviceToHost));
+    } else {  // Ht [L/LT][CTn][T][LT][CT]
+      const size_t CT = e->args.CT, CTn = e->args.CTn, LT = e->LT;
+      const size_t Kt = e->K - 1, T = Qh * Kt, t = q * Kt + k - 1, g = l / LT, i = l % LT;
+      for (size_t c = 0; c < CTn; ++c)
+        CK(cudaMemcpy(buf.data() + 2 * c * CT, e->args.Ht + (((g * CTn + c) * T + t) * LT + i) * CT,
+                      sizeof(float4) * CT, cudaMemcpyDeviceToHost));
+    }
     unpack_row(buf.data(), e->N, out);
   });
 }
@@ -913,10 +1009,18 @@ int aura_b200_afc_coeffs(aura_b200_engine* e, float* out) {
     if (!e->aur) fail(AURA_B200_E_INVALID_ARGUMENT, "not an auralizer");
     CK(cudaSetDevice(e->device));
     CK(cudaStreamSynchronize(e->stream));
-    std::vector<float2> buf(e->w_elems * 2);
+    std::vector<float4> buf(e->w_elems);
     CK(cudaMemcpy(buf.data(), e->args.W, sizeof(float4) * e->w_elems, cudaMemcpyDeviceToHost));
-    const size_t rows = e->P * e->L * e->KF;
-    for (size_t r = 0; r < rows; ++r) unpack_row(buf.data() + r * e->N, e->N, out + r * 2 * (e->N + 1));
+    // tiled [CTn][U][P][CT] -> reference rows [p][l][k], N + 1 bins each
+    const size_t CT = e->args.CT, CTn = e->args.CTn, P = e->P, U = e->L * e->KF;
+    std::vector<float4> row(e->N / 2);
+    for (size_t p = 0; p < P; ++p)
+      for (size_t u = 0; u < U; ++u) {
+        for (size_t c = 0; c < CTn; ++c)
+          std::memcpy(&row[c * CT], &buf[((c * U + u) * P + p) * CT], sizeof(float4) * CT);
+        unpack_row(reinterpret_cast<const float2*>(row.data()), e->N,
+                   out + (p * U + u) * 2 * (e->N + 1));
+      }
   });
 }
 
@@ -1027,6 +1131,11 @@ int aura_b200_shard_info(const aura_b200_engine* e, int* world, int* rank) {
 
 // ------------------------------------------------------------ measurement
 
+// Device-resident timing. block_us[b]: back-to-back block time, CUDA events
+// recorded on the engine stream between consecutive block graphs (so a
+// block's interval spans all of its kernels and the launch of the next).
+// latency_us[b] (optional, separate pass): block start -> output written,
+// from the graph's external event node after k_front.
 int aura_b200_time_device_blocks(aura_b200_engine* e, const float* host_in,
                                  size_t n_in_blocks, size_t blocks, float* latency_us,
                                  float* block_us) {
@@ -1038,40 +1147,59 @@ int aura_b200_time_device_blocks(aura_b200_engine* e, const float* host_in,
       const size_t nb = std::min(n_in_blocks, e->pool_blocks);
       CK(cudaMemcpy(e->d_in_pool, host_in, nb * per * sizeof(float), cudaMemcpyHostToDevice));
     }
-    // one block graph per pool slot (the input pointer is baked per slot);
-    // its output-event node is re-pointed at a fresh timing event per block
-    std::vector<aura_b200_engine::BlockGraph> gs;
+    // one block graph per pool slot (the input pointer is baked per slot)
     const size_t slots = std::max<size_t>(1, std::min(n_in_blocks, e->pool_blocks));
-    cudaEvent_t proto;
-    CK(cudaEventCreate(&proto));
+    std::vector<aura_b200_engine::BlockGraph> gs;
     for (size_t s = 0; s < slots; ++s) {
       BlockArgs a = e->dev_args;
       a.in = e->d_in_pool + s * per;
-      gs.push_back(e->capture_block(a, proto));
+      gs.push_back(e->capture_block(a, nullptr));
     }
-    std::vector<cudaEvent_t> ev(3 * blocks);
+    std::vector<cudaEvent_t> ev(blocks + 1);
     for (auto& x : ev) CK(cudaEventCreate(&x));
     for (size_t b = 0; b < blocks; ++b) {
-      auto& g = gs[b % slots];
-      CK(cudaGraphExecEventRecordNodeSetEvent(g.ex, g.out_node, ev[3 * b + 1]));
-      CK(cudaEventRecord(ev[3 * b], e->stream));
-      CK(cudaGraphLaunch(g.ex, e->stream));
-      CK(cudaEventRecord(ev[3 * b + 2], e->stream));
+      CK(cudaEventRecord(ev[b], e->stream));
+      CK(cudaGraphLaunch(gs[b % slots].ex, e->stream));
     }
+    CK(cudaEventRecord(ev[blocks], e->stream));
     CK(cudaStreamSynchronize(e->stream));
     for (size_t b = 0; b < blocks; ++b) {
       float ms = 0.f;
-      if (latency_us) {
-        CK(cudaEventElapsedTime(&ms, ev[3 * b], ev[3 * b + 1]));
-        latency_us[b] = ms * 1000.0f;
-      }
-      CK(cudaEventElapsedTime(&ms, ev[3 * b], ev[3 * b + 2]));
+      CK(cudaEventElapsedTime(&ms, ev[b], ev[b + 1]));
       block_us[b] = ms * 1000.0f;
     }
-    for (auto& x : ev) cudaEventDestroy(x);
     for (auto& g : gs) g.destroy();
-    cudaEventDestroy(proto);
     e->blocks += blocks;
+    if (latency_us) {
+      // separate pass: the output-ready event node is re-pointed per block
+      cudaEvent_t proto;
+      CK(cudaEventCreate(&proto));
+      std::vector<aura_b200_engine::BlockGraph> gl;
+      for (size_t s = 0; s < slots; ++s) {
+        BlockArgs a = e->dev_args;
+        a.in = e->d_in_pool + s * per;
+        gl.push_back(e->capture_block(a, proto));
+      }
+      std::vector<cudaEvent_t> ev2(2 * blocks);
+      for (auto& x : ev2) CK(cudaEventCreate(&x));
+      for (size_t b = 0; b < blocks; ++b) {
+        auto& g = gl[b % slots];
+        CK(cudaGraphExecEventRecordNodeSetEvent(g.ex, g.out_node, ev2[2 * b + 1]));
+        CK(cudaEventRecord(ev2[2 * b], e->stream));
+        CK(cudaGraphLaunch(g.ex, e->stream));
+      }
+      CK(cudaStreamSynchronize(e->stream));
+      for (size_t b = 0; b < blocks; ++b) {
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, ev2[2 * b], ev2[2 * b + 1]));
+        latency_us[b] = ms * 1000.0f;
+      }
+      for (auto& x : ev2) cudaEventDestroy(x);
+      for (auto& g : gl) g.destroy();
+      cudaEventDestroy(proto);
+      e->blocks += blocks;
+    }
+    for (auto& x : ev) cudaEventDestroy(x);
   });
 }
 
@@ -1140,8 +1268,10 @@ int aura_b200_profile_phases(aura_b200_engine* e, size_t blocks, float* phase_us
 
 int aura_b200_time_phase(aura_b200_engine* e, int phase, size_t reps, float* avg_us) {
   return guarded([&] {
-    if (phase != PH_MAC_PRE && phase != PH_FRONT)
-      fail(AURA_B200_E_INVALID_ARGUMENT, "only idempotent phases can be re-launched");
+    if (phase != PH_BACK && phase != PH_FRONT)
+      fail(AURA_B200_E_INVALID_ARGUMENT, "only the front and the streaming kernel can be re-launched");
+    if (phase == PH_BACK && !e->has_back())
+      fail(AURA_B200_E_INVALID_ARGUMENT, "this engine has no streaming work");
     CK(cudaSetDevice(e->device));
     CK(cudaStreamSynchronize(e->stream));
     BlockArgs a = e->dev_args;
@@ -1186,18 +1316,82 @@ int aura_b200_trace_blocks(aura_b200_engine* e, size_t blocks, double* out) {
     CK(cudaMemcpy(tr.data(), dtr, words * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
     cudaFree(dtr);
     g.destroy();
-    // out[i][k][2]: start/end in microseconds relative to block i's front start
+    // out[i][k][2]: start/end in microseconds relative to block i's front
+    // start; slot kTraceKernels-1 holds {next block's front start, 0}: the
+    // back-to-back cycle time. The device block counter (not e->blocks)
+    // names the trace slots: measurement relaunches may have advanced it.
+    DevState dst{};
+    CK(cudaMemcpy(&dst, e->args.st, sizeof(dst), cudaMemcpyDeviceToHost));
+    (void)first;
+    const uint64_t dev_first = (uint64_t)dst.block - blocks;
     for (size_t i = 0; i < blocks; ++i) {
-      const size_t slot = (first + i) % kTraceBlocks;
+      const size_t slot = (dev_first + i) % kTraceBlocks;
       const unsigned long long t0 = tr[(slot * kTraceKernels + TR_FRONT) * 2];
-      for (int k = 0; k < kTraceKernels; ++k) {
+      for (int k = 0; k < kTraceKernels - 1; ++k) {
         const unsigned long long s0 = tr[(slot * kTraceKernels + k) * 2];
         const unsigned long long s1 = tr[(slot * kTraceKernels + k) * 2 + 1];
         const bool ran = s0 != ~0ull;
         out[(i * kTraceKernels + k) * 2] = ran ? (double)(long long)(s0 - t0) * 1e-3 : -1.0;
         out[(i * kTraceKernels + k) * 2 + 1] = ran ? (double)(long long)(s1 - t0) * 1e-3 : -1.0;
       }
+      const size_t nslot = (dev_first + i + 1) % kTraceBlocks;
+      const unsigned long long t1 = tr[(nslot * kTraceKernels + TR_FRONT) * 2];
+      const bool nxt = i + 1 < blocks && t1 != ~0ull;
+      out[(i * kTraceKernels + kTraceKernels - 1) * 2] = nxt ? (double)(long long)(t1 - t0) * 1e-3 : -1.0;
+      out[(i * kTraceKernels + kTraceKernels - 1) * 2 + 1] = 0.0;
     }
+    e->blocks += blocks;
+  });
+}
+
+// Diagnostics: run `blocks` blocks with k_back's per-chunk / per-CTA
+// %globaltimer stamps on; report the last block's, in us from k_back's
+// earliest CTA start. out_segs[i] = {kind, tile, b, e, cta, start_us,
+// partial_written_us, end_us} per item; out_ctas[c] = {start_us,
+// first_data_us, exit_us}. Sizes via
+// *n_segs / *n_ctas (call with null outputs first).
+int aura_b200_trace_back(aura_b200_engine* e, size_t blocks, double* out_segs, size_t* n_segs,
+                         double* out_ctas, size_t* n_ctas) {
+  return guarded([&] {
+    const size_t ns = e->h_chunks.size(), nc = (size_t)e->back_ctas;
+    if (!out_segs || !out_ctas) {
+      *n_segs = ns;
+      *n_ctas = nc;
+      return;
+    }
+    if (!e->has_back()) fail(AURA_B200_E_INVALID_ARGUMENT, "this engine has no streaming work");
+    CK(cudaSetDevice(e->device));
+    CK(cudaStreamSynchronize(e->stream));
+    const size_t words = 4 * ns + 3 * nc;
+    unsigned long long* d = nullptr;
+    CK(cudaMalloc(&d, words * sizeof(unsigned long long)));
+    BlockArgs a = e->dev_args;
+    a.seg_trace = d;
+    auto g = e->capture_block(a, nullptr);
+    blocks = std::max<size_t>(1, blocks);
+    for (size_t i = 0; i < blocks; ++i) CK(cudaGraphLaunch(g.ex, e->stream));
+    CK(cudaStreamSynchronize(e->stream));
+    std::vector<unsigned long long> h(words);
+    CK(cudaMemcpy(h.data(), d, words * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    cudaFree(d);
+    g.destroy();
+    unsigned long long t0 = ~0ull;
+    for (size_t c = 0; c < nc; ++c) t0 = std::min(t0, h[4 * ns + 3 * c]);
+    auto us = [&](unsigned long long t) { return (double)(long long)(t - t0) * 1e-3; };
+    for (size_t i = 0; i < ns; ++i) {
+      const int4 s = e->h_chunks[i];
+      double* o = out_segs + 8 * i;
+      o[0] = s.x & 1;
+      o[1] = s.x >> 1;
+      o[2] = s.y;
+      o[3] = s.z;
+      o[4] = (double)h[4 * i + 3];
+      o[5] = us(h[4 * i]);
+      o[6] = us(h[4 * i + 1]);
+      o[7] = us(h[4 * i + 2]);
+    }
+    for (size_t c = 0; c < nc; ++c)
+      for (int k = 0; k < 3; ++k) out_ctas[3 * c + k] = us(h[4 * ns + 3 * c + k]);
     e->blocks += blocks;
   });
 }
@@ -1213,13 +1407,15 @@ int aura_b200_describe(const aura_b200_engine* e, char* buf, size_t cap) {
   return guarded([&] {
     const BlockArgs& a = e->args;
     std::snprintf(buf, cap,
-                  "N=%zu Q=%zu L=%zu P=%zu K=%zu KF=%zu mode=%d LT=%d PT=%d | front: grid=%zu "
-                  "cpb=%d smem=%zu | mac_pre: chunks=%d tc=%d nft=%d tiles=%d grid=(%d,%zu,%d)x%d "
-                  "| mac_afc: chunks=%d uc=%d nft=%d tiles=%d nlms=%d delta=%g",
+                  "N=%zu Q=%zu L=%zu P=%zu K=%zu KF=%zu mode=%d LT=%d PT=%d | front: grid=%zu cpb=%d "
+                  "smem=%zu | back: ctas=%d x %d thr, CT=%d CTn=%d sp=%d spa=%d stages=%d slot=%d B "
+                  "smem=%zu partials=%zu+%zu items=%d (static %d) | reduce: %d+%d ctas l2keep=%d "
+                  "nlms=%d delta=%g",
                   e->N, e->Q, e->L, e->P, e->K, e->KF, e->mode, e->LT, e->PT,
-                  (e->L + a.cpb - 1) / a.cpb, a.cpb, e->smem_front, a.syn_chunks, a.syn_tc,
-                  a.syn_nft, a.syn_tiles, a.syn_chunks, e->L / e->LT, a.syn_tiles, kMacThreads,
-                  a.afc_chunks, a.afc_uc, a.afc_nft, a.afc_tiles, a.nlms, (double)a.delta);
+                  (e->L + a.cpb - 1) / a.cpb, a.cpb, e->smem_front, e->back_ctas, kBackThreads, a.CT,
+                  a.CTn, a.sp, a.spa, a.stages, a.slot_f4 * 16, e->smem_back, e->n_syn_segs,
+                  e->n_afc_segs, a.n_chunks, a.n_static, a.red_syn_ctas, a.red_afc_ctas, a.h_in_l2, a.nlms,
+                  (double)a.delta);
   });
 }
 

@@ -21,6 +21,21 @@
 
 namespace aura_b200 {
 
+// The threads that run a transform together: the whole CTA (Cta), or the
+// 256 consumer threads of the warp-specialised streaming kernel (named
+// barrier 1, so its producer warp never has to join).
+struct Cta {
+  __device__ __forceinline__ int tid() const { return threadIdx.x; }
+  __device__ __forceinline__ int size() const { return blockDim.x; }
+  __device__ __forceinline__ void sync() const { __syncthreads(); }
+};
+template <int NT>
+struct Consumers {
+  __device__ __forceinline__ int tid() const { return threadIdx.x; }
+  __device__ __forceinline__ int size() const { return NT; }
+  __device__ __forceinline__ void sync() const { asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory"); }
+};
+
 // (a.x c - a.y d, a.x d + a.y c), each product rounded (= libstdc++
 // complex<float> multiply on x86-64 without FMA).
 __device__ __forceinline__ float2 cmul_rn(float2 a, float2 b) {
@@ -41,23 +56,36 @@ __device__ __forceinline__ float2 half_of(float2 a) {
 // In-place radix-2 DIT FFT of size M on shared z (input already in
 // bit-reversed order), butterflies as dft.hpp:163-176. tw[j] =
 // e^{-2 pi i j / M}, j < M/2. Ends with a barrier.
-__device__ void fft_dit_smem(float2* z, int M, const float2* __restrict__ tw) {
+template <typename Team = Cta>
+__device__ void fft_dit_smem(float2* z, int M, const float2* __restrict__ tw, Team tm = Team()) {
   for (int len = 2; len <= M; len <<= 1) {
     const int h = len >> 1;
     const int stride = M / len;
-    for (int b = threadIdx.x; b < (M >> 1); b += blockDim.x) {
+    for (int b = tm.tid(); b < (M >> 1); b += tm.size()) {
       const int pos = b & (h - 1);
       const int i0 = ((b - pos) << 1) + pos;  // base + k
       const int i1 = i0 + h;
-      const float2 w = __ldg(&tw[pos * stride]);
+      const float2 w = tw[pos * stride];
       const float2 u = z[i0];
       const float2 v = cmul_rn(z[i1], w);
       z[i0] = cadd_rn(u, v);
       z[i1] = csub_rn(u, v);
     }
-    __syncthreads();
+    tm.sync();
   }
 }
+
+// Stage the DftPlan tables in shared memory (tw: N/2, split: N/2 + 1 float2)
+// so the butterfly stages read them at shared-memory latency instead of one
+// dependent L2 round trip per stage. No barrier: the caller syncs.
+template <typename Team = Cta>
+__device__ __forceinline__ void stage_tables(float2* s_tw, float2* s_split, const float2* __restrict__ tw,
+                                             const float2* __restrict__ split, int N, Team tm = Team()) {
+  for (int j = tm.tid(); j < N / 2; j += tm.size()) s_tw[j] = __ldg(tw + j);
+  for (int j = tm.tid(); j <= N / 2; j += tm.size()) s_split[j] = __ldg(split + j);
+}
+// shared-memory float2 count of the staged tables
+__host__ __device__ constexpr int table_f2(int N) { return N + 2; }
 
 __device__ __forceinline__ int bitrev(int m, int logM) {
   return (int)(__brev((unsigned)m) >> (32 - logM));
@@ -67,15 +95,16 @@ __device__ __forceinline__ int bitrev(int m, int logM) {
 // `spec` (N complex; shared or global). z: N float2 shared scratch.
 // split[k] = e^{-2 pi i k / (2N)}, k <= N/2. dft.hpp:69-101. Ends with a
 // barrier.
+template <typename Team = Cta>
 __device__ void rfft_packed(const float* win, float2* z, float2* spec, int N,
                             int logN, const float2* __restrict__ tw,
-                            const float2* __restrict__ split) {
-  for (int m = threadIdx.x; m < N; m += blockDim.x)
+                            const float2* __restrict__ split, Team tm = Team()) {
+  for (int m = tm.tid(); m < N; m += tm.size())
     z[bitrev(m, logN)] = make_float2(win[2 * m], win[2 * m + 1]);
-  __syncthreads();
-  fft_dit_smem(z, N, tw);
+  tm.sync();
+  fft_dit_smem(z, N, tw, tm);
   const int H = N >> 1;
-  for (int k = threadIdx.x; k <= H; k += blockDim.x) {
+  for (int k = tm.tid(); k <= H; k += tm.size()) {
     if (k == 0) {
       const float2 z0 = z[0];
       spec[0] = make_float2(__fadd_rn(z0.x, z0.y), __fsub_rn(z0.x, z0.y));
@@ -87,13 +116,13 @@ __device__ void rfft_packed(const float* win, float2* z, float2* spec, int N,
     // odd = (0, -0.5) * (a - b), evaluated as the complex product
     const float2 d = csub_rn(a, b);
     const float2 odd = cmul_rn(make_float2(0.0f, -0.5f), d);
-    const float2 rot = cmul_rn(__ldg(&split[k]), odd);
+    const float2 rot = cmul_rn(split[k], odd);
     const float2 lo = cadd_rn(even, rot);
     const float2 hi = conjf2(csub_rn(even, rot));
     if (k != H) spec[k] = lo;  // at k = N/2 the reference's second store wins
     spec[N - k] = hi;
   }
-  __syncthreads();
+  tm.sync();
 }
 
 // c2r of the packed spectrum `spec` (shared, N complex) into the LAST N
@@ -101,13 +130,13 @@ __device__ void rfft_packed(const float* win, float2* z, float2* spec, int N,
 // convolver.hpp:202-205), scaled by 1/(2N): store(i, x[N + i]).
 // dft.hpp:124-153 (merge, conj -> forward FFT -> conj, scale 1/half).
 // z: N float2 shared scratch. Ends with a barrier.
-template <typename Store>
+template <typename Store, typename Team = Cta>
 __device__ void irfft_packed_tail(const float2* spec, float2* z, int N,
                                   int logN, const float2* __restrict__ tw,
                                   const float2* __restrict__ split,
-                                  Store store) {
+                                  Store store, Team tm = Team()) {
   const int H = N >> 1;
-  for (int k = threadIdx.x; k < N; k += blockDim.x) {
+  for (int k = tm.tid(); k < N; k += tm.size()) {
     float2 zk;
     if (k == 0) {
       const float2 s = spec[0];  // (DC, Nyquist)
@@ -120,9 +149,9 @@ __device__ void irfft_packed_tail(const float2* spec, float2* z, int N,
       const float2 even = half_of(cadd_rn(a, b));
       float2 tw2;
       if (k <= H) {
-        tw2 = __ldg(&split[k]);
+        tw2 = split[k];
       } else {
-        const float2 s = conjf2(__ldg(&split[N - k]));
+        const float2 s = conjf2(split[N - k]);
         tw2 = make_float2(-s.x, -s.y);
       }
       const float2 odd = cmul_rn(conjf2(tw2), half_of(csub_rn(a, b)));
@@ -131,16 +160,16 @@ __device__ void irfft_packed_tail(const float2* spec, float2* z, int N,
     }
     z[bitrev(k, logN)] = zk;
   }
-  __syncthreads();
-  fft_dit_smem(z, N, tw);
+  tm.sync();
+  fft_dit_smem(z, N, tw, tm);
   const float scale = 1.0f / (float)N;
   // samples N .. 2N-1 are z[m] for m in [N/2, N)
-  for (int m = threadIdx.x; m < H; m += blockDim.x) {
+  for (int m = tm.tid(); m < H; m += tm.size()) {
     const float2 v = z[H + m];
     store(2 * m, __fmul_rn(v.x, scale));
     store(2 * m + 1, __fmul_rn(-v.y, scale));
   }
-  __syncthreads();
+  tm.sync();
 }
 
 }  // namespace aura_b200

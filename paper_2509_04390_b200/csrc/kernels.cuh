@@ -1,34 +1,34 @@
-// kernels.cuh -- the per-block UPOLS + feedback-canceller kernels (sm_100a).
+// kernels.cuh -- the small per-block kernels of the UPOLS + feedback-
+// canceller block loop (sm_100a); the streaming MACs are in stream.cuh.
 //
-// Block n runs as two CUDA graphs on one stream; completion is observed by
-// the host through stream events (no system-scope fences inside kernels).
+// Block n is ONE CUDA graph on the engine stream:
 //
-//  FRONT (the latency-critical path, one kernel):
 //   k_front       m~ = g m - f^ (auralizer.hpp:73-76), window + r2c of every
 //                 input (convolver.hpp:180-191), FDL push, then per output
 //                 channel  Y_l = S_l + sum_q X_q,n (.) H_{l,q}[0],  c2r +
 //                 overlap-save straight into the (mapped) output buffer.
-//
-//  BACK (off the critical path; two concurrent branches, then k_advance):
-//   branch 1: k_mac_pre
-//                 S_l for block n+1 = sum_{j=0}^{K-2} X(age j) (.) H_l[j+1]:
-//                 every partition but the first depends only on inputs <= n.
-//   branch 2: k_back_head -> k_mac_afc [-> k_afc_finish when sharded]
-//                 canceller stage 1 on l_n (r2c, FDL push), NLMS error
-//                 spectra, canceller MAC with the fused NLMS update and the
-//                 loudspeaker power, one c2r per mic -> f^ for block n+1.
-//   Both MACs end with a fused split-K reduction (split_k_reduce): the last
-//   CTA of each group of chunks sums that group, the last group-reducer sums
-//   the groups -- no separate reduction kernel. The CTAs that finish a
-//   reduction tree tick the block ticket; the last one advances the block
-//   counter (k_advance only when a block has no MAC).
+//                 --> event node: the host returns the block here.
+//   k_back_head   canceller stage 1 on l_n (r2c, FDL push) and the NLMS error
+//                 spectra; triggers its dependent launch immediately, so
+//   k_back        (stream.cuh, programmatic dependent launch) starts its
+//                 synthesis stream while k_back_head runs: S_l for block
+//                 n+1 (every partition but the first -- they depend only on
+//                 inputs <= n) and the canceller MAC + NLMS -> f^ for n+1.
+//   k_afc_finish  only when the loudspeakers are sharded over GPUs.
 //
 // So the output of block n is c2r(X_n H_0 + sum_{k>=1} X_{n-k} H_k), exactly
 // the reference's accumulator (backend.hpp:212-235) with the partition sum
 // split in two; the work per block is unchanged, only its position in time.
-// All reductions run in a fixed order -- split-K partials are summed chunk
-// by chunk, then group by group, whichever CTA happens to arrive last -- so
-// results are bit-reproducible run to run (test_convolver.cpp:172-193).
+// All reductions run in a fixed order, so results are bit-reproducible run to
+// run (test_convolver.cpp:172-193).
+//
+// Device layouts (N = block size, NF = N/2 float4 per packed spectrum, CT =
+// min(NF, 32) float4 columns per column tile, CTn = NF / CT):
+//   input FDL X       [Qx][CTn][K][CT]         ring slot = block mod K
+//   canceller FDL XA  [L][CTn][KF+1][CT]       ring slot = block mod (KF+1)
+//   spectra H (k>=1)  [L/LT][CTn][Qh*(K-1)][LT][CT]   tap t = q (K-1) + k - 1
+//   partition 0  H0   [L][Qh][NF]
+//   canceller W       [CTn][L*KF][P][CT]       unit u = l KF + k
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -56,9 +56,7 @@ struct DevState {
 // kernel, the earliest CTA start and the latest CTA end.
 constexpr int kTraceBlocks = 64;
 constexpr int kTraceKernels = 8;
-enum TraceId {
-  TR_FRONT = 0, TR_MAC_PRE, TR_TAIL_PRE, TR_BACK_HEAD, TR_MAC_AFC, TR_TAIL_AFC, TR_AFC_FINISH
-};
+enum TraceId { TR_FRONT = 0, TR_BACK_HEAD, TR_BACK, TR_REDUCE, TR_AFC_DONE, TR_AFC_FINISH };
 
 // Loudspeaker-channel sharding: at most kMaxShards engines
 // (one per GPU, or virtual shards on one GPU) exchange their canceller
@@ -78,11 +76,29 @@ struct BlockArgs {
   int is_aur, nlms;
   float gain, mu, lambda, delta;
   int cpb;           // output channels per front CTA
-  int advance_total; // CTAs of the tail kernels that retire the block (ticket)
+  int advance_total; // CTAs that retire the block (k_afc_finish only; k_back counts its own)
   unsigned long long* trace;  // [kTraceBlocks][kTraceKernels][2] or null
-  // split-K geometry
-  int syn_chunks, syn_tc, syn_nft, syn_tiles, syn_g1;  // g1: chunks per level-1 reducer
-  int afc_chunks, afc_uc, afc_nft, afc_tiles, afc_g1;
+  // streaming kernel k_back (stream.cuh): tiling, pipeline, host-planned work
+  int CT, CTn;       // float4 columns per column tile, column tiles
+  int sp, spa;       // synthesis taps / canceller units per pipeline stage
+  int stages;        // shared-memory ring depth
+  int slot_f4;       // float4 per ring slot
+  int red_f4;        // float4 of reduction (and c2r) scratch
+  int n_syn_tiles;   // (L/LT) * CTn
+  int h_in_l2;       // spectra fit in L2: stream them with evict_normal
+  const int4* chunks;   // work items {kind | tile << 1, b, e, partial slot in tile}:
+                        //   [n_static] per-CTA static pieces, then [n_chunks - n_static] queue
+  int n_chunks, n_static;
+  const int* item_off;  // [ctas + 1] static items of each CTA
+  const int4* tinfo;    // per tile (synthesis, then canceller column tiles):
+                        //   {first partial, partials, first group, groups}
+  unsigned* tick;       // k_reduce tickets: [0] canceller CTAs, [1] all CTAs; [tick_queue] work queue
+  int tick_queue;
+  int LTr;              // channels per synthesis tile
+  int red_syn_ctas, red_syn_cpt;  // k_reduce: synthesis CTAs, CTAs per tile
+  int red_afc_ctas, red_afc_cpt;  // canceller CTAs, CTAs per column tile
+  int red_afc_rows;               // canceller partial rows: P (+1 power row with NLMS)
+  unsigned long long* seg_trace;  // diagnostics: [chunks] x {end, cta}, then [ctas] x {start, first data, exit}
   // tables
   const float2* tw;     // N/2, e^{-2 pi i j / N}
   const float2* split;  // N/2+1, e^{-2 pi i k / (2N)}
@@ -90,23 +106,19 @@ struct BlockArgs {
   DevState* st;
   float* prev_in;       // Qx x N    previous input block (after g m - f^)
   float* cur_mt;        // Q x N     this block's m~ (front -> background)
-  float4* X;            // input FDL [Qx][K][NF]
-  const float4* H;      // spectra   [L][Qh][K][NF] (Qh = Q for mimo, else 1)
+  float4* X;            // input FDL (tiled, see above)
+  const float4* Ht;     // spectra, partitions >= 1 (tiled)
   const float4* H0;     // partition 0 of every row, contiguous [L][Qh][NF]
   float4* S;            // [L][NF]   precomputed partitions >= 1 for next block
-  float4* part_syn;     // [syn_chunks][L][NF]   split-K partials
-  float4* part_syn2;    // [ceil(syn_chunks/8)][L][NF] level-2 partials
-  unsigned* tick_syn;   // [L/LT][syn_tiles][ceil(syn_chunks/8) + 1] reduction tickets
+  float4* part_syn;     // split-K partials [slot][LT][CT] (one per chunk)
   float* prev_spk;      // L x N     previous loudspeaker block
   float* spk;           // L x N     l_n (device copy for the canceller stage)
-  float4* XA;           // canceller FDL [L][KF+1][NF]
-  float4* W;            // canceller spectra [P][L][KF][NF]
+  float4* XA;           // canceller FDL (tiled)
+  float4* W;            // canceller spectra (tiled)
   float2* pw;           // [N]       smoothed power (packed: bin0 = DC,Nyq)
   float4* E;            // [P][NF]   error spectra
-  float4* part_afc;     // [afc_chunks][P+1][NF] (row P: loudspeaker power)
-  float4* part_afc2;    // [ceil(afc_chunks/8)][P+1][NF]
+  float4* part_afc;     // split-K partials [slot][P + nlms][CT] (row P: loudspeaker power)
   float4* yhat;         // [P+1][NF]  reduced canceller spectra (+ power row)
-  unsigned* tick_afc;   // [afc_tiles][ceil(afc_chunks/8) + 1] + 1 (tiles)
   float* fhat;          // P x N     feedback estimate for the next block
   float* fhat_host;     // P x N     same, mapped pinned host copy
   // sharding (G > 1): this engine is shard `grank` of G
@@ -202,99 +214,17 @@ __device__ void retire_block(const BlockArgs& a, uint32_t n) {
   }
 }
 
-// Sum cnt partial rows src[i*stride] (i = 0..cnt-1) for E elements with the
-// whole CTA. Each element gets `sub` threads; thread j of an element sums a
-// fixed contiguous range of rows in order with 8 loads in flight, and the
-// sub-sums are then added in j order through shared `red` (>= blockDim
-// float4). Fixed association => deterministic. Ends with a barrier.
-template <typename Src, typename Dst>
-__device__ void ordered_sum(int E, int cnt, size_t stride, Src src, Dst dst, float4* red) {
-  const int T = blockDim.x;
-  int sub = E >= T ? 1 : min(T / E, (cnt + 3) / 4);
-  sub = max(sub, 1);
-  const int per = (cnt + sub - 1) / sub;
-  const int active = E * sub;
-  for (int base = 0; base < E * sub; base += T) {
-    const int t = base + threadIdx.x;
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (t < active) {
-      const int e = t % E, j = t / E;
-      const int i0 = j * per, i1 = min(cnt, i0 + per);
-      const float4* p = src(e);
-      int i = i0;
-      if (i < i1) v = __ldcg(p + (size_t)i * stride);
-      ++i;
-      for (; i + 8 <= i1; i += 8) {
-        float4 b[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) b[u] = __ldcg(p + (size_t)(i + u) * stride);
-#pragma unroll
-        for (int u = 0; u < 8; ++u) v = f4add(v, b[u]);
-      }
-      for (; i < i1; ++i) v = f4add(v, __ldcg(p + (size_t)i * stride));
-      if (sub == 1) dst(e, v);
-    }
-    if (sub > 1) {
-      red[threadIdx.x] = v;
-      __syncthreads();
-      // T is a multiple of E*sub here (E*sub <= T), so base == 0
-      if (threadIdx.x < E) {
-        float4 w = red[threadIdx.x];
-        for (int j = 1; j < sub; ++j) w = f4add(w, red[j * E + threadIdx.x]);
-        dst(threadIdx.x, w);
-      }
-    }
+// Store the packed spectrum spec (N float2, shared) as ring slot `slot` of
+// delay-line channel ch, tiled [ch][CTn][cap][CT] float4 (see above).
+__device__ __forceinline__ void push_tiled(const BlockArgs& a, float4* fdl, int ch, int cap, int slot,
+                                           const float2* spec) {
+  const int CT = a.CT;
+  float2* d = reinterpret_cast<float2*>(fdl);
+  for (int j = threadIdx.x; j < a.N; j += blockDim.x) {
+    const int f = j >> 1;
+    const size_t i4 = (((size_t)ch * a.CTn + f / CT) * cap + slot) * CT + (f % CT);
+    d[2 * i4 + (j & 1)] = spec[j];
   }
-  __syncthreads();
-}
-
-// Fused, deterministic split-K reduction (the epilogue of both MACs).
-// Chunk `chunk` of `nchunks` has just written its partial: R rows x columns
-// [c0, c0 + nc) at part + chunk*cs + r*rs + c. Level 1: the last CTA to
-// arrive in each group of `gsz` consecutive chunks sums the group in chunk
-// order (into part2, or straight into out when there is one group); level
-// 2: the last level-1 reducer sums the groups in group order into
-// out + r*os + c. Which CTA arrives last never changes the association, so
-// the result is bit-reproducible. Tickets t1[group] and *t2 start at 0 and
-// are reset by their reducer. red: >= blockDim float4 of shared scratch.
-// Returns true in exactly one CTA: the one holding the final result.
-__device__ __noinline__ bool split_k_reduce(const float4* part, float4* part2, size_t cs, size_t rs, int R,
-                               int c0, int nc, int chunk, int nchunks, int gsz, unsigned* t1,
-                               unsigned* t2, float4* out, size_t os, float4* red) {
-  __shared__ unsigned s_last;
-  const int g = chunk / gsz;
-  const int n1 = (nchunks + gsz - 1) / gsz;
-  const int gsize = min(gsz, nchunks - g * gsz);
-  const int E = R * nc;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) s_last = atomicAdd(&t1[g], 1u) == (unsigned)gsize - 1u;
-  __syncthreads();
-  if (!s_last) return false;
-  if (threadIdx.x == 0) t1[g] = 0u;
-  __threadfence();
-  const float4* src0 = part + (size_t)g * gsz * cs;
-  auto at = [&](int e) { return (size_t)(e / nc) * rs + c0 + (e % nc); };
-  auto oat = [&](int e) { return (size_t)(e / nc) * os + c0 + (e % nc); };
-  if (n1 == 1) {
-    ordered_sum(E, gsize, cs, [&](int e) { return src0 + at(e); },
-                [&](int e, float4 v) { __stcg(out + oat(e), v); }, red);
-  } else {
-    ordered_sum(E, gsize, cs, [&](int e) { return src0 + at(e); },
-                [&](int e, float4 v) { __stcg(part2 + (size_t)g * cs + at(e), v); }, red);
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) s_last = atomicAdd(t2, 1u) == (unsigned)n1 - 1u;
-    __syncthreads();
-    if (!s_last) return false;
-    if (threadIdx.x == 0) *t2 = 0u;
-    __threadfence();
-    ordered_sum(E, n1, cs, [&](int e) { return (const float4*)part2 + at(e); },
-                [&](int e, float4 v) { __stcg(out + oat(e), v); }, red);
-  }
-  __threadfence();
-  __syncthreads();
-  return true;
 }
 
 // ------------------------------------------------------------- k_front
@@ -310,6 +240,9 @@ __global__ void __launch_bounds__(kFrontThreads) k_front(BlockArgs a) {
   float2* z = Xs + (size_t)Qs * N;                        // N
   float* wa = reinterpret_cast<float*>(z + N);            // 2N (window / acc)
   float2* acc = reinterpret_cast<float2*>(wa);
+  float2* tw = reinterpret_cast<float2*>(wa + 2 * N);     // DftPlan tables
+  float2* split = tw + N / 2;
+  stage_tables(tw, split, a.tw, a.split, N);
 
   const uint32_t n = a.st->block;
   trace_begin(a, TR_FRONT, n);
@@ -330,11 +263,8 @@ __global__ void __launch_bounds__(kFrontThreads) k_front(BlockArgs a) {
         wa[N + i] = v;
       }
       __syncthreads();
-      rfft_packed(wa, z, Xs + (size_t)q * N, N, a.logN, a.tw, a.split);
-      if (blockIdx.x == 0) {
-        float2* dst = reinterpret_cast<float2*>(a.X + ((size_t)q * a.K + n % (uint32_t)a.K) * NF);
-        for (int j = threadIdx.x; j < N; j += blockDim.x) dst[j] = Xs[(size_t)q * N + j];
-      }
+      rfft_packed(wa, z, Xs + (size_t)q * N, N, a.logN, tw, split);
+      if (blockIdx.x == 0) push_tiled(a, a.X, q, a.K, (int)(n % (uint32_t)a.K), Xs + (size_t)q * N);
     }
   }
 
@@ -349,9 +279,8 @@ __global__ void __launch_bounds__(kFrontThreads) k_front(BlockArgs a) {
       }
       __syncthreads();
       for (int i = threadIdx.x; i < N; i += blockDim.x) prev[i] = wa[N + i];
-      rfft_packed(wa, z, Xs, N, a.logN, a.tw, a.split);
-      float2* dst = reinterpret_cast<float2*>(a.X + ((size_t)l * a.K + n % (uint32_t)a.K) * NF);
-      for (int j = threadIdx.x; j < N; j += blockDim.x) dst[j] = Xs[j];
+      rfft_packed(wa, z, Xs, N, a.logN, tw, split);
+      push_tiled(a, a.X, l, a.K, (int)(n % (uint32_t)a.K), Xs);
     }
     const float2* Sl = reinterpret_cast<const float2*>(a.S + (size_t)l * NF);
     for (int j = threadIdx.x; j < N; j += blockDim.x) {
@@ -366,7 +295,7 @@ __global__ void __launch_bounds__(kFrontThreads) k_front(BlockArgs a) {
     float* out = a.out + (size_t)l * N;
     float* sp = a.spk + (size_t)l * N;
     const bool keep = a.is_aur;
-    irfft_packed_tail(acc, z, N, a.logN, a.tw, a.split, [&](int i, float v) {
+    irfft_packed_tail(acc, z, N, a.logN, tw, split, [&](int i, float v) {
       out[i] = v;
       if (keep) sp[i] = v;
     });
@@ -375,15 +304,22 @@ __global__ void __launch_bounds__(kFrontThreads) k_front(BlockArgs a) {
 }
 
 // ---------------------------------------------------------- k_back_head
-// Background of block n, canceller branch head. CTA l < L (auralizer):
-// canceller stage 1 on l_n (convolver.hpp:180-191 on fc_); CTAs [Lb, Lb + P): NLMS error spectra E_p = r2c([0_N,
-// m~_p]) (Appendix A step 2). CTA 0 also moves this block's m~ into the
-// input window history (broadcast / mimo).
+// Canceller branch head of block n. CTA l < L (auralizer): canceller stage 1
+// on l_n (convolver.hpp:180-191 on fc_): r2c([l_{n-1}, l_n]), FDL push; CTAs
+// [L, L + P): NLMS error spectra E_p = r2c([0_N, m~_p]) (Appendix A step 2).
+// CTA 0 also moves this block's m~ into the input window history
+// (broadcast / mimo). It lets k_back launch at once (PDL): k_back's
+// canceller work waits for this grid with griddepcontrol.wait.
 __global__ void __launch_bounds__(kFrontThreads) k_back_head(BlockArgs a) {
   extern __shared__ float4 smem4[];
-  const int N = a.N, NF = a.NF;
+  const int N = a.N;
   float2* z = reinterpret_cast<float2*>(smem4);  // N
   float* wa = reinterpret_cast<float*>(z + N);   // 2N
+  float2* sp = reinterpret_cast<float2*>(wa + 2 * N);  // N (spectrum)
+  float2* tw = sp + N;                                  // DftPlan tables
+  float2* split = tw + N / 2;
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  stage_tables(tw, split, a.tw, a.split, N);
   const uint32_t n = a.st->block;
   trace_begin(a, TR_BACK_HEAD, n);
   const int Lb = a.is_aur ? a.L : 1;
@@ -397,16 +333,15 @@ __global__ void __launch_bounds__(kFrontThreads) k_back_head(BlockArgs a) {
   if (b < Lb) {
     const int l = b;
     float* prev = a.prev_spk + (size_t)l * N;
-    const float* sp = a.spk + (size_t)l * N;
+    const float* spk = a.spk + (size_t)l * N;
     for (int i = threadIdx.x; i < N; i += blockDim.x) {
       wa[i] = prev[i];
-      wa[N + i] = sp[i];
+      wa[N + i] = spk[i];
     }
     __syncthreads();
     for (int i = threadIdx.x; i < N; i += blockDim.x) prev[i] = wa[N + i];
-    float2* xnew = reinterpret_cast<float2*>(
-        a.XA + ((size_t)l * (a.KF + 1) + n % (uint32_t)(a.KF + 1)) * NF);
-    rfft_packed(wa, z, xnew, N, a.logN, a.tw, a.split);
+    rfft_packed(wa, z, sp, N, a.logN, tw, split);
+    push_tiled(a, a.XA, l, a.KF + 1, (int)(n % (uint32_t)(a.KF + 1)), sp);
   } else {
     const int p = b - Lb;
     for (int i = threadIdx.x; i < N; i += blockDim.x) {
@@ -414,271 +349,13 @@ __global__ void __launch_bounds__(kFrontThreads) k_back_head(BlockArgs a) {
       wa[N + i] = a.cur_mt[(size_t)p * N + i];
     }
     __syncthreads();
-    rfft_packed(wa, z, reinterpret_cast<float2*>(a.E + (size_t)p * NF), N, a.logN, a.tw,
-                a.split);
+    rfft_packed(wa, z, reinterpret_cast<float2*>(a.E + (size_t)p * a.NF), N, a.logN, tw, split);
   }
   trace_end(a, TR_BACK_HEAD, n);
 }
 
 // ------------------------------------------------------------ k_advance
-__global__ void k_advance(DevState* st) { st->block += 1u; }  // blocks without tails
-
-// ------------------------------------------------------------ k_mac_pre
-// Split-K partials of S_l(n+1) = sum_q sum_{j=0}^{K-2} X_q(age j) H_{l,q}[j+1]
-// (backend.hpp:212-235 over every partition but the first).
-// grid = (syn_chunks, L/LT, syn_tiles), 256 threads; thread (kp, f): column
-// f of the tile, tap phase kp. LT channels share every X load (broadcast /
-// mimo): X comes from L2, H streams from HBM with 128-bit no-L1 loads.
-// ELEM: channel l reads FDL channel l.
-template <int LT, bool ELEM>
-__global__ void __launch_bounds__(kMacThreads, 2) k_mac_pre(BlockArgs a) {
-  __shared__ float4 red[kMacThreads * LT];
-  const int nft = a.syn_nft;
-  const int KP = kMacThreads / nft;
-  const int fl = threadIdx.x & (nft - 1);
-  const int kp = threadIdx.x / nft;
-  const int f = blockIdx.z * nft + fl;
-  const int l0 = blockIdx.y * LT;
-  const int K = a.K;
-  const int Kt = K - 1;                      // taps per input
-  const int Qh = ELEM ? 1 : a.Q;
-  const int T = Qh * Kt;
-  const int t0 = blockIdx.x * a.syn_tc;
-  const int t1 = min(t0 + a.syn_tc, T);
-  const uint32_t n = a.st->block;
-  trace_begin(a, TR_MAC_PRE, n);
-  const int nk = (int)(n % (uint32_t)K);
-  const bool dc = (f == 0);
-  const int NF = a.NF;
-
-  float4 acc[LT];
-#pragma unroll
-  for (int i = 0; i < LT; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-
-  int t = t0 + kp;
-  int q = t / Kt;
-  int j = t - q * Kt;
-#pragma unroll 2
-  for (; t < t1; t += KP) {
-    int slot = nk - j;
-    if (slot < 0) slot += K;
-    const size_t hrow = (size_t)q * K + j + 1;  // partition j+1 of input q
-    if (ELEM) {
-#pragma unroll
-      for (int i = 0; i < LT; ++i) {
-        const float4 xv = a.X[((size_t)(l0 + i) * K + slot) * NF + f];
-        const float4 h = ld_stream(a.H + ((size_t)(l0 + i) * K + j + 1) * NF + f);
-        cmac(acc[i], xpack(xv, dc), h, dc);
-      }
-    } else {
-      const XPack x = xpack(a.X[((size_t)q * K + slot) * NF + f], dc);
-      float4 h[LT];
-#pragma unroll
-      for (int i = 0; i < LT; ++i)
-        h[i] = ld_stream(a.H + ((size_t)(l0 + i) * Qh * K + hrow) * NF + f);
-#pragma unroll
-      for (int i = 0; i < LT; ++i) cmac(acc[i], x, h[i], dc);
-    }
-    j += KP;
-    while (j >= Kt) {
-      j -= Kt;
-      ++q;
-    }
-  }
-#pragma unroll
-  for (int i = 0; i < LT; ++i) red[(kp * LT + i) * nft + fl] = acc[i];
-  __syncthreads();
-  for (int e = threadIdx.x; e < LT * nft; e += kMacThreads) {
-    const int i = e / nft, c = e - i * nft;
-    float4 s = red[i * nft + c];
-    for (int p = 1; p < KP; ++p) s = f4add(s, red[(p * LT + i) * nft + c]);
-    __stcg(a.part_syn + ((size_t)blockIdx.x * a.L + l0 + i) * NF + blockIdx.z * nft + c, s);
-  }
-  // fused split-K reduction -> S for this CTA's LT channels x nft columns
-  __syncthreads();  // red is reused as reduction scratch
-  const int n1 = (a.syn_chunks + a.syn_g1 - 1) / a.syn_g1;
-  unsigned* tk = a.tick_syn + ((size_t)blockIdx.y * gridDim.z + blockIdx.z) * (n1 + 1);
-  const bool fin = split_k_reduce(a.part_syn + (size_t)l0 * NF, a.part_syn2 + (size_t)l0 * NF,
-                                  (size_t)a.L * NF, NF, LT, blockIdx.z * nft, nft, blockIdx.x,
-                                  a.syn_chunks, a.syn_g1, tk, tk + n1, a.S + (size_t)l0 * NF, NF,
-                                  red);
-  trace_end(a, TR_MAC_PRE, n);
-  if (fin) retire_block(a, n);
-}
-
-// ----------------------------------------------------------- k_mac_afc
-// Canceller MAC over units u = (l, k), all P mics per unit (X_l shared):
-//   NLMS (Appendix A step 2): W += mu/(P+delta) * conj(X_l(pre-push age k)) E_p
-//   filter (step 4):          Yhat_p += W * X_l(post-push age k)
-//   power (step 5):           row P += |X_l(age 0)|^2 on the units k = 0
-// Pre-push age k is post-push age k+1: the canceller FDL keeps KF+1 slots.
-// grid = (afc_chunks, 1, afc_tiles), 256 threads. Epilogue: fused split-K
-// reduction per column tile into yhat; the last tile-finisher then does one
-// c2r per mic (the sum over l and k is done in the frequency domain -- one
-// c2r per mic instead of the reference's L, auralizer.hpp:81-86) -> f^ for
-// the next block, and smooths the power (or, sharded, leaves both partials
-// in xmine for k_afc_finish). Dynamic shared memory: N float2 (c2r scratch).
-template <int PT>
-__global__ void __launch_bounds__(kMacThreads, (PT <= 2 ? 4 : 2)) k_mac_afc(BlockArgs a) {
-  __shared__ float4 red[kMacThreads * (PT + 1)];
-  extern __shared__ float4 afc_dyn[];
-  __shared__ unsigned s_last_tile;
-  const int nft = a.afc_nft;
-  const int KP = kMacThreads / nft;
-  const int fl = threadIdx.x & (nft - 1);
-  const int kp = threadIdx.x / nft;
-  const int f = blockIdx.z * nft + fl;
-  const int N = a.N, NF = a.NF, KF = a.KF, L = a.L, P = a.P;
-  const int cap = KF + 1;
-  const int U = L * KF;
-  const int u0 = blockIdx.x * a.afc_uc;
-  const int u1 = min(u0 + a.afc_uc, U);
-  const uint32_t n = a.st->block;
-  trace_begin(a, TR_MAC_AFC, n);
-  const int nk = (int)(n % (uint32_t)cap);
-  const bool dc = (f == 0);
-  const int R = P + (a.nlms ? 1 : 0);  // partial rows (row P: power)
-
-  float4 acc[PT];
-  float4 e[PT];
-  float4 pacc = make_float4(0.f, 0.f, 0.f, 0.f);
-  float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-  for (int p = 0; p < PT; ++p) {
-    acc[p] = make_float4(0.f, 0.f, 0.f, 0.f);
-    e[p] = (a.nlms && p < P) ? a.E[(size_t)p * NF + f] : acc[p];
-  }
-  if (a.nlms) {
-    const float2 p0 = a.pw[2 * f], p1 = a.pw[2 * f + 1];
-    s = make_float4(__fdiv_rn(a.mu, __fadd_rn(p0.x, a.delta)),
-                    __fdiv_rn(a.mu, __fadd_rn(p0.y, a.delta)),
-                    __fdiv_rn(a.mu, __fadd_rn(p1.x, a.delta)),
-                    __fdiv_rn(a.mu, __fadd_rn(p1.y, a.delta)));
-  }
-
-  int u = u0 + kp;
-  int l = u / KF;
-  int k = u - l * KF;
-  for (; u < u1; u += KP) {
-    const float4* xl = a.XA + (size_t)l * cap * NF;
-    const float4 xv = xl[(size_t)ring(nk - k, cap) * NF + f];
-    const XPack x0 = xpack(xv, dc);
-    float4 x1 = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (a.nlms) {
-      x1 = xl[(size_t)ring(nk - k - 1, cap) * NF + f];
-      if (k == 0) {  // packed |X_l(age 0)|^2 (bin 0: DC^2, Nyquist^2), rounded as the oracle
-        if (dc) {
-          pacc.x = __fadd_rn(pacc.x, __fmul_rn(xv.x, xv.x));
-          pacc.y = __fadd_rn(pacc.y, __fmul_rn(xv.y, xv.y));
-        } else {
-          const float m = __fadd_rn(__fmul_rn(xv.x, xv.x), __fmul_rn(xv.y, xv.y));
-          pacc.x = __fadd_rn(pacc.x, m);
-          pacc.y = __fadd_rn(pacc.y, m);
-        }
-        const float m2 = __fadd_rn(__fmul_rn(xv.z, xv.z), __fmul_rn(xv.w, xv.w));
-        pacc.z = __fadd_rn(pacc.z, m2);
-        pacc.w = __fadd_rn(pacc.w, m2);
-      }
-    }
-#pragma unroll
-    for (int p = 0; p < PT; ++p) {
-      if (p >= P) break;
-      float4* wp = a.W + (((size_t)p * L + l) * KF + k) * NF + f;
-      float4 w = *wp;
-      if (a.nlms) {
-        // g = conj(x1) * E_p ; packed bin 0 is (DC, Nyquist) real products.
-        // Rounded exactly as the oracle (aura_oracle.c nlms_update): no FMA.
-        float4 g;
-        if (dc) {
-          g.x = __fmul_rn(x1.x, e[p].x);
-          g.y = __fmul_rn(x1.y, e[p].y);
-        } else {
-          g.x = __fadd_rn(__fmul_rn(x1.x, e[p].x), __fmul_rn(x1.y, e[p].y));
-          g.y = __fsub_rn(__fmul_rn(x1.x, e[p].y), __fmul_rn(x1.y, e[p].x));
-        }
-        g.z = __fadd_rn(__fmul_rn(x1.z, e[p].z), __fmul_rn(x1.w, e[p].w));
-        g.w = __fsub_rn(__fmul_rn(x1.z, e[p].w), __fmul_rn(x1.w, e[p].z));
-        w.x = __fadd_rn(w.x, __fmul_rn(s.x, g.x));
-        w.y = __fadd_rn(w.y, __fmul_rn(s.y, g.y));
-        w.z = __fadd_rn(w.z, __fmul_rn(s.z, g.z));
-        w.w = __fadd_rn(w.w, __fmul_rn(s.w, g.w));
-        *wp = w;
-      }
-      cmac(acc[p], x0, w, dc);
-    }
-    k += KP;
-    while (k >= KF) {
-      k -= KF;
-      ++l;
-    }
-  }
-#pragma unroll
-  for (int p = 0; p < PT; ++p) red[(kp * (PT + 1) + p) * nft + fl] = acc[p];
-  red[(kp * (PT + 1) + PT) * nft + fl] = pacc;
-  __syncthreads();
-  const size_t rows = (size_t)P + 1;
-  for (int e2 = threadIdx.x; e2 < R * nft; e2 += kMacThreads) {
-    const int r = e2 / nft, c = e2 - r * nft;
-    const int rr = r < P ? r : PT;  // power row
-    float4 t = red[rr * nft + c];
-    for (int q = 1; q < KP; ++q) t = f4add(t, red[(q * (PT + 1) + rr) * nft + c]);
-    __stcg(a.part_afc + ((size_t)blockIdx.x * rows + r) * NF + blockIdx.z * nft + c, t);
-  }
-  const int n1 = (a.afc_chunks + a.afc_g1 - 1) / a.afc_g1;
-  unsigned* tk = a.tick_afc + (size_t)blockIdx.z * (n1 + 1);
-  __syncthreads();  // red is reused as reduction scratch
-  const bool fin = split_k_reduce(a.part_afc, a.part_afc2, rows * NF, NF, R, blockIdx.z * nft, nft,
-                                  blockIdx.x, a.afc_chunks, a.afc_g1, tk, tk + n1, a.yhat, NF,
-                                  red);
-  if (!fin) {
-    trace_end(a, TR_MAC_AFC, n);
-    return;
-  }
-  // last of the column tiles finishes the block's canceller
-  if (gridDim.z > 1) {
-    if (threadIdx.x == 0) {
-      unsigned* tt = a.tick_afc + (size_t)gridDim.z * (n1 + 1);
-      s_last_tile = atomicAdd(tt, 1u) == gridDim.z - 1u;
-      if (s_last_tile) *tt = 0u;
-    }
-    __syncthreads();
-    if (!s_last_tile) {
-      trace_end(a, TR_MAC_AFC, n);
-      return;
-    }
-    __threadfence();
-  }
-  const bool sharded = a.G > 1;
-  float2* z = reinterpret_cast<float2*>(afc_dyn);
-  for (int p = 0; p < P; ++p) {
-    // sharded: this shard's partial f^_p (c2r is linear), summed by k_afc_finish
-    float* fh = sharded ? a.xmine + (size_t)p * N : a.fhat + (size_t)p * N;
-    float* fhh = a.fhat_host + (size_t)p * N;
-    irfft_packed_tail(reinterpret_cast<const float2*>(a.yhat + (size_t)p * NF), z, N, a.logN, a.tw,
-                      a.split, [&](int i, float v) {
-                        fh[i] = v;
-                        if (!sharded) fhh[i] = v;
-                      });
-  }
-  if (a.nlms) {
-    const float2* sum = reinterpret_cast<const float2*>(a.yhat + (size_t)P * NF);
-    const float oml = __fsub_rn(1.0f, a.lambda);
-    for (int j = threadIdx.x; j < N; j += blockDim.x) {
-      const float2 v = __ldcg(sum + j);
-      if (sharded) {  // partial power of this shard's loudspeakers
-        reinterpret_cast<float2*>(a.xmine + (size_t)P * N)[j] = v;
-        continue;
-      }
-      // Appendix A step 5: lambda P + (1 - lambda) sum_l |X_l|^2
-      float2 w = a.pw[j];
-      w.x = __fadd_rn(__fmul_rn(a.lambda, w.x), __fmul_rn(oml, v.x));
-      w.y = __fadd_rn(__fmul_rn(a.lambda, w.y), __fmul_rn(oml, v.y));
-      a.pw[j] = w;
-    }
-  }
-  trace_end(a, TR_MAC_AFC, n);
-  if (!sharded) retire_block(a, n);
-}
+__global__ void k_advance(DevState* st) { st->block += 1u; }  // blocks without k_back
 
 __device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
@@ -758,14 +435,26 @@ __global__ void __launch_bounds__(kTailThreads) k_afc_finish(BlockArgs a) {
 
 // ------------------------------------------------------ k_partition
 // Setup (make_partitioned_filters, convolver.hpp:19-46) on the GPU: CTA
-// (k, r) transforms taps[r][kN .. kN+N) zero-padded to 2N into the packed
-// spectrum dst + row_off[r] + k*NF. taps rows are n_h long.
+// (k, r) transforms taps[r][kN .. kN+N) zero-padded to 2N and scatters the
+// packed spectrum into the device layout: column f of partition k of row r
+// goes to dst[base[r] + k*kstride + (f/CT)*cstride + f%CT], except partition
+// 0 when dst0 is set (-> dst0[base0[r] + f]). taps rows are n_h long.
+struct PartOut {
+  float4* dst;
+  float4* dst0;
+  long long kstride, cstride;
+  int CT;
+};
 __global__ void __launch_bounds__(256) k_partition(
-    const float* __restrict__ taps, size_t n_h, int rows, int K, int N, int logN,
-    const float2* tw, const float2* split, float4* dst, const size_t* __restrict__ row_off) {
+    const float* __restrict__ taps, size_t n_h, int K, int N, int logN, const float2* tw,
+    const float2* split, PartOut o, const long long* __restrict__ base,
+    const long long* __restrict__ base0) {
   extern __shared__ float smem[];
-  float* win = smem;
-  float2* z = reinterpret_cast<float2*>(win + 2 * N);
+  float* win = smem;                                   // 2N floats, then the spectrum
+  float2* z = reinterpret_cast<float2*>(win + 2 * N);  // N
+  float2* stw = z + N;                                 // DftPlan tables
+  float2* ssplit = stw + N / 2;
+  stage_tables(stw, ssplit, tw, split, N);
   const int k = blockIdx.x;
   const int r = blockIdx.y;
   const size_t begin = (size_t)k * N;
@@ -775,8 +464,20 @@ __global__ void __launch_bounds__(256) k_partition(
     win[i] = (i < N && t < n_h) ? src[t] : 0.0f;
   }
   __syncthreads();
-  float2* out = reinterpret_cast<float2*>(dst + row_off[r] + (size_t)k * (N / 2));
-  rfft_packed(win, z, out, N, logN, tw, split);
+  float2* spec = reinterpret_cast<float2*>(win);  // rfft reads win before it writes spec
+  rfft_packed(win, z, spec, N, logN, stw, ssplit);
+  if (k == 0 && o.dst0) {
+    float2* d = reinterpret_cast<float2*>(o.dst0 + base0[r]);
+    for (int j = threadIdx.x; j < N; j += blockDim.x) d[j] = spec[j];
+    return;
+  }
+  float2* d = reinterpret_cast<float2*>(o.dst);
+  const long long b = base[r] + (long long)k * o.kstride;
+  for (int j = threadIdx.x; j < N; j += blockDim.x) {
+    const int f = j >> 1;
+    const long long i4 = b + (long long)(f / o.CT) * o.cstride + (f % o.CT);
+    d[2 * i4 + (j & 1)] = spec[j];
+  }
 }
 
 }  // namespace aura_b200
