@@ -148,6 +148,7 @@ struct aura_b200_engine {
   BlockGraph g_block;
   // streaming kernel k_back
   BackFn back_fn = nullptr;
+  bool pdl_off = false;  // measurement: serialise k_back / k_reduce launches
   int back_ctas = 0;
   size_t smem_back = 0, smem_reduce = 0;
   size_t n_syn_segs = 0, n_afc_segs = 0;
@@ -211,12 +212,13 @@ struct aura_b200_engine {
           k_back_head<<<(unsigned)(aur ? L + (a.nlms ? P : 0) : 1), kFrontThreads, smem_head, s>>>(a);
         break;
       case PH_BACK:
-        if (has_back()) launch_pdl(back_fn, (unsigned)back_ctas, kBackThreads, smem_back, has_head(), a, s);
+        if (has_back())
+          launch_pdl(back_fn, (unsigned)back_ctas, kBackThreads, smem_back, has_head() && !pdl_off, a, s);
         break;
       case PH_REDUCE:
         if (has_back())
           launch_pdl(k_reduce, (unsigned)(a.red_syn_ctas + a.red_afc_ctas), kReduceThreads, smem_reduce,
-                     true, a, s);
+                     !pdl_off, a, s);
         break;
       case PH_AFC_FINISH:
         if (sharded()) k_afc_finish<<<1, kTailThreads, 0, s>>>(a);
@@ -500,7 +502,7 @@ void plan_back(aura_b200_engine* e, BlockArgs& a) {
   a.red_afc_rows = P + (e->args.nlms ? 1 : 0);
   a.red_afc_cpt = U > 0 ? cpt_for(a.red_afc_rows * CT, max_afc) : 1;
   a.red_afc_ctas = U > 0 ? CTn * a.red_afc_cpt : 0;
-  e->smem_reduce = (size_t)kReduceThreads * 16 + (e->aur ? 8 * ((size_t)N + table_f2(N)) : 0);
+  e->smem_reduce = (size_t)kReduceThreads * 16 + (e->aur ? 8 * (2 * (size_t)N + table_f2(N)) : 0);
   CK(cudaFuncSetAttribute(k_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem_reduce));
   // tickets: [0] canceller CTAs of k_reduce, [1] all k_reduce CTAs, [2] work queue
   a.tick_queue = 2;
@@ -582,8 +584,21 @@ void finish_init(aura_b200_engine* e) {
   // front: one CTA per cpb output channels
   a.cpb = (int)std::max<size_t>(1, (e->L + e->sms - 1) / e->sms);
   const size_t Qs = e->mode == AURA_B200_ELEMENTWISE ? 1 : e->Q;
-  e->smem_front = 8 * N * (Qs + 2) + 8 * (size_t)table_f2((int)N);
-  e->smem_head = 24 * N + 8 * (size_t)table_f2((int)N);
+  // shared memory: the FFT work areas, then (when they fit) the DftPlan
+  // tables and the first channel's S and partition-0 spectra
+  e->smem_front = 8 * N * (Qs + 2);
+  e->smem_head = 24 * N;
+  const size_t tables = 8 * (size_t)table_f2((int)N);
+  a.smem_tables = std::max(e->smem_front, e->smem_head) + tables <= 200 * 1024 ? 1 : 0;
+  if (a.smem_tables) {
+    e->smem_front += tables;
+    e->smem_head += tables;
+  }
+  {
+    const size_t pre = 8 * N * (1 + Qs);
+    a.front_pre = e->smem_front + pre <= 160 * 1024 ? 1 : 0;
+    if (a.front_pre) e->smem_front += pre;
+  }
   if (e->smem_front > 227 * 1024)
     fail(AURA_B200_E_INVALID_ARGUMENT, "block size too large for this many inputs (shared memory)");
   CK(cudaFuncSetAttribute(k_front, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem_front));
@@ -1274,7 +1289,10 @@ int aura_b200_time_phase(aura_b200_engine* e, int phase, size_t reps, float* avg
       fail(AURA_B200_E_INVALID_ARGUMENT, "this engine has no streaming work");
     CK(cudaSetDevice(e->device));
     CK(cudaStreamSynchronize(e->stream));
+    // single launches, back to back without programmatic overlap, so the
+    // mean is one launch's duration (ramp-up and tail included)
     BlockArgs a = e->dev_args;
+    e->pdl_off = true;
     e->launch_phase(phase, a, e->stream);  // warm
     cudaEvent_t t0, t1;
     CK(cudaEventCreate(&t0));
@@ -1282,6 +1300,7 @@ int aura_b200_time_phase(aura_b200_engine* e, int phase, size_t reps, float* avg
     CK(cudaEventRecord(t0, e->stream));
     for (size_t r = 0; r < reps; ++r) e->launch_phase(phase, a, e->stream);
     CK(cudaEventRecord(t1, e->stream));
+    e->pdl_off = false;
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(e->stream));
     float ms = 0.f;

@@ -76,6 +76,8 @@ struct BlockArgs {
   int is_aur, nlms;
   float gain, mu, lambda, delta;
   int cpb;           // output channels per front CTA
+  int front_pre;     // k_front stages its first channel's S and H0 up front
+  int smem_tables;   // k_front / k_back_head stage the DftPlan tables in shared memory
   int advance_total; // CTAs that retire the block (k_afc_finish only; k_back counts its own)
   unsigned long long* trace;  // [kTraceBlocks][kTraceKernels][2] or null
   // streaming kernel k_back (stream.cuh): tiling, pipeline, host-planned work
@@ -236,19 +238,29 @@ __global__ void __launch_bounds__(kFrontThreads) k_front(BlockArgs a) {
   const int N = a.N, NF = a.NF;
   const bool elem = a.mode == 1;
   const int Qs = elem ? 1 : a.Q;
+  const int Qh = a.mode == 2 ? a.Q : 1;
   float2* Xs = reinterpret_cast<float2*>(smem4);          // Qs x N
   float2* z = Xs + (size_t)Qs * N;                        // N
   float* wa = reinterpret_cast<float*>(z + N);            // 2N (window / acc)
   float2* acc = reinterpret_cast<float2*>(wa);
-  float2* tw = reinterpret_cast<float2*>(wa + 2 * N);     // DftPlan tables
-  float2* split = tw + N / 2;
-  stage_tables(tw, split, a.tw, a.split, N);
-
-  const uint32_t n = a.st->block;
-  trace_begin(a, TR_FRONT, n);
+  float2* stw = reinterpret_cast<float2*>(wa + 2 * N);    // DftPlan tables (if staged)
+  float2* pre = stw + (a.smem_tables ? table_f2(N) : 0);  // [S_l, H0_l,q] of the first channel
+  const float2* tw = a.smem_tables ? stw : a.tw;
+  const float2* split = a.smem_tables ? stw + N / 2 : a.split;
   const int c0 = blockIdx.x * a.cpb;
   const int c1 = min(c0 + a.cpb, a.L);
-  const int Qh = a.mode == 2 ? a.Q : 1;
+
+  // ---- one round of independent loads: tables, input windows, and the
+  // first channel's precomputed S_l and partition-0 spectra (front_pre)
+  if (a.smem_tables) stage_tables(stw, stw + N / 2, a.tw, a.split, N);
+  if (a.front_pre) {
+    const float2* Sl = reinterpret_cast<const float2*>(a.S + (size_t)c0 * NF);
+    const float2* H0 = reinterpret_cast<const float2*>(a.H0 + (size_t)c0 * Qh * NF);
+    for (int j = threadIdx.x; j < N; j += blockDim.x) pre[j] = Sl[j];
+    for (int j = threadIdx.x; j < Qs * N; j += blockDim.x) pre[N + j] = H0[j];
+  }
+  const uint32_t n = a.st->block;
+  trace_begin(a, TR_FRONT, n);
 
   // ---- stage 1 for the shared inputs (broadcast / mimo)
   if (!elem) {
@@ -282,13 +294,12 @@ __global__ void __launch_bounds__(kFrontThreads) k_front(BlockArgs a) {
       rfft_packed(wa, z, Xs, N, a.logN, tw, split);
       push_tiled(a, a.X, l, a.K, (int)(n % (uint32_t)a.K), Xs);
     }
-    const float2* Sl = reinterpret_cast<const float2*>(a.S + (size_t)l * NF);
+    const bool staged = a.front_pre && l == c0;
+    const float2* Sl = staged ? pre : reinterpret_cast<const float2*>(a.S + (size_t)l * NF);
+    const float2* H0 = staged ? pre + N : reinterpret_cast<const float2*>(a.H0 + (size_t)l * Qh * NF);
     for (int j = threadIdx.x; j < N; j += blockDim.x) {
       float2 y = Sl[j];
-      for (int q = 0; q < Qs; ++q) {
-        const float2 h = reinterpret_cast<const float2*>(a.H0 + ((size_t)l * Qh + q) * NF)[j];
-        y = cmac2(y, Xs[(size_t)q * N + j], h, j == 0);
-      }
+      for (int q = 0; q < Qs; ++q) y = cmac2(y, Xs[(size_t)q * N + j], H0[(size_t)q * N + j], j == 0);
       acc[j] = y;
     }
     __syncthreads();
@@ -316,10 +327,11 @@ __global__ void __launch_bounds__(kFrontThreads) k_back_head(BlockArgs a) {
   float2* z = reinterpret_cast<float2*>(smem4);  // N
   float* wa = reinterpret_cast<float*>(z + N);   // 2N
   float2* sp = reinterpret_cast<float2*>(wa + 2 * N);  // N (spectrum)
-  float2* tw = sp + N;                                  // DftPlan tables
-  float2* split = tw + N / 2;
+  float2* stw = sp + N;                                 // DftPlan tables (if staged)
+  const float2* tw = a.smem_tables ? stw : a.tw;
+  const float2* split = a.smem_tables ? stw + N / 2 : a.split;
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  stage_tables(tw, split, a.tw, a.split, N);
+  if (a.smem_tables) stage_tables(stw, stw + N / 2, a.tw, a.split, N);
   const uint32_t n = a.st->block;
   trace_begin(a, TR_BACK_HEAD, n);
   const int Lb = a.is_aur ? a.L : 1;

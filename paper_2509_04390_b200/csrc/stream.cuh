@@ -474,7 +474,7 @@ __global__ void __launch_bounds__(kBackThreads, 1) k_back(const __grid_constant_
 // grid = red_syn_ctas + red_afc_ctas, kReduceThreads threads.
 constexpr int kReduceThreads = 256;
 __global__ void __launch_bounds__(kReduceThreads) k_reduce(const __grid_constant__ BlockArgs a) {
-  extern __shared__ float4 rsm[];  // kReduceThreads float4, then c2r scratch (N float2) + tables
+  extern __shared__ float4 rsm[];  // kReduceThreads float4; canceller: c2r scratch, tables, power
   __shared__ int s_last;
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int CT = a.CT, NF = a.NF;
@@ -492,6 +492,17 @@ __global__ void __launch_bounds__(kReduceThreads) k_reduce(const __grid_constant
   const int ne = e1 - e0;
   const int sub = max(1, kReduceThreads / max(ne, 1));
   const int per = (ti.y + sub - 1) / sub;
+  // canceller CTAs: stage the DftPlan tables and the smoothed power now --
+  // they do not depend on k_back -- for whichever of them finishes f^
+  float2* z = reinterpret_cast<float2*>(rsm + kReduceThreads);
+  float2* tw = z + a.N;
+  float2* split = tw + a.N / 2;
+  float2* pws = split + a.N / 2 + 1;
+  if (afc) {
+    stage_tables(tw, split, a.tw, a.split, a.N);
+    if (a.nlms)
+      for (int jj = threadIdx.x; jj < a.N; jj += blockDim.x) pws[jj] = a.pw[jj];
+  }
   griddep_wait();  // k_back's partials
   const uint32_t n = a.st->block;
   trace_begin(a, TR_REDUCE, n);
@@ -538,11 +549,6 @@ __global__ void __launch_bounds__(kReduceThreads) k_reduce(const __grid_constant
       // the canceller of block n is complete: f^ for block n+1
       const int N = a.N, P = a.P;
       const bool sharded = a.G > 1;
-      float2* z = reinterpret_cast<float2*>(rsm + kReduceThreads);
-      float2* tw = z + N;  // DftPlan tables
-      float2* split = tw + N / 2;
-      stage_tables(tw, split, a.tw, a.split, N);
-      __syncthreads();
       for (int p = 0; p < P; ++p) {
         // sharded: this shard's partial f^_p (c2r is linear), summed by k_afc_finish
         float* fh = sharded ? a.xmine + (size_t)p * N : a.fhat + (size_t)p * N;
@@ -562,7 +568,7 @@ __global__ void __launch_bounds__(kReduceThreads) k_reduce(const __grid_constant
             reinterpret_cast<float2*>(a.xmine + (size_t)P * N)[jj] = x;
             continue;
           }
-          float2 w = a.pw[jj];
+          float2 w = pws[jj];
           w.x = __fadd_rn(__fmul_rn(a.lambda, w.x), __fmul_rn(oml, x.x));
           w.y = __fadd_rn(__fmul_rn(a.lambda, w.y), __fmul_rn(oml, x.y));
           a.pw[jj] = w;
@@ -573,8 +579,6 @@ __global__ void __launch_bounds__(kReduceThreads) k_reduce(const __grid_constant
         atomicMin(&a.trace[((n % kTraceBlocks) * kTraceKernels + TR_AFC_DONE) * 2], now);
         atomicMax(&a.trace[((n % kTraceBlocks) * kTraceKernels + TR_AFC_DONE) * 2 + 1], now);
       }
-      __threadfence();
-      __syncthreads();
     }
   }
   trace_end(a, TR_REDUCE, n);

@@ -11,6 +11,6 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>
 timeout 900 python bench.py > $O/bench.json 2> $O/bench.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches.csv \
    python bench.py --steps 20 --warmup 3 --no-cpu-baseline --no-paced > $O/ncu_launch_bench.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_back|k_front' -s 30 -c 3 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:'^(k_back|k_front|k_reduce)$' -s 30 -c 3 \
    -o $O/prof python bench.py --steps 20 --warmup 3 --no-cpu-baseline --no-paced > $O/ncu_full.log 2>&1
 for f in $O/*.log; do tail -n 3 $f; done
