@@ -86,6 +86,23 @@ def load_peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def load_traffic(config_name, kernel):
+    """DRAM bytes per launch of `kernel` from the committed ncu capture
+    (profiles/ncu_traffic.json), or None."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f).get(config_name)
+    except (OSError, ValueError):
+        return None, None
+    if not d or d.get("kernel") != kernel:
+        return None, None
+    return float(d["dram_read_bytes"] + d["dram_write_bytes"]), d.get("source")
+
+
+READ_PROBE_GBS = 7379.1  # tools/bw_probe.cu on this pool's B200 (profiles/r1s3_c3_stream_kernel.md)
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
@@ -303,6 +320,7 @@ def run_b200_arm(args, cfg, rank, world, local_rank):
     mac_us = eng.time_phase(mac_name, 20)
     achieved = mac_bytes / (mac_us * 1e-6) / 1e9
     n_launch = eng.launches_per_block()
+    traffic, traffic_src = load_traffic(args.config if not args.block else None, mac_name)
 
     paced = None
     if not args.no_paced:
@@ -356,8 +374,10 @@ def run_b200_arm(args, cfg, rank, world, local_rank):
         "paced_e2e": paced,
         "roofline": {"bound": "hbm", "kernel": mac_name, "achieved": achieved,
                      "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "peak_kind": peak_kind, "traffic": None,
-                     "bytes_per_launch": mac_bytes, "avg_launch_us": mac_us},
+                     "peak_kind": peak_kind, "traffic": traffic, "traffic_source": traffic_src,
+                     "frac_of_read_probe": achieved / READ_PROBE_GBS,
+                     "bytes_per_launch": mac_bytes, "avg_launch_us": mac_us,
+                     "timing": "CUDA events around 20 single launches of the kernel, back to back"},
         "phases_us_serial": {k: v[0] for k, v in phases.items()},
         "timeline_us": timeline,
         "phase_bytes": {k: v[1] for k, v in phases.items()},
