@@ -176,6 +176,7 @@ def lib():
     L.aura_b200_reset.argtypes = [vp]
     L.aura_b200_feedback_estimate.argtypes = [vp, _f32p]
     L.aura_b200_set_input_gain.argtypes = [vp, C.c_float]
+    L.aura_b200_set_launch_mode.argtypes = [vp, C.c_int]
     L.aura_b200_input_gain.argtypes = [vp]
     L.aura_b200_input_gain.restype = C.c_float
     for name in ("blocks_processed",):
@@ -333,6 +334,10 @@ class _Engine:
         _check(lib().aura_b200_trace_back(self._h, blocks, segs.ctypes.data, C.byref(ns),
                                           ctas.ctypes.data, C.byref(nc)))
         return segs, ctas
+
+    def set_launch_mode(self, mode: int):
+        """0: one CUDA graph per block (default); 1: kernels on the stream."""
+        _check(lib().aura_b200_set_launch_mode(self._h, mode))
 
     PHASES = {"k_front": 0, "k_back": 2}
 

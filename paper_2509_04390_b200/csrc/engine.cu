@@ -149,6 +149,7 @@ struct aura_b200_engine {
   // streaming kernel k_back
   BackFn back_fn = nullptr;
   bool pdl_off = false;  // measurement: serialise k_back / k_reduce launches
+  int launch_mode = 0;   // 0: one CUDA graph per block; 1: kernels launched on the stream
   int back_ctas = 0;
   size_t smem_back = 0, smem_reduce = 0;
   size_t n_syn_segs = 0, n_afc_segs = 0;
@@ -257,6 +258,19 @@ struct aura_b200_engine {
     }
     CK(cudaGraphInstantiate(&bg.ex, bg.g, 0));
     return bg;
+  }
+
+  // Enqueue one block on the stream: the graph, or (launch_mode 1) the same
+  // kernels launched directly (PDL edges included); out_event is recorded
+  // after k_front.
+  void enqueue_block(const BlockGraph& g, const BlockArgs& a, cudaEvent_t out_event) {
+    if (launch_mode == 0) {
+      CK(cudaGraphLaunch(g.ex, stream));
+      return;
+    }
+    launch_phase(PH_FRONT, a, stream);
+    if (out_event) CK(cudaEventRecord(out_event, stream));
+    for (int ph = PH_BACK_HEAD; ph < PH_COUNT; ++ph) launch_phase(ph, a, stream);
   }
 
   void rebuild_graphs() {
@@ -428,7 +442,10 @@ void plan_back(aura_b200_engine* e, BlockArgs& a) {
   // together whatever their share of HBM bandwidth.
   const long long TA = T > 0 ? std::max<long long>(1, (long long)std::ceil(0.15 * T)) : 0;
   const long long TB = T > 0 ? std::max<long long>(TA, (long long)std::ceil(0.85 * T)) : 0;
-  const long long CQ = 2LL * a.sp;  // taps per queue item
+  // queue items: ~12 per CTA, at least two stages (keeps the tail short and
+  // the partial count -- k_reduce's input -- small at c5 sizes)
+  const long long qtaps = (T - TB) * tiles;
+  const long long CQ = std::max<long long>(2LL * a.sp, (qtaps / (12LL * ctas) + a.sp - 1) / a.sp * a.sp);
   std::vector<int4> chunks;
   std::vector<int> item_off(ctas + 1, 0);
   std::vector<std::vector<std::pair<int, int>>> at(tiles + CTn);  // per tile: (b, item)
@@ -504,10 +521,11 @@ void plan_back(aura_b200_engine* e, BlockArgs& a) {
   a.red_afc_ctas = U > 0 ? CTn * a.red_afc_cpt : 0;
   e->smem_reduce = (size_t)kReduceThreads * 16 + (e->aur ? 8 * (2 * (size_t)N + table_f2(N)) : 0);
   CK(cudaFuncSetAttribute(k_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem_reduce));
-  // tickets: [0] canceller CTAs of k_reduce, [1] all k_reduce CTAs, [2] work queue
+  // tickets: [0] canceller CTAs of k_reduce, [1] all k_reduce CTAs, [2] work
+  // queue, [3] k_back exits
   a.tick_queue = 2;
-  a.tick = dalloc<unsigned>(3, e->dmem);
-  CK(cudaMemset(a.tick, 0, 3 * sizeof(unsigned)));
+  a.tick = dalloc<unsigned>(4, e->dmem);
+  CK(cudaMemset(a.tick, 0, 4 * sizeof(unsigned)));
   a.part_syn = dalloc<float4>(std::max<size_t>(1, (size_t)slot_syn * LT * CT), e->dmem);
   if (e->aur) {
     const size_t R = (size_t)P + 1;
@@ -582,7 +600,7 @@ void finish_init(aura_b200_engine* e) {
   CK(cudaMemset(a.cur_mt, 0, sizeof(float) * std::max<size_t>(1, e->Q) * N));
   set_advance_total(e);
   // front: one CTA per cpb output channels
-  a.cpb = (int)std::max<size_t>(1, (e->L + e->sms - 1) / e->sms);
+  a.cpb = (int)std::max<size_t>(1, (e->L + 4 * e->sms - 1) / (4 * e->sms));
   const size_t Qs = e->mode == AURA_B200_ELEMENTWISE ? 1 : e->Q;
   // shared memory: the FFT work areas, then (when they fit) the DftPlan
   // tables and the first channel's S and partition-0 spectra
@@ -902,7 +920,7 @@ int aura_b200_process(aura_b200_engine* e, const float* in, float* out) {
     // the previous block's front has completed, so the staging buffer is free
     std::memcpy(e->h_in, in, n_in * sizeof(float));
     std::atomic_thread_fence(std::memory_order_release);
-    CK(cudaGraphLaunch(e->g_block.ex, e->stream));  // records ev_front after k_front
+    e->enqueue_block(e->g_block, e->args, e->ev_front);  // records ev_front after k_front
     CK(cudaEventRecord(e->ev_back, e->stream));
     wait_event(e, e->ev_front, "block output");
     std::memcpy(out, e->h_out, e->L * e->N * sizeof(float));
@@ -973,6 +991,15 @@ int aura_b200_fdl_slot(aura_b200_engine* e, int which, size_t channel, size_t ag
                       sizeof(float4) * CT, cudaMemcpyDeviceToHost));
     }
     unpack_row(buf.data(), e->N, out);
+  });
+}
+
+int aura_b200_set_launch_mode(aura_b200_engine* e, int mode) {
+  return guarded([&] {
+    if (mode != 0 && mode != 1) fail(AURA_B200_E_INVALID_ARGUMENT, "launch mode is 0 (graph) or 1 (stream)");
+    CK(cudaSetDevice(e->device));
+    CK(cudaStreamSynchronize(e->stream));
+    e->launch_mode = mode;
   });
 }
 
@@ -1172,9 +1199,11 @@ int aura_b200_time_device_blocks(aura_b200_engine* e, const float* host_in,
     }
     std::vector<cudaEvent_t> ev(blocks + 1);
     for (auto& x : ev) CK(cudaEventCreate(&x));
+    std::vector<BlockArgs> sa(slots, e->dev_args);
+    for (size_t s = 0; s < slots; ++s) sa[s].in = e->d_in_pool + s * per;
     for (size_t b = 0; b < blocks; ++b) {
       CK(cudaEventRecord(ev[b], e->stream));
-      CK(cudaGraphLaunch(gs[b % slots].ex, e->stream));
+      e->enqueue_block(gs[b % slots], sa[b % slots], nullptr);
     }
     CK(cudaEventRecord(ev[blocks], e->stream));
     CK(cudaStreamSynchronize(e->stream));

@@ -94,7 +94,7 @@ struct BlockArgs {
   const int* item_off;  // [ctas + 1] static items of each CTA
   const int4* tinfo;    // per tile (synthesis, then canceller column tiles):
                         //   {first partial, partials, first group, groups}
-  unsigned* tick;       // k_reduce tickets: [0] canceller CTAs, [1] all CTAs; [tick_queue] work queue
+  unsigned* tick;       // k_reduce tickets [0] canceller CTAs, [1] all CTAs; [tick_queue] work queue, [+1] k_back exits
   int tick_queue;
   int LTr;              // channels per synthesis tile
   int red_syn_ctas, red_syn_cpt;  // k_reduce: synthesis CTAs, CTAs per tile

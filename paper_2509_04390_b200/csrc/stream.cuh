@@ -455,8 +455,16 @@ __global__ void __launch_bounds__(kBackThreads, 1) k_back(const __grid_constant_
     }
   }
   if (ctr && threadIdx.x == 0) ctr[2] = globaltimer();
-  if (a.trace && threadIdx.x == 0)
-    atomicMax(&a.trace[((n % kTraceBlocks) * kTraceKernels + TR_BACK) * 2 + 1], globaltimer());
+  if (threadIdx.x == 0) {
+    if (a.trace) atomicMax(&a.trace[((n % kTraceBlocks) * kTraceKernels + TR_BACK) * 2 + 1], globaltimer());
+    // the last CTA out resets the work queue: every producer has stopped
+    // claiming (its consumers saw the sentinel before getting here)
+    unsigned* ex = a.tick + a.tick_queue + 1;
+    if (atomicAdd(ex, 1u) == gridDim.x - 1u) {
+      *ex = 0u;
+      a.tick[a.tick_queue] = 0u;
+    }
+  }
 }
 
 // ----------------------------------------------------------------- k_reduce
@@ -470,7 +478,7 @@ __global__ void __launch_bounds__(kBackThreads, 1) k_back(const __grid_constant_
 // last canceller CTA does one c2r per mic (f^ for block n+1; the sum over
 // loudspeakers is done in the frequency domain -- one c2r per mic instead of
 // the reference's L, auralizer.hpp:81-86) and smooths the power (Appendix A
-// step 5). The last CTA resets the work queue and advances the block.
+// step 5). The last CTA advances the block (sharded: k_afc_finish does).
 // grid = red_syn_ctas + red_afc_ctas, kReduceThreads threads.
 constexpr int kReduceThreads = 256;
 __global__ void __launch_bounds__(kReduceThreads) k_reduce(const __grid_constant__ BlockArgs a) {
@@ -582,12 +590,11 @@ __global__ void __launch_bounds__(kReduceThreads) k_reduce(const __grid_constant
     }
   }
   trace_end(a, TR_REDUCE, n);
-  // retire: reset k_back's work queue; advance the block (sharded: k_afc_finish does)
+  // retire: advance the block (sharded: k_afc_finish does)
   if (threadIdx.x == 0) {
     unsigned* t = a.tick + 1;
     if (atomicAdd(t, 1u) == gridDim.x - 1u) {
       *t = 0u;
-      a.tick[a.tick_queue] = 0u;
       if (a.G <= 1) a.st->block = n + 1;
     }
   }

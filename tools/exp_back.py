@@ -16,7 +16,11 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2509_04390_b200 as A  # noqa: E402
 
 
+MODE = 0
+
+
 def run(name, eng, mic, blocks=200):
+    eng.set_launch_mode(MODE)
     eng.time_device_blocks(20, mic)
     lat, us = eng.time_device_blocks(blocks, mic)
     tr = eng.trace_blocks(16)
@@ -53,7 +57,10 @@ def main():
     ap.add_argument("--L", type=int, default=64)
     ap.add_argument("--N", type=int, default=64)
     ap.add_argument("--cases", default="nlms,mu0,synth,afc")
+    ap.add_argument("--mode", type=int, default=0, help="0 graph per block, 1 stream launches")
     args = ap.parse_args()
+    global MODE
+    MODE = args.mode
     N, L = args.N, args.L
     rng = np.random.default_rng(0)
     n_h, n_hf = 480000, 48000
