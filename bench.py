@@ -62,6 +62,24 @@ def decaying_noise(rng, rows, n, fs, t60_s=None, scale=1.0):
     return out
 
 
+class LazyRows:
+    """Row r of a decaying-noise filter set, generated on first use (seeded
+    per row): a loudspeaker shard materialises only its own rows."""
+
+    def __init__(self, n_rows, n_taps, fs, t60_s=None, scale=1.0, seed=1000):
+        self.n_rows, self.n_taps, self.fs = n_rows, n_taps, fs
+        self.t60_s, self.scale, self.seed = t60_s, scale, seed
+
+    def __len__(self):
+        return self.n_rows
+
+    def __getitem__(self, r):
+        if not 0 <= r < self.n_rows:
+            raise IndexError(r)
+        rng = np.random.default_rng((self.seed, r))
+        return decaying_noise(rng, 1, self.n_taps, self.fs, self.t60_s, self.scale)[0]
+
+
 def make_workload(cfg, seed=1000):
     rng = np.random.default_rng(seed)
     Q, L = cfg["Q"], cfg["L"]
@@ -206,6 +224,7 @@ def cpu_sample_channels(cfg, max_taps=200e6):
 def run_reference_arm(args, cfg, rank):
     if rank != 0:
         return 0
+    cfg = sharded_cfg(cfg, int(os.environ.get("WORLD_SIZE", "1")), args.scaling)
     synth, fc, mic = make_workload(cfg)
     blocks = max(1, args.steps)
     L_sub, scale = cpu_sample_channels(cfg)
@@ -221,8 +240,8 @@ def run_reference_arm(args, cfg, rank):
         "impl": "reference", "metric": METRIC, "value": p99, "unit": "us",
         "n_gpus": args.gpus, "steps": blocks, "warmup": args.warmup,
         "ms_per_step": float(np.mean(us)) / 1000.0, "higher_is_better": False,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": cfg["desc"]},
+        "scaling": args.scaling if args.gpus > 1 else "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "config": {"workload": cfg["desc"]},
         "p50_us": p50, "p99_us": p99, "budget_us": 1e6 * cfg["N"] / cfg["fs"],
         "cpu_baseline": {"value": p99, "unit": "us", "cores": workers, "kind": "reference",
                          "sample": sample},
@@ -418,12 +437,24 @@ def run_b200_arm(args, cfg, rank, world, local_rank):
     return 0
 
 
+def sharded_cfg(cfg, world, scaling):
+    """Weak scaling (default): every GPU keeps the config's L loudspeakers,
+    so the job has L x world; strong: the config's L is split."""
+    if scaling == "weak" and world > 1:
+        c = dict(cfg, L=cfg["L"] * world)
+        c["desc"] = cfg["desc"] + f" [weak scaling: {cfg['L']} loudspeakers per GPU x {world} GPUs]"
+        return c
+    return cfg
+
+
 def run_sharded(args, cfg, rank, world, local_rank):
     """N > 1: loudspeaker channels split over the ranks, one
     process per GPU. With the canceller on, the shards exchange their f^ /
-    power partials every block inside the CUDA graph (P2P over NVLink); the
-    synthesis shards are independent. Strong scaling: the config's L is
-    fixed and split. Per-block times are max over ranks."""
+    power partials every block inside the CUDA graph (k_afc_finish, P2P over
+    NVLink); the synthesis shards are independent. Weak scaling by default
+    (each GPU keeps the config's loudspeaker count; filter rows are generated
+    per shard); --scaling strong splits the config's L. Per-block times are
+    max over ranks."""
     import torch
     import torch.distributed as dist
     import paper_2509_04390_b200 as A
@@ -432,17 +463,20 @@ def run_sharded(args, cfg, rank, world, local_rank):
     device = local_rank % ndev
     torch.cuda.set_device(device)
     dist.init_process_group("gloo")
-    synth, fc, mic = make_workload(cfg)
+    cfg = sharded_cfg(cfg, world, args.scaling)
     N, Q, L = cfg["N"], cfg["Q"], cfg["L"]
+    synth = LazyRows(Q * L, cfg["n_h"], cfg["fs"], seed=1000)
+    fc = LazyRows(Q * L, cfg["n_hf"], cfg["fs"], t60_s=0.3, scale=0.1, seed=2000) if cfg["afc"] else None
+    mic = np.random.default_rng(7).standard_normal((64, Q, N)).astype(np.float32)
     ec = A.make_config(cfg["fs"], N, Q, L, mimo=Q > 1)
     t0 = time.perf_counter()
     if cfg["afc"]:
-        eng = S.ShardedAuralizer(list(synth), list(fc), ec, device=device,
+        eng = S.ShardedAuralizer(synth, fc, ec, device=device,
                                  afc=A.AfcParams(cfg.get("mu", 0.0), 0.9, None))
         local = eng.engine
     else:
         mode = A.ChannelMode.mimo if Q > 1 else A.ChannelMode.broadcast
-        eng = S.ShardedConvolver(list(synth), ec, world, rank, mode, device)
+        eng = S.ShardedConvolver(synth, ec, world, rank, mode, device)
         local = eng.engine
     t_setup = time.perf_counter() - t0
     del synth, fc
@@ -476,7 +510,7 @@ def run_sharded(args, cfg, rank, world, local_rank):
         line = {
             "metric": METRIC, "value": pct(dev, 99), "unit": "us", "n_gpus": world,
             "steps": K, "warmup": W, "ms_per_step": float(np.mean(dev)) / 1000.0,
-            "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+            "higher_is_better": False, "scaling": args.scaling, "vs_baseline": None,
             "dtype": "f32", "data": "synthetic: decaying-noise IRs, N(0,1) mic blocks",
             "config": {"workload": cfg["desc"], "block": N, "inputs": Q, "loudspeakers": L,
                        "taps": cfg["n_h"], "fc_taps": cfg.get("n_hf", 0),
@@ -519,6 +553,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--max-rt", action="store_true")
     ap.add_argument("--no-paced", action="store_true")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="N > 1: weak keeps the config's loudspeakers per GPU, strong splits them")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     if args.block:

@@ -143,6 +143,9 @@ int aura_b200_feedback_estimate(aura_b200_engine* e, float* out);
 int aura_b200_feedback_estimate_view(aura_b200_engine* e, const float** out);
 /* Auralizer::input_gain / set_input_gain (auralizer.hpp:51-52) */
 int aura_b200_set_input_gain(aura_b200_engine* e, float gain);
+/* How a block is enqueued (not in the reference): 0 = one CUDA graph per
+ * block (default), 1 = the same kernels launched on the engine stream. */
+int aura_b200_set_launch_mode(aura_b200_engine* e, int mode);
 float aura_b200_input_gain(const aura_b200_engine* e);
 
 /* ---- accessors (convolver.hpp:96-107, auralizer.hpp:44-49) ----------- */
