@@ -143,9 +143,18 @@ int aura_b200_feedback_estimate(aura_b200_engine* e, float* out);
 int aura_b200_feedback_estimate_view(aura_b200_engine* e, const float** out);
 /* Auralizer::input_gain / set_input_gain (auralizer.hpp:51-52) */
 int aura_b200_set_input_gain(aura_b200_engine* e, float gain);
-/* How a block is enqueued (not in the reference): 0 = one CUDA graph per
- * block (default), 1 = the same kernels launched on the engine stream. */
+/* How blocks run (not in the reference): 0 = one CUDA graph per block
+ * (default), 1 = the same kernels launched on the engine stream, 2 = one
+ * persistent cooperative kernel for the whole block loop, driven by a
+ * doorbell in mapped host memory (fails with BACKEND_UNAVAILABLE when the
+ * configuration does not fit it; not for sharded engines). */
 int aura_b200_set_launch_mode(aura_b200_engine* e, int mode);
+int aura_b200_launch_mode(const aura_b200_engine* e);
+/* Diagnostics: per-block phase stamps of the last loop-mode device timing,
+ * us from each block's release: {output written, input spectra pushed,
+ * canceller heads done, streaming done, block done, CTA 0's reduction done}
+ * per block (-1: n/a). */
+int aura_b200_loop_phases(const aura_b200_engine* e, size_t blocks, double* out);
 float aura_b200_input_gain(const aura_b200_engine* e);
 
 /* ---- accessors (convolver.hpp:96-107, auralizer.hpp:44-49) ----------- */

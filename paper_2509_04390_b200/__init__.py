@@ -177,6 +177,8 @@ def lib():
     L.aura_b200_feedback_estimate.argtypes = [vp, _f32p]
     L.aura_b200_set_input_gain.argtypes = [vp, C.c_float]
     L.aura_b200_set_launch_mode.argtypes = [vp, C.c_int]
+    L.aura_b200_launch_mode.argtypes = [vp]
+    L.aura_b200_loop_phases.argtypes = [vp, sz, vp]
     L.aura_b200_input_gain.argtypes = [vp]
     L.aura_b200_input_gain.restype = C.c_float
     for name in ("blocks_processed",):
@@ -336,8 +338,21 @@ class _Engine:
         return segs, ctas
 
     def set_launch_mode(self, mode: int):
-        """0: one CUDA graph per block (default); 1: kernels on the stream."""
+        """0: one CUDA graph per block (default); 1: kernels on the stream;
+        2: one persistent kernel for the block loop (doorbell-driven)."""
         _check(lib().aura_b200_set_launch_mode(self._h, mode))
+
+    def launch_mode(self) -> int:
+        return int(lib().aura_b200_launch_mode(self._h))
+
+    LOOP_PHASES = ("output", "x_pushed", "heads_done", "streamed", "done", "cta0_reduced")
+
+    def loop_phases(self, blocks: int):
+        """Per-block phase stamps (us from release) of the last loop-mode
+        time_device_blocks call."""
+        out = np.zeros((blocks, len(self.LOOP_PHASES)), np.float64)
+        _check(lib().aura_b200_loop_phases(self._h, blocks, out.ctypes.data))
+        return {k: out[:, i] for i, k in enumerate(self.LOOP_PHASES)}
 
     PHASES = {"k_front": 0, "k_back": 2}
 

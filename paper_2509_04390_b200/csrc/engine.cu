@@ -15,9 +15,11 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <thread>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -30,6 +32,7 @@
 #include "../../include/aura_b200.h"
 #include "kernels.cuh"
 #include "stream.cuh"
+#include "loop.cuh"
 #include <algorithm>
 
 using namespace aura_b200;
@@ -112,6 +115,20 @@ static const char* kPhaseNames[PH_COUNT] = {"k_front",  "k_back_head",  "k_back"
 
 using BackFn = void (*)(BlockArgs);
 
+// Poll until the stream has drained (true) or `seconds` pass (false).
+static bool wait_stream_idle(cudaStream_t s, double seconds) {
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    const cudaError_t q = cudaStreamQuery(s);
+    if (q != cudaErrorNotReady) {
+      cudaGetLastError();
+      return true;
+    }
+    if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > seconds) return false;
+    std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
+}
+
 struct aura_b200_engine {
   int device = 0;
   int sms = 148;
@@ -149,7 +166,23 @@ struct aura_b200_engine {
   // streaming kernel k_back
   BackFn back_fn = nullptr;
   bool pdl_off = false;  // measurement: serialise k_back / k_reduce launches
-  int launch_mode = 0;   // 0: one CUDA graph per block; 1: kernels launched on the stream
+  int launch_mode = 0;   // 0: one CUDA graph per block; 1: kernels on the stream; 2: persistent loop
+  // persistent loop (loop.cuh)
+  BackFn loop_fn = nullptr;
+  bool loop_ok = false;          // this configuration fits the loop kernel
+  std::string loop_why;          // ... or why not
+  size_t smem_loop = 0;
+  int loop_cpb = 1, loop_front = 0, loop_ctas = 0;
+  bool loop_running = false;
+  uint64_t loop_posted = 0;      // blocks released through the doorbell (device numbering)
+  LoopMailbox* h_mbox = nullptr; // pinned mapped
+  LoopMailbox* d_mbox = nullptr;
+  LoopCtl* d_ctl = nullptr;
+  unsigned long long* d_stamps = nullptr;
+  int loop_stages = 0;
+  bool loop_device_io = false;
+  std::vector<unsigned long long> loop_last_stamps;  // of the last loop-mode device timing
+  int loop_hold = 1;
   int back_ctas = 0;
   size_t smem_back = 0, smem_reduce = 0;
   size_t n_syn_segs = 0, n_afc_segs = 0;
@@ -164,6 +197,11 @@ struct aura_b200_engine {
 
   ~aura_b200_engine() {
     cudaSetDevice(device);
+    if (loop_running && h_mbox) {  // stop the persistent kernel (best effort, bounded)
+      reinterpret_cast<volatile LoopMailbox*>(h_mbox)->stop = 1u;
+      std::atomic_thread_fence(std::memory_order_seq_cst);
+      if (!wait_stream_idle(stream, 5.0)) return;  // wedged: leak rather than block (frees would sync)
+    }
     if (stream) cudaStreamSynchronize(stream);
     g_block.destroy();
     for (void* p : dmem) cudaFree(p);
@@ -171,6 +209,7 @@ struct aura_b200_engine {
     if (h_out) cudaFreeHost(h_out);
     if (h_fhat) cudaFreeHost(h_fhat);
     if (h_status) cudaFreeHost(h_status);
+    if (h_mbox) cudaFreeHost(h_mbox);
     for (void* p : ipc_opened) cudaIpcCloseMemHandle(p);
     if (ev_front) cudaEventDestroy(ev_front);
     if (ev_back) cudaEventDestroy(ev_back);
@@ -380,6 +419,18 @@ BackFn back_for(bool elem, int PT) {
   }
 }
 
+template <int LT>
+BackFn loop_for(bool elem, int PT) {
+  if (elem) return k_loop<LT, true, 0>;
+  switch (PT) {
+    case 0: return k_loop<LT, false, 0>;
+    case 1: return k_loop<LT, false, 1>;
+    case 2: return k_loop<LT, false, 2>;
+    case 4: return k_loop<LT, false, 4>;
+    default: return k_loop<LT, false, 8>;
+  }
+}
+
 // Plan k_back (stream.cuh): tiling, stage sizes, pipeline depth, and the
 // static work split. Three phases -- synthesis taps [0, TA) of every tile,
 // the canceller units, synthesis taps [TA, T) -- are each cut into
@@ -494,6 +545,7 @@ void plan_back(aura_b200_engine* e, BlockArgs& a) {
     (t < tiles ? max_syn : max_afc) = std::max(t < tiles ? max_syn : max_afc, cnt[t]);
   }
   a.n_chunks = (int)chunks.size();
+  a.plan_ctas = ctas;
   int* doff = dalloc<int>(item_off.size(), e->dmem);
   CK(cudaMemcpy(doff, item_off.data(), item_off.size() * sizeof(int), cudaMemcpyHostToDevice));
   a.item_off = doff;
@@ -519,7 +571,7 @@ void plan_back(aura_b200_engine* e, BlockArgs& a) {
   a.red_afc_rows = P + (e->args.nlms ? 1 : 0);
   a.red_afc_cpt = U > 0 ? cpt_for(a.red_afc_rows * CT, max_afc) : 1;
   a.red_afc_ctas = U > 0 ? CTn * a.red_afc_cpt : 0;
-  e->smem_reduce = (size_t)kReduceThreads * 16 + (e->aur ? 8 * (2 * (size_t)N + table_f2(N)) : 0);
+  e->smem_reduce = 16 * reduce_smem_f4(N, e->aur);
   CK(cudaFuncSetAttribute(k_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem_reduce));
   // tickets: [0] canceller CTAs of k_reduce, [1] all k_reduce CTAs, [2] work
   // queue, [3] k_back exits
@@ -566,6 +618,78 @@ void common_init(aura_b200_engine* e, int device) {
 // CTAs that tick the block ticket in retire_block: only the sharded
 // canceller's k_afc_finish (k_back retires a block itself).
 void set_advance_total(aura_b200_engine* e) { e->args.advance_total = e->sharded() ? 1 : 0; }
+
+// Persistent loop mode (loop.cuh): does this configuration fit one
+// cooperative CTA per SM with the ring, the reduction scratch and the
+// front's work area in shared memory? Allocates the mailbox and control
+// block when it does.
+void plan_loop(aura_b200_engine* e) {
+  BlockArgs& a = e->args;
+  e->loop_ok = false;
+  a.hist1 = dalloc<float>((size_t)e->Qx * e->N, e->dmem);
+  CK(cudaMemset(a.hist1, 0, sizeof(float) * e->Qx * e->N));
+  if (!e->has_back()) {
+    e->loop_why = "no streaming work (single-partition convolver)";
+    return;
+  }
+  int coop = 0;
+  CK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, e->device));
+  if (!coop) {
+    e->loop_why = "device has no cooperative launch";
+    return;
+  }
+  const int N = (int)e->N;
+  const int Qs = e->mode == AURA_B200_ELEMENTWISE ? 1 : (int)e->Q;
+  const int nerr = (e->aur && a.nlms) ? (int)e->P : 0;
+  // at least one front CTA beside the error-spectrum CTAs; CTAs beyond the
+  // plan's take queue items only (the work items, hence the bits, are the same)
+  e->loop_ctas = std::min(e->sms, std::max(e->back_ctas, nerr + 1));
+  const int avail = e->loop_ctas - nerr;
+  if (avail < 1) {
+    e->loop_why = "too few CTAs for the front half";
+    return;
+  }
+  e->loop_cpb = (int)((e->L + avail - 1) / avail);
+  e->loop_front = (int)((e->L + e->loop_cpb - 1) / e->loop_cpb);
+  const size_t front = 8 * (front_work_f2(N, Qs) + (a.smem_tables ? table_f2(N) : 0) +
+                            (a.front_pre ? (size_t)(1 + Qs) * N : 0));
+  const size_t fixed = kBackBarrierBytes + (size_t)a.red_f4 * 16 + front;
+  const size_t slot = (size_t)a.slot_f4 * 16;
+  const size_t budget = 225 * 1024;
+  const int stages = budget > fixed ? (int)std::min<size_t>(a.stages, (budget - fixed) / slot) : 0;
+  if (stages < 2) {
+    e->loop_why = "shared memory: ring + front work area do not fit one CTA";
+    return;
+  }
+  if ((size_t)stages * slot < 16 * reduce_smem_f4(N, e->aur)) {
+    e->loop_why = "shared memory: the reduction scratch does not fit the ring";
+    return;
+  }
+  const int LT = e->LT;
+  const bool elem = e->mode == AURA_B200_ELEMENTWISE;
+  switch (LT) {
+    case 1: e->loop_fn = loop_for<1>(elem, e->PT); break;
+    case 2: e->loop_fn = loop_for<2>(elem, e->PT); break;
+    case 4: e->loop_fn = loop_for<4>(elem, e->PT); break;
+    default: e->loop_fn = loop_for<8>(elem, e->PT); break;
+  }
+  e->smem_loop = fixed + (size_t)stages * slot;
+  CK(cudaFuncSetAttribute(e->loop_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem_loop));
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, e->loop_fn, kBackThreads, e->smem_loop));
+  if (per_sm < 1 || e->loop_ctas > per_sm * e->sms) {
+    e->loop_why = "the grid does not fit co-resident";
+    return;
+  }
+  e->loop_stages = stages;
+  if (const char* h = std::getenv("AURA_B200_LOOP_HOLD")) e->loop_hold = std::atoi(h);
+  CK(cudaHostAlloc(&e->h_mbox, sizeof(LoopMailbox), cudaHostAllocMapped | cudaHostAllocPortable));
+  std::memset(e->h_mbox, 0, sizeof(LoopMailbox));
+  CK(cudaHostGetDevicePointer((void**)&e->d_mbox, e->h_mbox, 0));
+  e->d_ctl = dalloc<LoopCtl>(1, e->dmem);
+  e->d_stamps = dalloc<unsigned long long>((size_t)kLoopStampCap * kLoopStamps, e->dmem);
+  e->loop_ok = true;
+}
 
 void finish_init(aura_b200_engine* e) {
   BlockArgs& a = e->args;
@@ -626,6 +750,7 @@ void finish_init(aura_b200_engine* e) {
   e->d_in_pool = dalloc<float>(e->pool_blocks * in_ch * N, e->dmem);
   CK(cudaMemset(e->d_in_pool, 0, e->pool_blocks * in_ch * N * sizeof(float)));
   e->d_out = dalloc<float>(e->L * N, e->dmem);
+  plan_loop(e);
   e->rebuild_graphs();
   e->dev_args = a;
   e->dev_args.out = e->d_out;
@@ -633,6 +758,122 @@ void finish_init(aura_b200_engine* e) {
   CK(cudaStreamSynchronize(e->stream));
 }
 
+// ------------------------------------------------------ persistent loop control
+volatile LoopMailbox* mbox(aura_b200_engine* e) { return reinterpret_cast<volatile LoopMailbox*>(e->h_mbox); }
+
+uint32_t device_block(aura_b200_engine* e) {
+  DevState ds{};
+  CK(cudaMemcpy(&ds, e->args.st, sizeof(ds), cudaMemcpyDeviceToHost));
+  return ds.block;
+}
+
+bool loop_exited(aura_b200_engine* e);
+void loop_reap(aura_b200_engine* e);
+void start_loop(aura_b200_engine* e, bool device_io);
+
+// Spin until mailbox field >= target (or the kernel reports an error);
+// relaunches a kernel that parked just as the block was released.
+void loop_wait(aura_b200_engine* e, volatile unsigned long long* field, uint64_t target, const char* what) {
+  const auto t0 = std::chrono::steady_clock::now();
+  uint64_t spins = 0;
+  while (*field < target) {
+    if (mbox(e)->err) fail(AURA_B200_E_TIMEOUT, std::string(what) + ": the persistent kernel reported a timeout");
+#if defined(__x86_64__)
+    _mm_pause();
+#endif
+    if ((++spins & 0xFFF) == 0) {
+      if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(20))
+        fail(AURA_B200_E_TIMEOUT, std::string(what) + ": not complete within 20 s");
+      if (loop_exited(e)) {  // parked just before our doorbell: relaunch (same I/O)
+        if (!mbox(e)->parked) fail(AURA_B200_E_CUDA, std::string(what) + ": the persistent kernel exited");
+        const bool dev = e->loop_device_io;
+        loop_reap(e);
+        start_loop(e, dev);
+      }
+    }
+  }
+  std::atomic_thread_fence(std::memory_order_acquire);
+}
+
+// Launch the persistent kernel at the device's current block. device_io:
+// inputs from the measurement pool (block n: slot n % pool_blocks), outputs
+// to device memory; else the mapped host I/O of process().
+void start_loop(aura_b200_engine* e, bool device_io) {
+  if (!e->loop_ok) fail(AURA_B200_E_BACKEND_UNAVAILABLE, "persistent loop mode unavailable: " + e->loop_why);
+  CK(cudaStreamSynchronize(e->stream));
+  const uint32_t n0 = device_block(e);
+  BlockArgs la = device_io ? e->dev_args : e->args;
+  // window history: block n reads (n odd ? hist1 : prev_in)
+  if (e->mode != AURA_B200_ELEMENTWISE && (n0 & 1u))
+    CK(cudaMemcpy(la.hist1, la.prev_in, sizeof(float) * e->Qx * e->N, cudaMemcpyDeviceToDevice));
+  CK(cudaMemset(e->d_ctl, 0, sizeof(LoopCtl)));
+  volatile LoopMailbox* mb = mbox(e);
+  // blocks already released (posted just as a previous launch parked) stay released
+  e->loop_posted = std::max<uint64_t>(e->loop_posted, n0);
+  mb->out_done = n0;
+  mb->bg_done = n0;
+  mb->stop = 0u;
+  mb->err = 0u;
+  mb->parked = 0u;
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  mb->doorbell = e->loop_posted;
+  la.stages = e->loop_stages;
+  la.cpb = e->loop_cpb;
+  la.loop_front_ctas = e->loop_front;
+  la.mbox = e->d_mbox;
+  la.ctl = e->d_ctl;
+  la.loop_stamps = e->d_stamps;
+  la.in_slots = device_io ? (int)e->pool_blocks : 1;
+  la.loop_idle_ns = 20ull * 1000 * 1000;
+  la.loop_hold = e->loop_hold;
+  la.trace = nullptr;
+  la.seg_trace = nullptr;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)e->loop_ctas);
+  cfg.blockDim = dim3(kBackThreads);
+  cfg.dynamicSmemBytes = e->smem_loop;
+  cfg.stream = e->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, e->loop_fn, la));
+  e->loop_running = true;
+  e->loop_device_io = device_io;
+}
+
+// The persistent kernel has exited (stopped, parked or failed): hand the
+// state back to the graph-mode conventions.
+void loop_reap(aura_b200_engine* e) {
+  const cudaError_t r = cudaStreamSynchronize(e->stream);
+  e->loop_running = false;
+  ck(r, "persistent loop exit");
+  if (mbox(e)->err) fail(AURA_B200_E_TIMEOUT, "persistent loop: internal timeout");
+  const uint32_t n = device_block(e);
+  if (e->mode != AURA_B200_ELEMENTWISE && (n & 1u))
+    CK(cudaMemcpy(e->args.prev_in, e->args.hist1, sizeof(float) * e->Qx * e->N, cudaMemcpyDeviceToDevice));
+}
+
+bool loop_exited(aura_b200_engine* e) { return e->loop_running && cudaStreamQuery(e->stream) != cudaErrorNotReady; }
+
+// Let every released block finish, stop the persistent kernel.
+void stop_loop(aura_b200_engine* e) {
+  if (!e->loop_running) return;
+  volatile LoopMailbox* mb = mbox(e);
+  std::string why;
+  try {
+    loop_wait(e, &mb->bg_done, e->loop_posted, "persistent loop");
+  } catch (const Fail& f) {
+    why = f.msg;
+  }
+  mb->stop = 1u;
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  if (!wait_stream_idle(e->stream, 5.0))
+    fail(AURA_B200_E_TIMEOUT, "persistent loop: the kernel did not stop within 5 s");
+  loop_reap(e);
+  if (!why.empty()) fail(AURA_B200_E_TIMEOUT, why);
+}
 void reset_state(aura_b200_engine* e) {
   BlockArgs& a = e->args;
   const size_t N = e->N, NF = N / 2;
@@ -656,6 +897,7 @@ void reset_state(aura_b200_engine* e) {
   }
   CK(cudaStreamSynchronize(s));
   e->blocks = 0;
+  e->loop_posted = 0;  // the persistent loop restarts at block 0 too
 }
 
 void alloc_synth(aura_b200_engine* e, BlockArgs& a) {
@@ -917,6 +1159,20 @@ int aura_b200_process(aura_b200_engine* e, const float* in, float* out) {
     CK(cudaSetDevice(e->device));
     if (e->h_status && *reinterpret_cast<volatile unsigned*>(e->h_status))
       fail(AURA_B200_E_TIMEOUT, "a shard peer missed the canceller exchange deadline");
+    if (e->launch_mode == 2) {  // persistent loop: doorbell in, mailbox out
+      if (loop_exited(e)) loop_reap(e);  // parked while idle
+      if (!e->loop_running || e->loop_device_io) {
+        stop_loop(e);
+        start_loop(e, false);
+      }
+      std::memcpy(e->h_in, in, n_in * sizeof(float));
+      std::atomic_thread_fence(std::memory_order_seq_cst);
+      mbox(e)->doorbell = ++e->loop_posted;
+      loop_wait(e, &mbox(e)->out_done, e->loop_posted, "block output");
+      std::memcpy(out, e->h_out, e->L * e->N * sizeof(float));
+      ++e->blocks;
+      return;
+    }
     // the previous block's front has completed, so the staging buffer is free
     std::memcpy(e->h_in, in, n_in * sizeof(float));
     std::atomic_thread_fence(std::memory_order_release);
@@ -931,6 +1187,10 @@ int aura_b200_process(aura_b200_engine* e, const float* in, float* out) {
 int aura_b200_synchronize(aura_b200_engine* e) {
   return guarded([&] {
     CK(cudaSetDevice(e->device));
+    if (e->loop_running) {
+      loop_wait(e, &mbox(e)->bg_done, e->loop_posted, "block background");
+      return;
+    }
     if (e->blocks) wait_event(e, e->ev_back, "block background");
     CK(cudaStreamSynchronize(e->stream));
   });
@@ -938,6 +1198,7 @@ int aura_b200_synchronize(aura_b200_engine* e) {
 
 int aura_b200_reset(aura_b200_engine* e) {
   return guarded([&] {
+    stop_loop(e);
     CK(cudaSetDevice(e->device));
     reset_state(e);
   });
@@ -947,8 +1208,12 @@ int aura_b200_feedback_estimate(aura_b200_engine* e, float* out) {
   return guarded([&] {
     if (!e->aur) fail(AURA_B200_E_INVALID_ARGUMENT, "not an auralizer");
     CK(cudaSetDevice(e->device));
-    if (e->blocks) wait_event(e, e->ev_back, "block background");
-    CK(cudaStreamSynchronize(e->stream));
+    if (e->loop_running) {  // f^ lands in the mapped copy when the block is done
+      loop_wait(e, &mbox(e)->bg_done, e->loop_posted, "block background");
+    } else {
+      if (e->blocks) wait_event(e, e->ev_back, "block background");
+      CK(cudaStreamSynchronize(e->stream));
+    }
     std::memcpy(out, e->h_fhat, sizeof(float) * e->P * e->N);
   });
 }
@@ -963,6 +1228,7 @@ int aura_b200_feedback_estimate_view(aura_b200_engine* e, const float** out) {
 int aura_b200_fdl_slot(aura_b200_engine* e, int which, size_t channel, size_t age,
                        float* out) {
   return guarded([&] {
+    stop_loop(e);
     CK(cudaSetDevice(e->device));
     CK(cudaStreamSynchronize(e->stream));
     const size_t NF = e->N / 2;
@@ -996,15 +1262,39 @@ int aura_b200_fdl_slot(aura_b200_engine* e, int which, size_t channel, size_t ag
 
 int aura_b200_set_launch_mode(aura_b200_engine* e, int mode) {
   return guarded([&] {
-    if (mode != 0 && mode != 1) fail(AURA_B200_E_INVALID_ARGUMENT, "launch mode is 0 (graph) or 1 (stream)");
+    if (mode < 0 || mode > 2)
+      fail(AURA_B200_E_INVALID_ARGUMENT, "launch mode is 0 (graph), 1 (stream) or 2 (persistent loop)");
     CK(cudaSetDevice(e->device));
+    stop_loop(e);
+    if (mode == 2 && !e->loop_ok)
+      fail(AURA_B200_E_BACKEND_UNAVAILABLE, "persistent loop mode unavailable: " + e->loop_why);
+    if (mode == 2 && e->G > 1)
+      fail(AURA_B200_E_INVALID_ARGUMENT, "persistent loop mode does not run sharded engines");
     CK(cudaStreamSynchronize(e->stream));
     e->launch_mode = mode;
   });
 }
 
+int aura_b200_launch_mode(const aura_b200_engine* e) { return e->launch_mode; }
+
+// Diagnostics: per-block phase stamps of the last loop-mode device timing,
+// us from the block's release: {output written, input spectra pushed,
+// canceller heads done, streaming done, block done} x blocks.
+int aura_b200_loop_phases(const aura_b200_engine* e, size_t blocks, double* out) {
+  return guarded([&] {
+    const size_t nb = e->loop_last_stamps.size() / kLoopStamps;
+    if (blocks > nb) fail(AURA_B200_E_INVALID_ARGUMENT, "fewer loop-mode blocks were timed");
+    for (size_t b = 0; b < blocks; ++b) {
+      const unsigned long long* t = &e->loop_last_stamps[(size_t)kLoopStamps * b];
+      for (int k = 1; k < kLoopStamps; ++k)
+        out[b * (kLoopStamps - 1) + k - 1] = t[k] ? (double)(long long)(t[k] - t[0]) * 1e-3 : -1.0;
+    }
+  });
+}
+
 int aura_b200_set_input_gain(aura_b200_engine* e, float gain) {
   return guarded([&] {
+    stop_loop(e);
     if (!e->aur) fail(AURA_B200_E_INVALID_ARGUMENT, "not an auralizer");
     CK(cudaSetDevice(e->device));
     CK(cudaStreamSynchronize(e->stream));
@@ -1024,6 +1314,7 @@ int aura_b200_mode(const aura_b200_engine* e) { return e->mode; }
 
 int aura_b200_filter_spectrum(aura_b200_engine* e, size_t row, size_t k, float* out) {
   return guarded([&] {
+    stop_loop(e);
     const size_t rows = e->mode == AURA_B200_MIMO ? e->Q * e->L : e->L;
     if (row >= rows || k >= e->K) fail(AURA_B200_E_INVALID_ARGUMENT, "spectrum index out of range");
     CK(cudaSetDevice(e->device));
@@ -1048,6 +1339,7 @@ int aura_b200_filter_spectrum(aura_b200_engine* e, size_t row, size_t k, float* 
 
 int aura_b200_afc_coeffs(aura_b200_engine* e, float* out) {
   return guarded([&] {
+    stop_loop(e);
     if (!e->aur) fail(AURA_B200_E_INVALID_ARGUMENT, "not an auralizer");
     CK(cudaSetDevice(e->device));
     CK(cudaStreamSynchronize(e->stream));
@@ -1107,6 +1399,7 @@ void shard_finalize(aura_b200_engine* e, char* const* peers) {
 
 int aura_b200_shard_export(aura_b200_engine* e, int world, int rank, void* handle) {
   return guarded([&] {
+    stop_loop(e);
     if (!e || !handle) fail(AURA_B200_E_INVALID_ARGUMENT, "null argument");
     shard_alloc(e, world, rank);
     cudaIpcMemHandle_t h;
@@ -1182,12 +1475,38 @@ int aura_b200_time_device_blocks(aura_b200_engine* e, const float* host_in,
                                  size_t n_in_blocks, size_t blocks, float* latency_us,
                                  float* block_us) {
   return guarded([&] {
+    stop_loop(e);
     CK(cudaSetDevice(e->device));
     CK(cudaStreamSynchronize(e->stream));
     const size_t per = (size_t)e->Qx * e->N;
     if (host_in && n_in_blocks) {
       const size_t nb = std::min(n_in_blocks, e->pool_blocks);
       CK(cudaMemcpy(e->d_in_pool, host_in, nb * per * sizeof(float), cudaMemcpyHostToDevice));
+    }
+    if (e->launch_mode == 2) {
+      // persistent loop: all blocks released at once (back to back); per
+      // block the kernel stamps %globaltimer when the leader released it,
+      // when its output was written and when it was complete
+      for (size_t done = 0; done < blocks;) {
+        const size_t nb = std::min<size_t>(blocks - done, kLoopStampCap);
+        start_loop(e, true);
+        const uint64_t n0 = e->loop_posted;
+        e->loop_posted = n0 + nb;
+        mbox(e)->doorbell = e->loop_posted;
+        std::atomic_thread_fence(std::memory_order_seq_cst);
+        stop_loop(e);
+        std::vector<unsigned long long> st((size_t)kLoopStamps * nb);
+        CK(cudaMemcpy(st.data(), e->d_stamps, st.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+        e->loop_last_stamps = st;
+        for (size_t b = 0; b < nb; ++b) {
+          const unsigned long long* t = &st[(size_t)kLoopStamps * b];
+          block_us[done + b] = (float)((double)(long long)(t[5] - t[0]) * 1e-3);
+          if (latency_us) latency_us[done + b] = (float)((double)(long long)(t[1] - t[0]) * 1e-3);
+        }
+        done += nb;
+      }
+      e->blocks += blocks;
+      return;
     }
     // one block graph per pool slot (the input pointer is baked per slot)
     const size_t slots = std::max<size_t>(1, std::min(n_in_blocks, e->pool_blocks));
@@ -1279,6 +1598,7 @@ int aura_b200_time_host_blocks(aura_b200_engine* e, const float* host_in,
 int aura_b200_profile_phases(aura_b200_engine* e, size_t blocks, float* phase_us,
                              int* n_phases) {
   return guarded([&] {
+    stop_loop(e);
     CK(cudaSetDevice(e->device));
     CK(cudaStreamSynchronize(e->stream));
     const int np = PH_COUNT;
@@ -1312,6 +1632,7 @@ int aura_b200_profile_phases(aura_b200_engine* e, size_t blocks, float* phase_us
 
 int aura_b200_time_phase(aura_b200_engine* e, int phase, size_t reps, float* avg_us) {
   return guarded([&] {
+    stop_loop(e);
     if (phase != PH_BACK && phase != PH_FRONT)
       fail(AURA_B200_E_INVALID_ARGUMENT, "only the front and the streaming kernel can be re-launched");
     if (phase == PH_BACK && !e->has_back())
@@ -1342,6 +1663,7 @@ int aura_b200_time_phase(aura_b200_engine* e, int phase, size_t reps, float* avg
 
 int aura_b200_trace_blocks(aura_b200_engine* e, size_t blocks, double* out) {
   return guarded([&] {
+    stop_loop(e);
     CK(cudaSetDevice(e->device));
     CK(cudaStreamSynchronize(e->stream));
     blocks = std::min<size_t>(blocks, kTraceBlocks);
@@ -1401,6 +1723,7 @@ int aura_b200_trace_blocks(aura_b200_engine* e, size_t blocks, double* out) {
 int aura_b200_trace_back(aura_b200_engine* e, size_t blocks, double* out_segs, size_t* n_segs,
                          double* out_ctas, size_t* n_ctas) {
   return guarded([&] {
+    stop_loop(e);
     const size_t ns = e->h_chunks.size(), nc = (size_t)e->back_ctas;
     if (!out_segs || !out_ctas) {
       *n_segs = ns;

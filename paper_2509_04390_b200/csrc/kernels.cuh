@@ -67,6 +67,27 @@ constexpr int kMaxShards = 8;
 constexpr size_t kXFlagBytes = 256;
 constexpr unsigned long long kShardTimeoutNs = 5ull * 1000 * 1000 * 1000;
 
+// Host <-> persistent kernel mailbox, in pinned mapped host memory.
+struct LoopMailbox {
+  unsigned long long doorbell;  // host: blocks released (block n runs once doorbell > n)
+  unsigned long long out_done;  // device: last block whose output is written, + 1
+  unsigned long long bg_done;   // device: last block completely done, + 1
+  unsigned stop;                // host: leave the loop before the next block
+  unsigned err;                 // device: an internal wait timed out
+  unsigned parked;              // device: left the loop after loop_idle_ns without a doorbell
+  unsigned pad;
+};
+// Device-side control block of the persistent kernel (zeroed at launch).
+struct LoopCtl {
+  unsigned long long go;         // leader -> grid: blocks released (or ~0: stop)
+  unsigned long long x_seq;      // front CTAs whose input spectra are pushed (cumulative)
+  unsigned long long head_seq;   // canceller heads + error spectra done (cumulative)
+  unsigned long long front_seq;  // front CTAs whose outputs are written (cumulative)
+  unsigned bar_count, bar_gen;   // grid barrier
+  unsigned err;
+  unsigned pad;
+};
+
 struct BlockArgs {
   // geometry
   int N, logN, NF;   // NF = N/2 float4 columns per packed spectrum
@@ -91,7 +112,8 @@ struct BlockArgs {
   const int4* chunks;   // work items {kind | tile << 1, b, e, partial slot in tile}:
                         //   [n_static] per-CTA static pieces, then [n_chunks - n_static] queue
   int n_chunks, n_static;
-  const int* item_off;  // [ctas + 1] static items of each CTA
+  const int* item_off;  // [plan_ctas + 1] static items of each CTA
+  int plan_ctas;        // CTAs the static pieces were planned for (a larger grid: queue only)
   const int4* tinfo;    // per tile (synthesis, then canceller column tiles):
                         //   {first partial, partials, first group, groups}
   unsigned* tick;       // k_reduce tickets [0] canceller CTAs, [1] all CTAs; [tick_queue] work queue, [+1] k_back exits
@@ -100,6 +122,15 @@ struct BlockArgs {
   int red_syn_ctas, red_syn_cpt;  // k_reduce: synthesis CTAs, CTAs per tile
   int red_afc_ctas, red_afc_cpt;  // canceller CTAs, CTAs per column tile
   int red_afc_rows;               // canceller partial rows: P (+1 power row with NLMS)
+  // persistent loop mode (loop.cuh)
+  struct LoopMailbox* mbox;     // pinned mapped: doorbell / output done / block done / stop / error
+  struct LoopCtl* ctl;          // device control block
+  int loop_front_ctas;          // CTAs running the front half
+  int in_slots;                 // input block n is in + (n % in_slots) * (inputs x N)
+  float* hist1;                 // second window-history buffer (the first is prev_in)
+  unsigned long long* loop_stamps;  // per block {released, output written, done} (%globaltimer)
+  unsigned long long loop_idle_ns;  // park (exit) after this long without a doorbell
+  int loop_hold;                    // producers start after the fronts' input spectra are pushed
   unsigned long long* seg_trace;  // diagnostics: [chunks] x {end, cta}, then [ctas] x {start, first data, exit}
   // tables
   const float2* tw;     // N/2, e^{-2 pi i j / N}
@@ -218,11 +249,12 @@ __device__ void retire_block(const BlockArgs& a, uint32_t n) {
 
 // Store the packed spectrum spec (N float2, shared) as ring slot `slot` of
 // delay-line channel ch, tiled [ch][CTn][cap][CT] float4 (see above).
+template <typename Team = Cta>
 __device__ __forceinline__ void push_tiled(const BlockArgs& a, float4* fdl, int ch, int cap, int slot,
-                                           const float2* spec) {
+                                           const float2* spec, Team tm = Team()) {
   const int CT = a.CT;
   float2* d = reinterpret_cast<float2*>(fdl);
-  for (int j = threadIdx.x; j < a.N; j += blockDim.x) {
+  for (int j = tm.tid(); j < a.N; j += tm.size()) {
     const int f = j >> 1;
     const size_t i4 = (((size_t)ch * a.CTn + f / CT) * cap + slot) * CT + (f % CT);
     d[2 * i4 + (j & 1)] = spec[j];
@@ -230,16 +262,30 @@ __device__ __forceinline__ void push_tiled(const BlockArgs& a, float4* fdl, int 
 }
 
 // ------------------------------------------------------------- k_front
-// grid = ceil(L / cpb), 256 threads; elementwise CTAs also own their
-// channels' inputs. Shared: Qs input spectra (N float2 each), FFT scratch z
-// (N float2), window/accumulator (2N floats).
-__global__ void __launch_bounds__(kFrontThreads) k_front(BlockArgs a) {
-  extern __shared__ float4 smem4[];
+// Shared-memory float2 count of the front's work area for Qs shared inputs
+// (tables and the first channel's staged S/H0 come on top, see finish_init).
+__host__ __device__ inline size_t front_work_f2(int N, int Qs) { return (size_t)N * (Qs + 2); }
+
+// The front of block n for output channels [c0, c1) with a team of threads:
+// m~ = g m - f^ (auralizer.hpp:73-76), window + r2c of every input
+// (convolver.hpp:180-191; the leader also pushes it into the FDL and writes
+// this block's m~ to cur_out), then per channel Y_l = S_l + sum_q X_q H0_l,q,
+// c2r + overlap-save into the output (and, for the canceller, into spk).
+// on_x() runs on the whole team once the leader has pushed the input
+// spectra. smem: front_work_f2 float2, then the tables (a.smem_tables) and
+// the staged S/H0 (a.front_pre).
+struct NoHook {
+  __device__ __forceinline__ void operator()() const {}
+};
+
+template <typename Team, typename OnX = NoHook>
+__device__ void front_body(const BlockArgs& a, uint32_t n, int c0, int c1, float2* Xs, const float* in,
+                           const float* prev_in, float* cur_out, bool leader, Team tm, OnX on_x = OnX()) {
   const int N = a.N, NF = a.NF;
+  const int tid = tm.tid(), nt = tm.size();
   const bool elem = a.mode == 1;
   const int Qs = elem ? 1 : a.Q;
   const int Qh = a.mode == 2 ? a.Q : 1;
-  float2* Xs = reinterpret_cast<float2*>(smem4);          // Qs x N
   float2* z = Xs + (size_t)Qs * N;                        // N
   float* wa = reinterpret_cast<float*>(z + N);            // 2N (window / acc)
   float2* acc = reinterpret_cast<float2*>(wa);
@@ -247,70 +293,117 @@ __global__ void __launch_bounds__(kFrontThreads) k_front(BlockArgs a) {
   float2* pre = stw + (a.smem_tables ? table_f2(N) : 0);  // [S_l, H0_l,q] of the first channel
   const float2* tw = a.smem_tables ? stw : a.tw;
   const float2* split = a.smem_tables ? stw + N / 2 : a.split;
-  const int c0 = blockIdx.x * a.cpb;
-  const int c1 = min(c0 + a.cpb, a.L);
 
   // ---- one round of independent loads: tables, input windows, and the
   // first channel's precomputed S_l and partition-0 spectra (front_pre)
-  if (a.smem_tables) stage_tables(stw, stw + N / 2, a.tw, a.split, N);
+  if (a.smem_tables) stage_tables(stw, stw + N / 2, a.tw, a.split, N, tm);
   if (a.front_pre) {
     const float2* Sl = reinterpret_cast<const float2*>(a.S + (size_t)c0 * NF);
     const float2* H0 = reinterpret_cast<const float2*>(a.H0 + (size_t)c0 * Qh * NF);
-    for (int j = threadIdx.x; j < N; j += blockDim.x) pre[j] = Sl[j];
-    for (int j = threadIdx.x; j < Qs * N; j += blockDim.x) pre[N + j] = H0[j];
+    for (int j = tid; j < N; j += nt) pre[j] = Sl[j];
+    for (int j = tid; j < Qs * N; j += nt) pre[N + j] = H0[j];
   }
-  const uint32_t n = a.st->block;
-  trace_begin(a, TR_FRONT, n);
 
   // ---- stage 1 for the shared inputs (broadcast / mimo)
   if (!elem) {
     for (int q = 0; q < Qs; ++q) {
-      const float* in = a.in + (size_t)q * N;
-      const float* prev = a.prev_in + (size_t)q * N;
-      for (int i = threadIdx.x; i < N; i += blockDim.x) {
-        float v = in[i];
+      const float* inq = in + (size_t)q * N;
+      const float* prev = prev_in + (size_t)q * N;
+      for (int i = tid; i < N; i += nt) {
+        float v = inq[i];
         if (a.is_aur) v = __fsub_rn(__fmul_rn(a.gain, v), a.fhat[(size_t)q * N + i]);
-        if (blockIdx.x == 0) a.cur_mt[(size_t)q * N + i] = v;
+        if (leader) cur_out[(size_t)q * N + i] = v;
         wa[i] = prev[i];
         wa[N + i] = v;
       }
-      __syncthreads();
-      rfft_packed(wa, z, Xs + (size_t)q * N, N, a.logN, tw, split);
-      if (blockIdx.x == 0) push_tiled(a, a.X, q, a.K, (int)(n % (uint32_t)a.K), Xs + (size_t)q * N);
+      tm.sync();
+      rfft_packed(wa, z, Xs + (size_t)q * N, N, a.logN, tw, split, tm);
+      if (leader) push_tiled(a, a.X, q, a.K, (int)(n % (uint32_t)a.K), Xs + (size_t)q * N, tm);
     }
+    on_x();
   }
 
   // ---- per output channel: Y = S + sum_q X_q H_q[0], c2r, overlap-save
   for (int l = c0; l < c1; ++l) {
     if (elem) {
-      const float* in = a.in + (size_t)l * N;
+      const float* inl = in + (size_t)l * N;
       float* prev = a.prev_in + (size_t)l * N;
-      for (int i = threadIdx.x; i < N; i += blockDim.x) {
+      for (int i = tid; i < N; i += nt) {
         wa[i] = prev[i];
-        wa[N + i] = in[i];
+        wa[N + i] = inl[i];
       }
-      __syncthreads();
-      for (int i = threadIdx.x; i < N; i += blockDim.x) prev[i] = wa[N + i];
-      rfft_packed(wa, z, Xs, N, a.logN, tw, split);
-      push_tiled(a, a.X, l, a.K, (int)(n % (uint32_t)a.K), Xs);
+      tm.sync();
+      for (int i = tid; i < N; i += nt) prev[i] = wa[N + i];
+      rfft_packed(wa, z, Xs, N, a.logN, tw, split, tm);
+      push_tiled(a, a.X, l, a.K, (int)(n % (uint32_t)a.K), Xs, tm);
+      if (l + 1 == c1) on_x();
     }
     const bool staged = a.front_pre && l == c0;
     const float2* Sl = staged ? pre : reinterpret_cast<const float2*>(a.S + (size_t)l * NF);
     const float2* H0 = staged ? pre + N : reinterpret_cast<const float2*>(a.H0 + (size_t)l * Qh * NF);
-    for (int j = threadIdx.x; j < N; j += blockDim.x) {
+    for (int j = tid; j < N; j += nt) {
       float2 y = Sl[j];
       for (int q = 0; q < Qs; ++q) y = cmac2(y, Xs[(size_t)q * N + j], H0[(size_t)q * N + j], j == 0);
       acc[j] = y;
     }
-    __syncthreads();
+    tm.sync();
     float* out = a.out + (size_t)l * N;
     float* sp = a.spk + (size_t)l * N;
     const bool keep = a.is_aur;
     irfft_packed_tail(acc, z, N, a.logN, tw, split, [&](int i, float v) {
       out[i] = v;
       if (keep) sp[i] = v;
-    });
+    }, tm);
   }
+}
+
+// Canceller stage 1 (convolver.hpp:180-191 on fc_) for loudspeakers
+// [c0, c1): r2c of [l_{n-1}, l_n] into the canceller FDL. Team-generic
+// (k_back_head and the loop kernel). smem: 3N float2 + tables.
+template <typename Team>
+__device__ void head_channels(const BlockArgs& a, uint32_t n, int c0, int c1, float2* z, const float2* tw,
+                              const float2* split, Team tm) {
+  const int N = a.N;
+  float* wa = reinterpret_cast<float*>(z + N);         // 2N
+  float2* sp = reinterpret_cast<float2*>(wa + 2 * N);  // N (spectrum)
+  for (int l = c0; l < c1; ++l) {
+    float* prev = a.prev_spk + (size_t)l * N;
+    const float* spk = a.spk + (size_t)l * N;
+    for (int i = tm.tid(); i < N; i += tm.size()) {
+      wa[i] = prev[i];
+      wa[N + i] = spk[i];
+    }
+    tm.sync();
+    for (int i = tm.tid(); i < N; i += tm.size()) prev[i] = wa[N + i];
+    rfft_packed(wa, z, sp, N, a.logN, tw, split, tm);
+    push_tiled(a, a.XA, l, a.KF + 1, (int)(n % (uint32_t)(a.KF + 1)), sp, tm);
+    tm.sync();
+  }
+}
+
+// NLMS error spectrum E_p = r2c([0_N, m~_p]) (Appendix A step 2) from the
+// raw input: m~_p = g m_p - f^_p. Team-generic. smem: 3N float2.
+template <typename Team>
+__device__ void error_spectrum(const BlockArgs& a, int p, const float* in, float2* z, const float2* tw,
+                               const float2* split, Team tm) {
+  const int N = a.N;
+  float* wa = reinterpret_cast<float*>(z + N);
+  for (int i = tm.tid(); i < N; i += tm.size()) {
+    wa[i] = 0.0f;
+    wa[N + i] = __fsub_rn(__fmul_rn(a.gain, in[(size_t)p * N + i]), a.fhat[(size_t)p * N + i]);
+  }
+  tm.sync();
+  rfft_packed(wa, z, reinterpret_cast<float2*>(a.E + (size_t)p * a.NF), N, a.logN, tw, split, tm);
+}
+
+__global__ void __launch_bounds__(kFrontThreads) k_front(BlockArgs a) {
+  extern __shared__ float4 smem4[];
+  const uint32_t n = a.st->block;
+  trace_begin(a, TR_FRONT, n);
+  const int c0 = blockIdx.x * a.cpb;
+  const int c1 = min(c0 + a.cpb, a.L);
+  front_body(a, n, c0, c1, reinterpret_cast<float2*>(smem4), a.in, a.prev_in, a.cur_mt, blockIdx.x == 0,
+             Cta());
   trace_end(a, TR_FRONT, n);
 }
 
@@ -324,10 +417,8 @@ __global__ void __launch_bounds__(kFrontThreads) k_front(BlockArgs a) {
 __global__ void __launch_bounds__(kFrontThreads) k_back_head(BlockArgs a) {
   extern __shared__ float4 smem4[];
   const int N = a.N;
-  float2* z = reinterpret_cast<float2*>(smem4);  // N
-  float* wa = reinterpret_cast<float*>(z + N);   // 2N
-  float2* sp = reinterpret_cast<float2*>(wa + 2 * N);  // N (spectrum)
-  float2* stw = sp + N;                                 // DftPlan tables (if staged)
+  float2* z = reinterpret_cast<float2*>(smem4);  // 3N float2 work area
+  float2* stw = z + 3 * N;                       // DftPlan tables (if staged)
   const float2* tw = a.smem_tables ? stw : a.tw;
   const float2* split = a.smem_tables ? stw + N / 2 : a.split;
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -342,20 +433,13 @@ __global__ void __launch_bounds__(kFrontThreads) k_back_head(BlockArgs a) {
     trace_end(a, TR_BACK_HEAD, n);
     return;
   }
+  __syncthreads();
   if (b < Lb) {
-    const int l = b;
-    float* prev = a.prev_spk + (size_t)l * N;
-    const float* spk = a.spk + (size_t)l * N;
-    for (int i = threadIdx.x; i < N; i += blockDim.x) {
-      wa[i] = prev[i];
-      wa[N + i] = spk[i];
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < N; i += blockDim.x) prev[i] = wa[N + i];
-    rfft_packed(wa, z, sp, N, a.logN, tw, split);
-    push_tiled(a, a.XA, l, a.KF + 1, (int)(n % (uint32_t)(a.KF + 1)), sp);
+    head_channels(a, n, b, b + 1, z, tw, split, Cta());
   } else {
+    // E_p = r2c([0_N, m~_p]) from the m~ the front saved
     const int p = b - Lb;
+    float* wa = reinterpret_cast<float*>(z + N);
     for (int i = threadIdx.x; i < N; i += blockDim.x) {
       wa[i] = 0.0f;
       wa[N + i] = a.cur_mt[(size_t)p * N + i];

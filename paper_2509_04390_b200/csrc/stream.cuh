@@ -71,6 +71,35 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// Bounded wait (persistent loop): false once *abort is set or ~2 s pass.
+__device__ __forceinline__ bool mbar_wait_bounded(uint64_t* b, uint32_t parity, const unsigned* abort) {
+  if (!abort) {
+    mbar_wait(b, parity);
+    return true;
+  }
+  const unsigned long long t0 = globaltimer();
+  for (unsigned spin = 0;; ++spin) {
+    uint32_t ok;
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+    if (ok) return true;
+    if ((spin & 255u) == 255u) {
+      if (*reinterpret_cast<const volatile unsigned*>(abort)) return false;
+      if (globaltimer() - t0 > 2000000000ull) {
+        atomicExch(const_cast<unsigned*>(abort), 1u);  // tell the rest of the grid
+        return false;
+      }
+    }
+  }
+}
+
 // global -> shared bulk copy completing on an mbarrier, with an L2 policy
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
                                          uint64_t policy) {
@@ -144,9 +173,22 @@ __device__ __forceinline__ void copy_ring(float4* dst, const float4* base, int v
 // (synthesis, MIMO) or a loudspeaker (canceller), so its delay-line rows are
 // one ring run. Canceller stages also carry the column tile's NLMS error
 // spectra and smoothed power.
-template <int LT, bool ELEM, int PT>
+// What the producer must wait for before streaming rows produced by the
+// current block's front half. Graph mode: k_front finished before k_back
+// launched (stream order), and k_back_head is the PDL primary.
+struct GraphDeps {
+  __device__ __forceinline__ const unsigned* abort() const { return nullptr; }
+  __device__ __forceinline__ bool wait_front(uint32_t) const { return true; }
+  __device__ __forceinline__ bool wait_head(uint32_t) const {
+    griddep_wait();
+    return true;
+  }
+};
+
+template <int LT, bool ELEM, int PT, typename Deps = GraphDeps>
 __device__ __forceinline__ void back_produce(const BlockArgs& a, uint32_t n, uint64_t* full,
-                                             uint64_t* empty, float4* slots, StageMeta* meta) {
+                                             uint64_t* empty, float4* slots, StageMeta* meta,
+                                             uint32_t& q, Deps deps = Deps()) {
   constexpr int XL = ELEM ? LT : 1;
   const int S = a.stages, CT = a.CT, CTn = a.CTn, K = a.K, KF = a.KF;
   const int Kt = K - 1, cap = KF + 1;
@@ -156,15 +198,15 @@ __device__ __forceinline__ void back_produce(const BlockArgs& a, uint32_t n, uin
   const uint64_t pol_stream = a.h_in_l2 ? policy_evict_normal() : policy_evict_first();
   const uint64_t pol_keep = policy_evict_last();
   unsigned* queue = a.tick + a.tick_queue;
-  const int s0 = a.item_off[blockIdx.x], s1 = a.item_off[blockIdx.x + 1];
+  const bool planned = (int)blockIdx.x < a.plan_ctas;
+  const int s0 = planned ? a.item_off[blockIdx.x] : 0, s1 = planned ? a.item_off[blockIdx.x + 1] : 0;
   // item sequence: static s0..s1-1, then queue claims
   auto claim = [&](int k) -> int {
     if (s0 + k < s1) return s0 + k;
     const int d = a.n_static + (int)atomicAdd(queue, 1u);
     return d < a.n_chunks ? d : -1;
   };
-  uint32_t q = 0;
-  bool waited = false;
+  bool waited = false, front_ok = false;
   int idx = claim(0);
   int4 rec = idx >= 0 ? a.chunks[idx] : make_int4(0, 0, 0, 0);
   for (int k = 0; idx >= 0; ++k) {
@@ -173,16 +215,27 @@ __device__ __forceinline__ void back_produce(const BlockArgs& a, uint32_t n, uin
     const int4 nrec = nidx >= 0 ? a.chunks[nidx] : make_int4(0, 0, 0, 0);
     const int kind = rec.x & 1, tile = rec.x >> 1;
     const int4 ti = a.tinfo[kind ? a.n_syn_tiles + tile : tile];
+    bool abort = false;
     if (PT > 0 && kind == 1 && !waited) {
-      griddep_wait();  // canceller inputs come from k_back_head
-      waited = true;
+      waited = deps.wait_head(n);  // canceller inputs come from the head (k_back_head)
+      abort = !waited;
     }
     const int B = kind ? KF : Kt;
     const int SP = kind ? a.spa : a.sp;
-    for (int t = rec.y; t < rec.z;) {
+    for (int t = rec.y; t < rec.z && !abort;) {
       const int t1 = min(min(t + SP, rec.z), (t / B + 1) * B);
+      if (!front_ok && kind == 0 && t - (t / Kt) * Kt == 0) {
+        front_ok = deps.wait_front(n);  // this stage reads X(age 0), pushed by the front
+        if (!front_ok) {
+          abort = true;
+          break;
+        }
+      }
       const int s = (int)(q % (uint32_t)S);
-      mbar_wait(empty + s, ((q / (uint32_t)S) & 1u) ^ 1u);
+      if (!mbar_wait_bounded(empty + s, ((q / (uint32_t)S) & 1u) ^ 1u, deps.abort())) {
+        abort = true;
+        break;
+      }
       meta[s] = StageMeta{idx, t, t1, (t1 == rec.z ? 1 : 0) | (kind << 1), tile, rec.w, ti};
       float4* dst = slots + (size_t)s * a.slot_f4;
       const int nt = t1 - t;
@@ -221,13 +274,15 @@ __device__ __forceinline__ void back_produce(const BlockArgs& a, uint32_t n, uin
       ++q;
       t = t1;
     }
+    if (abort) break;  // a dependency wait failed (loop mode timeout): stop streaming
     idx = nidx;
     rec = nrec;
   }
   const int s = (int)(q % (uint32_t)S);
-  mbar_wait(empty + s, ((q / (uint32_t)S) & 1u) ^ 1u);
+  if (!mbar_wait_bounded(empty + s, ((q / (uint32_t)S) & 1u) ^ 1u, deps.abort())) return;
   meta[s].item = -1;
   mbar_arrive(full + s);
+  ++q;
 }
 
 // Fixed-order split-K partial of R rows x CT columns from the consumers'
@@ -262,40 +317,18 @@ __device__ __forceinline__ void team_partial(float4 (&acc)[RM], int R, int CT, i
   consumers_sync();
 }
 
-// ------------------------------------------------------------------- k_back
-// grid = back_ctas (<= 148, one per SM), kBackThreads threads, dynamic smem:
-// [mbarriers + stage metadata | red (red_f4 float4; also the c2r scratch) |
-// stages x slot].
-template <int LT, bool ELEM, int PT>  // PT = 0: no canceller
-__global__ void __launch_bounds__(kBackThreads, 1) k_back(const __grid_constant__ BlockArgs a) {
-  extern __shared__ __align__(128) unsigned char bsm[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(bsm);
-  uint64_t* empty = full + kMaxStages;
-  StageMeta* meta = reinterpret_cast<StageMeta*>(empty + kMaxStages);
-  float4* red = reinterpret_cast<float4*>(bsm + kBackBarrierBytes);
-  float4* slots = red + a.red_f4;
+// --------------------------------------------------------------- consumers
+// Warps 0-7: consume this CTA's stages of block n until the producer's
+// sentinel (q is the CTA's running stage count, shared with the producer's
+// by construction), leaving one split-K partial per work item.
+template <int LT, bool ELEM, int PT>
+__device__ __forceinline__ void back_consume(const BlockArgs& a, uint32_t n, uint64_t* full,
+                                             uint64_t* empty, StageMeta* meta, float4* red,
+                                             float4* slots, uint32_t& q, unsigned long long* ctr,
+                                             const unsigned* abort = nullptr) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int S = a.stages;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < S; ++s) {
-      mbar_init(full + s, 1);
-      mbar_init(empty + s, kConsumers / 32);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  }
-  griddep_launch();  // k_reduce may take the SMs this kernel's CTAs leave
-  __syncthreads();
-  const uint32_t n = a.st->block;
-  if (warp == kConsumers / 32) {
-    if (lane == 0) back_produce<LT, ELEM, PT>(a, n, full, empty, slots, meta);
-    return;
-  }
-  if (a.trace && threadIdx.x == 0)
-    atomicMin(&a.trace[((n % kTraceBlocks) * kTraceKernels + TR_BACK) * 2], globaltimer());
-  unsigned long long* ctr = a.seg_trace ? a.seg_trace + 4 * (size_t)a.n_chunks + 3 * blockIdx.x : nullptr;
-  if (ctr && threadIdx.x == 0) ctr[0] = globaltimer();
-
+  (void)n;
   // consumer geometry: lane = pl * 8 + cl ; warp = pg * CG + cg
   const int CT = a.CT, CTn = a.CTn, K = a.K, KF = a.KF, NF = a.NF;
   const int CG = CT >> 3, PG = 8 / CG, PH = PG * 4;
@@ -309,12 +342,15 @@ __global__ void __launch_bounds__(kBackThreads, 1) k_back(const __grid_constant_
   const int R = P + nl;  // canceller partial rows; row P: loudspeaker power
   constexpr int PA = PT > 0 ? PT : 1;
 
-  uint32_t q = 0;
   for (;;) {
     int sl = (int)(q % (uint32_t)S);
-    mbar_wait(full + sl, (q / (uint32_t)S) & 1u);
+    if (!mbar_wait_bounded(full + sl, (q / (uint32_t)S) & 1u, abort)) return;
     StageMeta m = meta[sl];
-    if (m.item < 0) break;
+    if (m.item < 0) {  // sentinel: release its slot too (the ring persists in the loop)
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + sl);
+      break;
+    }
     if (ctr && q == 0 && threadIdx.x == 0) ctr[1] = globaltimer();
     const int item = m.item, tile = m.tile, slot = m.slot;
     const int4 ti = m.ti;
@@ -352,7 +388,7 @@ __global__ void __launch_bounds__(kBackThreads, 1) k_back(const __grid_constant_
         ++q;
         if (m.flags & 1) break;
         sl = (int)(q % (uint32_t)S);
-        mbar_wait(full + sl, (q / (uint32_t)S) & 1u);
+        if (!mbar_wait_bounded(full + sl, (q / (uint32_t)S) & 1u, abort)) return;
         m = meta[sl];
       }
       const int E = LT * CT;
@@ -440,7 +476,7 @@ __global__ void __launch_bounds__(kBackThreads, 1) k_back(const __grid_constant_
         ++q;
         if (m.flags & 1) break;
         sl = (int)(q % (uint32_t)S);
-        mbar_wait(full + sl, (q / (uint32_t)S) & 1u);
+        if (!mbar_wait_bounded(full + sl, (q / (uint32_t)S) & 1u, abort)) return;
         m = meta[sl];
       }
       const int E = R * CT;
@@ -454,6 +490,46 @@ __global__ void __launch_bounds__(kBackThreads, 1) k_back(const __grid_constant_
       a.seg_trace[4 * (size_t)item + 3] = blockIdx.x;
     }
   }
+  ++q;  // the sentinel stage
+}
+
+// ------------------------------------------------------------------- k_back
+// grid = back_ctas (<= 148, one per SM), kBackThreads threads, dynamic smem:
+// [mbarriers + stage metadata | red (red_f4 float4; also the c2r scratch) |
+// stages x slot].
+template <int LT, bool ELEM, int PT>  // PT = 0: no canceller
+__global__ void __launch_bounds__(kBackThreads, 1) k_back(const __grid_constant__ BlockArgs a) {
+  extern __shared__ __align__(128) unsigned char bsm[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(bsm);
+  uint64_t* empty = full + kMaxStages;
+  StageMeta* meta = reinterpret_cast<StageMeta*>(empty + kMaxStages);
+  float4* red = reinterpret_cast<float4*>(bsm + kBackBarrierBytes);
+  float4* slots = red + a.red_f4;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int S = a.stages;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, kConsumers / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  griddep_launch();  // k_reduce may take the SMs this kernel's CTAs leave
+  __syncthreads();
+  const uint32_t n = a.st->block;
+  if (warp == kConsumers / 32) {
+    uint32_t qp = 0;
+    if (lane == 0) back_produce<LT, ELEM, PT>(a, n, full, empty, slots, meta, qp);
+    return;
+  }
+  if (a.trace && threadIdx.x == 0)
+    atomicMin(&a.trace[((n % kTraceBlocks) * kTraceKernels + TR_BACK) * 2], globaltimer());
+  unsigned long long* ctr = a.seg_trace ? a.seg_trace + 4 * (size_t)a.n_chunks + 3 * blockIdx.x : nullptr;
+  if (ctr && threadIdx.x == 0) ctr[0] = globaltimer();
+
+  uint32_t q = 0;
+  back_consume<LT, ELEM, PT>(a, n, full, empty, meta, red, slots, q, ctr);
   if (ctr && threadIdx.x == 0) ctr[2] = globaltimer();
   if (threadIdx.x == 0) {
     if (a.trace) atomicMax(&a.trace[((n % kTraceBlocks) * kTraceKernels + TR_BACK) * 2 + 1], globaltimer());
@@ -481,14 +557,36 @@ __global__ void __launch_bounds__(kBackThreads, 1) k_back(const __grid_constant_
 // step 5). The last CTA advances the block (sharded: k_afc_finish does).
 // grid = red_syn_ctas + red_afc_ctas, kReduceThreads threads.
 constexpr int kReduceThreads = 256;
-__global__ void __launch_bounds__(kReduceThreads) k_reduce(const __grid_constant__ BlockArgs a) {
-  extern __shared__ float4 rsm[];  // kReduceThreads float4; canceller: c2r scratch, tables, power
-  __shared__ int s_last;
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+
+// Shared-memory float4 count of k_reduce's scratch: the combine buffer, and
+// for the canceller the c2r scratch (N float2), the DftPlan tables and the
+// smoothed power (N float2).
+__host__ __device__ inline size_t reduce_smem_f4(int N, bool aur) {
+  return kReduceThreads + (aur ? (2 * (size_t)N + table_f2(N) + 1) / 2 : 0);
+}
+
+// Canceller reduce CTAs: stage the DftPlan tables and the smoothed power --
+// they do not depend on the streaming kernel -- for whichever of them
+// finishes f^. Call before the partials are ready; the caller syncs.
+template <typename Team>
+__device__ __forceinline__ void reduce_prefetch(const BlockArgs& a, int b, float4* rsm, Team tm) {
+  if (b < a.red_syn_ctas) return;
+  float2* z = reinterpret_cast<float2*>(rsm + kReduceThreads);
+  float2* tw = z + a.N;
+  float2* split = tw + a.N / 2;
+  float2* pws = split + a.N / 2 + 1;
+  stage_tables(tw, split, a.tw, a.split, a.N, tm);
+  if (a.nlms)
+    for (int jj = tm.tid(); jj < a.N; jj += tm.size()) pws[jj] = a.pw[jj];
+}
+
+// Reduce CTA b of block n (see k_reduce) with a team of kReduceThreads
+// threads; s_last: shared int. The partials must be complete and visible.
+template <typename Team>
+__device__ void reduce_part(const BlockArgs& a, int b, uint32_t n, float4* rsm, int* s_last, Team tm) {
   const int CT = a.CT, NF = a.NF;
-  const int b = blockIdx.x;
+  const int tid = tm.tid();
   const bool afc = b >= a.red_syn_ctas;
-  // this CTA's tile and element range
   const int E = afc ? a.red_afc_rows * CT : a.LTr * CT;
   const int cpt = afc ? a.red_afc_cpt : a.red_syn_cpt;  // CTAs per tile
   const int bb = afc ? b - a.red_syn_ctas : b;
@@ -500,21 +598,7 @@ __global__ void __launch_bounds__(kReduceThreads) k_reduce(const __grid_constant
   const int ne = e1 - e0;
   const int sub = max(1, kReduceThreads / max(ne, 1));
   const int per = (ti.y + sub - 1) / sub;
-  // canceller CTAs: stage the DftPlan tables and the smoothed power now --
-  // they do not depend on k_back -- for whichever of them finishes f^
-  float2* z = reinterpret_cast<float2*>(rsm + kReduceThreads);
-  float2* tw = z + a.N;
-  float2* split = tw + a.N / 2;
-  float2* pws = split + a.N / 2 + 1;
-  if (afc) {
-    stage_tables(tw, split, a.tw, a.split, a.N);
-    if (a.nlms)
-      for (int jj = threadIdx.x; jj < a.N; jj += blockDim.x) pws[jj] = a.pw[jj];
-  }
-  griddep_wait();  // k_back's partials
-  const uint32_t n = a.st->block;
-  trace_begin(a, TR_REDUCE, n);
-  const int el = threadIdx.x % max(ne, 1), j = threadIdx.x / max(ne, 1);
+  const int el = tid % max(ne, 1), j = tid / max(ne, 1);
   float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
   if (ne > 0 && j < sub) {
     const float4* p = src + e0 + el;
@@ -529,12 +613,12 @@ __global__ void __launch_bounds__(kReduceThreads) k_reduce(const __grid_constant
         if (i + u < i1) v = (i + u == i0) ? t[u] : f4add(v, t[u]);
     }
   }
-  rsm[threadIdx.x] = v;
-  __syncthreads();
-  if (threadIdx.x < ne) {
-    float4 w = rsm[threadIdx.x];
-    for (int jj = 1; jj < sub; ++jj) w = f4add(w, rsm[jj * ne + threadIdx.x]);
-    const int e = e0 + threadIdx.x;
+  rsm[tid] = v;
+  tm.sync();
+  if (tid < ne) {
+    float4 w = rsm[tid];
+    for (int jj = 1; jj < sub; ++jj) w = f4add(w, rsm[jj * ne + tid]);
+    const int e = e0 + tid;
     const int r = e / CT, col = e - r * CT;
     if (afc) {
       __stcg(a.yhat + (size_t)r * NF + tile * CT + col, w);
@@ -544,51 +628,81 @@ __global__ void __launch_bounds__(kReduceThreads) k_reduce(const __grid_constant
     }
   }
   __threadfence();
-  __syncthreads();
-  if (afc) {
-    if (threadIdx.x == 0) {
-      unsigned* t = a.tick + 0;
-      s_last = atomicAdd(t, 1u) == (unsigned)a.red_afc_ctas - 1u;
-      if (s_last) *t = 0u;
-    }
-    __syncthreads();
-    if (s_last) {
-      __threadfence();
-      // the canceller of block n is complete: f^ for block n+1
-      const int N = a.N, P = a.P;
-      const bool sharded = a.G > 1;
-      for (int p = 0; p < P; ++p) {
-        // sharded: this shard's partial f^_p (c2r is linear), summed by k_afc_finish
-        float* fh = sharded ? a.xmine + (size_t)p * N : a.fhat + (size_t)p * N;
-        float* fhh = a.fhat_host + (size_t)p * N;
-        irfft_packed_tail(reinterpret_cast<const float2*>(a.yhat + (size_t)p * NF), z, N, a.logN, tw,
-                          split, [&](int i, float x) {
-                            fh[i] = x;
-                            if (!sharded) fhh[i] = x;
-                          });
+  tm.sync();
+  if (!afc) return;
+  if (tid == 0) {
+    unsigned* t = a.tick + 0;
+    *s_last = atomicAdd(t, 1u) == (unsigned)a.red_afc_ctas - 1u;
+    if (*s_last) *t = 0u;
+  }
+  tm.sync();
+  if (!*s_last) return;
+  __threadfence();
+  // the canceller of block n is complete: f^ for block n+1
+  const int N = a.N, P = a.P;
+  const bool sharded = a.G > 1;
+  float2* z = reinterpret_cast<float2*>(rsm + kReduceThreads);
+  float2* tw = z + N;
+  float2* split = tw + N / 2;
+  float2* pws = split + N / 2 + 1;
+  for (int p = 0; p < P; ++p) {
+    // sharded: this shard's partial f^_p (c2r is linear), summed by k_afc_finish
+    float* fh = sharded ? a.xmine + (size_t)p * N : a.fhat + (size_t)p * N;
+    float* fhh = a.fhat_host + (size_t)p * N;
+    irfft_packed_tail(
+        reinterpret_cast<const float2*>(a.yhat + (size_t)p * NF), z, N, a.logN, tw, split,
+        [&](int i, float x) {
+          fh[i] = x;
+          if (!sharded) fhh[i] = x;
+        },
+        tm);
+  }
+  if (a.nlms) {
+    const float2* sum = reinterpret_cast<const float2*>(a.yhat + (size_t)P * NF);
+    const float oml = __fsub_rn(1.0f, a.lambda);
+    for (int jj = tid; jj < N; jj += tm.size()) {
+      const float2 x = __ldcg(sum + jj);
+      if (sharded) {  // partial power of this shard's loudspeakers
+        reinterpret_cast<float2*>(a.xmine + (size_t)P * N)[jj] = x;
+        continue;
       }
-      if (a.nlms) {
-        const float2* sum = reinterpret_cast<const float2*>(a.yhat + (size_t)P * NF);
-        const float oml = __fsub_rn(1.0f, a.lambda);
-        for (int jj = threadIdx.x; jj < N; jj += blockDim.x) {
-          const float2 x = __ldcg(sum + jj);
-          if (sharded) {  // partial power of this shard's loudspeakers
-            reinterpret_cast<float2*>(a.xmine + (size_t)P * N)[jj] = x;
-            continue;
-          }
-          float2 w = pws[jj];
-          w.x = __fadd_rn(__fmul_rn(a.lambda, w.x), __fmul_rn(oml, x.x));
-          w.y = __fadd_rn(__fmul_rn(a.lambda, w.y), __fmul_rn(oml, x.y));
-          a.pw[jj] = w;
-        }
-      }
-      if (a.trace && threadIdx.x == 0) {
-        const unsigned long long now = globaltimer();
-        atomicMin(&a.trace[((n % kTraceBlocks) * kTraceKernels + TR_AFC_DONE) * 2], now);
-        atomicMax(&a.trace[((n % kTraceBlocks) * kTraceKernels + TR_AFC_DONE) * 2 + 1], now);
-      }
+      float2 w = pws[jj];
+      w.x = __fadd_rn(__fmul_rn(a.lambda, w.x), __fmul_rn(oml, x.x));
+      w.y = __fadd_rn(__fmul_rn(a.lambda, w.y), __fmul_rn(oml, x.y));
+      a.pw[jj] = w;
     }
   }
+  if (a.trace && tid == 0) {
+    const unsigned long long now = globaltimer();
+    atomicMin(&a.trace[((n % kTraceBlocks) * kTraceKernels + TR_AFC_DONE) * 2], now);
+    atomicMax(&a.trace[((n % kTraceBlocks) * kTraceKernels + TR_AFC_DONE) * 2 + 1], now);
+  }
+  __threadfence();
+  tm.sync();
+}
+
+// ----------------------------------------------------------------- k_reduce
+// The split-K reduction of block n, after k_back (programmatic dependent
+// launch: its CTAs take the SMs k_back's CTAs leave and wait for k_back with
+// griddepcontrol.wait). CTA b sums, for `epc` elements of one tile, the
+// tile's partials in slot order -- `sub` threads per element over contiguous
+// slot ranges, combined in order through shared memory -- so the association
+// is fixed and results are bit-reproducible. Synthesis tiles -> S (block
+// n+1's partitions >= 1); canceller column tiles -> Yhat, after which the
+// last canceller CTA does one c2r per mic (f^ for block n+1; the sum over
+// loudspeakers is done in the frequency domain -- one c2r per mic instead of
+// the reference's L, auralizer.hpp:81-86) and smooths the power (Appendix A
+// step 5). The last CTA advances the block (sharded: k_afc_finish does).
+// grid = red_syn_ctas + red_afc_ctas, kReduceThreads threads.
+__global__ void __launch_bounds__(kReduceThreads) k_reduce(const __grid_constant__ BlockArgs a) {
+  extern __shared__ float4 rsm[];  // reduce_smem_f4(N, aur) float4
+  __shared__ int s_last;
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  reduce_prefetch(a, blockIdx.x, rsm, Cta());
+  griddep_wait();  // k_back's partials
+  const uint32_t n = a.st->block;
+  trace_begin(a, TR_REDUCE, n);
+  reduce_part(a, blockIdx.x, n, rsm, &s_last, Cta());
   trace_end(a, TR_REDUCE, n);
   // retire: advance the block (sharded: k_afc_finish does)
   if (threadIdx.x == 0) {
