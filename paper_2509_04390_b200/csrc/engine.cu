@@ -182,6 +182,9 @@ struct aura_b200_engine {
   int loop_stages = 0;
   bool loop_device_io = false;
   std::vector<unsigned long long> loop_last_stamps;  // of the last loop-mode device timing
+  unsigned long long* h_outflag = nullptr;  // mapped: k_front writes block + 1 when the output is out
+  bool use_outflag = true;
+  uint64_t dev_block_base = 0;  // device block number of host block 0 (measurement calls advance both)
   int loop_hold = 1;
   int back_ctas = 0;
   size_t smem_back = 0, smem_reduce = 0;
@@ -210,6 +213,7 @@ struct aura_b200_engine {
     if (h_fhat) cudaFreeHost(h_fhat);
     if (h_status) cudaFreeHost(h_status);
     if (h_mbox) cudaFreeHost(h_mbox);
+    if (h_outflag) cudaFreeHost(h_outflag);
     for (void* p : ipc_opened) cudaIpcCloseMemHandle(p);
     if (ev_front) cudaEventDestroy(ev_front);
     if (ev_back) cudaEventDestroy(ev_back);
@@ -751,10 +755,18 @@ void finish_init(aura_b200_engine* e) {
   CK(cudaMemset(e->d_in_pool, 0, e->pool_blocks * in_ch * N * sizeof(float)));
   e->d_out = dalloc<float>(e->L * N, e->dmem);
   plan_loop(e);
+  // output-ready word for process(): mapped host memory, written by k_front
+  CK(cudaHostAlloc(&e->h_outflag, sizeof(unsigned long long), cudaHostAllocMapped | cudaHostAllocPortable));
+  *e->h_outflag = 0;
+  CK(cudaHostGetDevicePointer((void**)&a.out_flag, e->h_outflag, 0));
+  if (const char* f = std::getenv("AURA_B200_OUTFLAG")) e->use_outflag = std::atoi(f) != 0;
+  a.front_ticket = dalloc<unsigned>(1, e->dmem);
+  CK(cudaMemset(a.front_ticket, 0, sizeof(unsigned)));
   e->rebuild_graphs();
   e->dev_args = a;
   e->dev_args.out = e->d_out;
   e->dev_args.in = e->d_in_pool;
+  e->dev_args.out_flag = nullptr;  // device-resident measurement: no host handshake
   CK(cudaStreamSynchronize(e->stream));
 }
 
@@ -898,6 +910,7 @@ void reset_state(aura_b200_engine* e) {
   CK(cudaStreamSynchronize(s));
   e->blocks = 0;
   e->loop_posted = 0;  // the persistent loop restarts at block 0 too
+  if (e->h_outflag) *reinterpret_cast<volatile unsigned long long*>(e->h_outflag) = 0;
 }
 
 void alloc_synth(aura_b200_engine* e, BlockArgs& a) {
@@ -1126,6 +1139,29 @@ int aura_b200_auralizer_create(const aura_b200_config* cfg,
 void aura_b200_destroy(aura_b200_engine* e) { delete e; }
 
 namespace {
+// The device block number the next graph launch will process: the host
+// counts blocks; measurement calls advance host and device together.
+uint32_t device_block_hint(aura_b200_engine* e) { return (uint32_t)(e->blocks + e->dev_block_base); }
+
+// Spin until k_front has published `target` in the mapped output flag.
+void wait_flag(aura_b200_engine* e, unsigned long long target, const char* what) {
+  volatile unsigned long long* f = e->h_outflag;
+  uint64_t spins = 0;
+  const auto t0 = std::chrono::steady_clock::now();
+  while (*f < target) {
+#if defined(__x86_64__)
+    _mm_pause();
+#endif
+    if ((++spins & 0xFFFF) == 0) {
+      const cudaError_t q = cudaStreamQuery(e->stream);
+      if (q != cudaErrorNotReady && q != cudaSuccess) ck(q, what);
+      if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(20))
+        fail(AURA_B200_E_TIMEOUT, std::string(what) + ": not complete within 20 s");
+    }
+  }
+  std::atomic_thread_fence(std::memory_order_acquire);
+}
+
 // Spin until `ev` (recorded on the engine stream) has completed; kernel
 // completion makes the block's mapped-memory writes visible to the host.
 void wait_event(aura_b200_engine* e, cudaEvent_t ev, const char* what) {
@@ -1176,9 +1212,15 @@ int aura_b200_process(aura_b200_engine* e, const float* in, float* out) {
     // the previous block's front has completed, so the staging buffer is free
     std::memcpy(e->h_in, in, n_in * sizeof(float));
     std::atomic_thread_fence(std::memory_order_release);
+    const uint32_t nblk = device_block_hint(e);
     e->enqueue_block(e->g_block, e->args, e->ev_front);  // records ev_front after k_front
     CK(cudaEventRecord(e->ev_back, e->stream));
-    wait_event(e, e->ev_front, "block output");
+    if (e->use_outflag) {
+      // k_front's last CTA publishes block + 1 once every output is written
+      wait_flag(e, nblk + 1, "block output");
+    } else {
+      wait_event(e, e->ev_front, "block output");
+    }
     std::memcpy(out, e->h_out, e->L * e->N * sizeof(float));
     ++e->blocks;
   });
@@ -1392,6 +1434,7 @@ void shard_finalize(aura_b200_engine* e, char* const* peers) {
   BlockArgs d = a;
   d.out = e->d_out;
   d.in = e->d_in_pool;
+  d.out_flag = nullptr;
   e->dev_args = d;
 }
 

@@ -131,6 +131,10 @@ struct BlockArgs {
   unsigned long long* loop_stamps;  // per block {released, output written, done} (%globaltimer)
   unsigned long long loop_idle_ns;  // park (exit) after this long without a doorbell
   int loop_hold;                    // producers start after the fronts' input spectra are pushed
+  // graph mode: the last k_front CTA publishes (block + 1) here (mapped host
+  // memory) once every output is written -- the host polls it instead of an event
+  unsigned long long* out_flag;
+  unsigned* front_ticket;
   unsigned long long* seg_trace;  // diagnostics: [chunks] x {end, cta}, then [ctas] x {start, first data, exit}
   // tables
   const float2* tw;     // N/2, e^{-2 pi i j / N}
@@ -404,6 +408,17 @@ __global__ void __launch_bounds__(kFrontThreads) k_front(BlockArgs a) {
   const int c1 = min(c0 + a.cpb, a.L);
   front_body(a, n, c0, c1, reinterpret_cast<float2*>(smem4), a.in, a.prev_in, a.cur_mt, blockIdx.x == 0,
              Cta());
+  if (a.out_flag) {  // outputs written: the last CTA tells the host
+    __syncthreads();  // every thread's output stores precede thread 0's system fence
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      if (atomicAdd(a.front_ticket, 1u) == gridDim.x - 1u) {
+        *a.front_ticket = 0u;
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(a.out_flag), "l"((unsigned long long)n + 1)
+                     : "memory");
+      }
+    }
+  }
   trace_end(a, TR_FRONT, n);
 }
 
