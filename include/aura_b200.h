@@ -155,6 +155,11 @@ int aura_b200_launch_mode(const aura_b200_engine* e);
  * canceller heads done, streaming done, block done, CTA 0's reduction done}
  * per block (-1: n/a). */
 int aura_b200_loop_phases(const aura_b200_engine* e, size_t blocks, double* out);
+/* Diagnostics: host-side breakdown of process() in graph mode, per block
+ * (optionally paced): us from the call's start to {input staged, graph
+ * launched, background event recorded, output flag seen, output copied}. */
+int aura_b200_time_host_breakdown(aura_b200_engine* e, const float* host_in, size_t n_in_blocks,
+                                  size_t blocks, double pace_us, double* out);
 float aura_b200_input_gain(const aura_b200_engine* e);
 
 /* ---- accessors (convolver.hpp:96-107, auralizer.hpp:44-49) ----------- */

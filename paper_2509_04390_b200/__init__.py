@@ -179,6 +179,7 @@ def lib():
     L.aura_b200_set_launch_mode.argtypes = [vp, C.c_int]
     L.aura_b200_launch_mode.argtypes = [vp]
     L.aura_b200_loop_phases.argtypes = [vp, sz, vp]
+    L.aura_b200_time_host_breakdown.argtypes = [vp, vp, sz, sz, C.c_double, vp]
     L.aura_b200_input_gain.argtypes = [vp]
     L.aura_b200_input_gain.restype = C.c_float
     for name in ("blocks_processed",):
@@ -344,6 +345,16 @@ class _Engine:
 
     def launch_mode(self) -> int:
         return int(lib().aura_b200_launch_mode(self._h))
+
+    HOST_PHASES = ("staged", "launched", "event", "output_seen", "copied")
+
+    def time_host_breakdown(self, inputs: np.ndarray, blocks: int, pace_us: float = 0.0):
+        """Diagnostics: steady_clock offsets (us) inside process(), graph mode."""
+        inputs = np.ascontiguousarray(inputs, np.float32)
+        out = np.zeros((blocks, 5), np.float64)
+        _check(lib().aura_b200_time_host_breakdown(self._h, inputs.ctypes.data, inputs.shape[0], blocks,
+                                                   pace_us, out.ctypes.data))
+        return {k: out[:, i] for i, k in enumerate(self.HOST_PHASES)}
 
     LOOP_PHASES = ("output", "x_pushed", "heads_done", "streamed", "done", "cta0_reduced")
 

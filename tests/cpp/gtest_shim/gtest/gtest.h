@@ -1,7 +1,8 @@
 // gtest.h -- minimal GoogleTest-compatible shim (GTest is not installed in
 // this image). Enough of the API to compile the reference's own unit tests
 // (/root/reference/proj/tests/test_*.cpp) unchanged against the B200 drop-in
-// headers: TEST, EXPECT_/ASSERT_ {EQ,NE,LT,LE,GT,GE,NEAR,TRUE,FALSE,THROW,
+// headers: TEST, TEST_F (fixtures deriving ::testing::Test with SetUp /
+// TearDown), EXPECT_/ASSERT_ {EQ,NE,LT,LE,GT,GE,NEAR,TRUE,FALSE,THROW,
 // NO_THROW}, streaming of extra failure messages, and a main() that runs
 // every registered test, honours --gtest_filter=-A.B:C.D (negative filter
 // only) and prints one "[  PASSED  ]"/"[  FAILED  ]" line per test.
@@ -17,6 +18,26 @@
 #include <vector>
 
 namespace testing {
+
+// Fixture base: TEST_F(F, name) derives from F, runs SetUp, the body, then
+// TearDown (also when the body throws).
+class Test {
+ public:
+  virtual ~Test() = default;
+  virtual void SetUp() {}
+  virtual void TearDown() {}
+  virtual void TestBody() = 0;
+  void Run() {
+    SetUp();
+    try {
+      TestBody();
+    } catch (...) {
+      TearDown();
+      throw;
+    }
+    TearDown();
+  }
+};
 
 struct TestInfo {
   std::string suite, name;
@@ -144,6 +165,19 @@ inline int run_all(int argc, char** argv) {
   static ::testing::Registrar GTEST_SHIM_CAT(gtest_reg_##suite##_, name)(            \
       #suite, #name, &GTEST_SHIM_CAT(gtest_fn_##suite##_, name));                    \
   static void GTEST_SHIM_CAT(gtest_fn_##suite##_, name)()
+
+#define TEST_F(fixture, name)                                                        \
+  namespace {                                                                        \
+  struct GTEST_SHIM_CAT(fixture##_, name) : public fixture {                         \
+    void TestBody() override;                                                        \
+  };                                                                                 \
+  ::testing::Registrar GTEST_SHIM_CAT(gtest_reg_##fixture##_, name)(                 \
+      #fixture, #name, [] {                                                          \
+        GTEST_SHIM_CAT(fixture##_, name) t;                                          \
+        t.Run();                                                                     \
+      });                                                                            \
+  }                                                                                  \
+  void GTEST_SHIM_CAT(fixture##_, name)::TestBody()
 
 // non-fatal: report and continue; fatal: report and leave the test body
 #define GTEST_SHIM_CHECK(cond, what, fatal)                                          \

@@ -28,7 +28,12 @@ def main():
     mic = rng.standard_normal((64, 1, N)).astype(np.float32)
     pace = 1e6 * N / 48000
     q = lambda v: {p: round(float(np.percentile(v, p)), 2) for p in (50, 90, 99)}
-    for mode in (0, 2):
+    e.set_launch_mode(0)
+    for p in (0.0, pace):
+        br = e.time_host_breakdown(mic, 1000, pace_us=p)
+        print(json.dumps({"breakdown_pace_us": p, "p50": {k: round(float(np.median(v)), 2) for k, v in br.items()},
+                          "p99": {k: round(float(np.percentile(v, 99)), 2) for k, v in br.items()}}), flush=True)
+    for mode in (0, 1, 2):
         e.set_launch_mode(mode)
         e.time_host_blocks(mic, 200)
         b2b = e.time_host_blocks(mic, args.blocks)
