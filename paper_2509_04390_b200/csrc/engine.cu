@@ -222,7 +222,11 @@ struct aura_b200_engine {
 
   bool has_syn() const { return K > 1; }
   bool has_back() const { return has_syn() || aur; }
-  bool has_head() const { return aur || mode != AURA_B200_ELEMENTWISE; }
+  bool front_head = false;  // k_front runs the canceller head; k_back is its PDL dependent
+  bool has_head() const { return !front_head && (aur || mode != AURA_B200_ELEMENTWISE); }
+  int front_grid(const BlockArgs& a) const {
+    return (int)((L + a.cpb - 1) / a.cpb) + ((front_head && aur && a.nlms) ? (int)P : 0);
+  }
   bool sharded() const { return aur && G > 1; }
 
   // k_back after k_back_head is a programmatic dependent launch: it starts
@@ -246,18 +250,17 @@ struct aura_b200_engine {
 
   void launch_phase(int ph, const BlockArgs& a, cudaStream_t s) {
     switch (ph) {
-      case PH_FRONT: {
-        const int grid = (int)((L + a.cpb - 1) / a.cpb);
-        k_front<<<grid, kFrontThreads, smem_front, s>>>(a);
+      case PH_FRONT:
+        k_front<<<front_grid(a), kFrontThreads, smem_front, s>>>(a);
         break;
-      }
       case PH_BACK_HEAD:
         if (has_head())
           k_back_head<<<(unsigned)(aur ? L + (a.nlms ? P : 0) : 1), kFrontThreads, smem_head, s>>>(a);
         break;
       case PH_BACK:
         if (has_back())
-          launch_pdl(back_fn, (unsigned)back_ctas, kBackThreads, smem_back, has_head() && !pdl_off, a, s);
+          launch_pdl(back_fn, (unsigned)back_ctas, kBackThreads, smem_back,
+                     (has_head() || front_head) && !pdl_off, a, s);
         break;
       case PH_REDUCE:
         if (has_back())
@@ -755,6 +758,8 @@ void finish_init(aura_b200_engine* e) {
   CK(cudaMemset(e->d_in_pool, 0, e->pool_blocks * in_ch * N * sizeof(float)));
   e->d_out = dalloc<float>(e->L * N, e->dmem);
   plan_loop(e);
+  if (const char* fh = std::getenv("AURA_B200_FRONT_HEAD")) e->front_head = std::atoi(fh) != 0;
+  a.front_head = e->front_head ? 1 : 0;
   // output-ready word for process(): mapped host memory, written by k_front
   CK(cudaHostAlloc(&e->h_outflag, sizeof(unsigned long long), cudaHostAllocMapped | cudaHostAllocPortable));
   *e->h_outflag = 0;
@@ -816,7 +821,7 @@ void start_loop(aura_b200_engine* e, bool device_io) {
   const uint32_t n0 = device_block(e);
   BlockArgs la = device_io ? e->dev_args : e->args;
   // window history: block n reads (n odd ? hist1 : prev_in)
-  if (e->mode != AURA_B200_ELEMENTWISE && (n0 & 1u))
+  if (!e->front_head && e->mode != AURA_B200_ELEMENTWISE && (n0 & 1u))
     CK(cudaMemcpy(la.hist1, la.prev_in, sizeof(float) * e->Qx * e->N, cudaMemcpyDeviceToDevice));
   CK(cudaMemset(e->d_ctl, 0, sizeof(LoopCtl)));
   volatile LoopMailbox* mb = mbox(e);
@@ -863,7 +868,7 @@ void loop_reap(aura_b200_engine* e) {
   ck(r, "persistent loop exit");
   if (mbox(e)->err) fail(AURA_B200_E_TIMEOUT, "persistent loop: internal timeout");
   const uint32_t n = device_block(e);
-  if (e->mode != AURA_B200_ELEMENTWISE && (n & 1u))
+  if (!e->front_head && e->mode != AURA_B200_ELEMENTWISE && (n & 1u))
     CK(cudaMemcpy(e->args.prev_in, e->args.hist1, sizeof(float) * e->Qx * e->N, cudaMemcpyDeviceToDevice));
 }
 
@@ -893,6 +898,7 @@ void reset_state(aura_b200_engine* e) {
   CK(cudaStreamSynchronize(s));
   CK(cudaMemsetAsync(a.st, 0, sizeof(DevState), s));
   CK(cudaMemsetAsync(a.prev_in, 0, sizeof(float) * e->Qx * N, s));
+  if (a.hist1) CK(cudaMemsetAsync(a.hist1, 0, sizeof(float) * e->Qx * N, s));
   CK(cudaMemsetAsync(a.X, 0, sizeof(float4) * (size_t)e->Qx * e->K * NF, s));
   CK(cudaMemsetAsync(a.S, 0, sizeof(float4) * e->L * NF, s));
   if (e->aur) {
@@ -1636,6 +1642,55 @@ int aura_b200_time_host_blocks(aura_b200_engine* e, const float* host_in,
     block_us[b] = (float)std::chrono::duration<double, std::micro>(t1 - t0).count();
   }
   return AURA_B200_OK;
+}
+
+// Diagnostics: where the host-visible latency of process() goes (graph
+// mode). Per block (optionally paced), steady_clock offsets in us from the
+// call's start: {input staged, graph launched, background event recorded,
+// output flag seen, output copied}.
+int aura_b200_time_host_breakdown(aura_b200_engine* e, const float* host_in, size_t n_in_blocks,
+                                  size_t blocks, double pace_us, double* out) {
+  return guarded([&] {
+    stop_loop(e);
+    if (e->launch_mode != 0) fail(AURA_B200_E_INVALID_ARGUMENT, "graph mode only");
+    CK(cudaSetDevice(e->device));
+    const size_t per = (size_t)e->Qx * e->N;
+    std::vector<float> y(e->L * e->N);
+    using clk = std::chrono::steady_clock;
+    auto next = clk::now();
+    for (size_t b = 0; b < blocks; ++b) {
+      if (pace_us > 0) {
+        while (clk::now() < next) {
+#if defined(__x86_64__)
+          _mm_pause();
+#endif
+        }
+        next += std::chrono::nanoseconds((long long)(pace_us * 1000.0));
+      }
+      const auto t0 = clk::now();
+      auto us = [&](clk::time_point t) { return std::chrono::duration<double, std::micro>(t - t0).count(); };
+      std::memcpy(e->h_in, host_in + (b % n_in_blocks) * per, per * sizeof(float));
+      std::atomic_thread_fence(std::memory_order_release);
+      const auto t1 = clk::now();
+      const uint32_t nblk = device_block_hint(e);
+      CK(cudaGraphLaunch(e->g_block.ex, e->stream));
+      const auto t2 = clk::now();
+      CK(cudaEventRecord(e->ev_back, e->stream));
+      const auto t3 = clk::now();
+      wait_flag(e, nblk + 1, "block output");
+      const auto t4 = clk::now();
+      std::memcpy(y.data(), e->h_out, y.size() * sizeof(float));
+      const auto t5 = clk::now();
+      ++e->blocks;
+      double* o = out + 5 * b;
+      o[0] = us(t1);
+      o[1] = us(t2);
+      o[2] = us(t3);
+      o[3] = us(t4);
+      o[4] = us(t5);
+    }
+    CK(cudaStreamSynchronize(e->stream));
+  });
 }
 
 int aura_b200_profile_phases(aura_b200_engine* e, size_t blocks, float* phase_us,

@@ -135,6 +135,11 @@ struct BlockArgs {
   // memory) once every output is written -- the host polls it instead of an event
   unsigned long long* out_flag;
   unsigned* front_ticket;
+  // graph mode, fused head: k_front also runs the canceller head (and, on P
+  // extra CTAs, the NLMS error spectra) and k_back is its programmatic
+  // dependent; the window history then alternates prev_in / hist1 by block
+  // parity (as in the loop)
+  int front_head;
   unsigned long long* seg_trace;  // diagnostics: [chunks] x {end, cta}, then [ctas] x {start, first data, exit}
   // tables
   const float2* tw;     // N/2, e^{-2 pi i j / N}
@@ -402,22 +407,43 @@ __device__ void error_spectrum(const BlockArgs& a, int p, const float* in, float
 
 __global__ void __launch_bounds__(kFrontThreads) k_front(BlockArgs a) {
   extern __shared__ float4 smem4[];
+  if (a.front_head) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const uint32_t n = a.st->block;
   trace_begin(a, TR_FRONT, n);
+  const int nerr = (a.front_head && a.is_aur && a.nlms) ? a.P : 0;
+  const int nfront = (int)gridDim.x - nerr;
+  float2* work = reinterpret_cast<float2*>(smem4);
+  if ((int)blockIdx.x >= nfront) {  // NLMS error spectrum E_p (fused-head mode)
+    error_spectrum(a, (int)blockIdx.x - nfront, a.in, work, a.tw, a.split, Cta());
+    trace_end(a, TR_FRONT, n);
+    return;
+  }
   const int c0 = blockIdx.x * a.cpb;
   const int c1 = min(c0 + a.cpb, a.L);
-  front_body(a, n, c0, c1, reinterpret_cast<float2*>(smem4), a.in, a.prev_in, a.cur_mt, blockIdx.x == 0,
-             Cta());
-  if (a.out_flag) {  // outputs written: the last CTA tells the host
+  const float* prev = a.prev_in;
+  float* cur = a.cur_mt;
+  if (a.front_head) {
+    prev = (n & 1u) ? a.hist1 : a.prev_in;
+    cur = (n & 1u) ? a.prev_in : a.hist1;
+  }
+  front_body(a, n, c0, c1, work, a.in, prev, cur, blockIdx.x == 0, Cta());
+  if (a.out_flag) {  // outputs written: the last front CTA tells the host
     __syncthreads();  // every thread's output stores precede thread 0's system fence
     if (threadIdx.x == 0) {
       __threadfence_system();
-      if (atomicAdd(a.front_ticket, 1u) == gridDim.x - 1u) {
+      if (atomicAdd(a.front_ticket, 1u) == (unsigned)nfront - 1u) {
         *a.front_ticket = 0u;
         asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(a.out_flag), "l"((unsigned long long)n + 1)
                      : "memory");
       }
     }
+  }
+  if (a.front_head && a.is_aur) {  // canceller stage 1 on the loudspeakers just produced
+    const int N = a.N, Qs = a.mode == 1 ? 1 : a.Q;
+    const float2* tw = a.smem_tables ? work + front_work_f2(N, Qs) : a.tw;
+    const float2* split = a.smem_tables ? tw + N / 2 : a.split;
+    __syncthreads();
+    head_channels(a, n, c0, c1, work, tw, split, Cta());
   }
   trace_end(a, TR_FRONT, n);
 }

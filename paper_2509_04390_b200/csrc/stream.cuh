@@ -176,9 +176,15 @@ __device__ __forceinline__ void copy_ring(float4* dst, const float4* base, int v
 // What the producer must wait for before streaming rows produced by the
 // current block's front half. Graph mode: k_front finished before k_back
 // launched (stream order), and k_back_head is the PDL primary.
+// Fused-head mode (front_head): k_front itself is the PDL primary, so rows
+// it produces (X age 0) wait for it too.
 struct GraphDeps {
+  int front_pdl = 0;
   __device__ __forceinline__ const unsigned* abort() const { return nullptr; }
-  __device__ __forceinline__ bool wait_front(uint32_t) const { return true; }
+  __device__ __forceinline__ bool wait_front(uint32_t) const {
+    if (front_pdl) griddep_wait();
+    return true;
+  }
   __device__ __forceinline__ bool wait_head(uint32_t) const {
     griddep_wait();
     return true;
@@ -520,7 +526,9 @@ __global__ void __launch_bounds__(kBackThreads, 1) k_back(const __grid_constant_
   const uint32_t n = a.st->block;
   if (warp == kConsumers / 32) {
     uint32_t qp = 0;
-    if (lane == 0) back_produce<LT, ELEM, PT>(a, n, full, empty, slots, meta, qp);
+    GraphDeps deps;
+    deps.front_pdl = a.front_head;
+    if (lane == 0) back_produce<LT, ELEM, PT>(a, n, full, empty, slots, meta, qp, deps);
     return;
   }
   if (a.trace && threadIdx.x == 0)
@@ -533,6 +541,8 @@ __global__ void __launch_bounds__(kBackThreads, 1) k_back(const __grid_constant_
   if (ctr && threadIdx.x == 0) ctr[2] = globaltimer();
   if (threadIdx.x == 0) {
     if (a.trace) atomicMax(&a.trace[((n % kTraceBlocks) * kTraceKernels + TR_BACK) * 2 + 1], globaltimer());
+    // k_reduce (our dependent) must also find the front complete
+    if (a.front_head) griddep_wait();
     // the last CTA out resets the work queue: every producer has stopped
     // claiming (its consumers saw the sentinel before getting here)
     unsigned* ex = a.tick + a.tick_queue + 1;
