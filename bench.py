@@ -411,9 +411,13 @@ def run_b200_arm(args, cfg, rank, world, local_rank):
         "value_definition": "p99 device time of ALL of a block's work (front + background "
                             "graphs), back to back, inputs in HBM",
         "latency_to_output_us": {"p50": pct(lat_us, 50), "p99": pct(lat_us, 99),
-                                 "definition": "device time from block start to its output "
-                                               "written (front graph); the rest of the block's "
-                                               "work runs after the output is published"},
+                                 "definition": "CUDA events: graph launch -> end of k_front (which "
+                                               "also runs the canceller head after publishing the "
+                                               "output); the rest of the block's work follows",
+                                 "published_device_us": (float(np.median(trace["output"][:, 0]))
+                                                         if "output" in trace else None),
+                                 "published_definition": "%globaltimer: k_front's first CTA start -> "
+                                                         "the output-ready word published (median)"},
         "e2e": {"value": pct(host_us, 99), "unit": "us", "p50_us": pct(host_us, 50),
                 "h2d_bytes_per_step": 4 * Q * N, "d2h_bytes_per_step": 4 * L * N,
                 "path": "aura_b200_process() C-ABI, pinned mapped host I/O, back-to-back "

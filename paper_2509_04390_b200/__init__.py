@@ -312,7 +312,8 @@ class _Engine:
     def reset(self):
         _check(lib().aura_b200_reset(self._h))
 
-    TRACE_KERNELS = ("k_front", "k_back_head", "k_back", "k_reduce", "afc_done", "k_afc_finish")
+    TRACE_KERNELS = ("k_front", "k_back_head", "k_back", "k_reduce", "afc_done", "k_afc_finish",
+                     "output")
 
     def trace_blocks(self, blocks: int = 32):
         """Per-kernel [start, end] (us from the block's front start) of

@@ -182,7 +182,8 @@ struct aura_b200_engine {
   int loop_stages = 0;
   bool loop_device_io = false;
   std::vector<unsigned long long> loop_last_stamps;  // of the last loop-mode device timing
-  unsigned long long* h_outflag = nullptr;  // mapped: k_front writes block + 1 when the output is out
+  unsigned long long* h_outflag = nullptr;  // mapped: front CTA b writes block + 1 in [b] when its output is out
+  size_t n_outflags = 0;
   bool use_outflag = true;
   uint64_t dev_block_base = 0;  // device block number of host block 0 (measurement calls advance both)
   int loop_hold = 1;
@@ -222,7 +223,7 @@ struct aura_b200_engine {
 
   bool has_syn() const { return K > 1; }
   bool has_back() const { return has_syn() || aur; }
-  bool front_head = false;  // k_front runs the canceller head; k_back is its PDL dependent
+  bool front_head = true;  // k_front runs the canceller head; k_back is its PDL dependent
   bool has_head() const { return !front_head && (aur || mode != AURA_B200_ELEMENTWISE); }
   int front_grid(const BlockArgs& a) const {
     return (int)((L + a.cpb - 1) / a.cpb) + ((front_head && aur && a.nlms) ? (int)P : 0);
@@ -748,6 +749,19 @@ void finish_init(aura_b200_engine* e) {
     a.front_pre = e->smem_front + pre <= 160 * 1024 ? 1 : 0;
     if (a.front_pre) e->smem_front += pre;
   }
+  // one output channel per warp (8 per CTA) where the per-warp areas fit:
+  // small transforms synchronise with __syncwarp instead of CTA barriers
+  a.front_warps = 0;
+  {
+    const char* fw = std::getenv("AURA_B200_FRONT_WARPS");
+    const int W = kFrontThreads / 32;
+    const size_t sw = 8 * front_warps_f2((int)N, (int)Qs, W);
+    if (e->mode != AURA_B200_ELEMENTWISE && sw <= 160 * 1024 && !(fw && std::atoi(fw) == 0)) {
+      a.front_warps = W;
+      a.cpb = W;
+      e->smem_front = std::max(e->smem_front, sw);
+    }
+  }
   if (e->smem_front > 227 * 1024)
     fail(AURA_B200_E_INVALID_ARGUMENT, "block size too large for this many inputs (shared memory)");
   CK(cudaFuncSetAttribute(k_front, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem_front));
@@ -760,9 +774,16 @@ void finish_init(aura_b200_engine* e) {
   plan_loop(e);
   if (const char* fh = std::getenv("AURA_B200_FRONT_HEAD")) e->front_head = std::atoi(fh) != 0;
   a.front_head = e->front_head ? 1 : 0;
+  a.front_hold = 0;  // measured: holding the stream does not speed the front up (profiles/r1s4_front.md)
+  if (const char* fh = std::getenv("AURA_B200_FRONT_HOLD")) a.front_hold = std::atoi(fh);
+  a.front_seq = dalloc<unsigned long long>(2, e->dmem);
+  CK(cudaMemset(a.front_seq, 0, 2 * sizeof(unsigned long long)));
   // output-ready word for process(): mapped host memory, written by k_front
-  CK(cudaHostAlloc(&e->h_outflag, sizeof(unsigned long long), cudaHostAllocMapped | cudaHostAllocPortable));
-  *e->h_outflag = 0;
+  e->n_outflags = (size_t)((e->L + a.cpb - 1) / a.cpb);
+  a.front_ctas = (int)e->n_outflags;
+  CK(cudaHostAlloc(&e->h_outflag, e->n_outflags * sizeof(unsigned long long),
+                   cudaHostAllocMapped | cudaHostAllocPortable));
+  std::memset(e->h_outflag, 0, e->n_outflags * sizeof(unsigned long long));
   CK(cudaHostGetDevicePointer((void**)&a.out_flag, e->h_outflag, 0));
   if (const char* f = std::getenv("AURA_B200_OUTFLAG")) e->use_outflag = std::atoi(f) != 0;
   a.front_ticket = dalloc<unsigned>(1, e->dmem);
@@ -899,6 +920,7 @@ void reset_state(aura_b200_engine* e) {
   CK(cudaMemsetAsync(a.st, 0, sizeof(DevState), s));
   CK(cudaMemsetAsync(a.prev_in, 0, sizeof(float) * e->Qx * N, s));
   if (a.hist1) CK(cudaMemsetAsync(a.hist1, 0, sizeof(float) * e->Qx * N, s));
+  if (a.front_seq) CK(cudaMemsetAsync(a.front_seq, 0, 2 * sizeof(unsigned long long), s));
   CK(cudaMemsetAsync(a.X, 0, sizeof(float4) * (size_t)e->Qx * e->K * NF, s));
   CK(cudaMemsetAsync(a.S, 0, sizeof(float4) * e->L * NF, s));
   if (e->aur) {
@@ -916,7 +938,7 @@ void reset_state(aura_b200_engine* e) {
   CK(cudaStreamSynchronize(s));
   e->blocks = 0;
   e->loop_posted = 0;  // the persistent loop restarts at block 0 too
-  if (e->h_outflag) *reinterpret_cast<volatile unsigned long long*>(e->h_outflag) = 0;
+  for (size_t i = 0; i < e->n_outflags; ++i) reinterpret_cast<volatile unsigned long long*>(e->h_outflag)[i] = 0;
 }
 
 void alloc_synth(aura_b200_engine* e, BlockArgs& a) {
@@ -1149,12 +1171,15 @@ namespace {
 // counts blocks; measurement calls advance host and device together.
 uint32_t device_block_hint(aura_b200_engine* e) { return (uint32_t)(e->blocks + e->dev_block_base); }
 
-// Spin until k_front has published `target` in the mapped output flag.
+// Spin until every k_front CTA has published `target` in its mapped word.
 void wait_flag(aura_b200_engine* e, unsigned long long target, const char* what) {
   volatile unsigned long long* f = e->h_outflag;
   uint64_t spins = 0;
   const auto t0 = std::chrono::steady_clock::now();
-  while (*f < target) {
+  size_t i = 0;
+  for (;;) {
+    while (i < e->n_outflags && f[i] >= target) ++i;
+    if (i == e->n_outflags) break;
 #if defined(__x86_64__)
     _mm_pause();
 #endif
@@ -1776,6 +1801,9 @@ int aura_b200_trace_blocks(aura_b200_engine* e, size_t blocks, double* out) {
     CK(cudaMemcpy(dtr, init.data(), words * sizeof(unsigned long long), cudaMemcpyHostToDevice));
     BlockArgs a = e->dev_args;
     a.trace = dtr;
+    unsigned long long* dflag = nullptr;  // device-side output words, so the front stamps TR_OUTPUT
+    CK(cudaMalloc(&dflag, std::max<size_t>(1, e->n_outflags) * sizeof(unsigned long long)));
+    a.out_flag = dflag;
     auto g = e->capture_block(a, nullptr);
     const uint64_t first = e->blocks;
     for (size_t i = 0; i < blocks; ++i) CK(cudaGraphLaunch(g.ex, e->stream));
@@ -1783,6 +1811,7 @@ int aura_b200_trace_blocks(aura_b200_engine* e, size_t blocks, double* out) {
     std::vector<unsigned long long> tr(words);
     CK(cudaMemcpy(tr.data(), dtr, words * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
     cudaFree(dtr);
+    cudaFree(dflag);
     g.destroy();
     // out[i][k][2]: start/end in microseconds relative to block i's front
     // start; slot kTraceKernels-1 holds {next block's front start, 0}: the
@@ -1877,11 +1906,11 @@ int aura_b200_describe(const aura_b200_engine* e, char* buf, size_t cap) {
     const BlockArgs& a = e->args;
     std::snprintf(buf, cap,
                   "N=%zu Q=%zu L=%zu P=%zu K=%zu KF=%zu mode=%d LT=%d PT=%d | front: grid=%zu cpb=%d "
-                  "smem=%zu | back: ctas=%d x %d thr, CT=%d CTn=%d sp=%d spa=%d stages=%d slot=%d B "
+                  "warps=%d smem=%zu | back: ctas=%d x %d thr, CT=%d CTn=%d sp=%d spa=%d stages=%d slot=%d B "
                   "smem=%zu partials=%zu+%zu items=%d (static %d) | reduce: %d+%d ctas l2keep=%d "
                   "nlms=%d delta=%g",
                   e->N, e->Q, e->L, e->P, e->K, e->KF, e->mode, e->LT, e->PT,
-                  (e->L + a.cpb - 1) / a.cpb, a.cpb, e->smem_front, e->back_ctas, kBackThreads, a.CT,
+                  (e->L + a.cpb - 1) / a.cpb, a.cpb, a.front_warps, e->smem_front, e->back_ctas, kBackThreads, a.CT,
                   a.CTn, a.sp, a.spa, a.stages, a.slot_f4 * 16, e->smem_back, e->n_syn_segs,
                   e->n_afc_segs, a.n_chunks, a.n_static, a.red_syn_ctas, a.red_afc_ctas, a.h_in_l2, a.nlms,
                   (double)a.delta);

@@ -29,6 +29,12 @@ struct Cta {
   __device__ __forceinline__ int size() const { return blockDim.x; }
   __device__ __forceinline__ void sync() const { __syncthreads(); }
 };
+// One warp (independent of the rest of its CTA): __syncwarp between stages.
+struct Warp {
+  __device__ __forceinline__ int tid() const { return threadIdx.x & 31; }
+  __device__ __forceinline__ int size() const { return 32; }
+  __device__ __forceinline__ void sync() const { __syncwarp(); }
+};
 template <int NT>
 struct Consumers {
   __device__ __forceinline__ int tid() const { return threadIdx.x; }

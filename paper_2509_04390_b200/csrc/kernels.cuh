@@ -56,7 +56,7 @@ struct DevState {
 // kernel, the earliest CTA start and the latest CTA end.
 constexpr int kTraceBlocks = 64;
 constexpr int kTraceKernels = 8;
-enum TraceId { TR_FRONT = 0, TR_BACK_HEAD, TR_BACK, TR_REDUCE, TR_AFC_DONE, TR_AFC_FINISH };
+enum TraceId { TR_FRONT = 0, TR_BACK_HEAD, TR_BACK, TR_REDUCE, TR_AFC_DONE, TR_AFC_FINISH, TR_OUTPUT };
 
 // Loudspeaker-channel sharding: at most kMaxShards engines
 // (one per GPU, or virtual shards on one GPU) exchange their canceller
@@ -131,15 +131,20 @@ struct BlockArgs {
   unsigned long long* loop_stamps;  // per block {released, output written, done} (%globaltimer)
   unsigned long long loop_idle_ns;  // park (exit) after this long without a doorbell
   int loop_hold;                    // producers start after the fronts' input spectra are pushed
-  // graph mode: the last k_front CTA publishes (block + 1) here (mapped host
-  // memory) once every output is written -- the host polls it instead of an event
+  // graph mode: front CTA b publishes (block + 1) in out_flag[b] (mapped host
+  // memory) once its outputs are written -- the host polls these words
+  // instead of an event; one system-scope release store per CTA, no ticket
   unsigned long long* out_flag;
-  unsigned* front_ticket;
+  unsigned* front_ticket;  // (unused)
   // graph mode, fused head: k_front also runs the canceller head (and, on P
   // extra CTAs, the NLMS error spectra) and k_back is its programmatic
   // dependent; the window history then alternates prev_in / hist1 by block
   // parity (as in the loop)
   int front_head;
+  unsigned long long* front_seq;  // fused head: [block & 1] front CTAs done (k_reduce clears the slot)
+  int front_hold;                 // ... and k_back's producers wait for all of them before streaming
+  int front_ctas;                 // k_front CTAs that write outputs
+  int front_warps;                // > 0: k_front runs one output channel per warp (front_warps_body)
   unsigned long long* seg_trace;  // diagnostics: [chunks] x {end, cta}, then [ctas] x {start, first data, exit}
   // tables
   const float2* tw;     // N/2, e^{-2 pi i j / N}
@@ -405,6 +410,86 @@ __device__ void error_spectrum(const BlockArgs& a, int p, const float* in, float
   rfft_packed(wa, z, reinterpret_cast<float2*>(a.E + (size_t)p * a.NF), N, a.logN, tw, split, tm);
 }
 
+// Shared-memory float2 count of front_warps_body for Qs shared inputs and
+// W warps: input spectra + window/scratch + tables, then per warp the
+// channel's S and H0 (1 + Qs) N, its accumulator and c2r scratch 2N.
+__host__ __device__ inline size_t front_warps_f2(int N, int Qs, int W) {
+  return (size_t)N * (Qs + 2) + table_f2(N) + (size_t)W * N * (3 + Qs);
+}
+
+// The front with one output channel per warp (channels c0 + w, c0 + w + W,
+// ... for warp w): the shared input stage runs on the whole CTA, then each
+// warp does its channels' MAC and c2r with __syncwarp only -- a 64-point
+// transform has too little work for 256 threads and a CTA barrier per stage.
+// Same floating-point operations as front_body (bit-identical). Tables are
+// always staged. After every warp's outputs: publish (as k_front), then the
+// fused canceller head per channel on the same warps.
+template <typename OnX = NoHook>
+__device__ void front_warps_body(const BlockArgs& a, uint32_t n, int c0, int c1, float2* sm,
+                                 const float* in, const float* prev_in, float* cur_out, bool leader,
+                                 OnX on_x = OnX()) {
+  const int N = a.N, NF = a.NF;
+  const int Qs = a.mode == 1 ? 1 : a.Q;
+  const int Qh = a.mode == 2 ? a.Q : 1;
+  const int W = a.front_warps, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const Cta cta;
+  const Warp wt;
+  float2* Xs = sm;                                     // Qs x N
+  float2* z = Xs + (size_t)Qs * N;                     // N
+  float* wa = reinterpret_cast<float*>(z + N);         // 2N
+  float2* tw = reinterpret_cast<float2*>(wa + 2 * N);  // tables
+  float2* split = tw + N / 2;
+  float2* mine = tw + table_f2(N) + (size_t)w * N * (3 + Qs);  // this warp's area
+  float2* pS = mine;                                   // S_l, then H0_l,q (first channel)
+  float2* acc = mine + (size_t)N * (1 + Qs);           // N
+  float2* wz = acc + N;                                // N
+  stage_tables(tw, split, a.tw, a.split, N, cta);
+  const int l0 = c0 + w;
+  if (w < W && l0 < c1) {  // this warp's first channel: S and H0 in one round of loads
+    const float2* Sl = reinterpret_cast<const float2*>(a.S + (size_t)l0 * NF);
+    const float2* H0 = reinterpret_cast<const float2*>(a.H0 + (size_t)l0 * Qh * NF);
+    for (int j = lane; j < N; j += 32) pS[j] = Sl[j];
+    for (int j = lane; j < Qs * N; j += 32) pS[N + j] = H0[j];
+  }
+  // ---- stage 1 for the shared inputs (broadcast / mimo), whole CTA
+  for (int q = 0; q < Qs; ++q) {
+    const float* inq = in + (size_t)q * N;
+    const float* prev = prev_in + (size_t)q * N;
+    for (int i = threadIdx.x; i < N; i += blockDim.x) {
+      float v = inq[i];
+      if (a.is_aur) v = __fsub_rn(__fmul_rn(a.gain, v), a.fhat[(size_t)q * N + i]);
+      if (leader) cur_out[(size_t)q * N + i] = v;
+      wa[i] = prev[i];
+      wa[N + i] = v;
+    }
+    __syncthreads();
+    rfft_packed(wa, z, Xs + (size_t)q * N, N, a.logN, tw, split, cta);
+    if (leader) push_tiled(a, a.X, q, a.K, (int)(n % (uint32_t)a.K), Xs + (size_t)q * N, cta);
+  }
+  on_x();
+  // ---- per output channel (one warp each): Y = S + sum_q X_q H_q[0], c2r
+  if (w < W) {
+    for (int l = l0; l < c1; l += W) {
+      const bool staged = l == l0;
+      const float2* Sl = staged ? pS : reinterpret_cast<const float2*>(a.S + (size_t)l * NF);
+      const float2* H0 = staged ? pS + N : reinterpret_cast<const float2*>(a.H0 + (size_t)l * Qh * NF);
+      for (int j = lane; j < N; j += 32) {
+        float2 y = Sl[j];
+        for (int q = 0; q < Qs; ++q) y = cmac2(y, Xs[(size_t)q * N + j], H0[(size_t)q * N + j], j == 0);
+        acc[j] = y;
+      }
+      __syncwarp();
+      float* out = a.out + (size_t)l * N;
+      float* sp = a.spk + (size_t)l * N;
+      const bool keep = a.is_aur;
+      irfft_packed_tail(acc, wz, N, a.logN, tw, split, [&](int i, float v) {
+        out[i] = v;
+        if (keep) sp[i] = v;
+      }, wt);
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kFrontThreads) k_front(BlockArgs a) {
   extern __shared__ float4 smem4[];
   if (a.front_head) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -426,24 +511,43 @@ __global__ void __launch_bounds__(kFrontThreads) k_front(BlockArgs a) {
     prev = (n & 1u) ? a.hist1 : a.prev_in;
     cur = (n & 1u) ? a.prev_in : a.hist1;
   }
-  front_body(a, n, c0, c1, work, a.in, prev, cur, blockIdx.x == 0, Cta());
-  if (a.out_flag) {  // outputs written: the last front CTA tells the host
-    __syncthreads();  // every thread's output stores precede thread 0's system fence
+  if (a.front_warps)
+    front_warps_body(a, n, c0, c1, work, a.in, prev, cur, blockIdx.x == 0);
+  else
+    front_body(a, n, c0, c1, work, a.in, prev, cur, blockIdx.x == 0, Cta());
+  if (a.out_flag || a.front_head) {  // outputs written: tell the host (and k_back)
+    __syncthreads();  // every thread's output stores precede thread 0's release
     if (threadIdx.x == 0) {
-      __threadfence_system();
-      if (atomicAdd(a.front_ticket, 1u) == (unsigned)nfront - 1u) {
-        *a.front_ticket = 0u;
-        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(a.out_flag), "l"((unsigned long long)n + 1)
+      if (a.out_flag)
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(a.out_flag + blockIdx.x),
+                     "l"((unsigned long long)n + 1)
                      : "memory");
+      if (a.front_head) {
+        __threadfence();
+        atomicAdd(a.front_seq + (n & 1u), 1ull);
+      }
+      if (a.trace) {  // the moment this CTA's outputs are published (max over CTAs)
+        const unsigned long long now = globaltimer();
+        atomicMin(&a.trace[((n % kTraceBlocks) * kTraceKernels + TR_OUTPUT) * 2], now);
+        atomicMax(&a.trace[((n % kTraceBlocks) * kTraceKernels + TR_OUTPUT) * 2 + 1], now);
       }
     }
   }
   if (a.front_head && a.is_aur) {  // canceller stage 1 on the loudspeakers just produced
     const int N = a.N, Qs = a.mode == 1 ? 1 : a.Q;
-    const float2* tw = a.smem_tables ? work + front_work_f2(N, Qs) : a.tw;
-    const float2* split = a.smem_tables ? tw + N / 2 : a.split;
     __syncthreads();
-    head_channels(a, n, c0, c1, work, tw, split, Cta());
+    if (a.front_warps) {  // per warp, in the warp's own area (3N float2 from its S/H0 slot)
+      const int W = a.front_warps, w = threadIdx.x >> 5;
+      const float2* tw = work + (size_t)N * (Qs + 2);
+      if (w < W) {
+        float2* mine = const_cast<float2*>(tw) + table_f2(N) + (size_t)w * N * (3 + Qs);
+        for (int l = c0 + w; l < c1; l += W) head_channels(a, n, l, l + 1, mine, tw, tw + N / 2, Warp());
+      }
+    } else {
+      const float2* tw = a.smem_tables ? work + front_work_f2(N, Qs) : a.tw;
+      const float2* split = a.smem_tables ? tw + N / 2 : a.split;
+      head_channels(a, n, c0, c1, work, tw, split, Cta());
+    }
   }
   trace_end(a, TR_FRONT, n);
 }

@@ -528,7 +528,20 @@ __global__ void __launch_bounds__(kBackThreads, 1) k_back(const __grid_constant_
     uint32_t qp = 0;
     GraphDeps deps;
     deps.front_pdl = a.front_head;
-    if (lane == 0) back_produce<LT, ELEM, PT>(a, n, full, empty, slots, meta, qp, deps);
+    if (lane == 0) {
+      if (a.front_head && a.front_hold) {
+        // launched early (PDL) so this CTA is resident; hold the stream until
+        // the front's outputs are out -- its loads are the latency path and
+        // slow down badly under a saturated memory system (bounded: 2 s)
+        const unsigned long long t0 = globaltimer();
+        while (*reinterpret_cast<volatile unsigned long long*>(a.front_seq + (n & 1u)) <
+                   (unsigned long long)a.front_ctas &&
+               globaltimer() - t0 < 2000000000ull) {
+          __nanosleep(100);
+        }
+      }
+      back_produce<LT, ELEM, PT>(a, n, full, empty, slots, meta, qp, deps);
+    }
     return;
   }
   if (a.trace && threadIdx.x == 0)
@@ -719,6 +732,7 @@ __global__ void __launch_bounds__(kReduceThreads) k_reduce(const __grid_constant
     unsigned* t = a.tick + 1;
     if (atomicAdd(t, 1u) == gridDim.x - 1u) {
       *t = 0u;
+      if (a.front_seq) a.front_seq[n & 1u] = 0ull;  // every producer of block n is past its hold
       if (a.G <= 1) a.st->block = n + 1;
     }
   }
