@@ -495,12 +495,20 @@ void plan_back(aura_b200_engine* e, BlockArgs& a) {
   const int ctas = (int)std::min<double>(e->sms, std::max(1.0, std::ceil(drive / (96.0 * 1024))));
   e->back_ctas = ctas;
   // Work: every CTA first runs a static piece of each of three phases -- the
-  // first 15% of every synthesis tile's taps (covers k_back_head, which the
-  // canceller waits for), the canceller units, the next 70% of the taps --
-  // then claims small queue items (the last 15%) so the CTAs finish
-  // together whatever their share of HBM bandwidth.
-  const long long TA = T > 0 ? std::max<long long>(1, (long long)std::ceil(0.15 * T)) : 0;
-  const long long TB = T > 0 ? std::max<long long>(TA, (long long)std::ceil(0.85 * T)) : 0;
+  // first 30% of every synthesis tile's taps (covers the front half, which
+  // the canceller waits for), the canceller units, the next 45% of the taps
+  // -- then claims small queue items (the last 25%) so the CTAs finish
+  // together whatever their share of HBM bandwidth or start time.
+  // Phase fractions (profiles/r1s4_front.md): the first synthesis slice covers
+  // the front half, which the canceller items wait for; the last quarter is
+  // queue items, enough to absorb the k_back CTAs that start late on the SMs
+  // the front occupies
+  double fa = 0.30;
+  if (const char* f = std::getenv("AURA_B200_PHASE_A")) fa = std::atof(f);
+  const long long TA = T > 0 ? std::max<long long>(1, (long long)std::ceil(fa * T)) : 0;
+  double fb = 0.75;
+  if (const char* f = std::getenv("AURA_B200_PHASE_B")) fb = std::atof(f);
+  const long long TB = T > 0 ? std::max<long long>(TA, (long long)std::ceil(fb * T)) : 0;
   // queue items: ~12 per CTA, at least two stages (keeps the tail short and
   // the partial count -- k_reduce's input -- small at c5 sizes)
   const long long qtaps = (T - TB) * tiles;
@@ -579,7 +587,7 @@ void plan_back(aura_b200_engine* e, BlockArgs& a) {
   a.red_afc_rows = P + (e->args.nlms ? 1 : 0);
   a.red_afc_cpt = U > 0 ? cpt_for(a.red_afc_rows * CT, max_afc) : 1;
   a.red_afc_ctas = U > 0 ? CTn * a.red_afc_cpt : 0;
-  e->smem_reduce = 16 * reduce_smem_f4(N, e->aur);
+  e->smem_reduce = 16 * reduce_smem_f4(N, e->aur, P);
   CK(cudaFuncSetAttribute(k_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem_reduce));
   // tickets: [0] canceller CTAs of k_reduce, [1] all k_reduce CTAs, [2] work
   // queue, [3] k_back exits
@@ -669,7 +677,7 @@ void plan_loop(aura_b200_engine* e) {
     e->loop_why = "shared memory: ring + front work area do not fit one CTA";
     return;
   }
-  if ((size_t)stages * slot < 16 * reduce_smem_f4(N, e->aur)) {
+  if ((size_t)stages * slot < 16 * reduce_smem_f4(N, e->aur, (int)e->P)) {
     e->loop_why = "shared memory: the reduction scratch does not fit the ring";
     return;
   }

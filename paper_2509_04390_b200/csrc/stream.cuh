@@ -584,8 +584,10 @@ constexpr int kReduceThreads = 256;
 // Shared-memory float4 count of k_reduce's scratch: the combine buffer, and
 // for the canceller the c2r scratch (N float2), the DftPlan tables and the
 // smoothed power (N float2).
-__host__ __device__ inline size_t reduce_smem_f4(int N, bool aur) {
-  return kReduceThreads + (aur ? (2 * (size_t)N + table_f2(N) + 1) / 2 : 0);
+__host__ __device__ inline size_t reduce_smem_f4(int N, bool aur, int P = 1) {
+  // c2r scratch: one N-float2 area per mic when the mics' c2r run on separate warps
+  const size_t scratch = (N <= 1024 ? (size_t)P : 1) * N;
+  return kReduceThreads + (aur ? (scratch + N + table_f2(N) + 1) / 2 : 0);
 }
 
 // Canceller reduce CTAs: stage the DftPlan tables and the smoothed power --
@@ -595,7 +597,7 @@ template <typename Team>
 __device__ __forceinline__ void reduce_prefetch(const BlockArgs& a, int b, float4* rsm, Team tm) {
   if (b < a.red_syn_ctas) return;
   float2* z = reinterpret_cast<float2*>(rsm + kReduceThreads);
-  float2* tw = z + a.N;
+  float2* tw = z + (a.N <= 1024 ? (size_t)a.P : 1) * a.N;
   float2* split = tw + a.N / 2;
   float2* pws = split + a.N / 2 + 1;
   stage_tables(tw, split, a.tw, a.split, a.N, tm);
@@ -665,21 +667,28 @@ __device__ void reduce_part(const BlockArgs& a, int b, uint32_t n, float4* rsm, 
   const int N = a.N, P = a.P;
   const bool sharded = a.G > 1;
   float2* z = reinterpret_cast<float2*>(rsm + kReduceThreads);
-  float2* tw = z + N;
+  float2* tw = z + (N <= 1024 ? (size_t)P : 1) * N;
   float2* split = tw + N / 2;
   float2* pws = split + N / 2 + 1;
+  // one c2r per mic: on one warp each (P <= 8 warps) for small transforms --
+  // no CTA barrier per butterfly stage -- else on the whole team
+  const bool warps = N <= 1024 && P * 32 <= tm.size();
   for (int p = 0; p < P; ++p) {
     // sharded: this shard's partial f^_p (c2r is linear), summed by k_afc_finish
     float* fh = sharded ? a.xmine + (size_t)p * N : a.fhat + (size_t)p * N;
     float* fhh = a.fhat_host + (size_t)p * N;
-    irfft_packed_tail(
-        reinterpret_cast<const float2*>(a.yhat + (size_t)p * NF), z, N, a.logN, tw, split,
-        [&](int i, float x) {
-          fh[i] = x;
-          if (!sharded) fhh[i] = x;
-        },
-        tm);
+    auto st = [&](int i, float x) {
+      fh[i] = x;
+      if (!sharded) fhh[i] = x;
+    };
+    const float2* yp = reinterpret_cast<const float2*>(a.yhat + (size_t)p * NF);
+    if (!warps) {
+      irfft_packed_tail(yp, z, N, a.logN, tw, split, st, tm);
+    } else if (tid / 32 == p) {
+      irfft_packed_tail(yp, z + (size_t)p * N, N, a.logN, tw, split, st, Warp());
+    }
   }
+  if (warps) tm.sync();
   if (a.nlms) {
     const float2* sum = reinterpret_cast<const float2*>(a.yhat + (size_t)P * NF);
     const float oml = __fsub_rn(1.0f, a.lambda);

@@ -101,11 +101,16 @@ def test_one_block_causality():
 
 
 def test_fused_equals_manual_composition():
-    # test_auralizer.cpp:127-159, composed from the GPU Convolver
+    # test_auralizer.cpp:127-159, composed from the GPU Convolver, with a
+    # STABLE loop: the reference uses three unit-energy canceller filters
+    # (loop gain ~ sqrt(3) > 1), which grows the signal ~10x over 12 blocks
+    # and amplifies any fp32 summation-order difference past its 1e-5
+    # absolute bar (see EXCLUDED in test_gpu_dropin_cpp.py); scaled by 0.3
+    # the property -- fused path == explicit composition -- is tested as is.
     N, L, blocks = 64, 3, 12
     rng = np.random.default_rng(13)
     synth = scaled_filters(rng, L, 5 * N + 3)
-    fc = scaled_filters(rng, L, 2 * N + 1)
+    fc = scaled_filters(rng, L, 2 * N + 1, 0.3)
     aur = gpu_aur(synth, fc, N, 1, L)
     sref = A.Convolver(list(synth), A.make_config(48000, N, 1, L))
     fref = A.Convolver(list(fc), A.make_config(48000, N, L, L), A.ChannelMode.elementwise)
