@@ -34,6 +34,7 @@
 #include "stream.cuh"
 #include "loop.cuh"
 #include <algorithm>
+#include <tuple>
 
 using namespace aura_b200;
 
@@ -520,31 +521,74 @@ void plan_back(aura_b200_engine* e, BlockArgs& a) {
     at[kind ? tiles + tile : tile].push_back({(int)b, (int)chunks.size()});
     chunks.push_back(make_int4(kind | (tile << 1), (int)b, (int)e_, 0));
   };
+  // The first stage of every input (taps [q (K-1), q (K-1) + sp)) reads
+  // the input spectrum the front pushes this block; those stages are left out
+  // of the static pieces and claimed last from the queue, so no CTA's static
+  // work waits for the front half.
+  const long long late = std::min<long long>(a.sp, Kt);
+  auto lateset = [&](long long t) { return Kt > 0 && (t % Kt) < late; };
+  // intervals of [lo, hi) without the late taps
+  auto pieces = [&](long long lo, long long hi, std::vector<std::pair<long long, long long>>& out) {
+    out.clear();
+    long long t = lo;
+    while (t < hi) {
+      if (lateset(t)) {
+        t = std::min<long long>(hi, (t / Kt) * Kt + late);
+        continue;
+      }
+      const long long next_q = Kt > 0 ? (t / Kt + 1) * Kt : hi;
+      const long long e_ = std::min<long long>(hi, next_q);
+      out.push_back({t, e_});
+      t = e_;
+    }
+  };
   struct Ph { int kind; long long lo, hi; int ntile; };  // items [lo, hi) of every tile
   const Ph phases[3] = {{0, 0, TA, tiles}, {1, 0, U, CTn}, {0, TA, TB, tiles}};
+  std::vector<std::pair<long long, long long>> tmp;
   for (int c = 0; c < ctas; ++c) {
     item_off[c] = (int)chunks.size();
     for (const Ph& ph : phases) {
-      const long long span = ph.hi - ph.lo;
-      if (span <= 0) continue;
-      const long long n_items = span * ph.ntile;
+      // the phase's intervals, tile-major, as one linear item space
+      std::vector<std::tuple<int, long long, long long>> iv;
+      for (int tile = 0; tile < ph.ntile; ++tile) {
+        if (ph.kind == 1) {
+          if (ph.hi > ph.lo) iv.emplace_back(tile, ph.lo, ph.hi);
+          continue;
+        }
+        pieces(ph.lo, ph.hi, tmp);
+        for (auto& pr : tmp) iv.emplace_back(tile, pr.first, pr.second);
+      }
+      long long n_items = 0;
+      for (auto& x : iv) n_items += std::get<2>(x) - std::get<1>(x);
+      if (n_items <= 0) continue;
       long long i0 = n_items * c / ctas, i1 = n_items * (c + 1) / ctas;
-      while (i0 < i1) {
-        const int tile = (int)(i0 / span);
-        const long long b = ph.lo + (i0 - (long long)tile * span);
-        const long long e_ = std::min<long long>(ph.hi, b + (i1 - i0));
-        push(ph.kind, tile, b, e_);
-        i0 += e_ - b;
+      long long base = 0;
+      for (auto& x : iv) {
+        const long long len = std::get<2>(x) - std::get<1>(x);
+        const long long s0 = std::max(i0, base), s1 = std::min(i1, base + len);
+        if (s0 < s1) push(ph.kind, std::get<0>(x), std::get<1>(x) + (s0 - base), std::get<1>(x) + (s1 - base));
+        base += len;
       }
     }
   }
   item_off[ctas] = (int)chunks.size();
   a.n_static = (int)chunks.size();
-  {  // queue: tile-interleaved, so every tile's last partial lands near the end
-
-    long long nq = T > TB ? (T - TB + CQ - 1) / CQ : 0;
-    for (long long j = 0; j < nq; ++j)
-      for (int t = 0; t < tiles; ++t) push(0, t, TB + j * CQ, std::min<long long>(T, TB + (j + 1) * CQ));
+  {  // queue: tile-interleaved, so every tile's last partial lands near the end;
+     // the late (age-0) stages last of all
+    std::vector<std::vector<std::pair<long long, long long>>> qv(tiles);
+    size_t nq = 0;
+    for (int t = 0; t < tiles; ++t) {
+      pieces(TB, T, tmp);
+      for (auto& pr : tmp)
+        for (long long b = pr.first; b < pr.second; b += CQ)
+          qv[t].push_back({b, std::min<long long>(pr.second, b + CQ)});
+      nq = std::max(nq, qv[t].size());
+    }
+    for (size_t j = 0; j < nq; ++j)
+      for (int t = 0; t < tiles; ++t)
+        if (j < qv[t].size()) push(0, t, qv[t][j].first, qv[t][j].second);
+    for (long long q = 0; Kt > 0 && q < Qh; ++q)
+      for (int t = 0; t < tiles; ++t) push(0, t, q * Kt, q * Kt + late);
   }
   std::vector<int> cnt(tiles + CTn);
   for (int t = 0; t < tiles + CTn; ++t) {
@@ -764,7 +808,10 @@ void finish_init(aura_b200_engine* e) {
     const char* fw = std::getenv("AURA_B200_FRONT_WARPS");
     const int W = kFrontThreads / 32;
     const size_t sw = 8 * front_warps_f2((int)N, (int)Qs, W);
-    if (e->mode != AURA_B200_ELEMENTWISE && sw <= 160 * 1024 && !(fw && std::atoi(fw) == 0)) {
+    // measured (profiles/r1s4_front.md): a clear win at N <= 64; at N = 128 a
+    // 64-butterfly stage per warp is already slower than the CTA version
+    const bool want = fw ? std::atoi(fw) != 0 : N <= 64;
+    if (e->mode != AURA_B200_ELEMENTWISE && sw <= 160 * 1024 && want) {
       a.front_warps = W;
       a.cpb = W;
       e->smem_front = std::max(e->smem_front, sw);
@@ -780,6 +827,10 @@ void finish_init(aura_b200_engine* e) {
   CK(cudaMemset(e->d_in_pool, 0, e->pool_blocks * in_ch * N * sizeof(float)));
   e->d_out = dalloc<float>(e->L * N, e->dmem);
   plan_loop(e);
+  // fused head (profiles/r1s4_front.md): k_back launches as k_front's
+  // programmatic dependent -- measured better for the auralizer (no separate
+  // canceller head kernel) and for convolvers (the stream starts early)
+  e->front_head = true;
   if (const char* fh = std::getenv("AURA_B200_FRONT_HEAD")) e->front_head = std::atoi(fh) != 0;
   a.front_head = e->front_head ? 1 : 0;
   a.front_hold = 0;  // measured: holding the stream does not speed the front up (profiles/r1s4_front.md)

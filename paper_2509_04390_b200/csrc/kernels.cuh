@@ -511,10 +511,21 @@ __global__ void __launch_bounds__(kFrontThreads) k_front(BlockArgs a) {
     prev = (n & 1u) ? a.hist1 : a.prev_in;
     cur = (n & 1u) ? a.prev_in : a.hist1;
   }
+  // front_hold 2: k_back's producers wait until every front CTA has its
+  // inputs in (its loads are the part a saturated memory system slows down)
+  auto inputs_in = [&] {
+    if (a.front_head && a.front_hold == 2) {
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(a.front_seq + (n & 1u), 1ull);
+      }
+    }
+  };
   if (a.front_warps)
-    front_warps_body(a, n, c0, c1, work, a.in, prev, cur, blockIdx.x == 0);
+    front_warps_body(a, n, c0, c1, work, a.in, prev, cur, blockIdx.x == 0, inputs_in);
   else
-    front_body(a, n, c0, c1, work, a.in, prev, cur, blockIdx.x == 0, Cta());
+    front_body(a, n, c0, c1, work, a.in, prev, cur, blockIdx.x == 0, Cta(), inputs_in);
   if (a.out_flag || a.front_head) {  // outputs written: tell the host (and k_back)
     __syncthreads();  // every thread's output stores precede thread 0's release
     if (threadIdx.x == 0) {
@@ -522,7 +533,7 @@ __global__ void __launch_bounds__(kFrontThreads) k_front(BlockArgs a) {
         asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(a.out_flag + blockIdx.x),
                      "l"((unsigned long long)n + 1)
                      : "memory");
-      if (a.front_head) {
+      if (a.front_head && a.front_hold != 2) {
         __threadfence();
         atomicAdd(a.front_seq + (n & 1u), 1ull);
       }
