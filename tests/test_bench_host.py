@@ -41,3 +41,22 @@ def test_cpu_sample_channels_bounds_the_reference_setup():
     assert bench.cpu_sample_channels(bench.CONFIGS["c3"]) == (None, 1.0)
     L_sub, scale = bench.cpu_sample_channels(bench.CONFIGS["c5"])
     assert 1 <= L_sub < 512 and abs(scale - 512 / L_sub) < 1e-12
+
+
+def test_sweep_csv_keeps_the_reference_header_and_number_format():
+    """tools/sweep_csv.py extends the reference's CSV (bench.hpp:296-316);
+    its first ten columns are the header test_bench.cpp:148-151 pins."""
+    import importlib.util
+    import os
+    spec = importlib.util.spec_from_file_location(
+        "sweep_csv", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                  "tools", "sweep_csv.py"))
+    m = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(m)
+    assert m.HEADER == "subject,backend,parameter,value,mean_s,min_s,max_s,trials,budget_s,realtime"
+    assert m.fmt(32) == "32" and m.fmt(0.25) == "0.25" and m.fmt(0.001) == "0.001"
+    assert float(m.fmt(1 / 3)) == 1 / 3  # shortest round-trippable
+    # filter_length_s overrides the synthesis length (bench.hpp detail::resolve)
+    N, C, n_h, n_hf, fs = m.resolve("filter_length_s", 2.0)
+    assert (N, C, n_h, n_hf, fs) == (128, 32, 96000, 48000, 48000)
+    assert m.resolve("block_size", 64)[0] == 64 and m.resolve("channels", 8)[1] == 8
