@@ -124,6 +124,12 @@ __device__ __forceinline__ uint64_t policy_evict_normal() {
   asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+// 128-bit store with an L2 eviction-priority hint (the canceller's W; never
+// read back by this kernel, so no compiler memory barrier)
+__device__ __forceinline__ void st_hint(float4* p, float4 v, uint64_t policy) {
+  asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "f"(v.x),
+               "f"(v.y), "f"(v.z), "f"(v.w), "l"(policy));
+}
 // programmatic dependent launch: wait for the preceding kernel (k_back_head)
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void griddep_launch() {
@@ -266,7 +272,7 @@ __device__ __forceinline__ void back_produce(const BlockArgs& a, uint32_t n, uin
         const uint32_t cb = (uint32_t)CT * 16u;
         mbar_expect_tx(full + s, (uint32_t)(nt * P * CT + rows * CT) * 16u + (a.nlms ? (P + 1) * cb : 0u));
         bulk_g2s(dst, a.W + ((size_t)c * U + t) * P * CT, (uint32_t)(nt * P * CT) * 16u, full + s,
-                 pol_stream);
+                 a.w_in_l2 ? pol_keep : pol_stream);
         float4* xd = dst + (size_t)a.spa * P * CT;
         copy_ring(xd, a.XA + (size_t)(l * CTn + c) * cap * CT, nka - amax, nka - k0, cap, CT, full + s,
                   pol_keep);
@@ -346,6 +352,8 @@ __device__ __forceinline__ void back_consume(const BlockArgs& a, uint32_t n, uin
   const int P = PT > 0 ? a.P : 0;
   const int nl = PT > 0 ? a.nlms : 0;
   const int R = P + nl;  // canceller partial rows; row P: loudspeaker power
+  // the canceller's W store: kept in L2 when it fits, else streamed out
+  const uint64_t wpol = a.w_in_l2 ? policy_evict_last() : policy_evict_first();
   constexpr int PA = PT > 0 ? PT : 1;
 
   for (;;) {
@@ -410,71 +418,90 @@ __device__ __forceinline__ void back_consume(const BlockArgs& a, uint32_t n, uin
       float4 aac[PA + 1];  // P mics + the loudspeaker power
 #pragma unroll
       for (int p = 0; p < PA + 1; ++p) aac[p] = make_float4(0.f, 0.f, 0.f, 0.f);
+      // Each tap phase owns G consecutive units of a stage, so the row of age
+      // k + 1 it needs for unit k's update is the age row of unit k + 1:
+      // G + 1 delay-line rows per G units, all loads independent of the math.
+      const int G = a.spa / PH;
+      // NLMS error spectra and step mu / (power + delta) of this column: the
+      // same for every stage of the item (staged in each; read from the first)
+      float4 e4[PA];
+      float4 st = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (nl) {
+        const float4* es = slots + (size_t)sl * a.slot_f4 + (size_t)a.spa * P * CT + (size_t)(a.spa + 1) * CT;
+#pragma unroll
+        for (int p = 0; p < PA; ++p) e4[p] = p < P ? es[(size_t)p * CT + f] : st;
+        const float4 pw = es[(size_t)P * CT + f];  // packed power of bins 2fg, 2fg+1
+        st = make_float4(__fdiv_rn(a.mu, __fadd_rn(pw.x, a.delta)), __fdiv_rn(a.mu, __fadd_rn(pw.y, a.delta)),
+                         __fdiv_rn(a.mu, __fadd_rn(pw.z, a.delta)), __fdiv_rn(a.mu, __fadd_rn(pw.w, a.delta)));
+      }
       for (;;) {
         const int nt = m.t1 - m.t;
         const int l = m.t / KF, k0 = m.t - l * KF;
         const int amax = k0 + nt - 1 + nl;
         const float4* ws = slots + (size_t)sl * a.slot_f4;
         const float4* xs = ws + (size_t)a.spa * P * CT;
-        // NLMS error spectra and step mu / (power + delta) of this column (staged)
-        float4 e4[PA];
-        float4 st = make_float4(0.f, 0.f, 0.f, 0.f);
+        const int i0 = ph * G, i1 = min(i0 + G, nt);
+        // rows are oldest-first: unit i (age k0 + i) reads row amax - k0 - i
+        const float4* xr = xs + (size_t)(amax - k0 - i0) * CT + f;
+        const float4* wr = ws + (size_t)i0 * P * CT + f;
         if (nl) {
-          const float4* es = xs + (size_t)(a.spa + 1) * CT;
-#pragma unroll
-          for (int p = 0; p < PA; ++p) e4[p] = p < P ? es[(size_t)p * CT + f] : st;
-          const float4 pw = es[(size_t)P * CT + f];  // packed power of bins 2fg, 2fg+1
-          st = make_float4(__fdiv_rn(a.mu, __fadd_rn(pw.x, a.delta)), __fdiv_rn(a.mu, __fadd_rn(pw.y, a.delta)),
-                           __fdiv_rn(a.mu, __fadd_rn(pw.z, a.delta)), __fdiv_rn(a.mu, __fadd_rn(pw.w, a.delta)));
-        }
-        for (int i = ph; i < nt; i += PH) {
-          const int k = k0 + i;
-          const int r0 = amax - k;  // row of age k (rows are oldest-first)
-          const float4 xv = xs[(size_t)r0 * CT + f];
-          const XPack x0 = xpack(xv, dc);
-          float4 x1 = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (nl) {
-            x1 = xs[(size_t)(r0 - 1) * CT + f];  // pre-push age k = post-push age k + 1
-            if (k == 0) {  // packed |X_l(age 0)|^2, rounded as the oracle
-              float4& pa = aac[PA];
-              if (dc) {
-                pa.x = __fadd_rn(pa.x, __fmul_rn(xv.x, xv.x));
-                pa.y = __fadd_rn(pa.y, __fmul_rn(xv.y, xv.y));
-              } else {
-                const float mm = __fadd_rn(__fmul_rn(xv.x, xv.x), __fmul_rn(xv.y, xv.y));
-                pa.x = __fadd_rn(pa.x, mm);
-                pa.y = __fadd_rn(pa.y, mm);
-              }
-              const float m2 = __fadd_rn(__fmul_rn(xv.z, xv.z), __fmul_rn(xv.w, xv.w));
-              pa.z = __fadd_rn(pa.z, m2);
-              pa.w = __fadd_rn(pa.w, m2);
+          if (k0 == 0 && i0 == 0 && i1 > 0) {  // packed |X_l(age 0)|^2, rounded as the oracle
+            const float4 xv = xr[0];
+            float4& pa = aac[PA];
+            if (dc) {
+              pa.x = __fadd_rn(pa.x, __fmul_rn(xv.x, xv.x));
+              pa.y = __fadd_rn(pa.y, __fmul_rn(xv.y, xv.y));
+            } else {
+              const float mm = __fadd_rn(__fmul_rn(xv.x, xv.x), __fmul_rn(xv.y, xv.y));
+              pa.x = __fadd_rn(pa.x, mm);
+              pa.y = __fadd_rn(pa.y, mm);
             }
+            const float m2 = __fadd_rn(__fmul_rn(xv.z, xv.z), __fmul_rn(xv.w, xv.w));
+            pa.z = __fadd_rn(pa.z, m2);
+            pa.w = __fadd_rn(pa.w, m2);
           }
+          float4* wg = a.W + ((size_t)c * U + m.t + i0) * P * CT + f;
+          float4 xa = xr[0];
+#pragma unroll 4
+          for (int i = i0; i < i1; ++i) {
+            const float4 x1 = xr[-(int)CT];  // pre-push age k = post-push age k + 1
+            xr -= CT;
+            const XPack x0 = xpack(xa, dc);
 #pragma unroll
-          for (int p = 0; p < PA; ++p) {
-            if (p >= P) break;
-            float4 w = ws[((size_t)i * P + p) * CT + f];
-            if (nl) {
+            for (int p = 0; p < PA; ++p) {
+              if (p >= P) break;
+              float4 w = wr[(size_t)p * CT];
               // g = conj(x1) E_p (packed bin 0: DC and Nyquist real products),
               // rounded exactly as the oracle (aura_oracle.c nlms_update)
               const float4 ep = e4[p];
+              const float px = __fmul_rn(x1.x, ep.x), py = __fmul_rn(x1.y, ep.y);
               float4 gr;
-              if (dc) {
-                gr.x = __fmul_rn(x1.x, ep.x);
-                gr.y = __fmul_rn(x1.y, ep.y);
-              } else {
-                gr.x = __fadd_rn(__fmul_rn(x1.x, ep.x), __fmul_rn(x1.y, ep.y));
-                gr.y = __fsub_rn(__fmul_rn(x1.x, ep.y), __fmul_rn(x1.y, ep.x));
-              }
+              gr.x = dc ? px : __fadd_rn(px, py);
+              gr.y = dc ? py : __fsub_rn(__fmul_rn(x1.x, ep.y), __fmul_rn(x1.y, ep.x));
               gr.z = __fadd_rn(__fmul_rn(x1.z, ep.z), __fmul_rn(x1.w, ep.w));
               gr.w = __fsub_rn(__fmul_rn(x1.z, ep.w), __fmul_rn(x1.w, ep.z));
               w.x = __fadd_rn(w.x, __fmul_rn(st.x, gr.x));
               w.y = __fadd_rn(w.y, __fmul_rn(st.y, gr.y));
               w.z = __fadd_rn(w.z, __fmul_rn(st.z, gr.z));
               w.w = __fadd_rn(w.w, __fmul_rn(st.w, gr.w));
-              __stcs(a.W + (((size_t)c * U + m.t + i) * P + p) * CT + f, w);
+              st_hint(wg + (size_t)p * CT, w, wpol);
+              cmac(aac[p], x0, w, dc);
             }
-            cmac(aac[p], x0, w, dc);
+            xa = x1;
+            wr += P * CT;
+            wg += P * CT;
+          }
+        } else {
+#pragma unroll 4
+          for (int i = i0; i < i1; ++i) {
+            const XPack x0 = xpack(xr[0], dc);
+            xr -= CT;
+#pragma unroll
+            for (int p = 0; p < PA; ++p) {
+              if (p >= P) break;
+              cmac(aac[p], x0, wr[(size_t)p * CT], dc);
+            }
+            wr += P * CT;
           }
         }
         __syncwarp();
