@@ -462,9 +462,12 @@ void plan_back(aura_b200_engine* e, BlockArgs& a) {
   const long long U = e->aur ? (long long)e->L * e->KF : 0;
   if (T > INT32_MAX / 2 || U > INT32_MAX / 2) fail(AURA_B200_E_INVALID_ARGUMENT, "filters too long");
   // stage sizes: ~32 KB per stage, a whole number of tap phases
-  const int target_f4 = 32 * 1024 / 16;
+  int target_kb = 32;
+  if (const char* f = std::getenv("AURA_B200_STAGE_KB")) target_kb = std::max(4, std::atoi(f));
+  const int target_f4 = target_kb * 1024 / 16;
   const int syn_row = (LT + XL) * CT;
-  a.sp = PH * std::max(1, target_f4 / (PH * syn_row));
+  a.sp = std::getenv("AURA_B200_STAGE_KB") ? std::max(PH, target_f4 / syn_row)
+                                            : PH * std::max(1, target_f4 / (PH * syn_row));
   const int afc_row = (P + 1) * CT;
   a.spa = PH * std::max(1, target_f4 / (PH * std::max(afc_row, 1)));
   long long slot = 0;
@@ -479,6 +482,7 @@ void plan_back(aura_b200_engine* e, BlockArgs& a) {
   const size_t fixed = kBackBarrierBytes + (size_t)a.red_f4 * 16;
   const size_t per = (size_t)a.slot_f4 * 16;
   a.stages = per ? (int)std::min<size_t>(kMaxStages, (budget - fixed) / per) : 0;
+  if (const char* f = std::getenv("AURA_B200_STAGES")) a.stages = std::max(2, std::min(a.stages, std::atoi(f)));
   if (e->has_back() && a.stages < 2)
     fail(AURA_B200_E_INVALID_ARGUMENT, "block size / channel tile too large for the streaming kernel");
   e->smem_back = fixed + (size_t)a.stages * per;
@@ -494,6 +498,8 @@ void plan_back(aura_b200_engine* e, BlockArgs& a) {
   double w_l2_mb = 80.0;
   if (const char* f = std::getenv("AURA_B200_W_L2_MB")) w_l2_mb = std::atof(f);
   a.w_in_l2 = (P > 0 && afc_foot < w_l2_mb * 1e6) ? 1 : 0;
+  a.dbg = 0;
+  if (const char* f = std::getenv("AURA_B200_DBG")) a.dbg = std::atoi(f);
   // grid: one CTA per SM, fewer for small work (>= ~96 KB per CTA). Sized
   // and planned from the synthesis alone when there is one, so the
   // synthesis association -- and the output bits -- are the same with or
@@ -501,27 +507,33 @@ void plan_back(aura_b200_engine* e, BlockArgs& a) {
   const double syn_b = (double)tiles * T * syn_row * 16.0;
   const double afc_b = (double)CTn * U * (P * (e->args.nlms ? 2 : 1) + 1) * CT * 16.0;
   const double drive = T > 0 ? syn_b : afc_b;
-  const int ctas = (int)std::min<double>(e->sms, std::max(1.0, std::ceil(drive / (96.0 * 1024))));
+  int ctas = (int)std::min<double>(e->sms, std::max(1.0, std::ceil(drive / (96.0 * 1024))));
+  if (const char* f = std::getenv("AURA_B200_BACK_CTAS")) ctas = std::max(1, std::min(ctas, std::atoi(f)));
   e->back_ctas = ctas;
-  // Work: every CTA first runs a static piece of each of three phases -- the
-  // first 30% of every synthesis tile's taps (covers the front half, which
-  // the canceller waits for), the canceller units, the next 45% of the taps
-  // -- then claims small queue items (the last 25%) so the CTAs finish
-  // together whatever their share of HBM bandwidth or start time.
-  // Phase fractions (profiles/r1s4_front.md): the first synthesis slice covers
-  // the front half, which the canceller items wait for; the last quarter is
-  // queue items, enough to absorb the k_back CTAs that start late on the SMs
-  // the front occupies
+  // Work: every CTA first runs a static piece of the first 30% of every
+  // synthesis tile's taps (they start at t = 0, before anything can be
+  // claimed, and cover the front half, which the canceller waits for), then
+  // claims queue items until the queue is empty. The queue holds the rest of
+  // the synthesis as tile-interleaved items -- larger ones for the middle
+  // (to 75%), small ones for the last quarter so the CTAs finish together
+  // whatever their start time -- with the canceller's items spread evenly
+  // through the middle part: at any time about the canceller's share of the
+  // SMs runs canceller units (L2-resident W) while the rest keep HBM busy
+  // with the synthesis stream. Every item is one split-K partial with a fixed
+  // slot, so which CTA claims it does not change the bits.
   double fa = 0.30;
   if (const char* f = std::getenv("AURA_B200_PHASE_A")) fa = std::atof(f);
   const long long TA = T > 0 ? std::max<long long>(1, (long long)std::ceil(fa * T)) : 0;
   double fb = 0.75;
   if (const char* f = std::getenv("AURA_B200_PHASE_B")) fb = std::atof(f);
   const long long TB = T > 0 ? std::max<long long>(TA, (long long)std::ceil(fb * T)) : 0;
-  // queue items: ~12 per CTA, at least two stages (keeps the tail short and
-  // the partial count -- k_reduce's input -- small at c5 sizes)
+  // queue items: ~12 per CTA in the last quarter, at least two stages (keeps
+  // the tail short and the partial count -- k_reduce's input -- small at c5
+  // sizes); ~3 per CTA in the middle part
   const long long qtaps = (T - TB) * tiles;
   const long long CQ = std::max<long long>(2LL * a.sp, (qtaps / (12LL * ctas) + a.sp - 1) / a.sp * a.sp);
+  const long long btaps = (TB - TA) * tiles;
+  const long long CB = std::max<long long>(CQ, (btaps / (3LL * ctas) + a.sp - 1) / a.sp * a.sp);
   std::vector<int4> chunks;
   std::vector<int> item_off(ctas + 1, 0);
   std::vector<std::vector<std::pair<int, int>>> at(tiles + CTn);  // per tile: (b, item)
@@ -550,51 +562,71 @@ void plan_back(aura_b200_engine* e, BlockArgs& a) {
       t = e_;
     }
   };
-  struct Ph { int kind; long long lo, hi; int ntile; };  // items [lo, hi) of every tile
-  const Ph phases[3] = {{0, 0, TA, tiles}, {1, 0, U, CTn}, {0, TA, TB, tiles}};
   std::vector<std::pair<long long, long long>> tmp;
-  for (int c = 0; c < ctas; ++c) {
-    item_off[c] = (int)chunks.size();
-    for (const Ph& ph : phases) {
-      // the phase's intervals, tile-major, as one linear item space
-      std::vector<std::tuple<int, long long, long long>> iv;
-      for (int tile = 0; tile < ph.ntile; ++tile) {
-        if (ph.kind == 1) {
-          if (ph.hi > ph.lo) iv.emplace_back(tile, ph.lo, ph.hi);
-          continue;
-        }
-        pieces(ph.lo, ph.hi, tmp);
-        for (auto& pr : tmp) iv.emplace_back(tile, pr.first, pr.second);
-      }
-      long long n_items = 0;
-      for (auto& x : iv) n_items += std::get<2>(x) - std::get<1>(x);
+  {  // static: piece c of phase A's intervals (tile-major, one linear item space)
+    std::vector<std::tuple<int, long long, long long>> iv;
+    for (int tile = 0; tile < tiles; ++tile) {
+      pieces(0, TA, tmp);
+      for (auto& pr : tmp) iv.emplace_back(tile, pr.first, pr.second);
+    }
+    long long n_items = 0;
+    for (auto& x : iv) n_items += std::get<2>(x) - std::get<1>(x);
+    for (int c = 0; c < ctas; ++c) {
+      item_off[c] = (int)chunks.size();
       if (n_items <= 0) continue;
       long long i0 = n_items * c / ctas, i1 = n_items * (c + 1) / ctas;
       long long base = 0;
       for (auto& x : iv) {
         const long long len = std::get<2>(x) - std::get<1>(x);
         const long long s0 = std::max(i0, base), s1 = std::min(i1, base + len);
-        if (s0 < s1) push(ph.kind, std::get<0>(x), std::get<1>(x) + (s0 - base), std::get<1>(x) + (s1 - base));
+        if (s0 < s1) push(0, std::get<0>(x), std::get<1>(x) + (s0 - base), std::get<1>(x) + (s1 - base));
         base += len;
       }
     }
   }
   item_off[ctas] = (int)chunks.size();
   a.n_static = (int)chunks.size();
-  {  // queue: tile-interleaved, so every tile's last partial lands near the end;
-     // the late (age-0) stages last of all
-    std::vector<std::vector<std::pair<long long, long long>>> qv(tiles);
-    size_t nq = 0;
-    for (int t = 0; t < tiles; ++t) {
-      pieces(TB, T, tmp);
-      for (auto& pr : tmp)
-        for (long long b = pr.first; b < pr.second; b += CQ)
-          qv[t].push_back({b, std::min<long long>(pr.second, b + CQ)});
-      nq = std::max(nq, qv[t].size());
+  {  // queue
+    // synthesis [lo, hi) of every tile in items of `cs` taps, tile-interleaved
+    // so every tile's partials spread over the whole range
+    auto syn_items = [&](long long lo, long long hi, long long cs) {
+      std::vector<std::vector<std::pair<long long, long long>>> qv(tiles);
+      size_t nq = 0;
+      for (int t = 0; t < tiles; ++t) {
+        pieces(lo, hi, tmp);
+        for (auto& pr : tmp)
+          for (long long b = pr.first; b < pr.second; b += cs)
+            qv[t].push_back({b, std::min<long long>(pr.second, b + cs)});
+        nq = std::max(nq, qv[t].size());
+      }
+      std::vector<std::tuple<int, long long, long long>> out;
+      for (size_t j = 0; j < nq; ++j)
+        for (int t = 0; t < tiles; ++t)
+          if (j < qv[t].size()) out.emplace_back(t, qv[t][j].first, qv[t][j].second);
+      return out;
+    };
+    const auto mid = syn_items(TA, TB, CB);
+    // canceller: ~2 items per CTA, each a contiguous run of units of one
+    // column tile (units of several loudspeakers are fine: a stage never
+    // crosses one)
+    std::vector<std::tuple<int, long long, long long>> afc;
+    if (U > 0) {
+      const long long per = std::max<long long>(a.spa, (U * CTn / (2LL * ctas) + a.spa - 1) / a.spa * a.spa);
+      for (int c = 0; c < CTn; ++c)
+        for (long long b = 0; b < U; b += per) afc.emplace_back(c, b, std::min<long long>(U, b + per));
     }
-    for (size_t j = 0; j < nq; ++j)
-      for (int t = 0; t < tiles; ++t)
-        if (j < qv[t].size()) push(0, t, qv[t][j].first, qv[t][j].second);
+    // merge: canceller items evenly through the middle synthesis items (the
+    // first middle items go first: the canceller waits for the head)
+    const size_t nm = mid.size(), na = afc.size();
+    size_t im = 0;
+    for (size_t j = 0; j < na; ++j) {
+      const size_t upto = nm * (2 * j + 1) / (2 * na);  // middle items before canceller item j
+      for (; im < upto; ++im) push(0, std::get<0>(mid[im]), std::get<1>(mid[im]), std::get<2>(mid[im]));
+      push(1, std::get<0>(afc[j]), std::get<1>(afc[j]), std::get<2>(afc[j]));
+    }
+    for (; im < nm; ++im) push(0, std::get<0>(mid[im]), std::get<1>(mid[im]), std::get<2>(mid[im]));
+    for (auto& x : syn_items(TB, T, CQ)) push(0, std::get<0>(x), std::get<1>(x), std::get<2>(x));
+    // the late (age-0) stages last of all
     for (long long q = 0; Kt > 0 && q < Qh; ++q)
       for (int t = 0; t < tiles; ++t) push(0, t, q * Kt, q * Kt + late);
   }

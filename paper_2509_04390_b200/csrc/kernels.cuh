@@ -110,6 +110,7 @@ struct BlockArgs {
   int n_syn_tiles;   // (L/LT) * CTn
   int h_in_l2;       // spectra fit in L2: stream them with evict_normal
   int w_in_l2;       // canceller W + delay lines fit in L2: keep W there (evict_last)
+  int dbg;           // experiment switches (AURA_B200_DBG; 0 in production)
   const int4* chunks;   // work items {kind | tile << 1, b, e, partial slot in tile}:
                         //   [n_static] per-CTA static pieces, then [n_chunks - n_static] queue
   int n_chunks, n_static;

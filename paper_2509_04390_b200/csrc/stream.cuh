@@ -219,6 +219,9 @@ __device__ __forceinline__ void back_produce(const BlockArgs& a, uint32_t n, uin
     return d < a.n_chunks ? d : -1;
   };
   bool waited = false, front_ok = false;
+  // ring cursor, advanced incrementally (no divisions on the per-stage path)
+  int s = (int)(q % (uint32_t)S);
+  uint32_t par = ((q / (uint32_t)S) & 1u) ^ 1u;
   int idx = claim(0);
   int4 rec = idx >= 0 ? a.chunks[idx] : make_int4(0, 0, 0, 0);
   for (int k = 0; idx >= 0; ++k) {
@@ -232,19 +235,28 @@ __device__ __forceinline__ void back_produce(const BlockArgs& a, uint32_t n, uin
       waited = deps.wait_head(n);  // canceller inputs come from the head (k_back_head)
       abort = !waited;
     }
+    // per item: the input (synthesis) or loudspeaker (canceller) block b of
+    // the first stage; stages never cross a block boundary
     const int B = kind ? KF : Kt;
     const int SP = kind ? a.spa : a.sp;
+    int b = rec.y / B, b0 = b * B;
+    const int g = tile / CTn, c = tile - g * CTn;
+    const float4* hsrc = a.Ht + (size_t)tile * T * LT * CT;
+    const uint32_t syn_tx = (uint32_t)(((a.dbg & 2) ? LT : LT + XL) * CT) * 16u;
     for (int t = rec.y; t < rec.z && !abort;) {
-      const int t1 = min(min(t + SP, rec.z), (t / B + 1) * B);
-      if (!front_ok && kind == 0 && t - (t / Kt) * Kt == 0) {
+      if (t == b0 + B) {
+        ++b;
+        b0 += B;
+      }
+      const int t1 = min(min(t + SP, rec.z), b0 + B);
+      if (!front_ok && kind == 0 && t == b0) {
         front_ok = deps.wait_front(n);  // this stage reads X(age 0), pushed by the front
         if (!front_ok) {
           abort = true;
           break;
         }
       }
-      const int s = (int)(q % (uint32_t)S);
-      if (!mbar_wait_bounded(empty + s, ((q / (uint32_t)S) & 1u) ^ 1u, deps.abort())) {
+      if (!mbar_wait_bounded(empty + s, par, deps.abort())) {
         abort = true;
         break;
       }
@@ -252,46 +264,47 @@ __device__ __forceinline__ void back_produce(const BlockArgs& a, uint32_t n, uin
       float4* dst = slots + (size_t)s * a.slot_f4;
       const int nt = t1 - t;
       if (PT == 0 || kind == 0) {
-        const int g = tile / CTn, c = tile - g * CTn;
-        const int qi = t / Kt, j0 = t - qi * Kt, j1 = t1 - qi * Kt;
-        mbar_expect_tx(full + s, (uint32_t)(nt * (LT + XL) * CT) * 16u);
-        bulk_g2s(dst, a.Ht + ((size_t)(g * CTn + c) * T + t) * LT * CT, (uint32_t)(nt * LT * CT) * 16u,
-                 full + s, pol_stream);
+        const int j0 = t - b0, j1 = t1 - b0;
+        mbar_expect_tx(full + s, (uint32_t)nt * syn_tx);
+        bulk_g2s(dst, hsrc + (size_t)t * LT * CT, (uint32_t)(nt * LT * CT) * 16u, full + s, pol_stream);
         float4* xd = dst + (size_t)a.sp * LT * CT;
 #pragma unroll
-        for (int i = 0; i < XL; ++i) {
-          const int xc = ELEM ? g * LT + i : qi;
+        for (int i = 0; i < XL && !(a.dbg & 2); ++i) {
+          const int xc = ELEM ? g * LT + i : b;
           copy_ring(xd + (size_t)i * a.sp * CT, a.X + (size_t)(xc * CTn + c) * K * CT, nk - (j1 - 1),
                     nk - j0, K, CT, full + s, pol_keep);
         }
       } else {
-        const int c = tile, P = a.P, U = a.L * KF;
-        const int l = t / KF, k0 = t - l * KF;
+        const int P = a.P, U = a.L * KF;
+        const int l = b, k0 = t - b0;
         const int amax = k0 + nt - 1 + a.nlms;
         const int rows = amax - k0 + 1;
         const uint32_t cb = (uint32_t)CT * 16u;
         mbar_expect_tx(full + s, (uint32_t)(nt * P * CT + rows * CT) * 16u + (a.nlms ? (P + 1) * cb : 0u));
-        bulk_g2s(dst, a.W + ((size_t)c * U + t) * P * CT, (uint32_t)(nt * P * CT) * 16u, full + s,
+        bulk_g2s(dst, a.W + ((size_t)tile * U + t) * P * CT, (uint32_t)(nt * P * CT) * 16u, full + s,
                  a.w_in_l2 ? pol_keep : pol_stream);
         float4* xd = dst + (size_t)a.spa * P * CT;
-        copy_ring(xd, a.XA + (size_t)(l * CTn + c) * cap * CT, nka - amax, nka - k0, cap, CT, full + s,
+        copy_ring(xd, a.XA + (size_t)(l * CTn + tile) * cap * CT, nka - amax, nka - k0, cap, CT, full + s,
                   pol_keep);
         if (a.nlms) {  // E_p and the power of this column tile
           float4* ed = xd + (size_t)(a.spa + 1) * CT;
           for (int p = 0; p < P; ++p)
-            bulk_g2s(ed + (size_t)p * CT, a.E + (size_t)p * a.NF + c * CT, cb, full + s, pol_keep);
-          bulk_g2s(ed + (size_t)P * CT, a.pw + (size_t)2 * c * CT, cb, full + s, pol_keep);
+            bulk_g2s(ed + (size_t)p * CT, a.E + (size_t)p * a.NF + tile * CT, cb, full + s, pol_keep);
+          bulk_g2s(ed + (size_t)P * CT, a.pw + (size_t)2 * tile * CT, cb, full + s, pol_keep);
         }
       }
       ++q;
+      if (++s == S) {
+        s = 0;
+        par ^= 1u;
+      }
       t = t1;
     }
     if (abort) break;  // a dependency wait failed (loop mode timeout): stop streaming
     idx = nidx;
     rec = nrec;
   }
-  const int s = (int)(q % (uint32_t)S);
-  if (!mbar_wait_bounded(empty + s, ((q / (uint32_t)S) & 1u) ^ 1u, deps.abort())) return;
+  if (!mbar_wait_bounded(empty + s, par, deps.abort())) return;
   meta[s].item = -1;
   mbar_arrive(full + s);
   ++q;
@@ -356,9 +369,18 @@ __device__ __forceinline__ void back_consume(const BlockArgs& a, uint32_t n, uin
   const uint64_t wpol = a.w_in_l2 ? policy_evict_last() : policy_evict_first();
   constexpr int PA = PT > 0 ? PT : 1;
 
+  // ring cursor, advanced incrementally (no divisions on the per-stage path)
+  int sl = (int)(q % (uint32_t)S);
+  uint32_t par = (q / (uint32_t)S) & 1u;
+  auto advance = [&]() {
+    ++q;
+    if (++sl == S) {
+      sl = 0;
+      par ^= 1u;
+    }
+  };
   for (;;) {
-    int sl = (int)(q % (uint32_t)S);
-    if (!mbar_wait_bounded(full + sl, (q / (uint32_t)S) & 1u, abort)) return;
+    if (!mbar_wait_bounded(full + sl, par, abort)) return;
     StageMeta m = meta[sl];
     if (m.item < 0) {  // sentinel: release its slot too (the ring persists in the loop)
       __syncwarp();
@@ -380,7 +402,7 @@ __device__ __forceinline__ void back_consume(const BlockArgs& a, uint32_t n, uin
         const int nt = m.t1 - m.t;
         const float4* hs = slots + (size_t)sl * a.slot_f4;
         const float4* xs = hs + (size_t)a.sp * LT * CT;
-        for (int i = ph; i < nt; i += PH) {
+        for (int i = ph; i < nt && !(a.dbg & 1); i += PH) {
           const int r = nt - 1 - i;  // X rows are stored oldest-first
           if (ELEM) {
 #pragma unroll
@@ -399,10 +421,9 @@ __device__ __forceinline__ void back_consume(const BlockArgs& a, uint32_t n, uin
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(empty + sl);
-        ++q;
+        advance();
         if (m.flags & 1) break;
-        sl = (int)(q % (uint32_t)S);
-        if (!mbar_wait_bounded(full + sl, (q / (uint32_t)S) & 1u, abort)) return;
+        if (!mbar_wait_bounded(full + sl, par, abort)) return;
         m = meta[sl];
       }
       const int E = LT * CT;
@@ -506,10 +527,9 @@ __device__ __forceinline__ void back_consume(const BlockArgs& a, uint32_t n, uin
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(empty + sl);
-        ++q;
+        advance();
         if (m.flags & 1) break;
-        sl = (int)(q % (uint32_t)S);
-        if (!mbar_wait_bounded(full + sl, (q / (uint32_t)S) & 1u, abort)) return;
+        if (!mbar_wait_bounded(full + sl, par, abort)) return;
         m = meta[sl];
       }
       const int E = R * CT;

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <vector>
 
 #define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { printf("err %s at %d: %s\n", #x, __LINE__, cudaGetErrorString(e_)); exit(1);} } while (0)
@@ -95,6 +96,30 @@ int main() {
     cudaEventElapsedTime(&ms, t0, t1);
     return ms / reps;
   };
+  if (getenv("BW_PER_SM")) {  // per-SM ceiling: fewer CTAs than SMs
+    CK(cudaFuncSetAttribute(k_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    for (int grid : {16, 32, 64, 96, 148}) {
+      for (int stage : {16384, 32768, 49152}) {
+        for (int S : {3, 4, 6}) {
+          const size_t smem = 256 + (size_t)S * stage;
+          if (smem > 220 * 1024) continue;
+          for (int copies : {1, 4}) {
+            size_t per = bytes / 148;
+            per -= per % stage;
+            float ms = timeit([&] { k_bulk<<<grid, 288, smem>>>(buf, per, stage, S, copies, out); }, 5);
+            printf("{\"kind\": \"bulk\", \"ctas\": %d, \"stage\": %d, \"stages\": %d, \"copies\": %d, \"GBps\": %.1f, \"per_sm\": %.1f}\n",
+                   grid, stage, S, copies, (double)per * grid / ms / 1e6, (double)per / ms / 1e6);
+          }
+        }
+      }
+      for (int thr : {512, 1024}) {
+        float ms = timeit([&] { k_ldg<<<grid, thr>>>((const float4*)buf, bytes / 16 / 148 * grid, out); }, 5);
+        printf("{\"kind\": \"ldg128\", \"ctas\": %d, \"threads\": %d, \"per_sm\": %.1f}\n", grid, thr,
+               (double)(bytes / 148) / ms / 1e6);
+      }
+    }
+    return 0;
+  }
   for (int per_sm : {2, 4, 8}) {
     const int grid = sms * per_sm;
     float ms = timeit([&] { k_ldg<<<grid, 512>>>((const float4*)buf, bytes / 16, out); }, 10);
