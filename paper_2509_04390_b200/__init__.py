@@ -366,7 +366,7 @@ class _Engine:
         _check(lib().aura_b200_loop_phases(self._h, blocks, out.ctypes.data))
         return {k: out[:, i] for i, k in enumerate(self.LOOP_PHASES)}
 
-    PHASES = {"k_front": 0, "k_back": 2}
+    PHASES = {"k_front": 0, "k_back": 2, "k_reduce": 3}
 
     def time_phase(self, name: str, reps: int = 20) -> float:
         """Mean device time (us) of back-to-back launches of one idempotent

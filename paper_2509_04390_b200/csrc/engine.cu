@@ -22,6 +22,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -57,6 +58,20 @@ void ck(cudaError_t e, const char* what) {
   fail(AURA_B200_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 #define CK(x) ck((x), #x)
+
+// Raise a kernel's dynamic shared-memory limit on the current device, never
+// lower it: the attribute is per function, so engines of different shapes in
+// one process must not undo each other's (a smaller engine created after a
+// larger one would otherwise make the larger one's launches invalid).
+template <typename Fn>
+void raise_smem_limit(Fn fn, size_t bytes) {
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  cudaFuncAttributes fa{};
+  CK(cudaFuncGetAttributes(&fa, (const void*)fn));
+  if ((size_t)fa.maxDynamicSharedSizeBytes < bytes)
+    CK(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+}
 
 template <class F>
 int guarded(F&& f) {
@@ -387,7 +402,7 @@ void partition_rows(aura_b200_engine* e, const BlockArgs& a, const float* const*
   CK(cudaMalloc(&d_taps, nb * n_h * sizeof(float)));
   CK(cudaMalloc(&d_off, 2 * nb * sizeof(long long)));
   const size_t smem = 16 * N + 8 * (size_t)table_f2((int)N);
-  CK(cudaFuncSetAttribute(k_partition, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  raise_smem_limit(k_partition, smem);
   std::vector<long long> offs(2 * nb);
   for (size_t r0 = 0; r0 < n_rows; r0 += batch) {
     const size_t nr = std::min(batch, n_rows - r0);
@@ -672,7 +687,7 @@ void plan_back(aura_b200_engine* e, BlockArgs& a) {
   a.red_afc_cpt = U > 0 ? cpt_for(a.red_afc_rows * CT, max_afc) : 1;
   a.red_afc_ctas = U > 0 ? CTn * a.red_afc_cpt : 0;
   e->smem_reduce = 16 * reduce_smem_f4(N, e->aur, P);
-  CK(cudaFuncSetAttribute(k_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem_reduce));
+  raise_smem_limit(k_reduce, e->smem_reduce);
   // tickets: [0] canceller CTAs of k_reduce, [1] all k_reduce CTAs, [2] work
   // queue, [3] k_back exits
   a.tick_queue = 2;
@@ -692,7 +707,7 @@ void plan_back(aura_b200_engine* e, BlockArgs& a) {
     default: e->back_fn = back_for<8>(elem, e->PT); break;
   }
   if (e->has_back())
-    CK(cudaFuncSetAttribute(e->back_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem_back));
+    raise_smem_limit(e->back_fn, e->smem_back);
 }
 
 void common_init(aura_b200_engine* e, int device) {
@@ -774,7 +789,7 @@ void plan_loop(aura_b200_engine* e) {
     default: e->loop_fn = loop_for<8>(elem, e->PT); break;
   }
   e->smem_loop = fixed + (size_t)stages * slot;
-  CK(cudaFuncSetAttribute(e->loop_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem_loop));
+  raise_smem_limit(e->loop_fn, e->smem_loop);
   int per_sm = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, e->loop_fn, kBackThreads, e->smem_loop));
   if (per_sm < 1 || e->loop_ctas > per_sm * e->sms) {
@@ -859,8 +874,8 @@ void finish_init(aura_b200_engine* e) {
   }
   if (e->smem_front > 227 * 1024)
     fail(AURA_B200_E_INVALID_ARGUMENT, "block size too large for this many inputs (shared memory)");
-  CK(cudaFuncSetAttribute(k_front, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem_front));
-  CK(cudaFuncSetAttribute(k_back_head, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem_head));
+  raise_smem_limit(k_front, e->smem_front);
+  raise_smem_limit(k_back_head, e->smem_head);
   // device-resident I/O variant for measurement
   e->pool_blocks = 64;
   e->d_in_pool = dalloc<float>(e->pool_blocks * in_ch * N, e->dmem);
@@ -1855,8 +1870,8 @@ int aura_b200_profile_phases(aura_b200_engine* e, size_t blocks, float* phase_us
 int aura_b200_time_phase(aura_b200_engine* e, int phase, size_t reps, float* avg_us) {
   return guarded([&] {
     stop_loop(e);
-    if (phase != PH_BACK && phase != PH_FRONT)
-      fail(AURA_B200_E_INVALID_ARGUMENT, "only the front and the streaming kernel can be re-launched");
+    if (phase != PH_BACK && phase != PH_FRONT && phase != PH_REDUCE)
+      fail(AURA_B200_E_INVALID_ARGUMENT, "only the front, k_back and k_reduce can be re-launched");
     if (phase == PH_BACK && !e->has_back())
       fail(AURA_B200_E_INVALID_ARGUMENT, "this engine has no streaming work");
     CK(cudaSetDevice(e->device));
@@ -1864,6 +1879,13 @@ int aura_b200_time_phase(aura_b200_engine* e, int phase, size_t reps, float* avg
     // single launches, back to back without programmatic overlap, so the
     // mean is one launch's duration (ramp-up and tail included)
     BlockArgs a = e->dev_args;
+    // k_reduce advances the block counter: restore it afterwards (the
+    // re-launches re-sum the same partials; the canceller state is
+    // re-derived from them, as in the timed block)
+    DevState st0{};
+    CK(cudaMemcpy(&st0, a.st, sizeof(DevState), cudaMemcpyDeviceToHost));
+    std::vector<float2> pw0(a.pw && phase == PH_REDUCE ? (size_t)a.N : 0);  // the smoothed power too
+    if (!pw0.empty()) CK(cudaMemcpy(pw0.data(), a.pw, pw0.size() * sizeof(float2), cudaMemcpyDeviceToHost));
     e->pdl_off = true;
     e->launch_phase(phase, a, e->stream);  // warm
     cudaEvent_t t0, t1;
@@ -1880,6 +1902,8 @@ int aura_b200_time_phase(aura_b200_engine* e, int phase, size_t reps, float* avg
     cudaEventDestroy(t0);
     cudaEventDestroy(t1);
     *avg_us = 1000.0f * ms / (float)reps;
+    CK(cudaMemcpy(a.st, &st0, sizeof(DevState), cudaMemcpyHostToDevice));
+    if (!pw0.empty()) CK(cudaMemcpy(a.pw, pw0.data(), pw0.size() * sizeof(float2), cudaMemcpyHostToDevice));
   });
 }
 

@@ -207,3 +207,18 @@ def test_c3_config_streams_and_matches_oracle_subset():
     assert rel_err(np.stack(ys), np.stack(yo)) <= TOL
     assert rel_err(g.feedback_estimate(), o.feedback_estimate()) <= TOL
     assert rel_err(g.coeffs(), o.coeffs()) <= TOL
+
+
+def test_engines_of_different_shapes_coexist():
+    # kernel shared-memory limits are per function: a smaller engine created
+    # after a larger one must not invalidate the larger one's launches
+    g = golden("aur_n64")
+    N, L = int(g["N"]), int(g["L"])
+    aur = gpu_aur(g["synth"], g["fc"], N, 1, L, gain=float(g["gain"]))
+    rng = np.random.default_rng(5)
+    small = A.Convolver(list(scaled_filters(rng, 1, 4 * 32)), A.make_config(48000, 32, 1, 1))
+    ys = [aur.process(m) for m in g["mic"]]
+    small.process(np.zeros((1, 32), np.float32))
+    assert rel_err(np.stack(ys), g["y"]) <= TOL
+    small.close()
+    aur.close()
