@@ -689,10 +689,10 @@ void plan_back(aura_b200_engine* e, BlockArgs& a) {
   e->smem_reduce = 16 * reduce_smem_f4(N, e->aur, P);
   raise_smem_limit(k_reduce, e->smem_reduce);
   // tickets: [0] canceller CTAs of k_reduce, [1] all k_reduce CTAs, [2] work
-  // queue, [3] k_back exits
+  // queue, [3] k_back exits, [4] canceller items done (fused tail)
   a.tick_queue = 2;
-  a.tick = dalloc<unsigned>(4, e->dmem);
-  CK(cudaMemset(a.tick, 0, 4 * sizeof(unsigned)));
+  a.tick = dalloc<unsigned>(6, e->dmem);
+  CK(cudaMemset(a.tick, 0, 6 * sizeof(unsigned)));
   a.part_syn = dalloc<float4>(std::max<size_t>(1, (size_t)slot_syn * LT * CT), e->dmem);
   if (e->aur) {
     const size_t R = (size_t)P + 1;
@@ -2030,12 +2030,13 @@ int aura_b200_describe(const aura_b200_engine* e, char* buf, size_t cap) {
     std::snprintf(buf, cap,
                   "N=%zu Q=%zu L=%zu P=%zu K=%zu KF=%zu mode=%d LT=%d PT=%d | front: grid=%zu cpb=%d "
                   "warps=%d smem=%zu | back: ctas=%d x %d thr, CT=%d CTn=%d sp=%d spa=%d stages=%d slot=%d B "
-                  "smem=%zu partials=%zu+%zu items=%d (static %d) | reduce: %d+%d ctas l2keep=%d "
+                  "smem=%zu partials=%zu+%zu items=%d (static %d) w_l2=%d | reduce: %d+%d ctas l2keep=%d "
                   "nlms=%d delta=%g",
                   e->N, e->Q, e->L, e->P, e->K, e->KF, e->mode, e->LT, e->PT,
                   (e->L + a.cpb - 1) / a.cpb, a.cpb, a.front_warps, e->smem_front, e->back_ctas, kBackThreads, a.CT,
                   a.CTn, a.sp, a.spa, a.stages, a.slot_f4 * 16, e->smem_back, e->n_syn_segs,
-                  e->n_afc_segs, a.n_chunks, a.n_static, a.red_syn_ctas, a.red_afc_ctas, a.h_in_l2, a.nlms,
+                  e->n_afc_segs, a.n_chunks, a.n_static, a.w_in_l2, a.red_syn_ctas, a.red_afc_ctas, a.h_in_l2,
+                  a.nlms,
                   (double)a.delta);
   });
 }

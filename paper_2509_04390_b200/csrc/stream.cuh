@@ -280,13 +280,15 @@ __device__ __forceinline__ void back_produce(const BlockArgs& a, uint32_t n, uin
         const int amax = k0 + nt - 1 + a.nlms;
         const int rows = amax - k0 + 1;
         const uint32_t cb = (uint32_t)CT * 16u;
-        mbar_expect_tx(full + s, (uint32_t)(nt * P * CT + rows * CT) * 16u + (a.nlms ? (P + 1) * cb : 0u));
+        // E_p and the power: the consumers read them from the item's first stage only
+        const bool ep = a.nlms && t == rec.y;
+        mbar_expect_tx(full + s, (uint32_t)(nt * P * CT + rows * CT) * 16u + (ep ? (P + 1) * cb : 0u));
         bulk_g2s(dst, a.W + ((size_t)tile * U + t) * P * CT, (uint32_t)(nt * P * CT) * 16u, full + s,
                  a.w_in_l2 ? pol_keep : pol_stream);
         float4* xd = dst + (size_t)a.spa * P * CT;
         copy_ring(xd, a.XA + (size_t)(l * CTn + tile) * cap * CT, nka - amax, nka - k0, cap, CT, full + s,
                   pol_keep);
-        if (a.nlms) {  // E_p and the power of this column tile
+        if (ep) {  // E_p and the power of this column tile
           float4* ed = xd + (size_t)(a.spa + 1) * CT;
           for (int p = 0; p < P; ++p)
             bulk_g2s(ed + (size_t)p * CT, a.E + (size_t)p * a.NF + tile * CT, cb, full + s, pol_keep);
