@@ -863,9 +863,11 @@ void finish_init(aura_b200_engine* e) {
     const char* fw = std::getenv("AURA_B200_FRONT_WARPS");
     const int W = kFrontThreads / 32;
     const size_t sw = 8 * front_warps_f2((int)N, (int)Qs, W);
-    // measured (profiles/r1s4_front.md): a clear win at N <= 64; at N = 128 a
-    // 64-butterfly stage per warp is already slower than the CTA version
-    const bool want = fw ? std::atoi(fw) != 0 : N <= 64;
+    // measured (profiles/r1s4_front.md, r1s5_stream.md): a clear win at
+    // N <= 64; at N = 128 a warp's transform alone is slower than the CTA
+    // version, but 8x fewer front CTAs let k_back's CTAs start at once (c5:
+    // -13 us per block, c2 -2 us); at N = 256 the output comes later
+    const bool want = fw ? std::atoi(fw) != 0 : N <= 128;
     if (e->mode != AURA_B200_ELEMENTWISE && sw <= 160 * 1024 && want) {
       a.front_warps = W;
       a.cpb = W;
