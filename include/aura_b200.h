@@ -232,15 +232,19 @@ int aura_b200_time_host_blocks(aura_b200_engine* e, const float* host_in,
 int aura_b200_profile_phases(aura_b200_engine* e, size_t blocks,
                              float* phase_us, int* n_phases);
 const char* aura_b200_phase_name(const aura_b200_engine* e, int phase);
-/* Average device time of `reps` back-to-back launches of one idempotent
- * phase kernel (k_front = 0, k_mac_pre = 1) between two
- * CUDA events on the engine stream: the roofline denominator. */
+/* Average device time of `reps` back-to-back single launches (no
+ * programmatic overlap) of one phase kernel -- k_front = 0, k_back = 2,
+ * k_reduce = 3 -- between two CUDA events on the engine stream: the
+ * roofline denominator. The block counter and the canceller's smoothed
+ * power are restored afterwards. */
 int aura_b200_time_phase(aura_b200_engine* e, int phase, size_t reps, float* avg_us);
 /* Timeline of `blocks` (<= 64) back-to-back device-resident blocks from
- * %globaltimer stamps taken inside the kernels: out[(i*8 + k)*2 + {0,1}] =
- * start / end (us, relative to block i's front start) of kernel k in order
- * k_front, k_mac_pre, (unused), k_back_head, k_mac_afc, (unused), k_afc_finish
- * (-1 when the kernel did not run). Shows launch gaps and branch overlap. */
+ * %globaltimer stamps taken inside the kernels: out[(i*10 + k)*2 + {0,1}] =
+ * first / last stamp (us, relative to block i's front start) of event k in
+ * order k_front, k_back_head, k_back, k_reduce, canceller done, k_afc_finish,
+ * output published, canceller sums in, f^ written; slot 9 = {the next
+ * block's front start, 0}. -1 when the event did not occur. Shows launch
+ * gaps and overlap. */
 int aura_b200_trace_blocks(aura_b200_engine* e, size_t blocks, double* out);
 /* Diagnostics (not in the reference): per-segment / per-CTA timeline of the
  * streaming kernel k_back for the last of `blocks` blocks, us from the

@@ -313,19 +313,20 @@ class _Engine:
         _check(lib().aura_b200_reset(self._h))
 
     TRACE_KERNELS = ("k_front", "k_back_head", "k_back", "k_reduce", "afc_done", "k_afc_finish",
-                     "output")
+                     "output", "afc_summed", "afc_c2r")
+    _TRACE_SLOTS = 10  # kTraceKernels: the last slot is the next block's front start
 
     def trace_blocks(self, blocks: int = 32):
         """Per-kernel [start, end] (us from the block's front start) of
         back-to-back blocks, from %globaltimer stamps inside the kernels."""
         blocks = min(blocks, 64)
-        out = np.zeros(blocks * 8 * 2, np.float64)
+        out = np.zeros(blocks * self._TRACE_SLOTS * 2, np.float64)
         _check(lib().aura_b200_trace_blocks(self._h, blocks, out))
-        out = out.reshape(blocks, 8, 2)
+        out = out.reshape(blocks, self._TRACE_SLOTS, 2)
         res = {name: out[:, k, :] for k, name in enumerate(self.TRACE_KERNELS)
                if np.all(out[:, k, 0] >= 0)}
         if blocks > 1:  # front start -> next block's front start (back to back)
-            res["cycle"] = out[:-1, 7, :]
+            res["cycle"] = out[:-1, self._TRACE_SLOTS - 1, :]
         return res
 
     def trace_back(self, blocks: int = 8):

@@ -455,6 +455,14 @@ BackFn loop_for(bool elem, int PT) {
   }
 }
 
+// Canceller partials per column tile that one k_reduce CTA sums in two load
+// rounds per thread (kReduceThreads threads over E elements, 16 loads in
+// flight per round: reduce_part).
+long long afc_single_cap(int rows, int CT) {
+  const int E = rows * CT;
+  return E > kReduceThreads ? 0 : 2LL * 16LL * (kReduceThreads / E);
+}
+
 // Plan k_back (stream.cuh): tiling, stage sizes, pipeline depth, and the
 // static work split. Three phases -- synthesis taps [0, TA) of every tile,
 // the canceller units, synthesis taps [TA, T) -- are each cut into
@@ -626,16 +634,24 @@ void plan_back(aura_b200_engine* e, BlockArgs& a) {
     // crosses one)
     std::vector<std::tuple<int, long long, long long>> afc;
     if (U > 0) {
-      const long long per = std::max<long long>(a.spa, (U * CTn / (2LL * ctas) + a.spa - 1) / a.spa * a.spa);
+      long long per = std::max<long long>(a.spa, (U * CTn / (2LL * ctas) + a.spa - 1) / a.spa * a.spa);
+      if (CTn == 1) {
+        // one column tile: few enough partials that one k_reduce CTA sums
+        // them in one round of loads and runs the c2r from shared memory
+        // (reduce_part's single-CTA path; cpt_for below gives 1)
+        const long long cap = afc_single_cap(P + (e->args.nlms ? 1 : 0), CT);
+        if (cap > 0) per = std::max(per, ((U + cap - 1) / cap + a.spa - 1) / a.spa * a.spa);
+      }
       for (int c = 0; c < CTn; ++c)
         for (long long b = 0; b < U; b += per) afc.emplace_back(c, b, std::min<long long>(U, b + per));
     }
     // merge: canceller items evenly through the middle synthesis items (the
     // first middle items go first: the canceller waits for the head)
     const size_t nm = mid.size(), na = afc.size();
+    const size_t span = nm * 2 / 3;  // over the first two thirds: the long items end well before the tail
     size_t im = 0;
     for (size_t j = 0; j < na; ++j) {
-      const size_t upto = nm * (2 * j + 1) / (2 * na);  // middle items before canceller item j
+      const size_t upto = span * (2 * j + 1) / (2 * na);  // middle items before canceller item j
       for (; im < upto; ++im) push(0, std::get<0>(mid[im]), std::get<1>(mid[im]), std::get<2>(mid[im]));
       push(1, std::get<0>(afc[j]), std::get<1>(afc[j]), std::get<2>(afc[j]));
     }
@@ -685,6 +701,7 @@ void plan_back(aura_b200_engine* e, BlockArgs& a) {
   a.red_syn_ctas = T > 0 ? tiles * a.red_syn_cpt : 0;
   a.red_afc_rows = P + (e->args.nlms ? 1 : 0);
   a.red_afc_cpt = U > 0 ? cpt_for(a.red_afc_rows * CT, max_afc) : 1;
+  if (U > 0 && CTn == 1 && max_afc <= afc_single_cap(a.red_afc_rows, CT)) a.red_afc_cpt = 1;
   a.red_afc_ctas = U > 0 ? CTn * a.red_afc_cpt : 0;
   e->smem_reduce = 16 * reduce_smem_f4(N, e->aur, P);
   raise_smem_limit(k_reduce, e->smem_reduce);

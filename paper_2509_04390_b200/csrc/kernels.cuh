@@ -55,8 +55,12 @@ struct DevState {
 // Optional timeline trace (%globaltimer, ns): per traced block slot and
 // kernel, the earliest CTA start and the latest CTA end.
 constexpr int kTraceBlocks = 64;
-constexpr int kTraceKernels = 8;
-enum TraceId { TR_FRONT = 0, TR_BACK_HEAD, TR_BACK, TR_REDUCE, TR_AFC_DONE, TR_AFC_FINISH, TR_OUTPUT };
+constexpr int kTraceKernels = 10;  // the last slot carries the next block's front start (cycle)
+enum TraceId {
+  TR_FRONT = 0, TR_BACK_HEAD, TR_BACK, TR_REDUCE, TR_AFC_DONE, TR_AFC_FINISH, TR_OUTPUT,
+  TR_AFC_SUMMED,  // k_reduce: the canceller's split-K sums are in (the CTA that runs the c2r)
+  TR_AFC_C2R      // k_reduce: f^ written (before the power update)
+};
 
 // Loudspeaker-channel sharding: at most kMaxShards engines
 // (one per GPU, or virtual shards on one GPU) exchange their canceller

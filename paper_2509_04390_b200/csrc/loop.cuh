@@ -285,7 +285,7 @@ __global__ void __launch_bounds__(kBackThreads, 1) k_loop(const __grid_constant_
       for (int r = blockIdx.x; r < nred; r += gridDim.x) {
         reduce_prefetch(a, r, rsm, team);
         team.sync();
-        reduce_part(a, r, n, rsm, &s_ok, team);
+        reduce_part(a, r, n, rsm, &s_ok, team, reduce_tile_info(a, r));
         team.sync();
       }
       if (blockIdx.x == 0 && threadIdx.x == 0 && a.loop_stamps)

@@ -633,10 +633,13 @@ constexpr int kReduceThreads = 256;
 // Shared-memory float4 count of k_reduce's scratch: the combine buffer, and
 // for the canceller the c2r scratch (N float2), the DftPlan tables and the
 // smoothed power (N float2).
+// Canceller sums kept in shared memory by the single-CTA path (one column
+// tile, N <= 64): (P + 1) rows of NF float4.
+__host__ __device__ inline size_t afc_ys_f4(int N, int P) { return N <= 64 ? (size_t)(P + 1) * (N / 2) : 0; }
 __host__ __device__ inline size_t reduce_smem_f4(int N, bool aur, int P = 1) {
   // c2r scratch: one N-float2 area per mic when the mics' c2r run on separate warps
   const size_t scratch = (N <= 1024 ? (size_t)P : 1) * N;
-  return kReduceThreads + (aur ? (scratch + N + table_f2(N) + 1) / 2 : 0);
+  return kReduceThreads + (aur ? afc_ys_f4(N, P) + (scratch + N + table_f2(N) + 1) / 2 : 0);
 }
 
 // Canceller reduce CTAs: stage the DftPlan tables and the smoothed power --
@@ -645,7 +648,7 @@ __host__ __device__ inline size_t reduce_smem_f4(int N, bool aur, int P = 1) {
 template <typename Team>
 __device__ __forceinline__ void reduce_prefetch(const BlockArgs& a, int b, float4* rsm, Team tm) {
   if (b < a.red_syn_ctas) return;
-  float2* z = reinterpret_cast<float2*>(rsm + kReduceThreads);
+  float2* z = reinterpret_cast<float2*>(rsm + kReduceThreads + afc_ys_f4(a.N, a.P));
   float2* tw = z + (a.N <= 1024 ? (size_t)a.P : 1) * a.N;
   float2* split = tw + a.N / 2;
   float2* pws = split + a.N / 2 + 1;
@@ -654,10 +657,21 @@ __device__ __forceinline__ void reduce_prefetch(const BlockArgs& a, int b, float
     for (int jj = tm.tid(); jj < a.N; jj += tm.size()) pws[jj] = a.pw[jj];
 }
 
+// The plan record (first partial, count) of the tile reduce CTA b sums: a
+// static table, so k_reduce loads it before waiting for k_back.
+__device__ __forceinline__ int4 reduce_tile_info(const BlockArgs& a, int b) {
+  const bool afc = b >= a.red_syn_ctas;
+  const int cpt = afc ? a.red_afc_cpt : a.red_syn_cpt;
+  const int tile = (afc ? b - a.red_syn_ctas : b) / cpt;
+  return a.tinfo[afc ? a.n_syn_tiles + tile : tile];
+}
+
 // Reduce CTA b of block n (see k_reduce) with a team of kReduceThreads
-// threads; s_last: shared int. The partials must be complete and visible.
+// threads; ti = reduce_tile_info(a, b); s_last: shared int. The partials
+// must be complete and visible.
 template <typename Team>
-__device__ void reduce_part(const BlockArgs& a, int b, uint32_t n, float4* rsm, int* s_last, Team tm) {
+__device__ void reduce_part(const BlockArgs& a, int b, uint32_t n, float4* rsm, int* s_last, Team tm,
+                            const int4 ti) {
   const int CT = a.CT, NF = a.NF;
   const int tid = tm.tid();
   const bool afc = b >= a.red_syn_ctas;
@@ -667,7 +681,6 @@ __device__ void reduce_part(const BlockArgs& a, int b, uint32_t n, float4* rsm, 
   const int tile = bb / cpt, part = bb - tile * cpt;
   const int epc = (E + cpt - 1) / cpt;
   const int e0 = part * epc, e1 = min(E, e0 + epc);
-  const int4 ti = a.tinfo[afc ? a.n_syn_tiles + tile : tile];
   const float4* src = (afc ? a.part_afc : a.part_syn) + (size_t)ti.x * E;
   const int ne = e1 - e0;
   const int sub = max(1, kReduceThreads / max(ne, 1));
@@ -677,7 +690,7 @@ __device__ void reduce_part(const BlockArgs& a, int b, uint32_t n, float4* rsm, 
   if (ne > 0 && j < sub) {
     const float4* p = src + e0 + el;
     const int i0 = j * per, i1 = min(ti.y, i0 + per);
-    for (int i = i0; i < i1; i += 16) {
+    for (int i = i0; i < i1; i += 16) {  // 16 loads in flight, summed in slot order
       float4 t[16];
 #pragma unroll
       for (int u = 0; u < 16; ++u)
@@ -687,6 +700,10 @@ __device__ void reduce_part(const BlockArgs& a, int b, uint32_t n, float4* rsm, 
         if (i + u < i1) v = (i + u == i0) ? t[u] : f4add(v, t[u]);
     }
   }
+  // single: the whole canceller sum in this CTA (one column tile, few
+  // partials): Yhat stays in shared memory, no ticket, no global round trips
+  const bool single = afc && a.red_afc_ctas == 1 && afc_ys_f4(a.N, a.P) > 0;
+  float4* ys = rsm + kReduceThreads;
   rsm[tid] = v;
   tm.sync();
   if (tid < ne) {
@@ -694,28 +711,41 @@ __device__ void reduce_part(const BlockArgs& a, int b, uint32_t n, float4* rsm, 
     for (int jj = 1; jj < sub; ++jj) w = f4add(w, rsm[jj * ne + tid]);
     const int e = e0 + tid;
     const int r = e / CT, col = e - r * CT;
-    if (afc) {
+    if (single) {
+      ys[(size_t)r * NF + col] = w;
+    } else if (afc) {
       __stcg(a.yhat + (size_t)r * NF + tile * CT + col, w);
     } else {
       const int CTn = a.CTn, g = tile / CTn, c = tile - g * CTn;
       __stcg(a.S + (size_t)(g * a.LTr + r) * NF + c * CT + col, w);
     }
   }
-  __threadfence();
+  if (!single) __threadfence();
   tm.sync();
   if (!afc) return;
-  if (tid == 0) {
-    unsigned* t = a.tick + 0;
-    *s_last = atomicAdd(t, 1u) == (unsigned)a.red_afc_ctas - 1u;
-    if (*s_last) *t = 0u;
+  if (!single) {
+    if (tid == 0) {
+      unsigned* t = a.tick + 0;
+      *s_last = atomicAdd(t, 1u) == (unsigned)a.red_afc_ctas - 1u;
+      if (*s_last) *t = 0u;
+    }
+    tm.sync();
+    if (!*s_last) return;
+    __threadfence();
   }
-  tm.sync();
-  if (!*s_last) return;
-  __threadfence();
+  const float4* yh = single ? ys : a.yhat;
+  auto stamp = [&](int id) {
+    if (a.trace && tid == 0) {
+      const unsigned long long now = globaltimer();
+      atomicMin(&a.trace[((n % kTraceBlocks) * kTraceKernels + id) * 2], now);
+      atomicMax(&a.trace[((n % kTraceBlocks) * kTraceKernels + id) * 2 + 1], now);
+    }
+  };
+  stamp(TR_AFC_SUMMED);
   // the canceller of block n is complete: f^ for block n+1
   const int N = a.N, P = a.P;
   const bool sharded = a.G > 1;
-  float2* z = reinterpret_cast<float2*>(rsm + kReduceThreads);
+  float2* z = reinterpret_cast<float2*>(rsm + kReduceThreads + afc_ys_f4(N, P));
   float2* tw = z + (N <= 1024 ? (size_t)P : 1) * N;
   float2* split = tw + N / 2;
   float2* pws = split + N / 2 + 1;
@@ -730,7 +760,7 @@ __device__ void reduce_part(const BlockArgs& a, int b, uint32_t n, float4* rsm, 
       fh[i] = x;
       if (!sharded) fhh[i] = x;
     };
-    const float2* yp = reinterpret_cast<const float2*>(a.yhat + (size_t)p * NF);
+    const float2* yp = reinterpret_cast<const float2*>(yh + (size_t)p * NF);
     if (!warps) {
       irfft_packed_tail(yp, z, N, a.logN, tw, split, st, tm);
     } else if (tid / 32 == p) {
@@ -738,11 +768,12 @@ __device__ void reduce_part(const BlockArgs& a, int b, uint32_t n, float4* rsm, 
     }
   }
   if (warps) tm.sync();
+  stamp(TR_AFC_C2R);
   if (a.nlms) {
-    const float2* sum = reinterpret_cast<const float2*>(a.yhat + (size_t)P * NF);
+    const float2* sum = reinterpret_cast<const float2*>(yh + (size_t)P * NF);
     const float oml = __fsub_rn(1.0f, a.lambda);
     for (int jj = tid; jj < N; jj += tm.size()) {
-      const float2 x = __ldcg(sum + jj);
+      const float2 x = single ? sum[jj] : __ldcg(sum + jj);
       if (sharded) {  // partial power of this shard's loudspeakers
         reinterpret_cast<float2*>(a.xmine + (size_t)P * N)[jj] = x;
         continue;
@@ -780,10 +811,12 @@ __global__ void __launch_bounds__(kReduceThreads) k_reduce(const __grid_constant
   __shared__ int s_last;
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   reduce_prefetch(a, blockIdx.x, rsm, Cta());
-  griddep_wait();  // k_back's partials
+  // neither is written by k_back: load them before waiting for it
   const uint32_t n = a.st->block;
+  const int4 ti = reduce_tile_info(a, blockIdx.x);
+  griddep_wait();  // k_back's partials
   trace_begin(a, TR_REDUCE, n);
-  reduce_part(a, blockIdx.x, n, rsm, &s_last, Cta());
+  reduce_part(a, blockIdx.x, n, rsm, &s_last, Cta(), ti);
   trace_end(a, TR_REDUCE, n);
   // retire: advance the block (sharded: k_afc_finish does)
   if (threadIdx.x == 0) {
