@@ -485,12 +485,14 @@ void plan_back(aura_b200_engine* e, BlockArgs& a) {
   const long long U = e->aur ? (long long)e->L * e->KF : 0;
   if (T > INT32_MAX / 2 || U > INT32_MAX / 2) fail(AURA_B200_E_INVALID_ARGUMENT, "filters too long");
   // stage sizes: ~32 KB per stage, a whole number of tap phases
-  int target_kb = 32;
+  // ~46 KB synthesis stages, four in the ring: the single producer lane's
+  // per-stage cost is what bounds an SM's stream (profiles/r1s5_stream.md),
+  // so fewer, larger stages (sp need not be a multiple of the 8 tap phases)
+  int target_kb = 46;
   if (const char* f = std::getenv("AURA_B200_STAGE_KB")) target_kb = std::max(4, std::atoi(f));
   const int target_f4 = target_kb * 1024 / 16;
   const int syn_row = (LT + XL) * CT;
-  a.sp = std::getenv("AURA_B200_STAGE_KB") ? std::max(PH, target_f4 / syn_row)
-                                            : PH * std::max(1, target_f4 / (PH * syn_row));
+  a.sp = std::max(PH, target_f4 / syn_row);
   const int afc_row = (P + 1) * CT;
   a.spa = PH * std::max(1, target_f4 / (PH * std::max(afc_row, 1)));
   long long slot = 0;
@@ -639,8 +641,11 @@ void plan_back(aura_b200_engine* e, BlockArgs& a) {
         // one column tile: few enough partials that one k_reduce CTA sums
         // them in one round of loads and runs the c2r from shared memory
         // (reduce_part's single-CTA path; cpt_for below gives 1)
+        // (only while the items stay short enough to balance: <= ~1.5 MB)
         const long long cap = afc_single_cap(P + (e->args.nlms ? 1 : 0), CT);
-        if (cap > 0) per = std::max(per, ((U + cap - 1) / cap + a.spa - 1) / a.spa * a.spa);
+        const double unit_b = (double)(P * (e->args.nlms ? 2 : 1) + 1) * CT * 16.0;
+        const long long per1 = cap > 0 ? ((U + cap - 1) / cap + a.spa - 1) / a.spa * a.spa : 0;
+        if (cap > 0 && (double)per1 * unit_b <= 1.5e6) per = std::max(per, per1);
       }
       for (int c = 0; c < CTn; ++c)
         for (long long b = 0; b < U; b += per) afc.emplace_back(c, b, std::min<long long>(U, b + per));
