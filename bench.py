@@ -429,7 +429,14 @@ def run_b200_arm(args, cfg, rank, world, local_rank):
                      "frac_of_read_probe": achieved / READ_PROBE_GBS,
                      "bytes_per_launch": mac_bytes, "avg_launch_us": mac_us,
                      "timing": "CUDA events around 20 single launches of the kernel, back to back",
-                     "in_graph": in_graph},
+                     "in_graph": in_graph,
+                     # algorithmic bytes include the canceller's W read/write and
+                     # delay line, which stay L2-resident (evict-last) when they
+                     # fit: what HBM actually moved, from the ncu capture
+                     "dram": ({"GBps": traffic / (mac_us * 1e-6) / 1e9,
+                               "frac": traffic / (mac_us * 1e-6) / 1e9 / peak,
+                               "frac_of_read_probe": traffic / (mac_us * 1e-6) / 1e9 / READ_PROBE_GBS}
+                              if traffic and mac_us else None)},
         "phases_us_serial": {k: v[0] for k, v in phases.items()},
         "timeline_us": timeline,
         "phase_bytes": {k: v[1] for k, v in phases.items()},
