@@ -30,7 +30,7 @@ __all__ = [
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libaura_b200.so")
+LIB_PATH = os.environ.get("AURA_B200_LIB") or os.path.join(HERE, "libaura_b200.so")  # override: A/B experiments only
 
 
 class ErrorCode(enum.IntEnum):
