@@ -239,12 +239,12 @@ const char* aura_b200_phase_name(const aura_b200_engine* e, int phase);
  * power are restored afterwards. */
 int aura_b200_time_phase(aura_b200_engine* e, int phase, size_t reps, float* avg_us);
 /* Timeline of `blocks` (<= 64) back-to-back device-resident blocks from
- * %globaltimer stamps taken inside the kernels: out[(i*10 + k)*2 + {0,1}] =
+ * %globaltimer stamps taken inside the kernels: out[(i*11 + k)*2 + {0,1}] =
  * first / last stamp (us, relative to block i's front start) of event k in
  * order k_front, k_back_head, k_back, k_reduce, canceller done, k_afc_finish,
- * output published, canceller sums in, f^ written; slot 9 = {the next
- * block's front start, 0}. -1 when the event did not occur. Shows launch
- * gaps and overlap. */
+ * output published, canceller sums in, f^ written, input spectra pushed;
+ * slot 10 = {the next block's front start, 0}. -1 when the event did not
+ * occur. Shows launch gaps and overlap. */
 int aura_b200_trace_blocks(aura_b200_engine* e, size_t blocks, double* out);
 /* Diagnostics (not in the reference): per-segment / per-CTA timeline of the
  * streaming kernel k_back for the last of `blocks` blocks, us from the

@@ -313,8 +313,8 @@ class _Engine:
         _check(lib().aura_b200_reset(self._h))
 
     TRACE_KERNELS = ("k_front", "k_back_head", "k_back", "k_reduce", "afc_done", "k_afc_finish",
-                     "output", "afc_summed", "afc_c2r")
-    _TRACE_SLOTS = 10  # kTraceKernels: the last slot is the next block's front start
+                     "output", "afc_summed", "afc_c2r", "front_x")
+    _TRACE_SLOTS = 11  # kTraceKernels: the last slot is the next block's front start
 
     def trace_blocks(self, blocks: int = 32):
         """Per-kernel [start, end] (us from the block's front start) of

@@ -55,11 +55,12 @@ struct DevState {
 // Optional timeline trace (%globaltimer, ns): per traced block slot and
 // kernel, the earliest CTA start and the latest CTA end.
 constexpr int kTraceBlocks = 64;
-constexpr int kTraceKernels = 10;  // the last slot carries the next block's front start (cycle)
+constexpr int kTraceKernels = 11;  // the last slot carries the next block's front start (cycle)
 enum TraceId {
   TR_FRONT = 0, TR_BACK_HEAD, TR_BACK, TR_REDUCE, TR_AFC_DONE, TR_AFC_FINISH, TR_OUTPUT,
   TR_AFC_SUMMED,  // k_reduce: the canceller's split-K sums are in (the CTA that runs the c2r)
-  TR_AFC_C2R      // k_reduce: f^ written (before the power update)
+  TR_AFC_C2R,     // k_reduce: f^ written (before the power update)
+  TR_FRONT_X      // k_front: this block's input spectra computed and pushed (per front CTA)
 };
 
 // Loudspeaker-channel sharding: at most kMaxShards engines
@@ -520,6 +521,14 @@ __global__ void __launch_bounds__(kFrontThreads) k_front(BlockArgs a) {
   // front_hold 2: k_back's producers wait until every front CTA has its
   // inputs in (its loads are the part a saturated memory system slows down)
   auto inputs_in = [&] {
+    if (a.trace) {
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const unsigned long long now = globaltimer();
+        atomicMin(&a.trace[((n % kTraceBlocks) * kTraceKernels + TR_FRONT_X) * 2], now);
+        atomicMax(&a.trace[((n % kTraceBlocks) * kTraceKernels + TR_FRONT_X) * 2 + 1], now);
+      }
+    }
     if (a.front_head && a.front_hold == 2) {
       __syncthreads();
       if (threadIdx.x == 0) {
