@@ -295,6 +295,27 @@ __host__ __device__ inline size_t front_work_f2(int N, int Qs) { return (size_t)
 // on_x() runs on the whole team once the leader has pushed the input
 // spectra. smem: front_work_f2 float2, then the tables (a.smem_tables) and
 // the staged S/H0 (a.front_pre).
+// Issue every load of a window before its stores: a store in between may
+// alias the later loads as far as the compiler knows, which serialises the
+// load rounds -- one dependent memory round trip per round (profiles/
+// r1s5_stream.md: +2.5 us on a warp front). U rounds per batch.
+template <int U, typename Ld, typename St>
+__device__ __forceinline__ void batched(int tid, int nt, int n, Ld ld, St st) {
+  for (int i0 = tid; i0 < n; i0 += U * nt) {
+    decltype(ld(0)) v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = i0 + u * nt;
+      if (i < n) v[u] = ld(i);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = i0 + u * nt;
+      if (i < n) st(i, v[u]);
+    }
+  }
+}
+
 struct NoHook {
   __device__ __forceinline__ void operator()() const {}
 };
@@ -330,13 +351,15 @@ __device__ void front_body(const BlockArgs& a, uint32_t n, int c0, int c1, float
     for (int q = 0; q < Qs; ++q) {
       const float* inq = in + (size_t)q * N;
       const float* prev = prev_in + (size_t)q * N;
-      for (int i = tid; i < N; i += nt) {
-        float v = inq[i];
-        if (a.is_aur) v = __fsub_rn(__fmul_rn(a.gain, v), a.fhat[(size_t)q * N + i]);
-        if (leader) cur_out[(size_t)q * N + i] = v;
-        wa[i] = prev[i];
-        wa[N + i] = v;
-      }
+      const float* fq = a.fhat + (size_t)q * N;
+      batched<4>(tid, nt, N,
+                 [&](int i) { return make_float3(inq[i], a.is_aur ? fq[i] : 0.f, prev[i]); },
+                 [&](int i, float3 x) {
+                   const float v = a.is_aur ? __fsub_rn(__fmul_rn(a.gain, x.x), x.y) : x.x;
+                   if (leader) cur_out[(size_t)q * N + i] = v;
+                   wa[i] = x.z;
+                   wa[N + i] = v;
+                 });
       tm.sync();
       rfft_packed(wa, z, Xs + (size_t)q * N, N, a.logN, tw, split, tm);
       if (leader) push_tiled(a, a.X, q, a.K, (int)(n % (uint32_t)a.K), Xs + (size_t)q * N, tm);
@@ -349,10 +372,11 @@ __device__ void front_body(const BlockArgs& a, uint32_t n, int c0, int c1, float
     if (elem) {
       const float* inl = in + (size_t)l * N;
       float* prev = a.prev_in + (size_t)l * N;
-      for (int i = tid; i < N; i += nt) {
-        wa[i] = prev[i];
-        wa[N + i] = inl[i];
-      }
+      batched<4>(tid, nt, N, [&](int i) { return make_float2(prev[i], inl[i]); },
+                 [&](int i, float2 x) {
+                   wa[i] = x.x;
+                   wa[N + i] = x.y;
+                 });
       tm.sync();
       for (int i = tid; i < N; i += nt) prev[i] = wa[N + i];
       rfft_packed(wa, z, Xs, N, a.logN, tw, split, tm);
@@ -390,10 +414,11 @@ __device__ void head_channels(const BlockArgs& a, uint32_t n, int c0, int c1, fl
   for (int l = c0; l < c1; ++l) {
     float* prev = a.prev_spk + (size_t)l * N;
     const float* spk = a.spk + (size_t)l * N;
-    for (int i = tm.tid(); i < N; i += tm.size()) {
-      wa[i] = prev[i];
-      wa[N + i] = spk[i];
-    }
+    batched<4>(tm.tid(), tm.size(), N, [&](int i) { return make_float2(prev[i], spk[i]); },
+               [&](int i, float2 x) {
+                 wa[i] = x.x;
+                 wa[N + i] = x.y;
+               });
     tm.sync();
     for (int i = tm.tid(); i < N; i += tm.size()) prev[i] = wa[N + i];
     rfft_packed(wa, z, sp, N, a.logN, tw, split, tm);
@@ -409,10 +434,12 @@ __device__ void error_spectrum(const BlockArgs& a, int p, const float* in, float
                                const float2* split, Team tm) {
   const int N = a.N;
   float* wa = reinterpret_cast<float*>(z + N);
-  for (int i = tm.tid(); i < N; i += tm.size()) {
-    wa[i] = 0.0f;
-    wa[N + i] = __fsub_rn(__fmul_rn(a.gain, in[(size_t)p * N + i]), a.fhat[(size_t)p * N + i]);
-  }
+  batched<4>(tm.tid(), tm.size(), N,
+             [&](int i) { return make_float2(in[(size_t)p * N + i], a.fhat[(size_t)p * N + i]); },
+             [&](int i, float2 x) {
+               wa[i] = 0.0f;
+               wa[N + i] = __fsub_rn(__fmul_rn(a.gain, x.x), x.y);
+             });
   tm.sync();
   rfft_packed(wa, z, reinterpret_cast<float2*>(a.E + (size_t)p * a.NF), N, a.logN, tw, split, tm);
 }
@@ -458,21 +485,33 @@ __device__ void front_warps_body(const BlockArgs& a, uint32_t n, int c0, int c1,
     for (int j = lane; j < N; j += 32) pS[j] = Sl[j];
     for (int j = lane; j < Qs * N; j += 32) pS[N + j] = H0[j];
   }
-  // ---- stage 1 for the shared inputs (broadcast / mimo), whole CTA
-  for (int q = 0; q < Qs; ++q) {
-    const float* inq = in + (size_t)q * N;
-    const float* prev = prev_in + (size_t)q * N;
-    for (int i = threadIdx.x; i < N; i += blockDim.x) {
-      float v = inq[i];
-      if (a.is_aur) v = __fsub_rn(__fmul_rn(a.gain, v), a.fhat[(size_t)q * N + i]);
-      if (leader) cur_out[(size_t)q * N + i] = v;
-      wa[i] = prev[i];
-      wa[N + i] = v;
+  // ---- stage 1 for the shared inputs (broadcast / mimo): input q's window,
+  // r2c and FDL push on warp q in its own area, warp-synchronous (the same
+  // operations as the CTA transform, so the same bits), one CTA barrier
+  // after instead of one per butterfly stage
+  (void)z;
+  (void)wa;
+  __syncthreads();  // the staged tables
+  if (w < W) {
+    for (int q = w; q < Qs; q += W) {
+      const float* inq = in + (size_t)q * N;
+      const float* prev = prev_in + (size_t)q * N;
+      float* wq = reinterpret_cast<float*>(acc);  // 2N floats
+      const float* fq = a.fhat + (size_t)q * N;
+      batched<4>(lane, 32, N,
+                 [&](int i) { return make_float3(inq[i], a.is_aur ? fq[i] : 0.f, prev[i]); },
+                 [&](int i, float3 x) {
+                   const float v = a.is_aur ? __fsub_rn(__fmul_rn(a.gain, x.x), x.y) : x.x;
+                   if (leader) cur_out[(size_t)q * N + i] = v;
+                   wq[i] = x.z;
+                   wq[N + i] = v;
+                 });
+      __syncwarp();
+      rfft_packed(wq, wz, Xs + (size_t)q * N, N, a.logN, tw, split, wt);
+      if (leader) push_tiled(a, a.X, q, a.K, (int)(n % (uint32_t)a.K), Xs + (size_t)q * N, wt);
     }
-    __syncthreads();
-    rfft_packed(wa, z, Xs + (size_t)q * N, N, a.logN, tw, split, cta);
-    if (leader) push_tiled(a, a.X, q, a.K, (int)(n % (uint32_t)a.K), Xs + (size_t)q * N, cta);
   }
+  __syncthreads();  // every input spectrum
   on_x();
   // ---- per output channel (one warp each): Y = S + sum_q X_q H_q[0], c2r
   if (w < W) {
