@@ -431,8 +431,8 @@ def run_b200_arm(args, cfg, rank, world, local_rank):
                      "timing": "CUDA events around 20 single launches of the kernel, back to back",
                      "in_graph": in_graph,
                      # algorithmic bytes include the canceller's W read/write and
-                     # delay line, which stay L2-resident (evict-last) when they
-                     # fit: what HBM actually moved, from the ncu capture
+                     # delay line, mostly L2 hits in the steady state: what HBM
+                     # actually moved, from the (warm) ncu capture
                      "dram": ({"GBps": traffic / (mac_us * 1e-6) / 1e9,
                                "frac": traffic / (mac_us * 1e-6) / 1e9 / peak,
                                "frac_of_read_probe": traffic / (mac_us * 1e-6) / 1e9 / READ_PROBE_GBS}

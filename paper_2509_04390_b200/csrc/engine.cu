@@ -515,12 +515,15 @@ void plan_back(aura_b200_engine* e, BlockArgs& a) {
   const double foot = 8.0 * N * ((double)e->L * Qh * e->K + (double)e->Qx * e->K +
                                  (double)P * U + (double)(e->aur ? e->L * (e->KF + 1) : 0));
   a.h_in_l2 = foot < 80e6 ? 1 : 0;
-  // the canceller's working set (W read-modify-write, its delay lines, the
-  // input FDL) is re-touched every block: pin it in L2 with evict_last so the
-  // canceller phase leaves HBM to the synthesis stream
+  // Optionally pin the canceller's W (read-modify-write every block) in L2
+  // with evict-last hints when its working set (W, its delay line, the input
+  // FDL) is under AURA_B200_W_L2_MB. Off by default: measured at c3 it moves
+  // ~25 MB per block off HBM but k_back gets ~1 us SLOWER (45.3 vs 46.2 us,
+  // three A/B runs; profiles/r1s5_stream.md) -- the canceller units are not
+  // HBM-bound once they run interleaved with the synthesis stream.
   const double afc_foot = 8.0 * N * ((double)P * U + (double)(e->aur ? e->L * (e->KF + 1) : 0) +
                                      (double)e->Qx * e->K);
-  double w_l2_mb = 80.0;
+  double w_l2_mb = 0.0;
   if (const char* f = std::getenv("AURA_B200_W_L2_MB")) w_l2_mb = std::atof(f);
   a.w_in_l2 = (P > 0 && afc_foot < w_l2_mb * 1e6) ? 1 : 0;
   a.dbg = 0;
