@@ -558,10 +558,13 @@ void plan_back(aura_b200_engine* e, BlockArgs& a) {
   // queue items: ~12 per CTA in the last 15%, at least two stages (keeps
   // the tail short and the partial count -- k_reduce's input -- small at c5
   // sizes); ~3 per CTA in the middle part
+  long long nq_per = 12, nb_per = 3;  // queue items per CTA: last part, middle part
+  if (const char* f = std::getenv("AURA_B200_QITEMS")) nq_per = std::max(1, std::atoi(f));
+  if (const char* f = std::getenv("AURA_B200_BITEMS")) nb_per = std::max(1, std::atoi(f));
   const long long qtaps = (T - TB) * tiles;
-  const long long CQ = std::max<long long>(2LL * a.sp, (qtaps / (12LL * ctas) + a.sp - 1) / a.sp * a.sp);
+  const long long CQ = std::max<long long>(2LL * a.sp, (qtaps / (nq_per * ctas) + a.sp - 1) / a.sp * a.sp);
   const long long btaps = (TB - TA) * tiles;
-  const long long CB = std::max<long long>(CQ, (btaps / (3LL * ctas) + a.sp - 1) / a.sp * a.sp);
+  const long long CB = std::max<long long>(CQ, (btaps / (nb_per * ctas) + a.sp - 1) / a.sp * a.sp);
   std::vector<int4> chunks;
   std::vector<int> item_off(ctas + 1, 0);
   std::vector<std::vector<std::pair<int, int>>> at(tiles + CTn);  // per tile: (b, item)
@@ -656,7 +659,9 @@ void plan_back(aura_b200_engine* e, BlockArgs& a) {
     // merge: canceller items evenly through the middle synthesis items (the
     // first middle items go first: the canceller waits for the head)
     const size_t nm = mid.size(), na = afc.size();
-    const size_t span = nm * 2 / 3;  // over the first two thirds: the long items end well before the tail
+    double span_f = 2.0 / 3.0;  // over the first two thirds: the long items end well before the tail
+    if (const char* f = std::getenv("AURA_B200_AFC_SPAN")) span_f = std::min(1.0, std::max(0.05, std::atof(f)));
+    const size_t span = (size_t)((double)nm * span_f);
     size_t im = 0;
     for (size_t j = 0; j < na; ++j) {
       const size_t upto = span * (2 * j + 1) / (2 * na);  // middle items before canceller item j
