@@ -178,4 +178,144 @@ __device__ void irfft_packed_tail(const float2* spec, float2* z, int N,
   tm.sync();
 }
 
+// ------------------------------------------------ register-resident warp FFTs
+// One warp, M = 32 * PER points, element i in lane i % 32, register i / 32.
+// The SAME radix-2 DIT butterflies as fft_dit_smem (pairs (i0, i0 + h), twiddle
+// tw[(i0 mod h) * M / 2h], u + w v and u - w v with w v = cmul_rn(v, w), each
+// product rounded), so the same bits; partners h < 32 apart are exchanged with
+// shuffles, no shared memory and no barriers between stages. Measured
+// (tools/c2r_probe.cu): the shared-memory warp transform of N = 64 takes ~2460
+// cycles, the latency of the LDS -> math -> STS -> __syncwarp chain per stage.
+template <int PER>
+__device__ __forceinline__ void fft_dit_warp(float2 (&v)[PER], const float2* __restrict__ tw, int lane) {
+  constexpr int M = 32 * PER;
+#pragma unroll
+  for (int h = 1; h < M; h <<= 1) {
+    const int stride = M / (2 * h);
+    float2 nv[PER];
+#pragma unroll
+    for (int r = 0; r < PER; ++r) {
+      const int i = lane + 32 * r;
+      const float2 x = v[r];
+      float2 y;
+      if (h < 32) {
+        y.x = __shfl_xor_sync(0xffffffffu, x.x, h);
+        y.y = __shfl_xor_sync(0xffffffffu, x.y, h);
+      } else {
+        y = v[r ^ (h >> 5)];
+      }
+      const bool lo = (i & h) == 0;
+      const float2 w = tw[(i & (h - 1)) * stride];
+      const float2 wv = cmul_rn(lo ? y : x, w);
+      const float2 u = lo ? x : y;
+      nv[r] = lo ? cadd_rn(u, wv) : csub_rn(u, wv);
+    }
+#pragma unroll
+    for (int r = 0; r < PER; ++r) v[r] = nv[r];
+  }
+}
+
+// irfft_packed_tail on one warp with the transform in registers (N = 32 PER).
+template <int PER, typename Store>
+__device__ __forceinline__ void irfft_packed_tail_reg(const float2* spec, int logN, const float2* __restrict__ tw,
+                                                      const float2* __restrict__ split, Store store) {
+  constexpr int N = 32 * PER, H = N / 2;
+  const int lane = threadIdx.x & 31;
+  float2 v[PER];
+  float4 sv[PER];
+#pragma unroll
+  for (int r = 0; r < PER; ++r) {  // every load first
+    const int k = bitrev(lane + 32 * r, logN);
+    const float2 s0 = spec[k], s1 = spec[(N - k) & (N - 1)];
+    sv[r] = make_float4(s0.x, s0.y, s1.x, s1.y);
+  }
+#pragma unroll
+  for (int r = 0; r < PER; ++r) {
+    const int k = bitrev(lane + 32 * r, logN);
+    float2 zk;
+    if (k == 0) {
+      const float xe = __fmul_rn(0.5f, __fadd_rn(sv[r].x, sv[r].y));
+      const float xo = __fmul_rn(0.5f, __fsub_rn(sv[r].x, sv[r].y));
+      zk = make_float2(xe, -xo);
+    } else {
+      const float2 a = make_float2(sv[r].x, sv[r].y);
+      const float2 b = conjf2(make_float2(sv[r].z, sv[r].w));
+      const float2 even = half_of(cadd_rn(a, b));
+      float2 tw2;
+      if (k <= H) {
+        tw2 = split[k];
+      } else {
+        const float2 q = conjf2(split[N - k]);
+        tw2 = make_float2(-q.x, -q.y);
+      }
+      const float2 odd = cmul_rn(conjf2(tw2), half_of(csub_rn(a, b)));
+      const float2 iodd = cmul_rn(make_float2(0.0f, 1.0f), odd);
+      zk = conjf2(cadd_rn(even, iodd));
+    }
+    v[r] = zk;
+  }
+  fft_dit_warp<PER>(v, tw, lane);
+  const float scale = 1.0f / (float)N;
+#pragma unroll
+  for (int r = PER / 2; r < PER; ++r) {  // samples N .. 2N-1 are z[m], m in [N/2, N)
+    const int m = lane + 32 * r - H;
+    store(2 * m, __fmul_rn(v[r].x, scale));
+    store(2 * m + 1, __fmul_rn(-v[r].y, scale));
+  }
+  __syncwarp();  // the caller may overwrite `spec` next
+}
+
+// rfft_packed on one warp with the transform in registers (N = 32 PER); z:
+// N float2 shared scratch for the split step. Ends with __syncwarp.
+template <int PER>
+__device__ __forceinline__ void rfft_packed_reg(const float* win, float2* z, float2* spec, int logN,
+                                                const float2* __restrict__ tw, const float2* __restrict__ split) {
+  constexpr int N = 32 * PER, H = N / 2;
+  const int lane = threadIdx.x & 31;
+  float2 v[PER];
+#pragma unroll
+  for (int r = 0; r < PER; ++r) {
+    const int m = bitrev(lane + 32 * r, logN);
+    v[r] = make_float2(win[2 * m], win[2 * m + 1]);
+  }
+  fft_dit_warp<PER>(v, tw, lane);
+#pragma unroll
+  for (int r = 0; r < PER; ++r) z[lane + 32 * r] = v[r];
+  __syncwarp();
+  for (int k = lane; k <= H; k += 32) {
+    if (k == 0) {
+      const float2 z0 = z[0];
+      spec[0] = make_float2(__fadd_rn(z0.x, z0.y), __fsub_rn(z0.x, z0.y));
+      continue;
+    }
+    const float2 a = z[k];
+    const float2 b = conjf2(z[N - k]);
+    const float2 even = half_of(cadd_rn(a, b));
+    const float2 d = csub_rn(a, b);
+    const float2 odd = cmul_rn(make_float2(0.0f, -0.5f), d);
+    const float2 rot = cmul_rn(split[k], odd);
+    const float2 lo = cadd_rn(even, rot);
+    const float2 hi = conjf2(csub_rn(even, rot));
+    if (k != H) spec[k] = lo;  // at k = N/2 the reference's second store wins
+    spec[N - k] = hi;
+  }
+  __syncwarp();
+}
+
+// One warp's c2r / r2c: registers for N = 64 and 128, shared memory otherwise.
+template <typename Store>
+__device__ __forceinline__ void irfft_warp_any(const float2* spec, float2* z, int N, int logN,
+                                               const float2* __restrict__ tw, const float2* __restrict__ split,
+                                               Store store) {
+  if (N == 64) irfft_packed_tail_reg<2>(spec, logN, tw, split, store);
+  else if (N == 128) irfft_packed_tail_reg<4>(spec, logN, tw, split, store);
+  else irfft_packed_tail(spec, z, N, logN, tw, split, store, Warp());
+}
+__device__ __forceinline__ void rfft_warp_any(const float* win, float2* z, float2* spec, int N, int logN,
+                                              const float2* __restrict__ tw, const float2* __restrict__ split) {
+  if (N == 64) rfft_packed_reg<2>(win, z, spec, logN, tw, split);
+  else if (N == 128) rfft_packed_reg<4>(win, z, spec, logN, tw, split);
+  else rfft_packed(win, z, spec, N, logN, tw, split, Warp());
+}
+
 }  // namespace aura_b200

@@ -35,6 +35,8 @@
 
 #include <cooperative_groups.h>
 
+#include <type_traits>
+
 #include "fft.cuh"
 
 namespace aura_b200 {
@@ -421,7 +423,8 @@ __device__ void head_channels(const BlockArgs& a, uint32_t n, int c0, int c1, fl
                });
     tm.sync();
     for (int i = tm.tid(); i < N; i += tm.size()) prev[i] = wa[N + i];
-    rfft_packed(wa, z, sp, N, a.logN, tw, split, tm);
+    if constexpr (std::is_same<Team, Warp>::value) rfft_warp_any(wa, z, sp, N, a.logN, tw, split);
+    else rfft_packed(wa, z, sp, N, a.logN, tw, split, tm);
     push_tiled(a, a.XA, l, a.KF + 1, (int)(n % (uint32_t)(a.KF + 1)), sp, tm);
     tm.sync();
   }
@@ -507,7 +510,7 @@ __device__ void front_warps_body(const BlockArgs& a, uint32_t n, int c0, int c1,
                    wq[N + i] = v;
                  });
       __syncwarp();
-      rfft_packed(wq, wz, Xs + (size_t)q * N, N, a.logN, tw, split, wt);
+      rfft_warp_any(wq, wz, Xs + (size_t)q * N, N, a.logN, tw, split);
       if (leader) push_tiled(a, a.X, q, a.K, (int)(n % (uint32_t)a.K), Xs + (size_t)q * N, wt);
     }
   }
@@ -528,10 +531,10 @@ __device__ void front_warps_body(const BlockArgs& a, uint32_t n, int c0, int c1,
       float* out = a.out + (size_t)l * N;
       float* sp = a.spk + (size_t)l * N;
       const bool keep = a.is_aur;
-      irfft_packed_tail(acc, wz, N, a.logN, tw, split, [&](int i, float v) {
+      irfft_warp_any(acc, wz, N, a.logN, tw, split, [&](int i, float v) {
         out[i] = v;
         if (keep) sp[i] = v;
-      }, wt);
+      });
     }
   }
 }

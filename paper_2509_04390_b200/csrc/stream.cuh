@@ -764,7 +764,7 @@ __device__ void reduce_part(const BlockArgs& a, int b, uint32_t n, float4* rsm, 
     if (!warps) {
       irfft_packed_tail(yp, z, N, a.logN, tw, split, st, tm);
     } else if (tid / 32 == p) {
-      irfft_packed_tail(yp, z + (size_t)p * N, N, a.logN, tw, split, st, Warp());
+      irfft_warp_any(yp, z + (size_t)p * N, N, a.logN, tw, split, st);
     }
   }
   if (warps) tm.sync();
