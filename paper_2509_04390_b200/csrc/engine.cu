@@ -661,10 +661,17 @@ void plan_back(aura_b200_engine* e, BlockArgs& a) {
     const size_t nm = mid.size(), na = afc.size();
     double span_f = 2.0 / 3.0;  // over the first two thirds: the long items end well before the tail
     if (const char* f = std::getenv("AURA_B200_AFC_SPAN")) span_f = std::min(1.0, std::max(0.05, std::atof(f)));
-    const size_t span = (size_t)((double)nm * span_f);
+    // share of the middle items before the first canceller item: the CTAs
+    // that reach the queue first (at the end of the static slice, ~11 us into
+    // a c3 block) would otherwise wait for the front half's canceller head
+    // (c3: k_back -0.6 us; c4 unchanged)
+    double start_f = 0.3;
+    if (const char* f = std::getenv("AURA_B200_AFC_START")) start_f = std::min(0.9, std::max(0.0, std::atof(f)));
+    const size_t first = (size_t)((double)nm * start_f);
+    const size_t span = (size_t)((double)(nm - first) * span_f);
     size_t im = 0;
     for (size_t j = 0; j < na; ++j) {
-      const size_t upto = span * (2 * j + 1) / (2 * na);  // middle items before canceller item j
+      const size_t upto = first + span * (2 * j + 1) / (2 * na);  // middle items before canceller item j
       for (; im < upto; ++im) push(0, std::get<0>(mid[im]), std::get<1>(mid[im]), std::get<2>(mid[im]));
       push(1, std::get<0>(afc[j]), std::get<1>(afc[j]), std::get<2>(afc[j]));
     }
