@@ -13,6 +13,20 @@
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
+// L2-resident read: the same `n` float4 every launch, cached at L2 (.cg)
+__global__ void k_ldg_l2(const float4* __restrict__ p, size_t n, float* out) {
+  float4 acc = make_float4(0, 0, 0, 0);
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < n; i += 4 * stride) {
+    float4 a = __ldcg(p + i), b = __ldcg(p + i + stride), c = __ldcg(p + i + 2 * stride), d = __ldcg(p + i + 3 * stride);
+    acc.x += a.x + b.x + c.x + d.x; acc.y += a.y + b.y + c.y + d.y;
+    acc.z += a.z + b.z + c.z + d.z; acc.w += a.w + b.w + c.w + d.w;
+  }
+  for (; i < n; i += stride) { float4 a = __ldcg(p + i); acc.x += a.x; acc.y += a.y; acc.z += a.z; acc.w += a.w; }
+  if (acc.x == 123.f) out[0] = acc.y + acc.z + acc.w;
+}
+
 __global__ void k_ldg(const float4* __restrict__ p, size_t n, float* out) {
   float4 acc = make_float4(0, 0, 0, 0);
   const size_t stride = (size_t)gridDim.x * blockDim.x;
@@ -28,7 +42,7 @@ __global__ void k_ldg(const float4* __restrict__ p, size_t n, float* out) {
 
 // each CTA streams a contiguous range [cta*per, (cta+1)*per) bytes in stage-sized copies
 __global__ void __launch_bounds__(288) k_bulk(const char* __restrict__ src, size_t per, int stage, int S,
-                                              int copies, float* out) {
+                                              int copies, float* out, int l2_normal = 0) {
   extern __shared__ __align__(128) unsigned char sm[];
   uint64_t* full = (uint64_t*)sm;
   uint64_t* empty = full + 16;
@@ -47,7 +61,8 @@ __global__ void __launch_bounds__(288) k_bulk(const char* __restrict__ src, size
   if (warp == 8) {
     if (lane != 0) return;
     uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    if (l2_normal) asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+    else asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
     for (int q = 0; q < nst; ++q) {
       const int s = q % S;
       const uint32_t par = ((q / S) & 1) ^ 1;
@@ -96,6 +111,32 @@ int main() {
     cudaEventElapsedTime(&ms, t0, t1);
     return ms / reps;
   };
+  if (getenv("BW_L2")) {  // L2-resident read bandwidth at a footprint (same bytes every launch)
+    int l2 = 0;
+    CK(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, 0));
+    printf("{\"kind\": \"l2_size\", \"bytes\": %d}\n", l2);
+    CK(cudaFuncSetAttribute(k_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    for (double mb : {4.0, 8.0, 16.0, 24.0, 32.0, 48.0, 64.0, 80.0, 100.0, 126.0, 160.0, 256.0}) {
+      const size_t fb = (size_t)(mb * 1e6) / 65536 * 65536;
+      for (int per_sm : {2, 4}) {
+        const int grid = sms * per_sm;
+        float ms = timeit([&] { k_ldg_l2<<<grid, 512>>>((const float4*)buf, fb / 16, out); }, 50);
+        printf("{\"kind\": \"l2_ldg\", \"footprint_mb\": %.1f, \"ctas\": %d, \"GBps\": %.1f, \"us\": %.2f}\n",
+               fb / 1e6, grid, fb / ms / 1e6, ms * 1e3);
+      }
+      for (int stage : {16384, 32768}) {
+        const int S = 4;
+        const size_t smem = 256 + (size_t)S * stage;
+        size_t per = fb / sms;
+        per -= per % stage;
+        if (per == 0) continue;
+        float ms = timeit([&] { k_bulk<<<sms, 288, smem>>>(buf, per, stage, S, 1, out, 1); }, 50);
+        printf("{\"kind\": \"l2_bulk\", \"footprint_mb\": %.1f, \"stage\": %d, \"GBps\": %.1f, \"us\": %.2f}\n",
+               per * sms / 1e6, stage, (double)per * sms / ms / 1e6, ms * 1e3);
+      }
+    }
+    return 0;
+  }
   if (getenv("BW_PER_SM")) {  // per-SM ceiling: fewer CTAs than SMs
     CK(cudaFuncSetAttribute(k_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     for (int grid : {16, 32, 64, 96, 148}) {
