@@ -18,7 +18,7 @@ namespace aura {
 struct AfcParams {
   float mu = 0.0f;
   float lambda = 0.9f;
-  float delta = 0.0f;  // 0 -> 1e-2 * (2 * block_size)
+  float delta = 0.0f;  // 0 -> 1e-6 * block_size
 };
 
 class Auralizer {
@@ -53,16 +53,14 @@ class Auralizer {
     const auto f = b200_detail::row_pointers(fc_filters);
     const auto c = b200_detail::to_c(cfg_);
     const aura_b200_afc p{afc.mu, afc.lambda,
-                          afc.delta > 0.0f ? afc.delta : 2e-2f * static_cast<float>(cfg_.block_size)};
+                          afc.delta > 0.0f ? afc.delta : 1e-6f * static_cast<float>(cfg_.block_size)};
     aura_b200_engine* e = nullptr;
     b200_detail::check(aura_b200_auralizer_create(&c, s.data(), s.size(),
                                                   synth_filters.front().size(), f.data(),
                                                   f.size(), fc_filters.front().size(), input_gain,
                                                   &p, device, &e));
     engine_.reset(e);
-    const float* view = nullptr;
-    b200_detail::check(aura_b200_feedback_estimate_view(e, &view));
-    estimate_ = std::span<const float>(view, cfg_.block_size);
+    estimate_.assign(cfg_.block_size, 0.0f);
     synth_view_.emplace(Convolver(Convolver::ViewTag{}, cfg_, ChannelMode::broadcast,
                                   aura_b200_partition_count(e), synth_filters.front().size(),
                                   backend_));
@@ -83,9 +81,13 @@ class Auralizer {
   void set_input_gain(float gain) { b200_detail::check(aura_b200_set_input_gain(engine_.get(), gain)); }
 
   /// auralizer.hpp:56-58: the estimate subtracted from the next input block.
-  /// (Waits for the block's background work, which computes it.)
-  std::span<const float> feedback_estimate() const noexcept {
-    aura_b200_synchronize(engine_.get());
+  /// Waits for the last block's background work (which computes it) and
+  /// copies it into this object's own buffer, so the span stays complete
+  /// until the next process()/reset(), as the reference's does. Unlike the
+  /// reference it is not noexcept: a CUDA failure or a shard-exchange
+  /// timeout surfaces here as aura::Error instead of a stale estimate.
+  std::span<const float> feedback_estimate() const {
+    b200_detail::check(aura_b200_feedback_estimate(engine_.get(), estimate_.data()));
     return estimate_;
   }
 
@@ -114,7 +116,7 @@ class Auralizer {
   EngineConfig cfg_;
   std::shared_ptr<ExecutionBackend> backend_;
   b200_detail::EnginePtr engine_;
-  std::span<const float> estimate_;
+  mutable std::vector<float> estimate_;
   std::optional<Convolver> synth_view_, fc_view_;
 };
 

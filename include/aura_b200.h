@@ -4,9 +4,9 @@
  *
  * This is the drop-in boundary for the reference's C++ aura::Convolver /
  * aura::Auralizer hot path (/root/reference/proj/include/aura/). The C++
- * drop-in header include/aura/b200.hpp re-exposes these entry points with
- * the reference's class names, argument meaning and exceptions; a Python
- * mirror lives in paper_2509_04390_b200/__init__.py.
+ * drop-in headers include/aura/{convolver,auralizer,backend}.hpp re-expose
+ * these entry points with the reference's class names, argument meaning and
+ * exceptions; a Python mirror lives in paper_2509_04390_b200/__init__.py.
  *
  * Conventions
  *  - Every int-returning call returns AURA_B200_OK (0) or 1 + the value of
@@ -134,32 +134,12 @@ int aura_b200_process(aura_b200_engine* e, const float* in, float* out);
  * (auralizer.hpp:95-99); an NLMS canceller is restored to its initial F^. */
 int aura_b200_reset(aura_b200_engine* e);
 
-/* Auralizer::feedback_estimate (auralizer.hpp:56-58): inputs x N floats */
+/* Auralizer::feedback_estimate (auralizer.hpp:56-58): inputs x N floats,
+ * copied out once the last processed block's background work (canceller,
+ * f^ for the next block) is complete. */
 int aura_b200_feedback_estimate(aura_b200_engine* e, float* out);
-/* Zero-copy view of the same estimate: a pinned host buffer the GPU writes
- * at the end of every block (inputs x N floats), valid while the engine
- * lives and stable between process() calls. Backs the C++ drop-in's
- * span-returning feedback_estimate(). */
-int aura_b200_feedback_estimate_view(aura_b200_engine* e, const float** out);
 /* Auralizer::input_gain / set_input_gain (auralizer.hpp:51-52) */
 int aura_b200_set_input_gain(aura_b200_engine* e, float gain);
-/* How blocks run (not in the reference): 0 = one CUDA graph per block
- * (default), 1 = the same kernels launched on the engine stream, 2 = one
- * persistent cooperative kernel for the whole block loop, driven by a
- * doorbell in mapped host memory (fails with BACKEND_UNAVAILABLE when the
- * configuration does not fit it; not for sharded engines). */
-int aura_b200_set_launch_mode(aura_b200_engine* e, int mode);
-int aura_b200_launch_mode(const aura_b200_engine* e);
-/* Diagnostics: per-block phase stamps of the last loop-mode device timing,
- * us from each block's release: {output written, input spectra pushed,
- * canceller heads done, streaming done, block done, CTA 0's reduction done}
- * per block (-1: n/a). */
-int aura_b200_loop_phases(const aura_b200_engine* e, size_t blocks, double* out);
-/* Diagnostics: host-side breakdown of process() in graph mode, per block
- * (optionally paced): us from the call's start to {input staged, graph
- * launched, background event recorded, output flag seen, output copied}. */
-int aura_b200_time_host_breakdown(aura_b200_engine* e, const float* host_in, size_t n_in_blocks,
-                                  size_t blocks, double pace_us, double* out);
 float aura_b200_input_gain(const aura_b200_engine* e);
 
 /* ---- accessors (convolver.hpp:96-107, auralizer.hpp:44-49) ----------- */
@@ -207,59 +187,8 @@ int aura_b200_shard_connect(aura_b200_engine* e, const void* handles);
 int aura_b200_shard_connect_local(aura_b200_engine* const* engines, int world);
 int aura_b200_shard_info(const aura_b200_engine* e, int* world, int* rank);
 
-/* ---- measurement (bench.py; not part of the reference API) ----------- */
-/* Run `blocks` blocks back to back with device-resident I/O (inputs already
- * in HBM, uploaded from host_in: n_in_blocks x inputs x N floats, cycled),
- * front and background graphs per block, timed with CUDA events on the
- * engine stream. latency_us[i] (may be NULL) = device time from block start
- * to its output written; block_us[i] = device time of ALL of block i's work
- * (front + background). */
-int aura_b200_time_device_blocks(aura_b200_engine* e, const float* host_in,
-                                 size_t n_in_blocks, size_t blocks,
-                                 float* latency_us, float* block_us);
-/* End-to-end latency through aura_b200_process() itself: `blocks` calls
- * with HOST input (cycling over host_in: n_in_blocks x inputs x N) and host
- * output, each timed with steady_clock from call to return (host->device
- * input transfer, all kernels, device->host output, completion wait).
- * pace_us > 0 spaces the calls on a real-time grid (one block every
- * pace_us, as an audio callback would) instead of back to back. */
-int aura_b200_time_host_blocks(aura_b200_engine* e, const float* host_in,
-                               size_t n_in_blocks, size_t blocks,
-                               double pace_us, float* block_us);
-/* Same blocks launched kernel by kernel with an event pair around each
- * phase; phase_us[p] = mean device time of phase p over `blocks`, names
- * via aura_b200_phase_name. Returns the phase count in *n_phases. */
-int aura_b200_profile_phases(aura_b200_engine* e, size_t blocks,
-                             float* phase_us, int* n_phases);
-const char* aura_b200_phase_name(const aura_b200_engine* e, int phase);
-/* Average device time of `reps` back-to-back single launches (no
- * programmatic overlap) of one phase kernel -- k_front = 0, k_back = 2,
- * k_reduce = 3 -- between two CUDA events on the engine stream: the
- * roofline denominator. The block counter and the canceller's smoothed
- * power are restored afterwards. */
-int aura_b200_time_phase(aura_b200_engine* e, int phase, size_t reps, float* avg_us);
-/* Timeline of `blocks` (<= 64) back-to-back device-resident blocks from
- * %globaltimer stamps taken inside the kernels: out[(i*11 + k)*2 + {0,1}] =
- * first / last stamp (us, relative to block i's front start) of event k in
- * order k_front, k_back_head, k_back, k_reduce, canceller done, k_afc_finish,
- * output published, canceller sums in, f^ written, input spectra pushed;
- * slot 10 = {the next block's front start, 0}. -1 when the event did not
- * occur. Shows launch gaps and overlap. */
-int aura_b200_trace_blocks(aura_b200_engine* e, size_t blocks, double* out);
-/* Diagnostics (not in the reference): per-segment / per-CTA timeline of the
- * streaming kernel k_back for the last of `blocks` blocks, us from the
- * kernel's first CTA start. out_segs: n_segs x {kind, tile, begin, end,
- * cta, start_us, partial_us, end_us} (one row per work item); out_ctas:
- * n_ctas x {start_us, first_data_us, exit_us}. Call with null outputs to get
- * the sizes. */
-int aura_b200_trace_back(aura_b200_engine* e, size_t blocks, double* out_segs, size_t* n_segs,
-                         double* out_ctas, size_t* n_ctas);
-/* Kernels launched per block (front + background graphs). */
-int aura_b200_launches_per_block(const aura_b200_engine* e);
-/* Algorithmic bytes per block of each phase (SURVEY.md 8(d) formula). */
-double aura_b200_phase_bytes(const aura_b200_engine* e, int phase);
-/* Launch geometry summary as text ("grid=... block=... chunks=..."). */
-int aura_b200_describe(const aura_b200_engine* e, char* buf, size_t cap);
+/* Measurement and diagnostics entry points (bench.py, tools/): see
+ * aura_b200_diag.h -- not part of the reference-replacing API. */
 
 #ifdef __cplusplus
 }

@@ -195,7 +195,7 @@ class OracleAuralizer:
                  lam=0.9, delta=None):
         s, f = _f32(synth), _f32(fc)
         if delta is None:
-            delta = 1e-2 * 2 * block  # same default as the product
+            delta = 1e-6 * block  # same default as the product
         self.N, self.Q, self.L = block, inputs, outputs
         self._h = olib().ao_aur_new(block, inputs, outputs, s, s.shape[1], f,
                                     f.shape[1], gain, mu, lam, delta)

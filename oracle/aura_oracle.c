@@ -5,6 +5,11 @@
  * rounds exactly as the reference's (the C-vs-reference comparison in
  * tests/test_oracle.py is bit-exact).
  *
+ * Channel loops run on OpenMP threads (so the full-length parity runs at the
+ * BASELINE sizes take seconds, not minutes); every channel's arithmetic is
+ * unchanged and every cross-channel sum stays serial in channel order, so
+ * the results are bit-identical to a single-threaded run.
+ *
  * This file is the checker for the CUDA product in paper_2509_04390_b200/;
  * the product never links or calls it.
  */
@@ -13,6 +18,26 @@
 #include <math.h>
 #include <stdlib.h>
 #include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+static int n_threads(void) {
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
+}
+static int thread_id(void) {
+#ifdef _OPENMP
+  return omp_get_thread_num();
+#else
+  return 0;
+#endif
+}
+/* parallelise a channel loop only when it carries real work */
+#define AO_PAR_MIN_WORK ((size_t)1 << 18)
 
 #ifndef M_PI
 #define M_PI 3.14159265358979323846
@@ -90,10 +115,9 @@ static void fft_core(const ao_plan* p, cf* z) {
   }
 }
 
-/* dft.hpp:69-101 */
-void ao_forward(const ao_plan* p, const float* buf, float* spec_f) {
+/* dft.hpp:69-101 (z: n_f/2 complex scratch) */
+static void forward_w(const ao_plan* p, const float* buf, float* spec_f, cf* z) {
   cf* spec = (cf*)spec_f;
-  cf* z = p->work;
   const size_t n = p->half;
   for (size_t m = 0; m < n; ++m) {
     z[p->bitrev[m]].re = buf[2 * m];
@@ -114,10 +138,11 @@ void ao_forward(const ao_plan* p, const float* buf, float* spec_f) {
   }
 }
 
+void ao_forward(const ao_plan* p, const float* buf, float* spec_f) { forward_w(p, buf, spec_f, p->work); }
+
 /* dft.hpp:124-153 (inverse_unchecked: edge imaginary parts ignored) */
-void ao_inverse(const ao_plan* p, const float* spec_f, float* buf) {
+static void inverse_w(const ao_plan* p, const float* spec_f, float* buf, cf* z) {
   const cf* spec = (const cf*)spec_f;
-  cf* z = p->work;
   const size_t n = p->half;
   {
     const float xe = 0.5f * (spec[0].re + spec[n].re);
@@ -145,6 +170,8 @@ void ao_inverse(const ao_plan* p, const float* spec_f, float* buf) {
   }
 }
 
+void ao_inverse(const ao_plan* p, const float* spec_f, float* buf) { inverse_w(p, spec_f, buf, p->work); }
+
 /* ------------------------------------------------------------ convolver */
 /* One UPOLS engine = convolver.hpp:65-220 with its FDL (engine.hpp:233-279).
  * MIMO (Appendix B) = Q broadcast engines whose outputs are summed in q
@@ -161,18 +188,29 @@ typedef struct {
   cf* acc;       /* bins */
   float* time;   /* 2N */
   float* pad;    /* 2N */
+  int nt;        /* per-thread scratch: */
+  cf* tacc;      /*   nt x bins */
+  float* ttime;  /*   nt x 2N */
+  cf* twork;     /*   nt x N (FFT work) */
 } upols;
 
 static void upols_partition(upols* u, size_t row, const float* taps) {
   /* convolver.hpp:19-46: split into K blocks of N taps, zero-pad to 2N */
+  const int t = thread_id();
+  float* pad = u->ttime + (size_t)t * 2 * u->N;
   for (size_t k = 0; k < u->K; ++k) {
     const size_t begin = k * u->N;
     size_t n = u->n_h - begin;
     if (n > u->N) n = u->N;
-    memset(u->pad, 0, sizeof(float) * 2 * u->N);
-    memcpy(u->pad, taps + begin, sizeof(float) * n);
-    ao_forward(u->plan, u->pad, (float*)(u->H + (row * u->K + k) * u->bins));
+    memset(pad, 0, sizeof(float) * 2 * u->N);
+    memcpy(pad, taps + begin, sizeof(float) * n);
+    forward_w(u->plan, pad, (float*)(u->H + (row * u->K + k) * u->bins), u->twork + (size_t)t * u->N);
   }
+}
+
+static void upols_partition_rows(upols* u, size_t rows, const float* filters) {
+#pragma omp parallel for schedule(dynamic, 1) if (rows * u->K * u->bins >= AO_PAR_MIN_WORK)
+  for (size_t c = 0; c < rows; ++c) upols_partition(u, c, filters + c * u->n_h);
 }
 
 static int upols_init(upols* u, size_t N, size_t in_ch, size_t out_ch,
@@ -192,7 +230,11 @@ static int upols_init(upols* u, size_t N, size_t in_ch, size_t out_ch,
   u->acc = (cf*)calloc(u->bins, sizeof(cf));
   u->time = (float*)calloc(2 * N, sizeof(float));
   u->pad = (float*)calloc(2 * N, sizeof(float));
-  for (size_t c = 0; c < out_ch; ++c) upols_partition(u, c, filters + c * n_h);
+  u->nt = n_threads();
+  u->tacc = (cf*)calloc((size_t)u->nt * u->bins, sizeof(cf));
+  u->ttime = (float*)calloc((size_t)u->nt * 2 * N, sizeof(float));
+  u->twork = (cf*)calloc((size_t)u->nt * N, sizeof(cf));
+  upols_partition_rows(u, out_ch, filters);
   return 0;
 }
 
@@ -200,6 +242,7 @@ static void upols_free(upols* u) {
   ao_plan_free(u->plan);
   free(u->H); free(u->fdl); free(u->head); free(u->window);
   free(u->acc); free(u->time); free(u->pad);
+  free(u->tacc); free(u->ttime); free(u->twork);
 }
 
 static void upols_reset(upols* u) {
@@ -219,7 +262,14 @@ static void upols_stage1(upols* u, size_t ch, const float* in) {
   memmove(w, w + u->N, sizeof(float) * u->N);
   memcpy(w + u->N, in, sizeof(float) * u->N);
   u->head[ch] = (u->head[ch] + u->K - 1) % u->K; /* engine.hpp:250-258 */
-  ao_forward(u->plan, w, (float*)(u->fdl + (ch * u->K + u->head[ch]) * u->bins));
+  forward_w(u->plan, w, (float*)(u->fdl + (ch * u->K + u->head[ch]) * u->bins),
+            u->twork + (size_t)thread_id() * u->N);
+}
+
+/* stage 1 of channels [0, n): independent channels, one per thread */
+static void upols_stage1_all(upols* u, size_t n, const float* in) {
+#pragma omp parallel for schedule(static) if (n * u->bins * 16 >= AO_PAR_MIN_WORK)
+  for (size_t c = 0; c < n; ++c) upols_stage1(u, c, in + c * u->N);
 }
 
 /* backend.hpp:212-235: newest-to-oldest fp32 complex accumulation */
@@ -237,17 +287,28 @@ static void spectral_mac(const upols* u, const cf* H, size_t K, size_t fdl_ch,
   }
 }
 
-/* convolver.hpp:193-206: MAC, c2r, keep the last N samples */
-static void upols_stage23(upols* u, size_t ch, float* out) {
-  const size_t fdl_ch = u->elementwise ? ch : 0;
-  spectral_mac(u, u->H, u->K, fdl_ch, ch, u->acc);
-  ao_inverse(u->plan, (const float*)u->acc, u->time);
-  memcpy(out, u->time + u->N, sizeof(float) * u->N);
+/* MAC of row `row` of H (K partitions) against FDL channel fdl_ch, c2r,
+ * keep the last N samples (convolver.hpp:193-206), in the calling thread's
+ * scratch */
+static void mac_c2r(upols* u, const cf* H, size_t K, size_t fdl_ch, size_t row, float* out) {
+  const int t = thread_id();
+  cf* acc = u->tacc + (size_t)t * u->bins;
+  float* time = u->ttime + (size_t)t * 2 * u->N;
+  spectral_mac(u, H, K, fdl_ch, row, acc);
+  inverse_w(u->plan, (const float*)acc, time, u->twork + (size_t)t * u->N);
+  memcpy(out, time + u->N, sizeof(float) * u->N);
+}
+
+/* convolver.hpp:193-206 for every output channel (independent) */
+static void upols_stage23_all(upols* u, float* out) {
+#pragma omp parallel for schedule(dynamic, 1) if (u->out_ch * u->K * u->bins >= AO_PAR_MIN_WORK)
+  for (size_t c = 0; c < u->out_ch; ++c)
+    mac_c2r(u, u->H, u->K, u->elementwise ? c : 0, c, out + c * u->N);
 }
 
 static void upols_process(upols* u, const float* in, float* out) {
-  for (size_t c = 0; c < u->in_ch; ++c) upols_stage1(u, c, in + c * u->N);
-  for (size_t c = 0; c < u->out_ch; ++c) upols_stage23(u, c, out + c * u->N);
+  upols_stage1_all(u, u->in_ch, in);
+  upols_stage23_all(u, out);
 }
 
 struct ao_conv {
@@ -325,6 +386,7 @@ struct ao_aur {
   cf* E;               /* bins */
   float* power;        /* bins */
   float* scale;        /* bins */
+  float* fc_l;         /* L x N: per-loudspeaker canceller outputs */
 };
 
 ao_aur* ao_aur_new(size_t N, size_t Q, size_t L, const float* synth,
@@ -344,7 +406,7 @@ ao_aur* ao_aur_new(size_t N, size_t Q, size_t L, const float* synth,
   a->W = (cf*)calloc(a->P * wsz, sizeof(cf));
   memcpy(a->W, a->fc.H, sizeof(cf) * wsz);
   for (size_t p = 1; p < a->P; ++p) {
-    for (size_t l = 0; l < L; ++l) upols_partition(&a->fc, l, fc + (p * L + l) * n_hf);
+    upols_partition_rows(&a->fc, L, fc + p * L * n_hf);
     memcpy(a->W + p * wsz, a->fc.H, sizeof(cf) * wsz);
   }
   memcpy(a->fc.H, a->W, sizeof(cf) * wsz);
@@ -355,6 +417,7 @@ ao_aur* ao_aur_new(size_t N, size_t Q, size_t L, const float* synth,
   a->E = (cf*)calloc(a->bins, sizeof(cf));
   a->power = (float*)calloc(a->bins, sizeof(float));
   a->scale = (float*)calloc(a->bins, sizeof(float));
+  a->fc_l = (float*)calloc(L * N, sizeof(float));
   return a;
 }
 
@@ -363,7 +426,7 @@ void ao_aur_free(ao_aur* a) {
   ao_conv_free(a->synth);
   upols_free(&a->fc);
   free(a->W); free(a->fhat); free(a->mt); free(a->fc_out); free(a->ewin);
-  free(a->E); free(a->power); free(a->scale);
+  free(a->E); free(a->power); free(a->scale); free(a->fc_l);
   free(a);
 }
 
@@ -376,6 +439,7 @@ static void nlms_update(ao_aur* a) {
     memset(a->ewin, 0, sizeof(float) * N);
     memcpy(a->ewin + N, a->mt + p * N, sizeof(float) * N);
     ao_forward(a->fc.plan, a->ewin, (float*)a->E);
+#pragma omp parallel for schedule(static) if (L * Kf * bins >= AO_PAR_MIN_WORK)
     for (size_t l = 0; l < L; ++l)
       for (size_t k = 0; k < Kf; ++k) {
         const cf* x = fdl_slot(&a->fc, l, k);
@@ -399,17 +463,17 @@ void ao_aur_process(ao_aur* a, const float* mic, float* spk) {
   /* auralizer.hpp:78: synthesis */
   ao_conv_process(a->synth, a->mt, spk);
   /* auralizer.hpp:79: FC stage 1 on every loudspeaker channel */
-  for (size_t l = 0; l < L; ++l) upols_stage1(&a->fc, l, spk + l * N);
-  /* auralizer.hpp:79-86: per channel MAC + c2r, summed in time in l order */
+  upols_stage1_all(&a->fc, L, spk);
+  /* auralizer.hpp:79-86: per channel MAC + c2r (channels in parallel),
+   * summed in time in l order */
   const size_t wsz = L * a->K_f * bins;
   for (size_t p = 0; p < a->P; ++p) {
+#pragma omp parallel for schedule(dynamic, 1) if (L * a->K_f * bins >= AO_PAR_MIN_WORK)
+    for (size_t l = 0; l < L; ++l) mac_c2r(&a->fc, a->W + p * wsz, a->K_f, l, l, a->fc_l + l * N);
     float* f = a->fhat + p * N;
     for (size_t i = 0; i < N; ++i) f[i] = 0.0f;
-    for (size_t l = 0; l < L; ++l) {
-      spectral_mac(&a->fc, a->W + p * wsz, a->K_f, l, l, a->fc.acc);
-      ao_inverse(a->fc.plan, (const float*)a->fc.acc, a->fc.time);
-      for (size_t i = 0; i < N; ++i) f[i] += a->fc.time[N + i];
-    }
+    for (size_t l = 0; l < L; ++l)
+      for (size_t i = 0; i < N; ++i) f[i] += a->fc_l[l * N + i];
   }
   /* Appendix A step 5: smoothed loudspeaker power for the next update */
   if (a->mu != 0.0f) {

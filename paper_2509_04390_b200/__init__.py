@@ -178,7 +178,7 @@ def lib():
     L.aura_b200_set_input_gain.argtypes = [vp, C.c_float]
     L.aura_b200_set_launch_mode.argtypes = [vp, C.c_int]
     L.aura_b200_launch_mode.argtypes = [vp]
-    L.aura_b200_loop_phases.argtypes = [vp, sz, vp]
+    L.aura_b200_seek_block.argtypes = [vp, C.c_uint64]
     L.aura_b200_time_host_breakdown.argtypes = [vp, vp, sz, sz, C.c_double, vp]
     L.aura_b200_input_gain.argtypes = [vp]
     L.aura_b200_input_gain.restype = C.c_float
@@ -191,6 +191,7 @@ def lib():
     L.aura_b200_mode.argtypes = [vp]
     L.aura_b200_filter_spectrum.argtypes = [vp, sz, sz, _f32p]
     L.aura_b200_afc_coeffs.argtypes = [vp, _f32p]
+    L.aura_b200_fdl_slot.argtypes = [vp, C.c_int, sz, sz, _f32p]
     L.aura_b200_time_device_blocks.argtypes = [vp, C.c_void_p, sz, sz, _f32p, _f32p]
     L.aura_b200_synchronize.argtypes = [vp]
     L.aura_b200_time_host_blocks.argtypes = [vp, _f32p, sz, sz, C.c_double, _f32p]
@@ -312,6 +313,14 @@ class _Engine:
     def reset(self):
         _check(lib().aura_b200_reset(self._h))
 
+    def fdl_slot(self, which: int, channel: int, age: int) -> np.ndarray:
+        """FrequencyDelayLine::slot(channel, age) (engine.hpp:261-266) of the
+        input FDL (which = 0) or the canceller FDL (which = 1): N+1 complex64."""
+        n = self.cfg.block_size
+        out = np.zeros(2 * (n + 1), np.float32)
+        _check(lib().aura_b200_fdl_slot(self._h, which, channel, age, out))
+        return out.view(np.complex64)
+
     TRACE_KERNELS = ("k_front", "k_back_head", "k_back", "k_reduce", "afc_done", "k_afc_finish",
                      "output", "afc_summed", "afc_c2r", "front_x")
     _TRACE_SLOTS = 11  # kTraceKernels: the last slot is the next block's front start
@@ -341,12 +350,16 @@ class _Engine:
         return segs, ctas
 
     def set_launch_mode(self, mode: int):
-        """0: one CUDA graph per block (default); 1: kernels on the stream;
-        2: one persistent kernel for the block loop (doorbell-driven)."""
+        """0: one CUDA graph per block (default); 1: the same kernels
+        launched on the stream (bit-identical)."""
         _check(lib().aura_b200_set_launch_mode(self._h, mode))
 
     def launch_mode(self) -> int:
         return int(lib().aura_b200_launch_mode(self._h))
+
+    def seek_block(self, n: int):
+        """Testing: number the device blocks from n (fresh or reset engine)."""
+        _check(lib().aura_b200_seek_block(self._h, n))
 
     HOST_PHASES = ("staged", "launched", "event", "output_seen", "copied")
 
@@ -358,20 +371,12 @@ class _Engine:
                                                    pace_us, out.ctypes.data))
         return {k: out[:, i] for i, k in enumerate(self.HOST_PHASES)}
 
-    LOOP_PHASES = ("output", "x_pushed", "heads_done", "streamed", "done", "cta0_reduced")
-
-    def loop_phases(self, blocks: int):
-        """Per-block phase stamps (us from release) of the last loop-mode
-        time_device_blocks call."""
-        out = np.zeros((blocks, len(self.LOOP_PHASES)), np.float64)
-        _check(lib().aura_b200_loop_phases(self._h, blocks, out.ctypes.data))
-        return {k: out[:, i] for i, k in enumerate(self.LOOP_PHASES)}
-
     PHASES = {"k_front": 0, "k_back": 2, "k_reduce": 3}
 
     def time_phase(self, name: str, reps: int = 20) -> float:
-        """Mean device time (us) of back-to-back launches of one idempotent
-        phase kernel, CUDA events on the engine stream."""
+        """Mean device time (us) of back-to-back launches of one phase
+        kernel, CUDA events on the engine stream; the engine's state (block
+        counter, power, canceller W and partials) is restored afterwards."""
         v = C.c_float(0)
         _check(lib().aura_b200_time_phase(self._h, self.PHASES[name], reps, C.byref(v)))
         return float(v.value)
@@ -481,16 +486,16 @@ class Convolver(_Engine):
 @dataclass
 class AfcParams:
     """Feedback-canceller adaptation; mu = 0 is the
-    reference's fixed canceller. delta None -> 1e-2 * (2N)."""
+    reference's fixed canceller. delta None -> 1e-6 * N."""
     mu: float = 0.0
     lam: float = 0.9
     delta: Optional[float] = None
 
 
 def default_delta(block_size: int) -> float:
-    """NLMS regulariser default: -20 dB of the per-bin
-    power of one unit-variance loudspeaker signal."""
-    return 1e-2 * 2 * block_size
+    """NLMS regulariser default: SURVEY Appendix A's delta = 1e-6 * N
+    (DESIGN.md section 4 has the W-error evidence at this value)."""
+    return 1e-6 * block_size
 
 
 class Auralizer(_Engine):

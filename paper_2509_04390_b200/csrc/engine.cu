@@ -30,10 +30,9 @@
 #include <immintrin.h>
 #endif
 
-#include "../../include/aura_b200.h"
+#include "../../include/aura_b200_diag.h"
 #include "kernels.cuh"
 #include "stream.cuh"
-#include "loop.cuh"
 #include <algorithm>
 #include <tuple>
 
@@ -110,9 +109,10 @@ void validate(const aura_b200_config* c, bool mimo) {
          "input channels must be 1 or equal to output channels");
 }
 
-// NLMS regulariser default: 1e-2 x (2N), i.e. -20 dB of the per-bin power of
-// one unit-variance loudspeaker signal.
-constexpr float kDefaultDeltaPerBin = 1e-2f;
+// NLMS regulariser default: SURVEY Appendix A's delta = 1e-6 N (DESIGN.md
+// section 4: at this value the GPU's W error against a float64 run is within
+// 1.5x of the fp32 C oracle's own).
+constexpr float kDefaultDeltaPerN = 1e-6f;
 
 template <class T>
 T* dalloc(size_t count, std::vector<void*>& owned) {
@@ -182,27 +182,12 @@ struct aura_b200_engine {
   // streaming kernel k_back
   BackFn back_fn = nullptr;
   bool pdl_off = false;  // measurement: serialise k_back / k_reduce launches
-  int launch_mode = 0;   // 0: one CUDA graph per block; 1: kernels on the stream; 2: persistent loop
-  // persistent loop (loop.cuh)
-  BackFn loop_fn = nullptr;
-  bool loop_ok = false;          // this configuration fits the loop kernel
-  std::string loop_why;          // ... or why not
-  size_t smem_loop = 0;
-  int loop_cpb = 1, loop_front = 0, loop_ctas = 0;
-  bool loop_running = false;
-  uint64_t loop_posted = 0;      // blocks released through the doorbell (device numbering)
-  LoopMailbox* h_mbox = nullptr; // pinned mapped
-  LoopMailbox* d_mbox = nullptr;
-  LoopCtl* d_ctl = nullptr;
-  unsigned long long* d_stamps = nullptr;
-  int loop_stages = 0;
-  bool loop_device_io = false;
-  std::vector<unsigned long long> loop_last_stamps;  // of the last loop-mode device timing
-  unsigned long long* h_outflag = nullptr;  // mapped: front CTA b writes block + 1 in [b] when its output is out
-  size_t n_outflags = 0;
+  int launch_mode = 0;   // 0: one CUDA graph per block; 1: the same kernels launched on the stream
+  unsigned long long* h_outflag = nullptr;  // mapped: k_front CTA b writes block + 1 in [b] when done
+  size_t n_outflags = 0;    // = k_front's grid (every CTA that reads the mapped input)
   bool use_outflag = true;
-  uint64_t dev_block_base = 0;  // device block number of host block 0 (measurement calls advance both)
-  int loop_hold = 1;
+  std::string knobs;        // non-default AURA_B200_* tuning knobs in effect (describe())
+  uint64_t block_base = 0;  // device number of host block 0 (aura_b200_seek_block; else 0)
   int back_ctas = 0;
   size_t smem_back = 0, smem_reduce = 0;
   size_t n_syn_segs = 0, n_afc_segs = 0;
@@ -217,19 +202,15 @@ struct aura_b200_engine {
 
   ~aura_b200_engine() {
     cudaSetDevice(device);
-    if (loop_running && h_mbox) {  // stop the persistent kernel (best effort, bounded)
-      reinterpret_cast<volatile LoopMailbox*>(h_mbox)->stop = 1u;
-      std::atomic_thread_fence(std::memory_order_seq_cst);
-      if (!wait_stream_idle(stream, 5.0)) return;  // wedged: leak rather than block (frees would sync)
-    }
-    if (stream) cudaStreamSynchronize(stream);
+    // wedged (a shard peer that never arrives is bounded in-kernel, but be
+    // safe): leak rather than block, the frees below would synchronise
+    if (stream && !wait_stream_idle(stream, 10.0)) return;
     g_block.destroy();
     for (void* p : dmem) cudaFree(p);
     if (h_in) cudaFreeHost(h_in);
     if (h_out) cudaFreeHost(h_out);
     if (h_fhat) cudaFreeHost(h_fhat);
     if (h_status) cudaFreeHost(h_status);
-    if (h_mbox) cudaFreeHost(h_mbox);
     if (h_outflag) cudaFreeHost(h_outflag);
     for (void* p : ipc_opened) cudaIpcCloseMemHandle(p);
     if (ev_front) cudaEventDestroy(ev_front);
@@ -341,6 +322,35 @@ struct aura_b200_engine {
     g_block = capture_block(args, ev_front);
   }
 
+  // Every device buffer a block writes (measurement calls that relaunch
+  // kernels snapshot and restore them): {pointer, bytes}
+  std::vector<std::pair<void*, size_t>> mutable_state() const {
+    const size_t NF = N / 2, f4 = sizeof(float4), fl = sizeof(float);
+    const BlockArgs& a = args;
+    std::vector<std::pair<void*, size_t>> v = {
+        {a.st, sizeof(DevState)},
+        {a.prev_in, fl * Qx * N},
+        {a.hist1, fl * Qx * N},
+        {a.cur_mt, fl * std::max<size_t>(1, Q) * N},
+        {a.X, f4 * Qx * K * NF},
+        {a.S, f4 * L * NF},
+        {a.part_syn, f4 * std::max<size_t>(1, n_syn_segs * LT * a.CT)},
+        {a.front_seq, 2 * sizeof(unsigned long long)},
+        {a.tick, 6 * sizeof(unsigned)}};
+    if (aur) {
+      v.push_back({a.prev_spk, fl * L * N});
+      v.push_back({a.spk, fl * L * N});
+      v.push_back({a.XA, f4 * L * (KF + 1) * NF});
+      v.push_back({a.W, f4 * w_elems});
+      v.push_back({a.pw, sizeof(float2) * N});
+      v.push_back({a.E, f4 * Q * NF});
+      v.push_back({a.fhat, fl * P * N});
+      v.push_back({a.part_afc, f4 * std::max<size_t>(1, n_afc_segs * (P + 1) * a.CT)});
+      v.push_back({a.yhat, f4 * (P + 1) * NF});
+    }
+    return v;
+  }
+
   // algorithmic HBM bytes per block: 8N per packed partition
   double phase_bytes(int ph) const {
     const double row = 8.0 * (double)N;  // one packed partition
@@ -366,6 +376,24 @@ struct aura_b200_engine {
 };
 
 namespace {
+
+// Tuning knobs: AURA_B200_<name> environment overrides of measured defaults
+// (experiments only). Every knob that is set is recorded in e->knobs, which
+// describe() -- and so every bench line -- reports.
+const char* knob_raw(aura_b200_engine* e, const char* name) {
+  const std::string var = std::string("AURA_B200_") + name;
+  const char* v = std::getenv(var.c_str());
+  if (v) e->knobs += (e->knobs.empty() ? "" : ",") + std::string(name) + "=" + v;
+  return v;
+}
+int knob_i(aura_b200_engine* e, const char* name, int def) {
+  const char* v = knob_raw(e, name);
+  return v ? std::atoi(v) : def;
+}
+double knob_f(aura_b200_engine* e, const char* name, double def) {
+  const char* v = knob_raw(e, name);
+  return v ? std::atof(v) : def;
+}
 
 void setup_tables(aura_b200_engine* e, BlockArgs& a) {
   // DftPlan ctor (dft.hpp:36-52), bit for bit: angle step computed once in
@@ -443,18 +471,6 @@ BackFn back_for(bool elem, int PT) {
   }
 }
 
-template <int LT>
-BackFn loop_for(bool elem, int PT) {
-  if (elem) return k_loop<LT, true, 0>;
-  switch (PT) {
-    case 0: return k_loop<LT, false, 0>;
-    case 1: return k_loop<LT, false, 1>;
-    case 2: return k_loop<LT, false, 2>;
-    case 4: return k_loop<LT, false, 4>;
-    default: return k_loop<LT, false, 8>;
-  }
-}
-
 // Canceller partials per column tile that one k_reduce CTA sums in two load
 // rounds per thread (kReduceThreads threads over E elements, 16 loads in
 // flight per round: reduce_part).
@@ -488,8 +504,7 @@ void plan_back(aura_b200_engine* e, BlockArgs& a) {
   // ~46 KB synthesis stages, four in the ring: the single producer lane's
   // per-stage cost is what bounds an SM's stream (profiles/r1s5_stream.md),
   // so fewer, larger stages (sp need not be a multiple of the 8 tap phases)
-  int target_kb = 46;
-  if (const char* f = std::getenv("AURA_B200_STAGE_KB")) target_kb = std::max(4, std::atoi(f));
+  const int target_kb = std::max(4, knob_i(e, "STAGE_KB", 46));
   const int target_f4 = target_kb * 1024 / 16;
   const int syn_row = (LT + XL) * CT;
   a.sp = std::max(PH, target_f4 / syn_row);
@@ -507,7 +522,7 @@ void plan_back(aura_b200_engine* e, BlockArgs& a) {
   const size_t fixed = kBackBarrierBytes + (size_t)a.red_f4 * 16;
   const size_t per = (size_t)a.slot_f4 * 16;
   a.stages = per ? (int)std::min<size_t>(kMaxStages, (budget - fixed) / per) : 0;
-  if (const char* f = std::getenv("AURA_B200_STAGES")) a.stages = std::max(2, std::min(a.stages, std::atoi(f)));
+  if (const int st = knob_i(e, "STAGES", 0)) a.stages = std::max(2, std::min(a.stages, st));
   if (e->has_back() && a.stages < 2)
     fail(AURA_B200_E_INVALID_ARGUMENT, "block size / channel tile too large for the streaming kernel");
   e->smem_back = fixed + (size_t)a.stages * per;
@@ -523,11 +538,8 @@ void plan_back(aura_b200_engine* e, BlockArgs& a) {
   // HBM-bound once they run interleaved with the synthesis stream.
   const double afc_foot = 8.0 * N * ((double)P * U + (double)(e->aur ? e->L * (e->KF + 1) : 0) +
                                      (double)e->Qx * e->K);
-  double w_l2_mb = 0.0;
-  if (const char* f = std::getenv("AURA_B200_W_L2_MB")) w_l2_mb = std::atof(f);
+  const double w_l2_mb = knob_f(e, "W_L2_MB", 0.0);
   a.w_in_l2 = (P > 0 && afc_foot < w_l2_mb * 1e6) ? 1 : 0;
-  a.dbg = 0;
-  if (const char* f = std::getenv("AURA_B200_DBG")) a.dbg = std::atoi(f);
   // grid: one CTA per SM, fewer for small work (>= ~96 KB per CTA). Sized
   // and planned from the synthesis alone when there is one, so the
   // synthesis association -- and the output bits -- are the same with or
@@ -536,7 +548,7 @@ void plan_back(aura_b200_engine* e, BlockArgs& a) {
   const double afc_b = (double)CTn * U * (P * (e->args.nlms ? 2 : 1) + 1) * CT * 16.0;
   const double drive = T > 0 ? syn_b : afc_b;
   int ctas = (int)std::min<double>(e->sms, std::max(1.0, std::ceil(drive / (96.0 * 1024))));
-  if (const char* f = std::getenv("AURA_B200_BACK_CTAS")) ctas = std::max(1, std::min(ctas, std::atoi(f)));
+  if (const int c = knob_i(e, "BACK_CTAS", 0)) ctas = std::max(1, std::min(ctas, c));
   e->back_ctas = ctas;
   // Work: every CTA first runs a static piece of the first 30% of every
   // synthesis tile's taps (they start at t = 0, before anything can be
@@ -549,18 +561,16 @@ void plan_back(aura_b200_engine* e, BlockArgs& a) {
   // SMs runs canceller units (mostly L2 hits) while the rest keep HBM busy
   // with the synthesis stream. Every item is one split-K partial with a fixed
   // slot, so which CTA claims it does not change the bits.
-  double fa = 0.30;
-  if (const char* f = std::getenv("AURA_B200_PHASE_A")) fa = std::atof(f);
+  const double fa = knob_f(e, "PHASE_A", 0.30);
   const long long TA = T > 0 ? std::max<long long>(1, (long long)std::ceil(fa * T)) : 0;
-  double fb = 0.85;  // measured: 0.75 -> 0.85 gives c3 -2 us, c5 -2 us, c4 and c2 unchanged
-  if (const char* f = std::getenv("AURA_B200_PHASE_B")) fb = std::atof(f);
+  // measured: 0.75 -> 0.85 gives c3 -2 us, c5 -2 us, c4 and c2 unchanged
+  const double fb = knob_f(e, "PHASE_B", 0.85);
   const long long TB = T > 0 ? std::max<long long>(TA, (long long)std::ceil(fb * T)) : 0;
   // queue items: ~12 per CTA in the last 15%, at least two stages (keeps
   // the tail short and the partial count -- k_reduce's input -- small at c5
   // sizes); ~3 per CTA in the middle part
-  long long nq_per = 12, nb_per = 3;  // queue items per CTA: last part, middle part
-  if (const char* f = std::getenv("AURA_B200_QITEMS")) nq_per = std::max(1, std::atoi(f));
-  if (const char* f = std::getenv("AURA_B200_BITEMS")) nb_per = std::max(1, std::atoi(f));
+  // queue items per CTA: last part, middle part
+  const long long nq_per = std::max(1, knob_i(e, "QITEMS", 12)), nb_per = std::max(1, knob_i(e, "BITEMS", 3));
   const long long qtaps = (T - TB) * tiles;
   const long long CQ = std::max<long long>(2LL * a.sp, (qtaps / (nq_per * ctas) + a.sp - 1) / a.sp * a.sp);
   const long long btaps = (TB - TA) * tiles;
@@ -659,14 +669,13 @@ void plan_back(aura_b200_engine* e, BlockArgs& a) {
     // merge: canceller items evenly through the middle synthesis items (the
     // first middle items go first: the canceller waits for the head)
     const size_t nm = mid.size(), na = afc.size();
-    double span_f = 2.0 / 3.0;  // over the first two thirds: the long items end well before the tail
-    if (const char* f = std::getenv("AURA_B200_AFC_SPAN")) span_f = std::min(1.0, std::max(0.05, std::atof(f)));
+    // over the first two thirds: the long items end well before the tail
+    const double span_f = std::min(1.0, std::max(0.05, knob_f(e, "AFC_SPAN", 2.0 / 3.0)));
     // share of the middle items before the first canceller item: the CTAs
     // that reach the queue first (at the end of the static slice, ~11 us into
     // a c3 block) would otherwise wait for the front half's canceller head
     // (c3: k_back -0.6 us; c4 unchanged)
-    double start_f = 0.3;
-    if (const char* f = std::getenv("AURA_B200_AFC_START")) start_f = std::min(0.9, std::max(0.0, std::atof(f)));
+    const double start_f = std::min(0.9, std::max(0.0, knob_f(e, "AFC_START", 0.3)));
     const size_t first = (size_t)((double)nm * start_f);
     const size_t span = (size_t)((double)(nm - first) * span_f);
     size_t im = 0;
@@ -771,78 +780,6 @@ void common_init(aura_b200_engine* e, int device) {
 // canceller's k_afc_finish (k_back retires a block itself).
 void set_advance_total(aura_b200_engine* e) { e->args.advance_total = e->sharded() ? 1 : 0; }
 
-// Persistent loop mode (loop.cuh): does this configuration fit one
-// cooperative CTA per SM with the ring, the reduction scratch and the
-// front's work area in shared memory? Allocates the mailbox and control
-// block when it does.
-void plan_loop(aura_b200_engine* e) {
-  BlockArgs& a = e->args;
-  e->loop_ok = false;
-  a.hist1 = dalloc<float>((size_t)e->Qx * e->N, e->dmem);
-  CK(cudaMemset(a.hist1, 0, sizeof(float) * e->Qx * e->N));
-  if (!e->has_back()) {
-    e->loop_why = "no streaming work (single-partition convolver)";
-    return;
-  }
-  int coop = 0;
-  CK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, e->device));
-  if (!coop) {
-    e->loop_why = "device has no cooperative launch";
-    return;
-  }
-  const int N = (int)e->N;
-  const int Qs = e->mode == AURA_B200_ELEMENTWISE ? 1 : (int)e->Q;
-  const int nerr = (e->aur && a.nlms) ? (int)e->P : 0;
-  // at least one front CTA beside the error-spectrum CTAs; CTAs beyond the
-  // plan's take queue items only (the work items, hence the bits, are the same)
-  e->loop_ctas = std::min(e->sms, std::max(e->back_ctas, nerr + 1));
-  const int avail = e->loop_ctas - nerr;
-  if (avail < 1) {
-    e->loop_why = "too few CTAs for the front half";
-    return;
-  }
-  e->loop_cpb = (int)((e->L + avail - 1) / avail);
-  e->loop_front = (int)((e->L + e->loop_cpb - 1) / e->loop_cpb);
-  const size_t front = 8 * (front_work_f2(N, Qs) + (a.smem_tables ? table_f2(N) : 0) +
-                            (a.front_pre ? (size_t)(1 + Qs) * N : 0));
-  const size_t fixed = kBackBarrierBytes + (size_t)a.red_f4 * 16 + front;
-  const size_t slot = (size_t)a.slot_f4 * 16;
-  const size_t budget = 225 * 1024;
-  const int stages = budget > fixed ? (int)std::min<size_t>(a.stages, (budget - fixed) / slot) : 0;
-  if (stages < 2) {
-    e->loop_why = "shared memory: ring + front work area do not fit one CTA";
-    return;
-  }
-  if ((size_t)stages * slot < 16 * reduce_smem_f4(N, e->aur, (int)e->P)) {
-    e->loop_why = "shared memory: the reduction scratch does not fit the ring";
-    return;
-  }
-  const int LT = e->LT;
-  const bool elem = e->mode == AURA_B200_ELEMENTWISE;
-  switch (LT) {
-    case 1: e->loop_fn = loop_for<1>(elem, e->PT); break;
-    case 2: e->loop_fn = loop_for<2>(elem, e->PT); break;
-    case 4: e->loop_fn = loop_for<4>(elem, e->PT); break;
-    default: e->loop_fn = loop_for<8>(elem, e->PT); break;
-  }
-  e->smem_loop = fixed + (size_t)stages * slot;
-  raise_smem_limit(e->loop_fn, e->smem_loop);
-  int per_sm = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, e->loop_fn, kBackThreads, e->smem_loop));
-  if (per_sm < 1 || e->loop_ctas > per_sm * e->sms) {
-    e->loop_why = "the grid does not fit co-resident";
-    return;
-  }
-  e->loop_stages = stages;
-  if (const char* h = std::getenv("AURA_B200_LOOP_HOLD")) e->loop_hold = std::atoi(h);
-  CK(cudaHostAlloc(&e->h_mbox, sizeof(LoopMailbox), cudaHostAllocMapped | cudaHostAllocPortable));
-  std::memset(e->h_mbox, 0, sizeof(LoopMailbox));
-  CK(cudaHostGetDevicePointer((void**)&e->d_mbox, e->h_mbox, 0));
-  e->d_ctl = dalloc<LoopCtl>(1, e->dmem);
-  e->d_stamps = dalloc<unsigned long long>((size_t)kLoopStampCap * kLoopStamps, e->dmem);
-  e->loop_ok = true;
-}
-
 void finish_init(aura_b200_engine* e) {
   BlockArgs& a = e->args;
   const size_t N = e->N, NF = N / 2;
@@ -897,7 +834,7 @@ void finish_init(aura_b200_engine* e) {
   // small transforms synchronise with __syncwarp instead of CTA barriers
   a.front_warps = 0;
   {
-    const char* fw = std::getenv("AURA_B200_FRONT_WARPS");
+    const char* fw = knob_raw(e, "FRONT_WARPS");
     const int W = kFrontThreads / 32;
     const size_t sw = 8 * front_warps_f2((int)N, (int)Qs, W);
     // measured (profiles/r1s4_front.md, r1s5_stream.md): a clear win at
@@ -920,27 +857,29 @@ void finish_init(aura_b200_engine* e) {
   e->d_in_pool = dalloc<float>(e->pool_blocks * in_ch * N, e->dmem);
   CK(cudaMemset(e->d_in_pool, 0, e->pool_blocks * in_ch * N * sizeof(float)));
   e->d_out = dalloc<float>(e->L * N, e->dmem);
-  plan_loop(e);
+  // second window-history buffer (fused head: prev_in / hist1 by block parity)
+  a.hist1 = dalloc<float>(in_ch * N, e->dmem);
+  CK(cudaMemset(a.hist1, 0, sizeof(float) * in_ch * N));
   // fused head (profiles/r1s4_front.md): k_back launches as k_front's
   // programmatic dependent -- measured better for the auralizer (no separate
   // canceller head kernel) and for convolvers (the stream starts early)
   e->front_head = true;
-  if (const char* fh = std::getenv("AURA_B200_FRONT_HEAD")) e->front_head = std::atoi(fh) != 0;
+  e->front_head = knob_i(e, "FRONT_HEAD", 1) != 0;
   a.front_head = e->front_head ? 1 : 0;
   a.front_hold = 0;  // measured: holding the stream does not speed the front up (profiles/r1s4_front.md)
-  if (const char* fh = std::getenv("AURA_B200_FRONT_HOLD")) a.front_hold = std::atoi(fh);
+  a.front_hold = knob_i(e, "FRONT_HOLD", 0);
   a.front_seq = dalloc<unsigned long long>(2, e->dmem);
   CK(cudaMemset(a.front_seq, 0, 2 * sizeof(unsigned long long)));
-  // output-ready word for process(): mapped host memory, written by k_front
-  e->n_outflags = (size_t)((e->L + a.cpb - 1) / a.cpb);
-  a.front_ctas = (int)e->n_outflags;
+  // output-ready words for process(): mapped host memory, one per k_front
+  // CTA -- the output CTAs and the NLMS error-spectrum CTAs, which read the
+  // mapped input too (the host refills it only once all of them are done)
+  a.front_ctas = (int)((e->L + a.cpb - 1) / a.cpb);
+  e->n_outflags = (size_t)e->front_grid(a);
   CK(cudaHostAlloc(&e->h_outflag, e->n_outflags * sizeof(unsigned long long),
                    cudaHostAllocMapped | cudaHostAllocPortable));
   std::memset(e->h_outflag, 0, e->n_outflags * sizeof(unsigned long long));
   CK(cudaHostGetDevicePointer((void**)&a.out_flag, e->h_outflag, 0));
-  if (const char* f = std::getenv("AURA_B200_OUTFLAG")) e->use_outflag = std::atoi(f) != 0;
-  a.front_ticket = dalloc<unsigned>(1, e->dmem);
-  CK(cudaMemset(a.front_ticket, 0, sizeof(unsigned)));
+  e->use_outflag = knob_i(e, "OUTFLAG", 1) != 0;
   e->rebuild_graphs();
   e->dev_args = a;
   e->dev_args.out = e->d_out;
@@ -949,122 +888,6 @@ void finish_init(aura_b200_engine* e) {
   CK(cudaStreamSynchronize(e->stream));
 }
 
-// ------------------------------------------------------ persistent loop control
-volatile LoopMailbox* mbox(aura_b200_engine* e) { return reinterpret_cast<volatile LoopMailbox*>(e->h_mbox); }
-
-uint32_t device_block(aura_b200_engine* e) {
-  DevState ds{};
-  CK(cudaMemcpy(&ds, e->args.st, sizeof(ds), cudaMemcpyDeviceToHost));
-  return ds.block;
-}
-
-bool loop_exited(aura_b200_engine* e);
-void loop_reap(aura_b200_engine* e);
-void start_loop(aura_b200_engine* e, bool device_io);
-
-// Spin until mailbox field >= target (or the kernel reports an error);
-// relaunches a kernel that parked just as the block was released.
-void loop_wait(aura_b200_engine* e, volatile unsigned long long* field, uint64_t target, const char* what) {
-  const auto t0 = std::chrono::steady_clock::now();
-  uint64_t spins = 0;
-  while (*field < target) {
-    if (mbox(e)->err) fail(AURA_B200_E_TIMEOUT, std::string(what) + ": the persistent kernel reported a timeout");
-#if defined(__x86_64__)
-    _mm_pause();
-#endif
-    if ((++spins & 0xFFF) == 0) {
-      if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(20))
-        fail(AURA_B200_E_TIMEOUT, std::string(what) + ": not complete within 20 s");
-      if (loop_exited(e)) {  // parked just before our doorbell: relaunch (same I/O)
-        if (!mbox(e)->parked) fail(AURA_B200_E_CUDA, std::string(what) + ": the persistent kernel exited");
-        const bool dev = e->loop_device_io;
-        loop_reap(e);
-        start_loop(e, dev);
-      }
-    }
-  }
-  std::atomic_thread_fence(std::memory_order_acquire);
-}
-
-// Launch the persistent kernel at the device's current block. device_io:
-// inputs from the measurement pool (block n: slot n % pool_blocks), outputs
-// to device memory; else the mapped host I/O of process().
-void start_loop(aura_b200_engine* e, bool device_io) {
-  if (!e->loop_ok) fail(AURA_B200_E_BACKEND_UNAVAILABLE, "persistent loop mode unavailable: " + e->loop_why);
-  CK(cudaStreamSynchronize(e->stream));
-  const uint32_t n0 = device_block(e);
-  BlockArgs la = device_io ? e->dev_args : e->args;
-  // window history: block n reads (n odd ? hist1 : prev_in)
-  if (!e->front_head && e->mode != AURA_B200_ELEMENTWISE && (n0 & 1u))
-    CK(cudaMemcpy(la.hist1, la.prev_in, sizeof(float) * e->Qx * e->N, cudaMemcpyDeviceToDevice));
-  CK(cudaMemset(e->d_ctl, 0, sizeof(LoopCtl)));
-  volatile LoopMailbox* mb = mbox(e);
-  // blocks already released (posted just as a previous launch parked) stay released
-  e->loop_posted = std::max<uint64_t>(e->loop_posted, n0);
-  mb->out_done = n0;
-  mb->bg_done = n0;
-  mb->stop = 0u;
-  mb->err = 0u;
-  mb->parked = 0u;
-  std::atomic_thread_fence(std::memory_order_seq_cst);
-  mb->doorbell = e->loop_posted;
-  la.stages = e->loop_stages;
-  la.cpb = e->loop_cpb;
-  la.loop_front_ctas = e->loop_front;
-  la.mbox = e->d_mbox;
-  la.ctl = e->d_ctl;
-  la.loop_stamps = e->d_stamps;
-  la.in_slots = device_io ? (int)e->pool_blocks : 1;
-  la.loop_idle_ns = 20ull * 1000 * 1000;
-  la.loop_hold = e->loop_hold;
-  la.trace = nullptr;
-  la.seg_trace = nullptr;
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3((unsigned)e->loop_ctas);
-  cfg.blockDim = dim3(kBackThreads);
-  cfg.dynamicSmemBytes = e->smem_loop;
-  cfg.stream = e->stream;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeCooperative;
-  at[0].val.cooperative = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  CK(cudaLaunchKernelEx(&cfg, e->loop_fn, la));
-  e->loop_running = true;
-  e->loop_device_io = device_io;
-}
-
-// The persistent kernel has exited (stopped, parked or failed): hand the
-// state back to the graph-mode conventions.
-void loop_reap(aura_b200_engine* e) {
-  const cudaError_t r = cudaStreamSynchronize(e->stream);
-  e->loop_running = false;
-  ck(r, "persistent loop exit");
-  if (mbox(e)->err) fail(AURA_B200_E_TIMEOUT, "persistent loop: internal timeout");
-  const uint32_t n = device_block(e);
-  if (!e->front_head && e->mode != AURA_B200_ELEMENTWISE && (n & 1u))
-    CK(cudaMemcpy(e->args.prev_in, e->args.hist1, sizeof(float) * e->Qx * e->N, cudaMemcpyDeviceToDevice));
-}
-
-bool loop_exited(aura_b200_engine* e) { return e->loop_running && cudaStreamQuery(e->stream) != cudaErrorNotReady; }
-
-// Let every released block finish, stop the persistent kernel.
-void stop_loop(aura_b200_engine* e) {
-  if (!e->loop_running) return;
-  volatile LoopMailbox* mb = mbox(e);
-  std::string why;
-  try {
-    loop_wait(e, &mb->bg_done, e->loop_posted, "persistent loop");
-  } catch (const Fail& f) {
-    why = f.msg;
-  }
-  mb->stop = 1u;
-  std::atomic_thread_fence(std::memory_order_seq_cst);
-  if (!wait_stream_idle(e->stream, 5.0))
-    fail(AURA_B200_E_TIMEOUT, "persistent loop: the kernel did not stop within 5 s");
-  loop_reap(e);
-  if (!why.empty()) fail(AURA_B200_E_TIMEOUT, why);
-}
 void reset_state(aura_b200_engine* e) {
   BlockArgs& a = e->args;
   const size_t N = e->N, NF = N / 2;
@@ -1090,8 +913,10 @@ void reset_state(aura_b200_engine* e) {
   }
   CK(cudaStreamSynchronize(s));
   e->blocks = 0;
-  e->loop_posted = 0;  // the persistent loop restarts at block 0 too
+  e->block_base = 0;
   for (size_t i = 0; i < e->n_outflags; ++i) reinterpret_cast<volatile unsigned long long*>(e->h_outflag)[i] = 0;
+  // a shard-exchange timeout is cleared by a coordinated reset of every shard
+  *reinterpret_cast<volatile unsigned*>(e->h_status) = 0u;
 }
 
 void alloc_synth(aura_b200_engine* e, BlockArgs& a) {
@@ -1281,7 +1106,7 @@ int aura_b200_auralizer_create(const aura_b200_config* cfg,
     a.gain = input_gain;
     a.mu = mu;
     a.lambda = afc ? afc->lambda : 0.9f;
-    a.delta = afc ? afc->delta : kDefaultDeltaPerBin * (float)(2 * N);
+    a.delta = afc ? afc->delta : kDefaultDeltaPerN * (float)N;
     a.nlms = mu > 0.0f;
     e->w_elems = Q * L * e->KF * NF;
     a.W = dalloc<float4>(e->w_elems, e->dmem);
@@ -1322,7 +1147,15 @@ void aura_b200_destroy(aura_b200_engine* e) { delete e; }
 namespace {
 // The device block number the next graph launch will process: the host
 // counts blocks; measurement calls advance host and device together.
-uint32_t device_block_hint(aura_b200_engine* e) { return (uint32_t)(e->blocks + e->dev_block_base); }
+uint64_t device_block_hint(aura_b200_engine* e) { return e->blocks + e->block_base; }
+
+// A shard peer missed the canceller exchange deadline (k_afc_finish): the
+// engine's f^ stopped tracking the other shards', so every call fails until
+// a coordinated reset of all shards.
+void check_shard_status(aura_b200_engine* e) {
+  if (e->h_status && *reinterpret_cast<volatile unsigned*>(e->h_status))
+    fail(AURA_B200_E_TIMEOUT, "a shard peer missed the canceller exchange deadline (reset every shard)");
+}
 
 // Spin until every k_front CTA has published `target` in its mapped word.
 void wait_flag(aura_b200_engine* e, unsigned long long target, const char* what) {
@@ -1377,26 +1210,12 @@ int aura_b200_process(aura_b200_engine* e, const float* in, float* out) {
     for (size_t i = 0; i < n_in; ++i)
       if (!std::isfinite(in[i])) fail(AURA_B200_E_NON_FINITE_INPUT, "input contains NaN or Inf");
     CK(cudaSetDevice(e->device));
-    if (e->h_status && *reinterpret_cast<volatile unsigned*>(e->h_status))
-      fail(AURA_B200_E_TIMEOUT, "a shard peer missed the canceller exchange deadline");
-    if (e->launch_mode == 2) {  // persistent loop: doorbell in, mailbox out
-      if (loop_exited(e)) loop_reap(e);  // parked while idle
-      if (!e->loop_running || e->loop_device_io) {
-        stop_loop(e);
-        start_loop(e, false);
-      }
-      std::memcpy(e->h_in, in, n_in * sizeof(float));
-      std::atomic_thread_fence(std::memory_order_seq_cst);
-      mbox(e)->doorbell = ++e->loop_posted;
-      loop_wait(e, &mbox(e)->out_done, e->loop_posted, "block output");
-      std::memcpy(out, e->h_out, e->L * e->N * sizeof(float));
-      ++e->blocks;
-      return;
-    }
-    // the previous block's front has completed, so the staging buffer is free
+    check_shard_status(e);
+    // every k_front CTA of the previous block (output and error-spectrum
+    // CTAs) has published its word, so none still reads the staging buffer
     std::memcpy(e->h_in, in, n_in * sizeof(float));
     std::atomic_thread_fence(std::memory_order_release);
-    const uint32_t nblk = device_block_hint(e);
+    const uint64_t nblk = device_block_hint(e);
     e->enqueue_block(e->g_block, e->args, e->ev_front);  // records ev_front after k_front
     CK(cudaEventRecord(e->ev_back, e->stream));
     if (e->use_outflag) {
@@ -1413,18 +1232,14 @@ int aura_b200_process(aura_b200_engine* e, const float* in, float* out) {
 int aura_b200_synchronize(aura_b200_engine* e) {
   return guarded([&] {
     CK(cudaSetDevice(e->device));
-    if (e->loop_running) {
-      loop_wait(e, &mbox(e)->bg_done, e->loop_posted, "block background");
-      return;
-    }
     if (e->blocks) wait_event(e, e->ev_back, "block background");
     CK(cudaStreamSynchronize(e->stream));
+    check_shard_status(e);
   });
 }
 
 int aura_b200_reset(aura_b200_engine* e) {
   return guarded([&] {
-    stop_loop(e);
     CK(cudaSetDevice(e->device));
     reset_state(e);
   });
@@ -1434,30 +1249,18 @@ int aura_b200_feedback_estimate(aura_b200_engine* e, float* out) {
   return guarded([&] {
     if (!e->aur) fail(AURA_B200_E_INVALID_ARGUMENT, "not an auralizer");
     CK(cudaSetDevice(e->device));
-    if (e->loop_running) {  // f^ lands in the mapped copy when the block is done
-      loop_wait(e, &mbox(e)->bg_done, e->loop_posted, "block background");
-    } else {
-      if (e->blocks) wait_event(e, e->ev_back, "block background");
-      CK(cudaStreamSynchronize(e->stream));
-    }
+    if (e->blocks) wait_event(e, e->ev_back, "block background");
+    CK(cudaStreamSynchronize(e->stream));
+    check_shard_status(e);
     std::memcpy(out, e->h_fhat, sizeof(float) * e->P * e->N);
-  });
-}
-
-int aura_b200_feedback_estimate_view(aura_b200_engine* e, const float** out) {
-  return guarded([&] {
-    if (!e->aur) fail(AURA_B200_E_INVALID_ARGUMENT, "not an auralizer");
-    *out = e->h_fhat;
   });
 }
 
 int aura_b200_fdl_slot(aura_b200_engine* e, int which, size_t channel, size_t age,
                        float* out) {
   return guarded([&] {
-    stop_loop(e);
     CK(cudaSetDevice(e->device));
     CK(cudaStreamSynchronize(e->stream));
-    const size_t NF = e->N / 2;
     size_t cap, chans;
     const float4* base;
     if (which == 0) {
@@ -1472,11 +1275,12 @@ int aura_b200_fdl_slot(aura_b200_engine* e, int which, size_t channel, size_t ag
     }
     if (channel >= chans || age >= (which == 0 ? e->K : e->KF))
       fail(AURA_B200_E_INVALID_ARGUMENT, "delay-line index out of range");
-    // block b's spectrum lives at slot b % cap; age a is block (blocks-1-a)
-    const long long blk = (long long)e->blocks - 1 - (long long)age;
+    // device block b's spectrum lives at slot b % cap; age a is host block
+    // (blocks-1-a), device block (blocks-1-a) + block_base
     std::vector<float2> buf(e->N, make_float2(0.f, 0.f));
-    if (blk >= 0) {  // tiled [ch][CTn][cap][CT]
-      const size_t slot = (size_t)(blk % (long long)cap);
+    if (age < e->blocks) {  // tiled [ch][CTn][cap][CT]
+      const uint64_t blk = e->blocks - 1 - age + e->block_base;
+      const size_t slot = (size_t)(blk % (uint64_t)cap);
       const size_t CT = e->args.CT, CTn = e->args.CTn;
       for (size_t c = 0; c < CTn; ++c)
         CK(cudaMemcpy(buf.data() + 2 * c * CT, base + ((channel * CTn + c) * cap + slot) * CT,
@@ -1486,16 +1290,26 @@ int aura_b200_fdl_slot(aura_b200_engine* e, int which, size_t channel, size_t ag
   });
 }
 
+int aura_b200_seek_block(aura_b200_engine* e, uint64_t n) {
+  return guarded([&] {
+    if (e->blocks) fail(AURA_B200_E_INVALID_ARGUMENT, "seek only before the first block (or after reset)");
+    if (e->G > 1) fail(AURA_B200_E_INVALID_ARGUMENT, "seek does not apply to sharded engines");
+    CK(cudaSetDevice(e->device));
+    CK(cudaStreamSynchronize(e->stream));
+    // every delay line is zero here, so starting the ring slots (block mod
+    // K) at n instead of 0 changes no value
+    DevState st{};
+    st.block = n;
+    CK(cudaMemcpy(e->args.st, &st, sizeof(st), cudaMemcpyHostToDevice));
+    e->block_base = n;
+  });
+}
+
 int aura_b200_set_launch_mode(aura_b200_engine* e, int mode) {
   return guarded([&] {
-    if (mode < 0 || mode > 2)
-      fail(AURA_B200_E_INVALID_ARGUMENT, "launch mode is 0 (graph), 1 (stream) or 2 (persistent loop)");
+    if (mode < 0 || mode > 1)
+      fail(AURA_B200_E_INVALID_ARGUMENT, "launch mode is 0 (one CUDA graph per block) or 1 (kernels on the stream)");
     CK(cudaSetDevice(e->device));
-    stop_loop(e);
-    if (mode == 2 && !e->loop_ok)
-      fail(AURA_B200_E_BACKEND_UNAVAILABLE, "persistent loop mode unavailable: " + e->loop_why);
-    if (mode == 2 && e->G > 1)
-      fail(AURA_B200_E_INVALID_ARGUMENT, "persistent loop mode does not run sharded engines");
     CK(cudaStreamSynchronize(e->stream));
     e->launch_mode = mode;
   });
@@ -1503,24 +1317,8 @@ int aura_b200_set_launch_mode(aura_b200_engine* e, int mode) {
 
 int aura_b200_launch_mode(const aura_b200_engine* e) { return e->launch_mode; }
 
-// Diagnostics: per-block phase stamps of the last loop-mode device timing,
-// us from the block's release: {output written, input spectra pushed,
-// canceller heads done, streaming done, block done} x blocks.
-int aura_b200_loop_phases(const aura_b200_engine* e, size_t blocks, double* out) {
-  return guarded([&] {
-    const size_t nb = e->loop_last_stamps.size() / kLoopStamps;
-    if (blocks > nb) fail(AURA_B200_E_INVALID_ARGUMENT, "fewer loop-mode blocks were timed");
-    for (size_t b = 0; b < blocks; ++b) {
-      const unsigned long long* t = &e->loop_last_stamps[(size_t)kLoopStamps * b];
-      for (int k = 1; k < kLoopStamps; ++k)
-        out[b * (kLoopStamps - 1) + k - 1] = t[k] ? (double)(long long)(t[k] - t[0]) * 1e-3 : -1.0;
-    }
-  });
-}
-
 int aura_b200_set_input_gain(aura_b200_engine* e, float gain) {
   return guarded([&] {
-    stop_loop(e);
     if (!e->aur) fail(AURA_B200_E_INVALID_ARGUMENT, "not an auralizer");
     CK(cudaSetDevice(e->device));
     CK(cudaStreamSynchronize(e->stream));
@@ -1540,7 +1338,6 @@ int aura_b200_mode(const aura_b200_engine* e) { return e->mode; }
 
 int aura_b200_filter_spectrum(aura_b200_engine* e, size_t row, size_t k, float* out) {
   return guarded([&] {
-    stop_loop(e);
     const size_t rows = e->mode == AURA_B200_MIMO ? e->Q * e->L : e->L;
     if (row >= rows || k >= e->K) fail(AURA_B200_E_INVALID_ARGUMENT, "spectrum index out of range");
     CK(cudaSetDevice(e->device));
@@ -1565,7 +1362,6 @@ int aura_b200_filter_spectrum(aura_b200_engine* e, size_t row, size_t k, float* 
 
 int aura_b200_afc_coeffs(aura_b200_engine* e, float* out) {
   return guarded([&] {
-    stop_loop(e);
     if (!e->aur) fail(AURA_B200_E_INVALID_ARGUMENT, "not an auralizer");
     CK(cudaSetDevice(e->device));
     CK(cudaStreamSynchronize(e->stream));
@@ -1626,7 +1422,6 @@ void shard_finalize(aura_b200_engine* e, char* const* peers) {
 
 int aura_b200_shard_export(aura_b200_engine* e, int world, int rank, void* handle) {
   return guarded([&] {
-    stop_loop(e);
     if (!e || !handle) fail(AURA_B200_E_INVALID_ARGUMENT, "null argument");
     shard_alloc(e, world, rank);
     cudaIpcMemHandle_t h;
@@ -1702,38 +1497,12 @@ int aura_b200_time_device_blocks(aura_b200_engine* e, const float* host_in,
                                  size_t n_in_blocks, size_t blocks, float* latency_us,
                                  float* block_us) {
   return guarded([&] {
-    stop_loop(e);
     CK(cudaSetDevice(e->device));
     CK(cudaStreamSynchronize(e->stream));
     const size_t per = (size_t)e->Qx * e->N;
     if (host_in && n_in_blocks) {
       const size_t nb = std::min(n_in_blocks, e->pool_blocks);
       CK(cudaMemcpy(e->d_in_pool, host_in, nb * per * sizeof(float), cudaMemcpyHostToDevice));
-    }
-    if (e->launch_mode == 2) {
-      // persistent loop: all blocks released at once (back to back); per
-      // block the kernel stamps %globaltimer when the leader released it,
-      // when its output was written and when it was complete
-      for (size_t done = 0; done < blocks;) {
-        const size_t nb = std::min<size_t>(blocks - done, kLoopStampCap);
-        start_loop(e, true);
-        const uint64_t n0 = e->loop_posted;
-        e->loop_posted = n0 + nb;
-        mbox(e)->doorbell = e->loop_posted;
-        std::atomic_thread_fence(std::memory_order_seq_cst);
-        stop_loop(e);
-        std::vector<unsigned long long> st((size_t)kLoopStamps * nb);
-        CK(cudaMemcpy(st.data(), e->d_stamps, st.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
-        e->loop_last_stamps = st;
-        for (size_t b = 0; b < nb; ++b) {
-          const unsigned long long* t = &st[(size_t)kLoopStamps * b];
-          block_us[done + b] = (float)((double)(long long)(t[5] - t[0]) * 1e-3);
-          if (latency_us) latency_us[done + b] = (float)((double)(long long)(t[1] - t[0]) * 1e-3);
-        }
-        done += nb;
-      }
-      e->blocks += blocks;
-      return;
     }
     // one block graph per pool slot (the input pointer is baked per slot)
     const size_t slots = std::max<size_t>(1, std::min(n_in_blocks, e->pool_blocks));
@@ -1829,7 +1598,6 @@ int aura_b200_time_host_blocks(aura_b200_engine* e, const float* host_in,
 int aura_b200_time_host_breakdown(aura_b200_engine* e, const float* host_in, size_t n_in_blocks,
                                   size_t blocks, double pace_us, double* out) {
   return guarded([&] {
-    stop_loop(e);
     if (e->launch_mode != 0) fail(AURA_B200_E_INVALID_ARGUMENT, "graph mode only");
     CK(cudaSetDevice(e->device));
     const size_t per = (size_t)e->Qx * e->N;
@@ -1850,7 +1618,7 @@ int aura_b200_time_host_breakdown(aura_b200_engine* e, const float* host_in, siz
       std::memcpy(e->h_in, host_in + (b % n_in_blocks) * per, per * sizeof(float));
       std::atomic_thread_fence(std::memory_order_release);
       const auto t1 = clk::now();
-      const uint32_t nblk = device_block_hint(e);
+      const uint64_t nblk = device_block_hint(e);
       CK(cudaGraphLaunch(e->g_block.ex, e->stream));
       const auto t2 = clk::now();
       CK(cudaEventRecord(e->ev_back, e->stream));
@@ -1874,7 +1642,6 @@ int aura_b200_time_host_breakdown(aura_b200_engine* e, const float* host_in, siz
 int aura_b200_profile_phases(aura_b200_engine* e, size_t blocks, float* phase_us,
                              int* n_phases) {
   return guarded([&] {
-    stop_loop(e);
     CK(cudaSetDevice(e->device));
     CK(cudaStreamSynchronize(e->stream));
     const int np = PH_COUNT;
@@ -1908,23 +1675,35 @@ int aura_b200_profile_phases(aura_b200_engine* e, size_t blocks, float* phase_us
 
 int aura_b200_time_phase(aura_b200_engine* e, int phase, size_t reps, float* avg_us) {
   return guarded([&] {
-    stop_loop(e);
     if (phase != PH_BACK && phase != PH_FRONT && phase != PH_REDUCE)
       fail(AURA_B200_E_INVALID_ARGUMENT, "only the front, k_back and k_reduce can be re-launched");
     if (phase == PH_BACK && !e->has_back())
       fail(AURA_B200_E_INVALID_ARGUMENT, "this engine has no streaming work");
+    if (e->G > 1) fail(AURA_B200_E_INVALID_ARGUMENT, "time phases on an unsharded engine");
     CK(cudaSetDevice(e->device));
     CK(cudaStreamSynchronize(e->stream));
+    // The relaunches are not idempotent (k_reduce advances the block
+    // counter, k_back updates W in place, the fused canceller head shifts
+    // the loudspeaker history): snapshot every mutable device buffer and put
+    // it back afterwards, so the engine continues as if this never ran.
+    const auto state = e->mutable_state();
+    size_t total = 0;
+    for (auto& b : state) total += (b.second + 255) & ~size_t(255);
+    char* snap = nullptr;
+    CK(cudaMalloc(&snap, std::max<size_t>(total, 1)));
+    auto copy_all = [&](bool save) {
+      size_t off = 0;
+      for (auto& b : state) {
+        char* s0 = snap + off;
+        CK(cudaMemcpyAsync(save ? s0 : b.first, save ? b.first : s0, b.second, cudaMemcpyDeviceToDevice,
+                           e->stream));
+        off += (b.second + 255) & ~size_t(255);
+      }
+    };
+    copy_all(true);
     // single launches, back to back without programmatic overlap, so the
     // mean is one launch's duration (ramp-up and tail included)
     BlockArgs a = e->dev_args;
-    // k_reduce advances the block counter: restore it afterwards (the
-    // re-launches re-sum the same partials; the canceller state is
-    // re-derived from them, as in the timed block)
-    DevState st0{};
-    CK(cudaMemcpy(&st0, a.st, sizeof(DevState), cudaMemcpyDeviceToHost));
-    std::vector<float2> pw0(a.pw && phase == PH_REDUCE ? (size_t)a.N : 0);  // the smoothed power too
-    if (!pw0.empty()) CK(cudaMemcpy(pw0.data(), a.pw, pw0.size() * sizeof(float2), cudaMemcpyDeviceToHost));
     e->pdl_off = true;
     e->launch_phase(phase, a, e->stream);  // warm
     cudaEvent_t t0, t1;
@@ -1941,14 +1720,16 @@ int aura_b200_time_phase(aura_b200_engine* e, int phase, size_t reps, float* avg
     cudaEventDestroy(t0);
     cudaEventDestroy(t1);
     *avg_us = 1000.0f * ms / (float)reps;
-    CK(cudaMemcpy(a.st, &st0, sizeof(DevState), cudaMemcpyHostToDevice));
-    if (!pw0.empty()) CK(cudaMemcpy(a.pw, pw0.data(), pw0.size() * sizeof(float2), cudaMemcpyHostToDevice));
+    copy_all(false);
+    CK(cudaStreamSynchronize(e->stream));
+    CK(cudaFree(snap));
+    if (e->aur)  // the mapped host copy of f^ (k_reduce rewrote it)
+      CK(cudaMemcpy(e->h_fhat, e->args.fhat, sizeof(float) * e->P * e->N, cudaMemcpyDeviceToHost));
   });
 }
 
 int aura_b200_trace_blocks(aura_b200_engine* e, size_t blocks, double* out) {
   return guarded([&] {
-    stop_loop(e);
     CK(cudaSetDevice(e->device));
     CK(cudaStreamSynchronize(e->stream));
     blocks = std::min<size_t>(blocks, kTraceBlocks);
@@ -2012,7 +1793,6 @@ int aura_b200_trace_blocks(aura_b200_engine* e, size_t blocks, double* out) {
 int aura_b200_trace_back(aura_b200_engine* e, size_t blocks, double* out_segs, size_t* n_segs,
                          double* out_ctas, size_t* n_ctas) {
   return guarded([&] {
-    stop_loop(e);
     const size_t ns = e->h_chunks.size(), nc = (size_t)e->back_ctas;
     if (!out_segs || !out_ctas) {
       *n_segs = ns;
@@ -2070,13 +1850,12 @@ int aura_b200_describe(const aura_b200_engine* e, char* buf, size_t cap) {
                   "N=%zu Q=%zu L=%zu P=%zu K=%zu KF=%zu mode=%d LT=%d PT=%d | front: grid=%zu cpb=%d "
                   "warps=%d smem=%zu | back: ctas=%d x %d thr, CT=%d CTn=%d sp=%d spa=%d stages=%d slot=%d B "
                   "smem=%zu partials=%zu+%zu items=%d (static %d) w_l2=%d | reduce: %d+%d ctas l2keep=%d "
-                  "nlms=%d delta=%g",
+                  "nlms=%d delta=%g knobs=%s",
                   e->N, e->Q, e->L, e->P, e->K, e->KF, e->mode, e->LT, e->PT,
                   (e->L + a.cpb - 1) / a.cpb, a.cpb, a.front_warps, e->smem_front, e->back_ctas, kBackThreads, a.CT,
                   a.CTn, a.sp, a.spa, a.stages, a.slot_f4 * 16, e->smem_back, e->n_syn_segs,
                   e->n_afc_segs, a.n_chunks, a.n_static, a.w_in_l2, a.red_syn_ctas, a.red_afc_ctas, a.h_in_l2,
-                  a.nlms,
-                  (double)a.delta);
+                  a.nlms, (double)a.delta, e->knobs.empty() ? "none" : e->knobs.c_str());
   });
 }
 

@@ -45,13 +45,18 @@ constexpr int kMacThreads = 256;
 constexpr int kTailThreads = 256;
 constexpr int kFrontThreads = 256;
 
+// Block numbers are 64-bit: a 32-bit counter wraps after 2^32 blocks (16.6
+// days at N = 16, 48 kHz) and, as 2^32 is no multiple of K, would reorder
+// the delay-line rings (slot = block mod K) at the wrap.
+typedef unsigned long long blk_t;
+
 // Device-resident stream state: index of the block in flight. Every kernel
 // of block n (front and background) reads it; the last CTA of the
 // background's tail kernels (ticket) moves it to n + 1.
 struct DevState {
-  uint32_t block;
+  blk_t block;
   uint32_t ticket;
-  uint32_t pad[2];
+  uint32_t pad;
 };
 
 // Optional timeline trace (%globaltimer, ns): per traced block slot and
@@ -68,32 +73,11 @@ enum TraceId {
 // Loudspeaker-channel sharding: at most kMaxShards engines
 // (one per GPU, or virtual shards on one GPU) exchange their canceller
 // partials every block. Each engine owns an exchange buffer: kMaxShards
-// uint32 flags (flag g = 1 + last block whose partial shard g delivered),
+// u64 flags (flag g = 1 + last block whose partial shard g delivered),
 // padded to kXFlagBytes, then slots[2 parities][G][P*N + 2N] floats.
 constexpr int kMaxShards = 8;
 constexpr size_t kXFlagBytes = 256;
 constexpr unsigned long long kShardTimeoutNs = 5ull * 1000 * 1000 * 1000;
-
-// Host <-> persistent kernel mailbox, in pinned mapped host memory.
-struct LoopMailbox {
-  unsigned long long doorbell;  // host: blocks released (block n runs once doorbell > n)
-  unsigned long long out_done;  // device: last block whose output is written, + 1
-  unsigned long long bg_done;   // device: last block completely done, + 1
-  unsigned stop;                // host: leave the loop before the next block
-  unsigned err;                 // device: an internal wait timed out
-  unsigned parked;              // device: left the loop after loop_idle_ns without a doorbell
-  unsigned pad;
-};
-// Device-side control block of the persistent kernel (zeroed at launch).
-struct LoopCtl {
-  unsigned long long go;         // leader -> grid: blocks released (or ~0: stop)
-  unsigned long long x_seq;      // front CTAs whose input spectra are pushed (cumulative)
-  unsigned long long head_seq;   // canceller heads + error spectra done (cumulative)
-  unsigned long long front_seq;  // front CTAs whose outputs are written (cumulative)
-  unsigned bar_count, bar_gen;   // grid barrier
-  unsigned err;
-  unsigned pad;
-};
 
 struct BlockArgs {
   // geometry
@@ -117,7 +101,6 @@ struct BlockArgs {
   int n_syn_tiles;   // (L/LT) * CTn
   int h_in_l2;       // spectra fit in L2: stream them with evict_normal
   int w_in_l2;       // canceller W + delay lines fit in L2: keep W there (evict_last)
-  int dbg;           // experiment switches (AURA_B200_DBG; 0 in production)
   const int4* chunks;   // work items {kind | tile << 1, b, e, partial slot in tile}:
                         //   [n_static] per-CTA static pieces, then [n_chunks - n_static] queue
   int n_chunks, n_static;
@@ -131,24 +114,16 @@ struct BlockArgs {
   int red_syn_ctas, red_syn_cpt;  // k_reduce: synthesis CTAs, CTAs per tile
   int red_afc_ctas, red_afc_cpt;  // canceller CTAs, CTAs per column tile
   int red_afc_rows;               // canceller partial rows: P (+1 power row with NLMS)
-  // persistent loop mode (loop.cuh)
-  struct LoopMailbox* mbox;     // pinned mapped: doorbell / output done / block done / stop / error
-  struct LoopCtl* ctl;          // device control block
-  int loop_front_ctas;          // CTAs running the front half
-  int in_slots;                 // input block n is in + (n % in_slots) * (inputs x N)
   float* hist1;                 // second window-history buffer (the first is prev_in)
-  unsigned long long* loop_stamps;  // per block {released, output written, done} (%globaltimer)
-  unsigned long long loop_idle_ns;  // park (exit) after this long without a doorbell
-  int loop_hold;                    // producers start after the fronts' input spectra are pushed
-  // graph mode: front CTA b publishes (block + 1) in out_flag[b] (mapped host
-  // memory) once its outputs are written -- the host polls these words
-  // instead of an event; one system-scope release store per CTA, no ticket
+  // front CTA b publishes (block + 1) in out_flag[b] (mapped host memory)
+  // once it is done with the block's input and its outputs are written --
+  // the host polls these words instead of an event; one system-scope
+  // release store per CTA (every k_front CTA, the error-spectrum CTAs too,
+  // so no CTA still reads the mapped input when process() returns)
   unsigned long long* out_flag;
-  unsigned* front_ticket;  // (unused)
-  // graph mode, fused head: k_front also runs the canceller head (and, on P
-  // extra CTAs, the NLMS error spectra) and k_back is its programmatic
-  // dependent; the window history then alternates prev_in / hist1 by block
-  // parity (as in the loop)
+  // fused head: k_front also runs the canceller head (and, on P extra CTAs,
+  // the NLMS error spectra) and k_back is its programmatic dependent; the
+  // window history then alternates prev_in / hist1 by block parity
   int front_head;
   unsigned long long* front_seq;  // fused head: [block & 1] front CTAs done (k_reduce clears the slot)
   int front_hold;                 // ... and k_back's producers wait for all of them before streaming
@@ -245,11 +220,11 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-__device__ __forceinline__ void trace_begin(const BlockArgs& a, int id, uint32_t n) {
+__device__ __forceinline__ void trace_begin(const BlockArgs& a, int id, blk_t n) {
   if (a.trace && threadIdx.x == 0)
     atomicMin(&a.trace[((n % kTraceBlocks) * kTraceKernels + id) * 2], globaltimer());
 }
-__device__ __forceinline__ void trace_end(const BlockArgs& a, int id, uint32_t n) {
+__device__ __forceinline__ void trace_end(const BlockArgs& a, int id, blk_t n) {
   if (a.trace) {
     __syncthreads();
     if (threadIdx.x == 0)
@@ -260,7 +235,7 @@ __device__ __forceinline__ void trace_end(const BlockArgs& a, int id, uint32_t n
 // Device scope suffices: every reader of st->block for block n has read it
 // before its CTA reached this point, and the next block's front is
 // stream-ordered after the whole background graph.
-__device__ void retire_block(const BlockArgs& a, uint32_t n) {
+__device__ void retire_block(const BlockArgs& a, blk_t n) {
   __syncthreads();
   if (threadIdx.x == 0) {
     if (atomicAdd(&a.st->ticket, 1u) == (uint32_t)a.advance_total - 1) {
@@ -323,7 +298,7 @@ struct NoHook {
 };
 
 template <typename Team, typename OnX = NoHook>
-__device__ void front_body(const BlockArgs& a, uint32_t n, int c0, int c1, float2* Xs, const float* in,
+__device__ void front_body(const BlockArgs& a, blk_t n, int c0, int c1, float2* Xs, const float* in,
                            const float* prev_in, float* cur_out, bool leader, Team tm, OnX on_x = OnX()) {
   const int N = a.N, NF = a.NF;
   const int tid = tm.tid(), nt = tm.size();
@@ -364,7 +339,7 @@ __device__ void front_body(const BlockArgs& a, uint32_t n, int c0, int c1, float
                  });
       tm.sync();
       rfft_packed(wa, z, Xs + (size_t)q * N, N, a.logN, tw, split, tm);
-      if (leader) push_tiled(a, a.X, q, a.K, (int)(n % (uint32_t)a.K), Xs + (size_t)q * N, tm);
+      if (leader) push_tiled(a, a.X, q, a.K, (int)(n % (blk_t)a.K), Xs + (size_t)q * N, tm);
     }
     on_x();
   }
@@ -382,7 +357,7 @@ __device__ void front_body(const BlockArgs& a, uint32_t n, int c0, int c1, float
       tm.sync();
       for (int i = tid; i < N; i += nt) prev[i] = wa[N + i];
       rfft_packed(wa, z, Xs, N, a.logN, tw, split, tm);
-      push_tiled(a, a.X, l, a.K, (int)(n % (uint32_t)a.K), Xs, tm);
+      push_tiled(a, a.X, l, a.K, (int)(n % (blk_t)a.K), Xs, tm);
       if (l + 1 == c1) on_x();
     }
     const bool staged = a.front_pre && l == c0;
@@ -406,9 +381,9 @@ __device__ void front_body(const BlockArgs& a, uint32_t n, int c0, int c1, float
 
 // Canceller stage 1 (convolver.hpp:180-191 on fc_) for loudspeakers
 // [c0, c1): r2c of [l_{n-1}, l_n] into the canceller FDL. Team-generic
-// (k_back_head and the loop kernel). smem: 3N float2 + tables.
+// (k_front's fused head and k_back_head). smem: 3N float2 + tables.
 template <typename Team>
-__device__ void head_channels(const BlockArgs& a, uint32_t n, int c0, int c1, float2* z, const float2* tw,
+__device__ void head_channels(const BlockArgs& a, blk_t n, int c0, int c1, float2* z, const float2* tw,
                               const float2* split, Team tm) {
   const int N = a.N;
   float* wa = reinterpret_cast<float*>(z + N);         // 2N
@@ -425,7 +400,7 @@ __device__ void head_channels(const BlockArgs& a, uint32_t n, int c0, int c1, fl
     for (int i = tm.tid(); i < N; i += tm.size()) prev[i] = wa[N + i];
     if constexpr (std::is_same<Team, Warp>::value) rfft_warp_any(wa, z, sp, N, a.logN, tw, split);
     else rfft_packed(wa, z, sp, N, a.logN, tw, split, tm);
-    push_tiled(a, a.XA, l, a.KF + 1, (int)(n % (uint32_t)(a.KF + 1)), sp, tm);
+    push_tiled(a, a.XA, l, a.KF + 1, (int)(n % (blk_t)(a.KF + 1)), sp, tm);
     tm.sync();
   }
 }
@@ -462,7 +437,7 @@ __host__ __device__ inline size_t front_warps_f2(int N, int Qs, int W) {
 // always staged. After every warp's outputs: publish (as k_front), then the
 // fused canceller head per channel on the same warps.
 template <typename OnX = NoHook>
-__device__ void front_warps_body(const BlockArgs& a, uint32_t n, int c0, int c1, float2* sm,
+__device__ void front_warps_body(const BlockArgs& a, blk_t n, int c0, int c1, float2* sm,
                                  const float* in, const float* prev_in, float* cur_out, bool leader,
                                  OnX on_x = OnX()) {
   const int N = a.N, NF = a.NF;
@@ -511,7 +486,7 @@ __device__ void front_warps_body(const BlockArgs& a, uint32_t n, int c0, int c1,
                  });
       __syncwarp();
       rfft_warp_any(wq, wz, Xs + (size_t)q * N, N, a.logN, tw, split);
-      if (leader) push_tiled(a, a.X, q, a.K, (int)(n % (uint32_t)a.K), Xs + (size_t)q * N, wt);
+      if (leader) push_tiled(a, a.X, q, a.K, (int)(n % (blk_t)a.K), Xs + (size_t)q * N, wt);
     }
   }
   __syncthreads();  // every input spectrum
@@ -542,13 +517,19 @@ __device__ void front_warps_body(const BlockArgs& a, uint32_t n, int c0, int c1,
 __global__ void __launch_bounds__(kFrontThreads) k_front(BlockArgs a) {
   extern __shared__ float4 smem4[];
   if (a.front_head) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  const uint32_t n = a.st->block;
+  const blk_t n = a.st->block;
   trace_begin(a, TR_FRONT, n);
   const int nerr = (a.front_head && a.is_aur && a.nlms) ? a.P : 0;
   const int nfront = (int)gridDim.x - nerr;
   float2* work = reinterpret_cast<float2*>(smem4);
   if ((int)blockIdx.x >= nfront) {  // NLMS error spectrum E_p (fused-head mode)
     error_spectrum(a, (int)blockIdx.x - nfront, a.in, work, a.tw, a.split, Cta());
+    if (a.out_flag) {  // done with the mapped input: the host may refill it
+      __syncthreads();
+      if (threadIdx.x == 0)
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(a.out_flag + blockIdx.x), "l"(n + 1)
+                     : "memory");
+    }
     trace_end(a, TR_FRONT, n);
     return;
   }
@@ -587,8 +568,7 @@ __global__ void __launch_bounds__(kFrontThreads) k_front(BlockArgs a) {
     __syncthreads();  // every thread's output stores precede thread 0's release
     if (threadIdx.x == 0) {
       if (a.out_flag)
-        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(a.out_flag + blockIdx.x),
-                     "l"((unsigned long long)n + 1)
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(a.out_flag + blockIdx.x), "l"(n + 1)
                      : "memory");
       if (a.front_head && a.front_hold != 2) {
         __threadfence();
@@ -636,7 +616,7 @@ __global__ void __launch_bounds__(kFrontThreads) k_back_head(BlockArgs a) {
   const float2* split = a.smem_tables ? stw + N / 2 : a.split;
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (a.smem_tables) stage_tables(stw, stw + N / 2, a.tw, a.split, N);
-  const uint32_t n = a.st->block;
+  const blk_t n = a.st->block;
   trace_begin(a, TR_BACK_HEAD, n);
   const int Lb = a.is_aur ? a.L : 1;
   const int b = blockIdx.x;
@@ -666,12 +646,12 @@ __global__ void __launch_bounds__(kFrontThreads) k_back_head(BlockArgs a) {
 // ------------------------------------------------------------ k_advance
 __global__ void k_advance(DevState* st) { st->block += 1u; }  // blocks without k_back
 
-__device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
-  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+__device__ __forceinline__ void st_release_sys(blk_t* p, blk_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+__device__ __forceinline__ blk_t ld_acquire_sys(const blk_t* p) {
+  blk_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
 
@@ -686,9 +666,12 @@ __device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
 // block n+1's partial after finishing block n, which needed every shard's
 // block-n partial, and each shard consumes its block-n slots before it
 // produces block n+1 (stream order). The wait is bounded (kShardTimeoutNs):
-// a missing peer sets status_host instead of hanging the GPU.
+// a missing peer sets status_host (the host fails the next call on this
+// engine until a coordinated reset) and the block keeps the previous f^ and
+// power instead of summing stale slots; the block still retires, so the
+// device block counter stays in step with the host's.
 __global__ void __launch_bounds__(kTailThreads) k_afc_finish(BlockArgs a) {
-  const uint32_t n = a.st->block;
+  const blk_t n = a.st->block;
   trace_begin(a, TR_AFC_FINISH, n);
   const int N = a.N, P = a.P, G = a.G;
   const size_t S = (size_t)P * N + 2 * (size_t)N;
@@ -702,40 +685,43 @@ __global__ void __launch_bounds__(kTailThreads) k_afc_finish(BlockArgs a) {
   if (threadIdx.x == 0) {
     timed_out = 0;
     __threadfence_system();
-    for (int g = 0; g < G; ++g) st_release_sys(reinterpret_cast<unsigned*>(a.xpeer[g]) + a.grank, n + 1);
-    const unsigned* flags = reinterpret_cast<const unsigned*>(a.xpeer[a.grank]);
+    for (int g = 0; g < G; ++g) st_release_sys(reinterpret_cast<blk_t*>(a.xpeer[g]) + a.grank, n + 1);
+    const blk_t* flags = reinterpret_cast<const blk_t*>(a.xpeer[a.grank]);
     const unsigned long long t0 = globaltimer();
     for (int g = 0; g < G && !timed_out; ++g)
       while (ld_acquire_sys(flags + g) < n + 1) {
         if (globaltimer() - t0 > kShardTimeoutNs) {
           timed_out = 1;
           *reinterpret_cast<volatile unsigned*>(a.status_host) = 1u;
+          __threadfence_system();
           break;
         }
         __nanosleep(64);
       }
   }
   __syncthreads();
-  const float* slots = reinterpret_cast<const float*>(a.xpeer[a.grank] + kXFlagBytes) + (size_t)par * G * S;
-  for (int i = threadIdx.x; i < P * N; i += blockDim.x) {
-    float v = __ldcg(slots + i);
-    for (int g = 1; g < G; ++g) v = __fadd_rn(v, __ldcg(slots + (size_t)g * S + i));
-    a.fhat[i] = v;
-    a.fhat_host[i] = v;
-  }
-  if (a.nlms) {
-    const float oml = __fsub_rn(1.0f, a.lambda);
-    for (int j = threadIdx.x; j < N; j += blockDim.x) {
-      const float* b = slots + (size_t)P * N + 2 * j;
-      float2 sum = make_float2(__ldcg(b), __ldcg(b + 1));
-      for (int g = 1; g < G; ++g) {
-        sum.x = __fadd_rn(sum.x, __ldcg(b + (size_t)g * S));
-        sum.y = __fadd_rn(sum.y, __ldcg(b + (size_t)g * S + 1));
+  if (!timed_out) {
+    const float* slots = reinterpret_cast<const float*>(a.xpeer[a.grank] + kXFlagBytes) + (size_t)par * G * S;
+    for (int i = threadIdx.x; i < P * N; i += blockDim.x) {
+      float v = __ldcg(slots + i);
+      for (int g = 1; g < G; ++g) v = __fadd_rn(v, __ldcg(slots + (size_t)g * S + i));
+      a.fhat[i] = v;
+      a.fhat_host[i] = v;
+    }
+    if (a.nlms) {
+      const float oml = __fsub_rn(1.0f, a.lambda);
+      for (int j = threadIdx.x; j < N; j += blockDim.x) {
+        const float* b = slots + (size_t)P * N + 2 * j;
+        float2 sum = make_float2(__ldcg(b), __ldcg(b + 1));
+        for (int g = 1; g < G; ++g) {
+          sum.x = __fadd_rn(sum.x, __ldcg(b + (size_t)g * S));
+          sum.y = __fadd_rn(sum.y, __ldcg(b + (size_t)g * S + 1));
+        }
+        float2 w = a.pw[j];
+        w.x = __fadd_rn(__fmul_rn(a.lambda, w.x), __fmul_rn(oml, sum.x));
+        w.y = __fadd_rn(__fmul_rn(a.lambda, w.y), __fmul_rn(oml, sum.y));
+        a.pw[j] = w;
       }
-      float2 w = a.pw[j];
-      w.x = __fadd_rn(__fmul_rn(a.lambda, w.x), __fmul_rn(oml, sum.x));
-      w.y = __fadd_rn(__fmul_rn(a.lambda, w.y), __fmul_rn(oml, sum.y));
-      a.pw[j] = w;
     }
   }
   trace_end(a, TR_AFC_FINISH, n);

@@ -71,35 +71,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-// Bounded wait (persistent loop): false once *abort is set or ~2 s pass.
-__device__ __forceinline__ bool mbar_wait_bounded(uint64_t* b, uint32_t parity, const unsigned* abort) {
-  if (!abort) {
-    mbar_wait(b, parity);
-    return true;
-  }
-  const unsigned long long t0 = globaltimer();
-  for (unsigned spin = 0;; ++spin) {
-    uint32_t ok;
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-        "selp.u32 %0, 1, 0, p;\n"
-        "}\n"
-        : "=r"(ok)
-        : "r"(smem_u32(b)), "r"(parity)
-        : "memory");
-    if (ok) return true;
-    if ((spin & 255u) == 255u) {
-      if (*reinterpret_cast<const volatile unsigned*>(abort)) return false;
-      if (globaltimer() - t0 > 2000000000ull) {
-        atomicExch(const_cast<unsigned*>(abort), 1u);  // tell the rest of the grid
-        return false;
-      }
-    }
-  }
-}
-
 // global -> shared bulk copy completing on an mbarrier, with an L2 policy
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
                                          uint64_t policy) {
@@ -179,34 +150,21 @@ __device__ __forceinline__ void copy_ring(float4* dst, const float4* base, int v
 // (synthesis, MIMO) or a loudspeaker (canceller), so its delay-line rows are
 // one ring run. Canceller stages also carry the column tile's NLMS error
 // spectra and smoothed power.
-// What the producer must wait for before streaming rows produced by the
-// current block's front half. Graph mode: k_front finished before k_back
-// launched (stream order), and k_back_head is the PDL primary.
-// Fused-head mode (front_head): k_front itself is the PDL primary, so rows
-// it produces (X age 0) wait for it too.
-struct GraphDeps {
-  int front_pdl = 0;
-  __device__ __forceinline__ const unsigned* abort() const { return nullptr; }
-  __device__ __forceinline__ bool wait_front(uint32_t) const {
-    if (front_pdl) griddep_wait();
-    return true;
-  }
-  __device__ __forceinline__ bool wait_head(uint32_t) const {
-    griddep_wait();
-    return true;
-  }
-};
-
-template <int LT, bool ELEM, int PT, typename Deps = GraphDeps>
-__device__ __forceinline__ void back_produce(const BlockArgs& a, uint32_t n, uint64_t* full,
+// What the producer waits for before streaming rows produced by the
+// current block's front half: with a separate k_back_head, k_front finished
+// before k_back launched (stream order) and k_back_head is the PDL primary;
+// in fused-head mode (front_head) k_front itself is the PDL primary, so rows
+// it produces (X age 0) wait for it too (griddepcontrol.wait).
+template <int LT, bool ELEM, int PT>
+__device__ __forceinline__ void back_produce(const BlockArgs& a, blk_t n, uint64_t* full,
                                              uint64_t* empty, float4* slots, StageMeta* meta,
-                                             uint32_t& q, Deps deps = Deps()) {
+                                             uint32_t& q) {
   constexpr int XL = ELEM ? LT : 1;
   const int S = a.stages, CT = a.CT, CTn = a.CTn, K = a.K, KF = a.KF;
   const int Kt = K - 1, cap = KF + 1;
   const int T = (a.mode == 2 ? a.Q : 1) * Kt;
-  const int nk = (int)(n % (uint32_t)K);
-  const int nka = PT > 0 ? (int)(n % (uint32_t)cap) : 0;
+  const int nk = (int)(n % (blk_t)K);
+  const int nka = PT > 0 ? (int)(n % (blk_t)cap) : 0;
   const uint64_t pol_stream = a.h_in_l2 ? policy_evict_normal() : policy_evict_first();
   const uint64_t pol_keep = policy_evict_last();
   unsigned* queue = a.tick + a.tick_queue;
@@ -218,7 +176,7 @@ __device__ __forceinline__ void back_produce(const BlockArgs& a, uint32_t n, uin
     const int d = a.n_static + (int)atomicAdd(queue, 1u);
     return d < a.n_chunks ? d : -1;
   };
-  bool waited = false, front_ok = false;
+  bool waited = false, front_ok = !a.front_head;
   // ring cursor, advanced incrementally (no divisions on the per-stage path)
   int s = (int)(q % (uint32_t)S);
   uint32_t par = ((q / (uint32_t)S) & 1u) ^ 1u;
@@ -230,10 +188,9 @@ __device__ __forceinline__ void back_produce(const BlockArgs& a, uint32_t n, uin
     const int4 nrec = nidx >= 0 ? a.chunks[nidx] : make_int4(0, 0, 0, 0);
     const int kind = rec.x & 1, tile = rec.x >> 1;
     const int4 ti = a.tinfo[kind ? a.n_syn_tiles + tile : tile];
-    bool abort = false;
     if (PT > 0 && kind == 1 && !waited) {
-      waited = deps.wait_head(n);  // canceller inputs come from the head (k_back_head)
-      abort = !waited;
+      griddep_wait();  // canceller inputs come from the head
+      waited = true;
     }
     // per item: the input (synthesis) or loudspeaker (canceller) block b of
     // the first stage; stages never cross a block boundary
@@ -242,24 +199,18 @@ __device__ __forceinline__ void back_produce(const BlockArgs& a, uint32_t n, uin
     int b = rec.y / B, b0 = b * B;
     const int g = tile / CTn, c = tile - g * CTn;
     const float4* hsrc = a.Ht + (size_t)tile * T * LT * CT;
-    const uint32_t syn_tx = (uint32_t)(((a.dbg & 2) ? LT : LT + XL) * CT) * 16u;
-    for (int t = rec.y; t < rec.z && !abort;) {
+    const uint32_t syn_tx = (uint32_t)((LT + XL) * CT) * 16u;
+    for (int t = rec.y; t < rec.z;) {
       if (t == b0 + B) {
         ++b;
         b0 += B;
       }
       const int t1 = min(min(t + SP, rec.z), b0 + B);
       if (!front_ok && kind == 0 && t == b0) {
-        front_ok = deps.wait_front(n);  // this stage reads X(age 0), pushed by the front
-        if (!front_ok) {
-          abort = true;
-          break;
-        }
+        griddep_wait();  // this stage reads X(age 0), pushed by the front
+        front_ok = true;
       }
-      if (!mbar_wait_bounded(empty + s, par, deps.abort())) {
-        abort = true;
-        break;
-      }
+      mbar_wait(empty + s, par);
       meta[s] = StageMeta{idx, t, t1, (t1 == rec.z ? 1 : 0) | (kind << 1), tile, rec.w, ti};
       float4* dst = slots + (size_t)s * a.slot_f4;
       const int nt = t1 - t;
@@ -269,7 +220,7 @@ __device__ __forceinline__ void back_produce(const BlockArgs& a, uint32_t n, uin
         bulk_g2s(dst, hsrc + (size_t)t * LT * CT, (uint32_t)(nt * LT * CT) * 16u, full + s, pol_stream);
         float4* xd = dst + (size_t)a.sp * LT * CT;
 #pragma unroll
-        for (int i = 0; i < XL && !(a.dbg & 2); ++i) {
+        for (int i = 0; i < XL; ++i) {
           const int xc = ELEM ? g * LT + i : b;
           copy_ring(xd + (size_t)i * a.sp * CT, a.X + (size_t)(xc * CTn + c) * K * CT, nk - (j1 - 1),
                     nk - j0, K, CT, full + s, pol_keep);
@@ -302,11 +253,10 @@ __device__ __forceinline__ void back_produce(const BlockArgs& a, uint32_t n, uin
       }
       t = t1;
     }
-    if (abort) break;  // a dependency wait failed (loop mode timeout): stop streaming
     idx = nidx;
     rec = nrec;
   }
-  if (!mbar_wait_bounded(empty + s, par, deps.abort())) return;
+  mbar_wait(empty + s, par);
   meta[s].item = -1;
   mbar_arrive(full + s);
   ++q;
@@ -349,21 +299,19 @@ __device__ __forceinline__ void team_partial(float4 (&acc)[RM], int R, int CT, i
 // sentinel (q is the CTA's running stage count, shared with the producer's
 // by construction), leaving one split-K partial per work item.
 template <int LT, bool ELEM, int PT>
-__device__ __forceinline__ void back_consume(const BlockArgs& a, uint32_t n, uint64_t* full,
+__device__ __forceinline__ void back_consume(const BlockArgs& a, blk_t n, uint64_t* full,
                                              uint64_t* empty, StageMeta* meta, float4* red,
-                                             float4* slots, uint32_t& q, unsigned long long* ctr,
-                                             const unsigned* abort = nullptr) {
+                                             float4* slots, uint32_t& q, unsigned long long* ctr) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int S = a.stages;
   (void)n;
   // consumer geometry: lane = pl * 8 + cl ; warp = pg * CG + cg
-  const int CT = a.CT, CTn = a.CTn, K = a.K, KF = a.KF, NF = a.NF;
+  const int CT = a.CT, CTn = a.CTn, KF = a.KF;
   const int CG = CT >> 3, PG = 8 / CG, PH = PG * 4;
   const int cl = lane & 7, pl = lane >> 3;
   const int cg = warp % CG, pg = warp / CG;
   const int f = cg * 8 + cl;     // column within the tile
   const int ph = pg * 4 + pl;    // tap phase
-  const int Kt = K - 1;
   const int P = PT > 0 ? a.P : 0;
   const int nl = PT > 0 ? a.nlms : 0;
   const int R = P + nl;  // canceller partial rows; row P: loudspeaker power
@@ -382,9 +330,9 @@ __device__ __forceinline__ void back_consume(const BlockArgs& a, uint32_t n, uin
     }
   };
   for (;;) {
-    if (!mbar_wait_bounded(full + sl, par, abort)) return;
+    mbar_wait(full + sl, par);
     StageMeta m = meta[sl];
-    if (m.item < 0) {  // sentinel: release its slot too (the ring persists in the loop)
+    if (m.item < 0) {  // sentinel: release its slot too
       __syncwarp();
       if (lane == 0) mbar_arrive(empty + sl);
       break;
@@ -404,7 +352,7 @@ __device__ __forceinline__ void back_consume(const BlockArgs& a, uint32_t n, uin
         const int nt = m.t1 - m.t;
         const float4* hs = slots + (size_t)sl * a.slot_f4;
         const float4* xs = hs + (size_t)a.sp * LT * CT;
-        for (int i = ph; i < nt && !(a.dbg & 1); i += PH) {
+        for (int i = ph; i < nt; i += PH) {
           const int r = nt - 1 - i;  // X rows are stored oldest-first
           if (ELEM) {
 #pragma unroll
@@ -425,7 +373,7 @@ __device__ __forceinline__ void back_consume(const BlockArgs& a, uint32_t n, uin
         if (lane == 0) mbar_arrive(empty + sl);
         advance();
         if (m.flags & 1) break;
-        if (!mbar_wait_bounded(full + sl, par, abort)) return;
+        mbar_wait(full + sl, par);
         m = meta[sl];
       }
       const int E = LT * CT;
@@ -531,7 +479,7 @@ __device__ __forceinline__ void back_consume(const BlockArgs& a, uint32_t n, uin
         if (lane == 0) mbar_arrive(empty + sl);
         advance();
         if (m.flags & 1) break;
-        if (!mbar_wait_bounded(full + sl, par, abort)) return;
+        mbar_wait(full + sl, par);
         m = meta[sl];
       }
       const int E = R * CT;
@@ -572,11 +520,9 @@ __global__ void __launch_bounds__(kBackThreads, 1) k_back(const __grid_constant_
   }
   griddep_launch();  // k_reduce may take the SMs this kernel's CTAs leave
   __syncthreads();
-  const uint32_t n = a.st->block;
+  const blk_t n = a.st->block;
   if (warp == kConsumers / 32) {
     uint32_t qp = 0;
-    GraphDeps deps;
-    deps.front_pdl = a.front_head;
     if (lane == 0) {
       if (a.front_head && a.front_hold) {
         // launched early (PDL) so this CTA is resident; hold the stream until
@@ -589,7 +535,7 @@ __global__ void __launch_bounds__(kBackThreads, 1) k_back(const __grid_constant_
           __nanosleep(100);
         }
       }
-      back_produce<LT, ELEM, PT>(a, n, full, empty, slots, meta, qp, deps);
+      back_produce<LT, ELEM, PT>(a, n, full, empty, slots, meta, qp);
     }
     return;
   }
@@ -670,7 +616,7 @@ __device__ __forceinline__ int4 reduce_tile_info(const BlockArgs& a, int b) {
 // threads; ti = reduce_tile_info(a, b); s_last: shared int. The partials
 // must be complete and visible.
 template <typename Team>
-__device__ void reduce_part(const BlockArgs& a, int b, uint32_t n, float4* rsm, int* s_last, Team tm,
+__device__ void reduce_part(const BlockArgs& a, int b, blk_t n, float4* rsm, int* s_last, Team tm,
                             const int4 ti) {
   const int CT = a.CT, NF = a.NF;
   const int tid = tm.tid();
@@ -812,7 +758,7 @@ __global__ void __launch_bounds__(kReduceThreads) k_reduce(const __grid_constant
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   reduce_prefetch(a, blockIdx.x, rsm, Cta());
   // neither is written by k_back: load them before waiting for it
-  const uint32_t n = a.st->block;
+  const blk_t n = a.st->block;
   const int4 ti = reduce_tile_info(a, blockIdx.x);
   griddep_wait();  // k_back's partials
   trace_begin(a, TR_REDUCE, n);

@@ -47,3 +47,13 @@ def decaying_filters(rng, rows, n, fs=48000, t60_s=None, scale=1.0):
     h = rng.standard_normal((rows, n)) * env
     h /= np.sqrt(np.sum(h * h, axis=1, keepdims=True))
     return (h * scale).astype(np.float32)
+
+
+def c1_inputs():
+    """BASELINE configs[0] inputs (SURVEY 8(d) seeds): 2 decaying-noise IRs of
+    96,000 taps (seed 1000) and K + 3 = 378 blocks of N(0,1) input (seed 7)."""
+    N, L, n_h = 256, 2, 96000
+    blocks = -(-n_h // N) + 3
+    filt = decaying_filters(np.random.default_rng(1000), L, n_h)
+    x = np.random.default_rng(7).standard_normal((blocks, 1, N)).astype(np.float32)
+    return N, L, n_h, blocks, filt, x

@@ -14,7 +14,9 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
 import oracle as O  # noqa: E402
+from conftest import c1_inputs  # noqa: E402
 
 OUT = os.path.dirname(os.path.abspath(__file__))
 
@@ -76,7 +78,23 @@ def direct_case():
                         y=O.ref_direct_convolve(x, h))
 
 
+def c1_case():
+    """BASELINE configs[0] at its exact size: 1 input x 2 loudspeakers, 48 kHz,
+    N = 256, 2 s decaying-noise IRs (96,000 taps), K + 3 = 378 blocks of N(0,1)
+    input through the reference Convolver. Inputs are regenerated from their
+    seeds (tests/conftest.py c1_inputs), so only the output is stored."""
+    N, L, n_h, blocks, filt, x = c1_inputs()
+    ref = O.RefConvolver(filt, N, 1, L, O.BROADCAST)
+    assert ref.partitions == 375
+    y = np.stack([ref.process(x[b]) for b in range(blocks)])
+    np.savez_compressed(os.path.join(OUT, "c1_full.npz"), N=N, L=L, n_h=n_h, blocks=blocks, y=y)
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["c1"]:
+        c1_case()
+        sys.exit(0)
+    c1_case()
     fft_case()
     direct_case()
     conv_case("conv_bcast_n64", 64, 300, 3, O.BROADCAST, 8, 1)

@@ -1,5 +1,6 @@
 """CPU: the product C-ABI library loads, exports every symbol declared in
-include/aura_b200.h, and -- with no B200 present -- fails loudly instead of
+include/aura_b200.h (the drop-in boundary) and include/aura_b200_diag.h
+(measurement), and -- with no B200 present -- fails loudly instead of
 falling back to a CPU path."""
 import ctypes as C
 import os
@@ -12,11 +13,13 @@ import paper_2509_04390_b200 as A
 from conftest import ROOT
 
 HEADER = os.path.join(ROOT, "include", "aura_b200.h")
+DIAG = os.path.join(ROOT, "include", "aura_b200_diag.h")
 
 
-def declared_symbols():
-    text = open(HEADER).read()
-    return sorted(set(re.findall(r"\b(aura_b200_[a-z_0-9]+)\s*\(", text)))
+def declared_symbols(path=HEADER):
+    text = open(path).read()
+    # declarations only: "<type> aura_b200_x(" at the start of a line
+    return sorted(set(re.findall(r"^[a-z][\w *]*?\b(aura_b200_[a-z_0-9]+)\s*\(", text, re.M)))
 
 
 def test_library_built_and_loads():
@@ -26,9 +29,11 @@ def test_library_built_and_loads():
 
 def test_every_declared_symbol_is_exported():
     syms = declared_symbols()
-    assert len(syms) >= 24
+    diag = declared_symbols(DIAG)
+    assert len(syms) >= 22 and len(diag) >= 10
+    assert not set(syms) & set(diag)
     lib = C.CDLL(A.LIB_PATH)
-    missing = [s for s in syms if not hasattr(lib, s)]
+    missing = [s for s in syms + diag if not hasattr(lib, s)]
     assert not missing, missing
 
 

@@ -1,0 +1,96 @@
+"""GPU: engine robustness -- the 64-bit block counter across 2^32, the
+shard-exchange timeout path, and measurement calls that must leave the
+canceller state untouched."""
+import numpy as np
+import pytest
+
+import paper_2509_04390_b200 as A
+from paper_2509_04390_b200 import shard as S
+from conftest import decaying_filters
+
+pytestmark = pytest.mark.gpu
+
+
+def small_aur(mu=0.02, N=64, L=8, seed=3):
+    rng = np.random.default_rng(seed)
+    synth = decaying_filters(rng, L, 9 * N + 5, scale=0.5)
+    fc = decaying_filters(rng, L, 3 * N + 1, scale=0.1)
+    mk = lambda: A.Auralizer(list(synth), list(fc), A.make_config(48000, N, 1, L),
+                             input_gain=0.9, afc=A.AfcParams(mu, 0.9, 1e-2))
+    return mk, rng
+
+
+@pytest.mark.parametrize("mu", [0.0, 0.02])
+def test_block_counter_crosses_2_32(mu):
+    """A 32-bit block counter wraps after 2^32 blocks (16.6 days at N = 16)
+    and, as 2^32 is no multiple of K, reorders every delay-line ring at the
+    wrap. Numbered from 2^32 - 5, an engine must stream bit-identically to
+    a fresh one across the boundary (ring slots are block mod K)."""
+    mk, rng = small_aur(mu)
+    fresh, seeked = mk(), mk()
+    seeked.seek_block(2**32 - 5)
+    for b in range(30):
+        m = rng.standard_normal((1, 64)).astype(np.float32)
+        assert np.array_equal(fresh.process(m), seeked.process(m)), b
+        assert np.array_equal(fresh.feedback_estimate(), seeked.feedback_estimate()), b
+    for age in (0, 3, 9):
+        assert np.array_equal(fresh.fdl_slot(0, 0, age), seeked.fdl_slot(0, 0, age))
+        assert np.array_equal(fresh.fdl_slot(1, 5, min(age, 3)), seeked.fdl_slot(1, 5, min(age, 3)))
+    assert np.array_equal(fresh.coeffs(), seeked.coeffs())
+    with pytest.raises(A.Error):
+        seeked.seek_block(7)  # only before the first block
+    seeked.reset()
+    seeked.seek_block(2**40 + 3)
+
+
+def test_time_phase_leaves_engine_state_untouched():
+    """time_phase relaunches single kernels for the roofline timing -- k_back
+    applies the NLMS update in place, k_reduce advances the block, the fused
+    canceller head shifts the loudspeaker history: W and every later output
+    must be exactly as if it had never run."""
+    mk, rng = small_aur(0.02)
+    a, b = mk(), mk()
+    mics = rng.standard_normal((20, 1, 64)).astype(np.float32)
+    for i in range(10):
+        a.process(mics[i])
+        b.process(mics[i])
+    a.synchronize()
+    W = a.coeffs().copy()
+    a.time_phase("k_back", 7)
+    a.time_phase("k_reduce", 5)
+    a.time_phase("k_front", 5)
+    assert np.array_equal(a.coeffs(), W)
+    for i in range(10, 20):
+        assert np.array_equal(a.process(mics[i]), b.process(mics[i]))
+    assert np.array_equal(a.coeffs(), b.coeffs())
+
+
+def test_shard_exchange_timeout_reports_and_reset_recovers():
+    """A shard whose peer never delivers its canceller partial waits 5 s
+    (bounded, never a hung GPU), keeps its previous f^ instead of summing
+    stale slots, and fails every call with TIMEOUT until a coordinated
+    reset of all shards."""
+    N, L = 64, 8
+    rng = np.random.default_rng(9)
+    synth = decaying_filters(rng, L, 9 * N, scale=0.5)
+    fc = decaying_filters(rng, L, 3 * N, scale=0.1)
+    cfg = A.make_config(48000, N, 1, L)
+    afc = A.AfcParams(0.02, 0.9, 1e-2)
+    v = S.VirtualShards(list(synth), list(fc), cfg, 2, afc=afc)
+    ref = S.VirtualShards(list(synth), list(fc), cfg, 2, afc=afc)
+    m = rng.standard_normal((1, N)).astype(np.float32)
+    v.shards[0].process(m)  # shard 1 never runs this block
+    with pytest.raises(A.Error) as ei:
+        v.shards[0].synchronize()
+    assert ei.value.code == A.ErrorCode.timeout
+    with pytest.raises(A.Error):
+        v.shards[0].process(m)
+    for s in v.shards:
+        s.reset()
+    mics = rng.standard_normal((12, 1, N)).astype(np.float32)
+    for i in range(12):
+        assert np.array_equal(v.process(mics[i]), ref.process(mics[i]))
+    ests = v.feedback_estimates()
+    assert np.array_equal(ests[0], ests[1])
+    v.close()
+    ref.close()
