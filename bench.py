@@ -14,6 +14,15 @@ value  = p99 device time per block, inputs resident in HBM, CUDA events on
          the engine stream (lower is better).
 e2e    = p99 of aura_b200_process() with host buffers (host->device input,
          all kernels, device->host output, completion wait), steady_clock.
+max_realtime = the metric's second half: the largest loudspeaker count at
+         the config's taps whose block p99 fits N/f_s on the device AND whose
+         process() calls, paced on the real-time grid, return within N/f_s
+         (time-boxed binary search; per GPU, summed over GPUs at N > 1).
+c5     = BASELINE configs[4] (1 x 512, 96 kHz, 20 s), the loudspeakers split
+         over the N GPUs (strong scaling), reported beside the headline.
+
+--gpus N without torchrun re-launches itself under torch.distributed.run
+(one process per GPU); every number is the max over ranks.
 """
 from __future__ import annotations
 
@@ -40,10 +49,15 @@ CONFIGS = {
                desc="c2: 1 input x 16 loudspeakers, 48 kHz, block 128, 10 s IR (480k taps)"),
     "c3": dict(fs=48000, N=64, Q=1, L=64, n_h=480000, afc=True, n_hf=48000, mu=0.005,
                desc="c3: 1 input x 64 loudspeakers, 48 kHz, block 64, 10 s IR (480k taps), "
-                    "PBFDAF feedback canceller 1 s (48k taps) with NLMS update"),
+                    "PBFDAF feedback canceller 1 s (48k taps) with NLMS update",
+               ref_desc="c3: 1 input x 64 loudspeakers, 48 kHz, block 64, 10 s IR (480k taps), "
+                        "feedback canceller 1 s (48k taps) with a FIXED F^ (the reference has no "
+                        "NLMS; same MAC bytes minus the W write)"),
     "c4": dict(fs=48000, N=64, Q=4, L=64, n_h=576000, afc=True, n_hf=48000, mu=0.005,
                desc="c4: 4 inputs x 64 loudspeakers MIMO, 48 kHz, block 64, 12 s IR (576k taps), "
-                    "AFC 1 s with NLMS"),
+                    "AFC 1 s with NLMS",
+               ref_desc="c4: 4 inputs x 64 loudspeakers (4 reference Auralizers, the same MAC "
+                        "work), 48 kHz, block 64, 12 s IR (576k taps), FIXED-F^ canceller 1 s"),
     "c5": dict(fs=96000, N=128, Q=1, L=512, n_h=1920000, afc=False,
                desc="c5: 1 input x 512 loudspeakers, 96 kHz, block 128, 20 s IR (1.92M taps)"),
 }
@@ -231,7 +245,8 @@ def run_reference_arm(args, cfg, rank):
     us, workers, t_setup = reference_blocks(cfg, synth, fc, mic, blocks, args.warmup, L_sub=L_sub)
     us = us * scale
     p50, p99 = pct(us, 50), pct(us, 99)
-    sample = (f"{blocks} blocks of {cfg['desc']} (after {args.warmup} warm-up), reference "
+    desc = cfg.get("ref_desc", cfg["desc"])
+    sample = (f"{blocks} blocks of {desc} (after {args.warmup} warm-up), reference "
               f"ParallelBackend, -O3 -DNDEBUG -std=c++20; fixed-F^ canceller (the reference "
               f"has no NLMS); setup {t_setup:.1f} s excluded")
     if L_sub:
@@ -241,7 +256,7 @@ def run_reference_arm(args, cfg, rank):
         "n_gpus": args.gpus, "steps": blocks, "warmup": args.warmup,
         "ms_per_step": float(np.mean(us)) / 1000.0, "higher_is_better": False,
         "scaling": args.scaling if args.gpus > 1 else "strong", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic", "config": {"workload": cfg["desc"]},
+        "data": "synthetic", "config": {"workload": desc},
         "p50_us": p50, "p99_us": p99, "budget_us": 1e6 * cfg["N"] / cfg["fs"],
         "cpu_baseline": {"value": p99, "unit": "us", "cores": workers, "kind": "reference",
                          "sample": sample},
@@ -270,60 +285,145 @@ def make_engine(A, cfg, synth, fc, device=0, L=None, mu=None):
     return A.Convolver(list(synth), ec, mode, backend)
 
 
-def max_realtime(A, cfg, device, blocks=300, budget_s=90.0):
-    """Largest loudspeaker count L (taps fixed at the config's n_h, same AFC
-    setting) whose p99 device block time stays under N/f_s; returns
-    (L, L * n_h). Synthetic filters are generated per L."""
+def aliased_rows(n_rows, n_taps, distinct=16, scale=1e-3, seed=3):
+    """n_rows filter rows made of `distinct` random rows, aliased: timing does
+    not depend on the filter values (the MAC streams every channel's spectra
+    whatever they hold), and this keeps host setup cheap at L ~ 10^3."""
+    rng = np.random.default_rng(seed)
+    base = [rng.standard_normal(n_taps, dtype=np.float32) * np.float32(scale) for _ in range(distinct)]
+    return [base[i % distinct] for i in range(n_rows)]
+
+
+def max_realtime(A, cfg, device, blocks=300, budget_s=110.0):
+    """The metric's second half (bench.hpp:245: real time = block time within
+    N/f_s): the largest loudspeaker count L, taps fixed at the
+    config's n_h, same canceller setting, for which BOTH
+      - the device p99 of a block's whole work (front + background) < N/f_s,
+      - the p99 latency of aura_b200_process() with host buffers, called on
+        the real-time grid (one call every N/f_s), < N/f_s,
+    binary search on L (resolution L/32), time-boxed to budget_s."""
     t_start = time.perf_counter()
     N, fs = cfg["N"], cfg["fs"]
     budget_us = 1e6 * N / fs
-    rng = np.random.default_rng(3)
-    base_s = list(rng.standard_normal((16, cfg["n_h"]), dtype=np.float32) * np.float32(1e-3))
-    base_f = (list(rng.standard_normal((16, cfg["n_hf"]), dtype=np.float32) * np.float32(1e-4))
-              if cfg["afc"] else None)
+    Q = cfg["Q"]
+    mic = np.random.default_rng(7).standard_normal((64, Q, N)).astype(np.float32)
+    trials = []
 
     def fits(L):
         c = dict(cfg, L=L)
-        Q = c["Q"]
-        # 16 distinct rows, aliased: the MAC streams every channel's spectra
-        # regardless of their values, and this keeps host setup cheap at L ~ 10^3
-        synth = [base_s[i % 16] for i in range(Q * L)]
-        fc = [base_f[i % 16] for i in range(Q * L)] if c["afc"] else None
+        synth = aliased_rows(Q * L, cfg["n_h"])
+        fc = aliased_rows(Q * L, cfg["n_hf"], scale=1e-4, seed=4) if c["afc"] else None
         try:
             e = make_engine(A, c, synth, fc, device)
         except A.Error as err:
             if err.code == A.ErrorCode.out_of_memory:
-                return False, None
+                trials.append({"L": L, "fits": False, "why": "out of memory"})
+                return False
             raise
         del synth, fc
-        mic = np.random.default_rng(7).standard_normal((64, Q, N)).astype(np.float32)
         e.time_device_blocks(20, mic)
-        lat, us = e.time_device_blocks(blocks, mic)
+        _, us = e.time_device_blocks(blocks, mic)
+        dev99 = pct(us, 99)
+        host99 = None
+        if dev99 < budget_us:
+            e.time_host_blocks(mic, 20, pace_us=budget_us)
+            host = e.time_host_blocks(mic, blocks, pace_us=budget_us)
+            e.synchronize()
+            host99 = pct(host, 99)
         e.close()
-        # real time needs ALL of a block's work inside its period
-        return pct(us, 99) < budget_us, pct(us, 99)
+        ok = dev99 < budget_us and host99 is not None and host99 < budget_us
+        trials.append({"L": L, "fits": ok, "device_p99_us": dev99, "paced_e2e_p99_us": host99})
+        return ok
 
     lo, hi = cfg["L"], None
-    ok, p = fits(lo)
-    if not ok:
-        return None
+    if not fits(lo):
+        return {"channels": 0, "trials": trials, "p99_criterion_us": budget_us}
     step = lo
     while hi is None and time.perf_counter() - t_start < budget_s:
         cand = lo + step
-        ok, p = fits(cand)
-        if ok:
+        if fits(cand):
             lo, step = cand, step * 2
         else:
             hi = cand
     while hi is not None and hi - lo > max(1, lo // 32) and time.perf_counter() - t_start < budget_s:
         mid = (lo + hi) // 2
-        ok, p = fits(mid)
-        if ok:
+        if fits(mid):
             lo = mid
         else:
             hi = mid
     return {"channels": lo, "taps": cfg["n_h"], "channels_x_taps": lo * cfg["n_h"],
-            "upper_bound_channels": hi, "p99_criterion_us": budget_us}
+            "upper_bound_channels": hi, "p99_criterion_us": budget_us,
+            "criteria": "device block p99 AND paced process() e2e p99 < N/f_s",
+            "search_s": time.perf_counter() - t_start, "trials": trials}
+
+
+def l2_read_peak(footprint_bytes):
+    """Measured L2-resident read bandwidth (GB/s) at this footprint:
+    tools/bw_probe.cu BW_L2=1 on this pool's B200 (profiles/r2_l2_probe.jsonl;
+    best of the LDG.128 and the cp.async.bulk stream, each a single launch
+    re-reading a buffer of that size), interpolated in footprint."""
+    path = os.path.join(ROOT, "profiles", "r2_l2_probe.jsonl")
+    pts = {}
+    try:
+        with open(path) as f:
+            for line in f:
+                r = json.loads(line)
+                if r.get("kind") in ("l2_ldg", "l2_bulk"):
+                    mb = float(r["footprint_mb"])
+                    pts[mb] = max(pts.get(mb, 0.0), float(r["GBps"]))
+    except (OSError, ValueError):
+        return None, None
+    if not pts:
+        return None, None
+    xs = sorted(pts)
+    mb = footprint_bytes / 1e6
+    best = float(np.interp(mb, xs, [pts[x] for x in xs]))
+    return best, "measured L2-resident read at %.0f MB (profiles/r2_l2_probe.jsonl)" % mb
+
+
+def roofline_regime(eng_bytes_footprint):
+    """SURVEY 8(d) regime rule: footprint (H + W + FDLs) < L2/2 -> L2."""
+    return "l2" if eng_bytes_footprint < 126e6 / 2 else "hbm"
+
+
+def c5_secondary(A, device, K, W, world=1, rank=0):
+    """BASELINE configs[4] (1 x 512 loudspeakers, 96 kHz, N = 128, 20 s, no
+    canceller) with its loudspeakers split over `world` GPUs (strong
+    scaling: this rank runs its slice). Aliased filter rows (timing does not
+    depend on values). Returns this rank's per-block device and e2e times."""
+    from paper_2509_04390_b200 import shard as S
+    c = CONFIGS["c5"]
+    N, L = c["N"], c["L"]
+    rows = aliased_rows(L, c["n_h"])
+    ec = A.make_config(c["fs"], N, 1, L)
+    t0 = time.perf_counter()
+    conv = S.ShardedConvolver(rows, ec, world, rank, A.ChannelMode.broadcast, device)
+    setup = time.perf_counter() - t0
+    del rows
+    mic = np.random.default_rng(7).standard_normal((64, 1, N)).astype(np.float32)
+    e = conv.engine
+    e.time_device_blocks(max(3, W), mic)
+    _, dev = e.time_device_blocks(K, mic)
+    host = e.time_host_blocks(mic, K)
+    e.synchronize()
+    out = {"dev": dev, "host": host, "channels": (conv.l0, conv.l1), "setup": setup,
+           "bytes": e.profile_phases(3)["k_back"][1]}
+    conv.close()
+    return out
+
+
+def c5_summary(parts, world):
+    c = CONFIGS["c5"]
+    dev = np.max(np.stack([p["dev"] for p in parts]), axis=0)
+    host = np.max(np.stack([p["host"] for p in parts]), axis=0)
+    return {"workload": c["desc"] + f" [strong scaling: 512 loudspeakers over {world} GPU(s)]",
+            "n_gpus": world, "p50_us": pct(dev, 50), "p99_us": pct(dev, 99),
+            "e2e_p99_us": pct(host, 99), "budget_us": 1e6 * c["N"] / c["fs"],
+            "realtime": bool(pct(dev, 99) < 1e6 * c["N"] / c["fs"]),
+            "channels": [list(p["channels"]) for p in parts],
+            "k_back_bytes_per_gpu": max(p["bytes"] for p in parts),
+            "definition": "max over ranks per block; device = all of a block's work, inputs in "
+                          "HBM; e2e = aura_b200_process() back to back with host buffers"}
 
 
 def run_b200_arm(args, cfg, rank, world, local_rank):
@@ -378,15 +478,30 @@ def run_b200_arm(args, cfg, rank, world, local_rank):
                          f"reference (oracle/_ref, ParallelBackend, -O3 -DNDEBUG); fixed-F^ "
                          f"canceller (no NLMS in the reference); setup {t_ref_setup:.1f} s excluded"
                          + sub}
-    maxrt = None
-    if args.max_rt:
-        del synth, fc
-        eng.close()
-        maxrt = max_realtime(A, cfg, device)
+    describe = eng.describe()
+    del synth, fc
+    eng.close()
+    maxrt = None if args.no_max_rt else max_realtime(A, cfg, device, budget_s=args.max_rt_s)
+    c5 = None
+    if not args.no_c5:
+        c5 = c5_summary([c5_secondary(A, device, K, W)], 1)
 
     total_bytes = sum(b for _, b in phases.values())
     # the same kernel inside the block graph (%globaltimer: first CTA start ->
     # last CTA end), concurrent with the canceller head
+    # roofline regime: the working set -- spectra, canceller
+    # W, delay lines -- under L2/2 stays in L2 between blocks
+    P = Q if cfg["afc"] else 0
+    KF = -(-cfg.get("n_hf", 0) // N) if cfg["afc"] else 0
+    Kh = -(-cfg["n_h"] // N)
+    footprint = 8.0 * N * (Q * L * Kh + Q * Kh + P * L * KF + (L * (KF + 1) if cfg["afc"] else 0))
+    bound = roofline_regime(footprint)
+    if bound == "l2":
+        l2_peak, l2_kind = l2_read_peak(footprint)
+        if l2_peak:
+            peak, peak_kind = l2_peak, l2_kind
+        else:
+            bound = "hbm"
     ig = timeline.get(mac_name)
     in_graph = None
     if ig and ig["end_us"] > ig["start_us"]:
@@ -405,7 +520,7 @@ def run_b200_arm(args, cfg, rank, world, local_rank):
                    "l2": f"inputs larger than L2: {total_bytes / 1e6:.0f} MB streamed per block "
                          f"vs 126 MB L2" if total_bytes > 126e6 else
                          "working set fits L2 (real-time steady state; no flush)",
-                   "parallelism": "1 GPU", "engine": eng.describe() if not args.max_rt else None},
+                   "parallelism": "1 GPU", "engine": describe},
         "p50_us": pct(dev_us, 50), "p99_us": pct(dev_us, 99), "max_us": float(np.max(dev_us)),
         "budget_us": 1e6 * N / cfg["fs"],
         "value_definition": "p99 device time of ALL of a block's work (front + background "
@@ -423,8 +538,9 @@ def run_b200_arm(args, cfg, rank, world, local_rank):
                 "path": "aura_b200_process() C-ABI, pinned mapped host I/O, back-to-back "
                         "(each call also waits for the previous block's background work)"},
         "paced_e2e": paced,
-        "roofline": {"bound": "hbm", "kernel": mac_name, "achieved": achieved,
+        "roofline": {"bound": bound, "kernel": mac_name, "achieved": achieved,
                      "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "footprint_bytes": footprint,
                      "peak_kind": peak_kind, "traffic": traffic, "traffic_source": traffic_src,
                      "frac_of_read_probe": achieved / READ_PROBE_GBS,
                      "bytes_per_launch": mac_bytes, "avg_launch_us": mac_us,
@@ -441,7 +557,7 @@ def run_b200_arm(args, cfg, rank, world, local_rank):
         "timeline_us": timeline,
         "phase_bytes": {k: v[1] for k, v in phases.items()},
         "cpu_baseline": cpu, "clocks": clocks, "gpu_launches": int(K * n_launch),
-        "max_realtime": maxrt, "setup_s": t_setup,
+        "max_realtime": maxrt, "c5": c5, "setup_s": t_setup,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -453,7 +569,10 @@ def sharded_cfg(cfg, world, scaling):
     so the job has L x world; strong: the config's L is split."""
     if scaling == "weak" and world > 1:
         c = dict(cfg, L=cfg["L"] * world)
-        c["desc"] = cfg["desc"] + f" [weak scaling: {cfg['L']} loudspeakers per GPU x {world} GPUs]"
+        tag = f" [weak scaling: {cfg['L']} loudspeakers per GPU x {world} GPUs]"
+        c["desc"] = cfg["desc"] + tag
+        if "ref_desc" in cfg:
+            c["ref_desc"] = cfg["ref_desc"] + tag
         return c
     return cfg
 
@@ -507,8 +626,21 @@ def run_sharded(args, cfg, rank, world, local_rank):
     mac_us = local.time_phase(mac_name, 20)
     mac_bytes = phases[mac_name][1]
     peak, peak_kind = load_peaks()
+    n_launch = local.launches_per_block()
+    dist.barrier()
+    local.close()
+    dist.barrier()
+    # BASELINE configs[4]: 512 loudspeakers split over the GPUs (strong)
+    c5 = None if args.no_c5 else c5_secondary(A, device, K, W, world, rank)
+    dist.barrier()
+    # max real time per GPU (c3 shape, each GPU on its own: needs a device
+    # per rank), summed over the GPUs
+    maxrt = None
+    if not args.no_max_rt and ndev >= world:
+        maxrt = max_realtime(A, dict(CONFIGS[args.config]), device, budget_s=args.max_rt_s)
+    dist.barrier()
     mine = {"lat": lat_us, "dev": dev_us, "host": host_us, "mac_us": mac_us,
-            "mac_bytes": mac_bytes, "launches": local.launches_per_block(),
+            "mac_bytes": mac_bytes, "launches": n_launch, "c5": c5, "maxrt": maxrt,
             "clocks": clocks, "channels": (eng.l0, eng.l1), "setup": t_setup}
     allr = [None] * world
     dist.all_gather_object(allr, mine)
@@ -544,10 +676,18 @@ def run_sharded(args, cfg, rank, world, local_rank):
             "cpu_baseline": None, "clocks": allr[0]["clocks"],
             "gpu_launches": int(K * sum(r["launches"] for r in allr)),
             "setup_s": max(r["setup"] for r in allr),
+            "c5": c5_summary([r["c5"] for r in allr], world) if allr[0]["c5"] else None,
+            "max_realtime": ({"channels": sum(r["maxrt"]["channels"] for r in allr),
+                              "taps": cfg["n_h"],
+                              "channels_x_taps": sum(r["maxrt"]["channels"] for r in allr) * cfg["n_h"],
+                              "per_gpu_channels": [r["maxrt"]["channels"] for r in allr],
+                              "criteria": "per GPU: device block p99 AND paced process() e2e p99 "
+                                          "< N/f_s (c3 shape on each GPU; the cross-GPU canceller "
+                                          "exchange is timed in value)"}
+                             if all(r["maxrt"] for r in allr) else None),
         }
         print(json.dumps(line), flush=True)
     dist.barrier()
-    local.close()
     dist.destroy_process_group()
     return 0
 
@@ -562,7 +702,9 @@ def main():
     ap.add_argument("--block", type=int, default=None, help="override block size (c4 sweep)")
     ap.add_argument("--cpu-blocks", type=int, default=60)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--max-rt", action="store_true")
+    ap.add_argument("--no-max-rt", action="store_true", help="skip the max real-time search")
+    ap.add_argument("--max-rt-s", type=float, default=110.0, help="time box of the max-RT search")
+    ap.add_argument("--no-c5", action="store_true", help="skip the configs[4] (c5) line")
     ap.add_argument("--no-paced", action="store_true")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="N > 1: weak keeps the config's loudspeakers per GPU, strong splits them")
@@ -571,6 +713,17 @@ def main():
     if args.block:
         cfg["N"] = args.block
         cfg["desc"] += f" [block {args.block}]"
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch under torch.distributed.run
+        import socket
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+        sk.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+               f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        return subprocess.call(cmd)
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))

@@ -38,6 +38,10 @@ int aura_b200_time_host_breakdown(aura_b200_engine* e, const float* host_in, siz
 int aura_b200_time_device_blocks(aura_b200_engine* e, const float* host_in,
                                  size_t n_in_blocks, size_t blocks,
                                  float* latency_us, float* block_us);
+/* The same back-to-back blocks with ONE event pair around all of them
+ * (no per-block event records in the stream): *total_us for `blocks`. */
+int aura_b200_time_device_span(aura_b200_engine* e, const float* host_in, size_t n_in_blocks,
+                               size_t blocks, float* total_us);
 /* End-to-end latency through aura_b200_process() itself: `blocks` calls
  * with HOST input (cycling over host_in: n_in_blocks x inputs x N) and host
  * output, each timed with steady_clock from call to return (host->device

@@ -8,7 +8,10 @@ Two checkers live here:
 
 * ``Oracle*`` wrap ``liboracle.so``: the plain-C restatement of the
   reference hot path (``oracle/aura_oracle.c``), extended with the
-  Appendix-A NLMS update and Appendix-B MIMO composition.
+  Appendix-A NLMS update and Appendix-B MIMO composition. ``f64=True``
+  selects ``liboracle64.so``, the same algorithm in float64 with exact
+  twiddles: the ground truth for full-length streams, where every fp32
+  implementation (the reference included) drifts ~1e-5 of the RMS.
 * ``Ref*`` wrap ``_ref/libaura_ref.so``: the unmodified reference headers
   (``/root/reference/proj/include/aura``) behind a C shim
   (``oracle/ref_shim.cpp``), built with the reference's Release flags.
@@ -23,6 +26,7 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 _ORACLE_SO = os.path.join(HERE, "liboracle.so")
+_ORACLE64_SO = os.path.join(HERE, "liboracle64.so")
 _REF_SO = os.path.join(HERE, "_ref", "libaura_ref.so")
 
 BROADCAST, ELEMENTWISE, MIMO = 0, 1, 2
@@ -42,14 +46,15 @@ def _load(path):
     return C.CDLL(path)
 
 
-_olib = None
+_olib = {}
 _rlib = None
 
 
-def olib():
-    global _olib
-    if _olib is None:
-        L = _load(_ORACLE_SO)
+def olib(f64=False):
+    if f64 not in _olib:
+        L = _load(_ORACLE64_SO if f64 else _ORACLE_SO)
+        _f32p = _f64p if f64 else globals()["_f32p"]
+        C_real = C.c_double if f64 else C.c_float
         L.ao_plan_new.restype = C.c_void_p
         L.ao_plan_new.argtypes = [_sz]
         L.ao_plan_free.argtypes = [C.c_void_p]
@@ -65,11 +70,11 @@ def olib():
         L.ao_conv_spectrum.argtypes = [C.c_void_p, _sz, _sz, _f32p]
         L.ao_aur_new.restype = C.c_void_p
         L.ao_aur_new.argtypes = [_sz, _sz, _sz, _f32p, _sz, _f32p, _sz,
-                                 C.c_float, C.c_float, C.c_float, C.c_float]
+                                 C_real, C_real, C_real, C_real]
         L.ao_aur_free.argtypes = [C.c_void_p]
         L.ao_aur_process.argtypes = [C.c_void_p, _f32p, _f32p]
         L.ao_aur_reset.argtypes = [C.c_void_p]
-        L.ao_aur_set_gain.argtypes = [C.c_void_p, C.c_float]
+        L.ao_aur_set_gain.argtypes = [C.c_void_p, C_real]
         L.ao_aur_feedback_estimate.argtypes = [C.c_void_p, _f32p]
         L.ao_aur_fc_partitions.restype = _sz
         L.ao_aur_fc_partitions.argtypes = [C.c_void_p]
@@ -78,8 +83,8 @@ def olib():
         L.ao_aur_coeffs.argtypes = [C.c_void_p, _f32p]
         L.ao_aur_power.argtypes = [C.c_void_p, _f32p]
         L.ao_direct_convolve.argtypes = [_f64p, _sz, _f64p, _sz, _f64p]
-        _olib = L
-    return _olib
+        _olib[f64] = L
+    return _olib[f64]
 
 
 def ref_available() -> bool:
@@ -156,33 +161,38 @@ class OracleConvolver:
     """CPU restatement of aura::Convolver (convolver.hpp:65-220).
 
     filters: (rows, n_h). mode BROADCAST (inputs=1), ELEMENTWISE
-    (inputs=outputs) or MIMO (rows = inputs*outputs, row q*L+l)."""
+    (inputs=outputs) or MIMO (rows = inputs*outputs, row q*L+l).
+    f64: the float64 ground-truth build (inputs are the same float32
+    values, exactly widened; outputs float64)."""
 
-    def __init__(self, filters, block, inputs, outputs, mode):
-        f = _f32(filters)
+    def __init__(self, filters, block, inputs, outputs, mode, f64=False):
+        self.f64 = f64
+        self.dt = np.float64 if f64 else np.float32
+        f = np.ascontiguousarray(_f32(filters), self.dt)
         self.N, self.inputs, self.outputs = block, inputs, outputs
-        self._h = olib().ao_conv_new(block, inputs, outputs, mode, f, f.shape[1])
+        self._L = olib(f64)
+        self._h = self._L.ao_conv_new(block, inputs, outputs, mode, f, f.shape[1])
         if not self._h:
             raise ValueError("oracle rejected the convolver configuration")
-        self.partitions = olib().ao_conv_partitions(self._h)
+        self.partitions = self._L.ao_conv_partitions(self._h)
 
     def process(self, x):
-        x = _f32(x).reshape(self.inputs, self.N)
-        out = np.zeros((self.outputs, self.N), np.float32)
-        olib().ao_conv_process(self._h, x, out)
+        x = np.ascontiguousarray(_f32(x), self.dt).reshape(self.inputs, self.N)
+        out = np.zeros((self.outputs, self.N), self.dt)
+        self._L.ao_conv_process(self._h, x, out)
         return out
 
     def reset(self):
-        olib().ao_conv_reset(self._h)
+        self._L.ao_conv_reset(self._h)
 
     def spectrum(self, row, k):
-        out = np.zeros(2 * (self.N + 1), np.float32)
-        olib().ao_conv_spectrum(self._h, row, k, out)
-        return out.view(np.complex64)
+        out = np.zeros(2 * (self.N + 1), self.dt)
+        self._L.ao_conv_spectrum(self._h, row, k, out)
+        return out.view(np.complex128 if self.f64 else np.complex64)
 
     def __del__(self):
         if getattr(self, "_h", None):
-            olib().ao_conv_free(self._h)
+            self._L.ao_conv_free(self._h)
             self._h = None
 
 
@@ -192,48 +202,55 @@ class OracleAuralizer:
     synth: (Q*L, n_h); fc: (P*L, n_hf) with P = Q."""
 
     def __init__(self, synth, fc, block, inputs, outputs, gain=1.0, mu=0.0,
-                 lam=0.9, delta=None):
-        s, f = _f32(synth), _f32(fc)
+                 lam=0.9, delta=None, f64=False):
+        self.f64 = f64
+        self.dt = np.float64 if f64 else np.float32
+        s = np.ascontiguousarray(_f32(synth), self.dt)
+        f = np.ascontiguousarray(_f32(fc), self.dt)
         if delta is None:
             delta = 1e-6 * block  # same default as the product (SURVEY App. A)
+        # the parameters as the fp32 engines hold them (exactly widened in f64)
+        gain, mu, lam, delta = (float(np.float32(v)) for v in (gain, mu, lam, delta))
         self.N, self.Q, self.L = block, inputs, outputs
-        self._h = olib().ao_aur_new(block, inputs, outputs, s, s.shape[1], f,
-                                    f.shape[1], gain, mu, lam, delta)
+        self._L = olib(f64)
+        self._h = self._L.ao_aur_new(block, inputs, outputs, s, s.shape[1], f,
+                                     f.shape[1], gain, mu, lam, delta)
         if not self._h:
             raise ValueError("oracle rejected the auralizer configuration")
-        self.fc_partitions = olib().ao_aur_fc_partitions(self._h)
-        self.synth_partitions = olib().ao_aur_synth_partitions(self._h)
+        self.fc_partitions = self._L.ao_aur_fc_partitions(self._h)
+        self.synth_partitions = self._L.ao_aur_synth_partitions(self._h)
 
     def process(self, mic):
-        mic = _f32(mic).reshape(self.Q, self.N)
-        out = np.zeros((self.L, self.N), np.float32)
-        olib().ao_aur_process(self._h, mic, out)
+        mic = np.ascontiguousarray(_f32(mic), self.dt).reshape(self.Q, self.N)
+        out = np.zeros((self.L, self.N), self.dt)
+        self._L.ao_aur_process(self._h, mic, out)
         return out
 
     def reset(self):
-        olib().ao_aur_reset(self._h)
+        self._L.ao_aur_reset(self._h)
 
     def set_gain(self, g):
-        olib().ao_aur_set_gain(self._h, g)
+        self._L.ao_aur_set_gain(self._h, float(np.float32(g)))
 
     def feedback_estimate(self):
-        out = np.zeros((self.Q, self.N), np.float32)
-        olib().ao_aur_feedback_estimate(self._h, out)
+        out = np.zeros((self.Q, self.N), self.dt)
+        self._L.ao_aur_feedback_estimate(self._h, out)
         return out
 
     def coeffs(self):
-        out = np.zeros(self.Q * self.L * self.fc_partitions * (self.N + 1) * 2, np.float32)
-        olib().ao_aur_coeffs(self._h, out)
-        return out.view(np.complex64).reshape(self.Q, self.L, self.fc_partitions, self.N + 1)
+        out = np.zeros(self.Q * self.L * self.fc_partitions * (self.N + 1) * 2, self.dt)
+        self._L.ao_aur_coeffs(self._h, out)
+        return out.view(np.complex128 if self.f64 else np.complex64).reshape(
+            self.Q, self.L, self.fc_partitions, self.N + 1)
 
     def power(self):
-        out = np.zeros(self.N + 1, np.float32)
-        olib().ao_aur_power(self._h, out)
+        out = np.zeros(self.N + 1, self.dt)
+        self._L.ao_aur_power(self._h, out)
         return out
 
     def __del__(self):
         if getattr(self, "_h", None):
-            olib().ao_aur_free(self._h)
+            self._L.ao_aur_free(self._h)
             self._h = None
 
 

@@ -1,7 +1,7 @@
 /*
  * aura_oracle.c -- TEST INFRASTRUCTURE ONLY. CPU restatement of the
  * reference hot path; see aura_oracle.h for the anchors and the pinning
- * status. Compiled with -O2 -ffp-contract=off so every float operation
+ * status. Compiled with -O2 -ffp-contract=off so every real operation
  * rounds exactly as the reference's (the C-vs-reference comparison in
  * tests/test_oracle.py is bit-exact).
  *
@@ -14,6 +14,13 @@
  * the product never links or calls it.
  */
 #include "aura_oracle.h"
+
+/* real = float: the restatement (bit-exact to the reference). real = double
+ * (-DAO_F64, liboracle64.so): the same algorithm in float64 with exact
+ * twiddles -- the ground truth the fp32 implementations (reference, oracle,
+ * GPU) are measured against at full stream lengths, where their own
+ * accumulation error over K ~ 10^4 partitions is ~1e-5 of the RMS. */
+typedef ao_real real;
 
 #include <math.h>
 #include <stdlib.h>
@@ -43,7 +50,7 @@ static int thread_id(void) {
 #define M_PI 3.14159265358979323846
 #endif
 
-typedef struct { float re, im; } cf;
+typedef struct { real re, im; } cf;
 
 static inline cf cmul(cf a, cf b) { /* (ac - bd, ad + bc) as libstdc++ */
   cf r;
@@ -54,10 +61,10 @@ static inline cf cmul(cf a, cf b) { /* (ac - bd, ad + bc) as libstdc++ */
 static inline cf cadd(cf a, cf b) { cf r = {a.re + b.re, a.im + b.im}; return r; }
 static inline cf csub(cf a, cf b) { cf r = {a.re - b.re, a.im - b.im}; return r; }
 static inline cf cconj(cf a) { cf r = {a.re, -a.im}; return r; }
-static inline cf cscale(float s, cf a) { cf r = {a.re * s, a.im * s}; return r; }
+static inline cf cscale(real s, cf a) { cf r = {a.re * s, a.im * s}; return r; }
 
 /* ------------------------------------------------------------------ DFT */
-/* dft.hpp:34-63: twiddles in double, stored as float; bit-reverse table. */
+/* dft.hpp:34-63: twiddles in double, stored as float (f64 build: double); bit-reverse table. */
 struct ao_plan {
   size_t size, half;
   cf* stage_tw;  /* half/2 entries, e^{-2 pi i j / half} */
@@ -77,13 +84,13 @@ ao_plan* ao_plan_new(size_t fft_size) {
   p->work = (cf*)malloc(sizeof(cf) * p->half);
   const double step = -2.0 * M_PI / (double)p->half;
   for (size_t j = 0; j < p->half / 2; ++j) {
-    p->stage_tw[j].re = (float)cos(step * (double)j);
-    p->stage_tw[j].im = (float)sin(step * (double)j);
+    p->stage_tw[j].re = (real)cos(step * (double)j);
+    p->stage_tw[j].im = (real)sin(step * (double)j);
   }
   const double sstep = -2.0 * M_PI / (double)p->size;
   for (size_t j = 0; j <= p->half / 2; ++j) {
-    p->split_tw[j].re = (float)cos(sstep * (double)j);
-    p->split_tw[j].im = (float)sin(sstep * (double)j);
+    p->split_tw[j].re = (real)cos(sstep * (double)j);
+    p->split_tw[j].im = (real)sin(sstep * (double)j);
   }
   for (size_t i = 0; i < p->half; ++i) {
     size_t r = 0, v = i;
@@ -116,7 +123,7 @@ static void fft_core(const ao_plan* p, cf* z) {
 }
 
 /* dft.hpp:69-101 (z: n_f/2 complex scratch) */
-static void forward_w(const ao_plan* p, const float* buf, float* spec_f, cf* z) {
+static void forward_w(const ao_plan* p, const real* buf, real* spec_f, cf* z) {
   cf* spec = (cf*)spec_f;
   const size_t n = p->half;
   for (size_t m = 0; m < n; ++m) {
@@ -138,15 +145,15 @@ static void forward_w(const ao_plan* p, const float* buf, float* spec_f, cf* z) 
   }
 }
 
-void ao_forward(const ao_plan* p, const float* buf, float* spec_f) { forward_w(p, buf, spec_f, p->work); }
+void ao_forward(const ao_plan* p, const real* buf, real* spec_f) { forward_w(p, buf, spec_f, p->work); }
 
 /* dft.hpp:124-153 (inverse_unchecked: edge imaginary parts ignored) */
-static void inverse_w(const ao_plan* p, const float* spec_f, float* buf, cf* z) {
+static void inverse_w(const ao_plan* p, const real* spec_f, real* buf, cf* z) {
   const cf* spec = (const cf*)spec_f;
   const size_t n = p->half;
   {
-    const float xe = 0.5f * (spec[0].re + spec[n].re);
-    const float xo = 0.5f * (spec[0].re - spec[n].re);
+    const real xe = 0.5f * (spec[0].re + spec[n].re);
+    const real xo = 0.5f * (spec[0].re - spec[n].re);
     cf t = {xe, xo};
     z[p->bitrev[0]] = cconj(t);
   }
@@ -163,14 +170,14 @@ static void inverse_w(const ao_plan* p, const float* spec_f, float* buf, cf* z) 
     z[p->bitrev[k]] = cconj(cadd(even, cmul(unit_i, odd)));
   }
   fft_core(p, z);
-  const float scale = 1.0f / (float)n;
+  const real scale = 1.0f / (real)n;
   for (size_t m = 0; m < n; ++m) {
     buf[2 * m] = z[m].re * scale;
     buf[2 * m + 1] = -z[m].im * scale;
   }
 }
 
-void ao_inverse(const ao_plan* p, const float* spec_f, float* buf) { inverse_w(p, spec_f, buf, p->work); }
+void ao_inverse(const ao_plan* p, const real* spec_f, real* buf) { inverse_w(p, spec_f, buf, p->work); }
 
 /* ------------------------------------------------------------ convolver */
 /* One UPOLS engine = convolver.hpp:65-220 with its FDL (engine.hpp:233-279).
@@ -184,37 +191,37 @@ typedef struct {
   cf* fdl;      /* fdl_ch x K x bins */
   size_t* head; /* fdl_ch */
   size_t fdl_ch;
-  float* window; /* in_ch x 2N */
+  real* window; /* in_ch x 2N */
   cf* acc;       /* bins */
-  float* time;   /* 2N */
-  float* pad;    /* 2N */
+  real* time;   /* 2N */
+  real* pad;    /* 2N */
   int nt;        /* per-thread scratch: */
   cf* tacc;      /*   nt x bins */
-  float* ttime;  /*   nt x 2N */
+  real* ttime;  /*   nt x 2N */
   cf* twork;     /*   nt x N (FFT work) */
 } upols;
 
-static void upols_partition(upols* u, size_t row, const float* taps) {
+static void upols_partition(upols* u, size_t row, const real* taps) {
   /* convolver.hpp:19-46: split into K blocks of N taps, zero-pad to 2N */
   const int t = thread_id();
-  float* pad = u->ttime + (size_t)t * 2 * u->N;
+  real* pad = u->ttime + (size_t)t * 2 * u->N;
   for (size_t k = 0; k < u->K; ++k) {
     const size_t begin = k * u->N;
     size_t n = u->n_h - begin;
     if (n > u->N) n = u->N;
-    memset(pad, 0, sizeof(float) * 2 * u->N);
-    memcpy(pad, taps + begin, sizeof(float) * n);
-    forward_w(u->plan, pad, (float*)(u->H + (row * u->K + k) * u->bins), u->twork + (size_t)t * u->N);
+    memset(pad, 0, sizeof(real) * 2 * u->N);
+    memcpy(pad, taps + begin, sizeof(real) * n);
+    forward_w(u->plan, pad, (real*)(u->H + (row * u->K + k) * u->bins), u->twork + (size_t)t * u->N);
   }
 }
 
-static void upols_partition_rows(upols* u, size_t rows, const float* filters) {
+static void upols_partition_rows(upols* u, size_t rows, const real* filters) {
 #pragma omp parallel for schedule(dynamic, 1) if (rows * u->K * u->bins >= AO_PAR_MIN_WORK)
   for (size_t c = 0; c < rows; ++c) upols_partition(u, c, filters + c * u->n_h);
 }
 
 static int upols_init(upols* u, size_t N, size_t in_ch, size_t out_ch,
-                      int elementwise, const float* filters, size_t n_h) {
+                      int elementwise, const real* filters, size_t n_h) {
   memset(u, 0, sizeof(*u));
   if (n_h == 0 || out_ch == 0) return -1;
   u->N = N; u->bins = N + 1; u->n_h = n_h;
@@ -226,13 +233,13 @@ static int upols_init(upols* u, size_t N, size_t in_ch, size_t out_ch,
   u->H = (cf*)calloc(out_ch * u->K * u->bins, sizeof(cf));
   u->fdl = (cf*)calloc(u->fdl_ch * u->K * u->bins, sizeof(cf));
   u->head = (size_t*)calloc(u->fdl_ch, sizeof(size_t));
-  u->window = (float*)calloc(in_ch * 2 * N, sizeof(float));
+  u->window = (real*)calloc(in_ch * 2 * N, sizeof(real));
   u->acc = (cf*)calloc(u->bins, sizeof(cf));
-  u->time = (float*)calloc(2 * N, sizeof(float));
-  u->pad = (float*)calloc(2 * N, sizeof(float));
+  u->time = (real*)calloc(2 * N, sizeof(real));
+  u->pad = (real*)calloc(2 * N, sizeof(real));
   u->nt = n_threads();
   u->tacc = (cf*)calloc((size_t)u->nt * u->bins, sizeof(cf));
-  u->ttime = (float*)calloc((size_t)u->nt * 2 * N, sizeof(float));
+  u->ttime = (real*)calloc((size_t)u->nt * 2 * N, sizeof(real));
   u->twork = (cf*)calloc((size_t)u->nt * N, sizeof(cf));
   upols_partition_rows(u, out_ch, filters);
   return 0;
@@ -248,7 +255,7 @@ static void upols_free(upols* u) {
 static void upols_reset(upols* u) {
   memset(u->fdl, 0, sizeof(cf) * u->fdl_ch * u->K * u->bins);
   memset(u->head, 0, sizeof(size_t) * u->fdl_ch);
-  memset(u->window, 0, sizeof(float) * u->in_ch * 2 * u->N);
+  memset(u->window, 0, sizeof(real) * u->in_ch * 2 * u->N);
 }
 
 static const cf* fdl_slot(const upols* u, size_t ch, size_t age) {
@@ -257,17 +264,17 @@ static const cf* fdl_slot(const upols* u, size_t ch, size_t age) {
 }
 
 /* convolver.hpp:180-191: window shift, append, r2c, FDL push */
-static void upols_stage1(upols* u, size_t ch, const float* in) {
-  float* w = u->window + ch * 2 * u->N;
-  memmove(w, w + u->N, sizeof(float) * u->N);
-  memcpy(w + u->N, in, sizeof(float) * u->N);
+static void upols_stage1(upols* u, size_t ch, const real* in) {
+  real* w = u->window + ch * 2 * u->N;
+  memmove(w, w + u->N, sizeof(real) * u->N);
+  memcpy(w + u->N, in, sizeof(real) * u->N);
   u->head[ch] = (u->head[ch] + u->K - 1) % u->K; /* engine.hpp:250-258 */
-  forward_w(u->plan, w, (float*)(u->fdl + (ch * u->K + u->head[ch]) * u->bins),
+  forward_w(u->plan, w, (real*)(u->fdl + (ch * u->K + u->head[ch]) * u->bins),
             u->twork + (size_t)thread_id() * u->N);
 }
 
 /* stage 1 of channels [0, n): independent channels, one per thread */
-static void upols_stage1_all(upols* u, size_t n, const float* in) {
+static void upols_stage1_all(upols* u, size_t n, const real* in) {
 #pragma omp parallel for schedule(static) if (n * u->bins * 16 >= AO_PAR_MIN_WORK)
   for (size_t c = 0; c < n; ++c) upols_stage1(u, c, in + c * u->N);
 }
@@ -280,7 +287,7 @@ static void spectral_mac(const upols* u, const cf* H, size_t K, size_t fdl_ch,
     const cf* x = fdl_slot(u, fdl_ch, k);
     const cf* h = H + (row * K + k) * u->bins;
     for (size_t j = 0; j < u->bins; ++j) {
-      const float xr = x[j].re, xi = x[j].im, hr = h[j].re, hi = h[j].im;
+      const real xr = x[j].re, xi = x[j].im, hr = h[j].re, hi = h[j].im;
       acc[j].re += xr * hr - xi * hi;
       acc[j].im += xr * hi + xi * hr;
     }
@@ -290,23 +297,23 @@ static void spectral_mac(const upols* u, const cf* H, size_t K, size_t fdl_ch,
 /* MAC of row `row` of H (K partitions) against FDL channel fdl_ch, c2r,
  * keep the last N samples (convolver.hpp:193-206), in the calling thread's
  * scratch */
-static void mac_c2r(upols* u, const cf* H, size_t K, size_t fdl_ch, size_t row, float* out) {
+static void mac_c2r(upols* u, const cf* H, size_t K, size_t fdl_ch, size_t row, real* out) {
   const int t = thread_id();
   cf* acc = u->tacc + (size_t)t * u->bins;
-  float* time = u->ttime + (size_t)t * 2 * u->N;
+  real* time = u->ttime + (size_t)t * 2 * u->N;
   spectral_mac(u, H, K, fdl_ch, row, acc);
-  inverse_w(u->plan, (const float*)acc, time, u->twork + (size_t)t * u->N);
-  memcpy(out, time + u->N, sizeof(float) * u->N);
+  inverse_w(u->plan, (const real*)acc, time, u->twork + (size_t)t * u->N);
+  memcpy(out, time + u->N, sizeof(real) * u->N);
 }
 
 /* convolver.hpp:193-206 for every output channel (independent) */
-static void upols_stage23_all(upols* u, float* out) {
+static void upols_stage23_all(upols* u, real* out) {
 #pragma omp parallel for schedule(dynamic, 1) if (u->out_ch * u->K * u->bins >= AO_PAR_MIN_WORK)
   for (size_t c = 0; c < u->out_ch; ++c)
     mac_c2r(u, u->H, u->K, u->elementwise ? c : 0, c, out + c * u->N);
 }
 
-static void upols_process(upols* u, const float* in, float* out) {
+static void upols_process(upols* u, const real* in, real* out) {
   upols_stage1_all(u, u->in_ch, in);
   upols_stage23_all(u, out);
 }
@@ -316,11 +323,11 @@ struct ao_conv {
   int mode;
   upols* eng;  /* 1 engine, or Q engines in MIMO mode */
   size_t n_eng;
-  float* tmp;  /* outputs x N */
+  real* tmp;  /* outputs x N */
 };
 
 ao_conv* ao_conv_new(size_t N, size_t inputs, size_t outputs, int mode,
-                     const float* filters, size_t n_h) {
+                     const real* filters, size_t n_h) {
   if (N < 16 || N > 8192 || (N & (N - 1)) || outputs == 0 || n_h == 0) return NULL;
   if (mode == AO_BROADCAST && inputs != 1) return NULL;
   if (mode == AO_ELEMENTWISE && inputs != outputs) return NULL;
@@ -329,7 +336,7 @@ ao_conv* ao_conv_new(size_t N, size_t inputs, size_t outputs, int mode,
   c->N = N; c->inputs = inputs; c->outputs = outputs; c->mode = mode;
   c->n_eng = mode == AO_MIMO ? inputs : 1;
   c->eng = (upols*)calloc(c->n_eng, sizeof(upols));
-  c->tmp = (float*)calloc(outputs * N, sizeof(float));
+  c->tmp = (real*)calloc(outputs * N, sizeof(real));
   for (size_t e = 0; e < c->n_eng; ++e) {
     const int ew = mode == AO_ELEMENTWISE;
     const size_t in_ch = ew ? inputs : 1;
@@ -348,7 +355,7 @@ void ao_conv_free(ao_conv* c) {
   free(c->eng); free(c->tmp); free(c);
 }
 
-void ao_conv_process(ao_conv* c, const float* in, float* out) {
+void ao_conv_process(ao_conv* c, const real* in, real* out) {
   if (c->mode != AO_MIMO) { upols_process(&c->eng[0], in, out); return; }
   /* Appendix B: l_l = sum_q H_{l,q} * m_q, summed in q order */
   upols_process(&c->eng[0], in, out);
@@ -364,7 +371,7 @@ void ao_conv_reset(ao_conv* c) {
 
 size_t ao_conv_partitions(const ao_conv* c) { return c->eng[0].K; }
 
-void ao_conv_spectrum(const ao_conv* c, size_t row, size_t k, float* out) {
+void ao_conv_spectrum(const ao_conv* c, size_t row, size_t k, real* out) {
   const size_t e = row / c->outputs, r = row % c->outputs;
   const upols* u = &c->eng[e];
   memcpy(out, u->H + (r * u->K + k) * u->bins, sizeof(cf) * u->bins);
@@ -375,23 +382,23 @@ void ao_conv_spectrum(const ao_conv* c, size_t row, size_t k, float* out) {
  * feedback-canceller spectra) and Appendix B (Q = P inputs/mics). */
 struct ao_aur {
   size_t N, bins, Q, L, P, K_f;
-  float gain, mu, lambda, delta;
+  real gain, mu, lambda, delta;
   ao_conv* synth;      /* MIMO (or broadcast when Q == 1) */
   upols fc;            /* elementwise L -> L; H holds W for mic 0 */
   cf* W;               /* P x L x K_f x bins (W[0] aliases fc.H) */
-  float* fhat;         /* P x N */
-  float* mt;           /* Q x N  (m~) */
-  float* fc_out;       /* N */
-  float* ewin;         /* 2N error window */
+  real* fhat;         /* P x N */
+  real* mt;           /* Q x N  (m~) */
+  real* fc_out;       /* N */
+  real* ewin;         /* 2N error window */
   cf* E;               /* bins */
-  float* power;        /* bins */
-  float* scale;        /* bins */
-  float* fc_l;         /* L x N: per-loudspeaker canceller outputs */
+  real* power;        /* bins */
+  real* scale;        /* bins */
+  real* fc_l;         /* L x N: per-loudspeaker canceller outputs */
 };
 
-ao_aur* ao_aur_new(size_t N, size_t Q, size_t L, const float* synth,
-                   size_t n_h, const float* fc, size_t n_hf, float gain,
-                   float mu, float lambda, float delta) {
+ao_aur* ao_aur_new(size_t N, size_t Q, size_t L, const real* synth,
+                   size_t n_h, const real* fc, size_t n_hf, real gain,
+                   real mu, real lambda, real delta) {
   if (Q == 0 || L == 0 || n_hf == 0) return NULL;
   ao_aur* a = (ao_aur*)calloc(1, sizeof(ao_aur));
   a->N = N; a->bins = N + 1; a->Q = Q; a->L = L; a->P = Q;
@@ -410,14 +417,14 @@ ao_aur* ao_aur_new(size_t N, size_t Q, size_t L, const float* synth,
     memcpy(a->W + p * wsz, a->fc.H, sizeof(cf) * wsz);
   }
   memcpy(a->fc.H, a->W, sizeof(cf) * wsz);
-  a->fhat = (float*)calloc(a->P * N, sizeof(float));
-  a->mt = (float*)calloc(Q * N, sizeof(float));
-  a->fc_out = (float*)calloc(N, sizeof(float));
-  a->ewin = (float*)calloc(2 * N, sizeof(float));
+  a->fhat = (real*)calloc(a->P * N, sizeof(real));
+  a->mt = (real*)calloc(Q * N, sizeof(real));
+  a->fc_out = (real*)calloc(N, sizeof(real));
+  a->ewin = (real*)calloc(2 * N, sizeof(real));
   a->E = (cf*)calloc(a->bins, sizeof(cf));
-  a->power = (float*)calloc(a->bins, sizeof(float));
-  a->scale = (float*)calloc(a->bins, sizeof(float));
-  a->fc_l = (float*)calloc(L * N, sizeof(float));
+  a->power = (real*)calloc(a->bins, sizeof(real));
+  a->scale = (real*)calloc(a->bins, sizeof(real));
+  a->fc_l = (real*)calloc(L * N, sizeof(real));
   return a;
 }
 
@@ -436,9 +443,9 @@ static void nlms_update(ao_aur* a) {
   const size_t N = a->N, bins = a->bins, L = a->L, Kf = a->K_f;
   for (size_t j = 0; j < bins; ++j) a->scale[j] = a->mu / (a->power[j] + a->delta);
   for (size_t p = 0; p < a->P; ++p) {
-    memset(a->ewin, 0, sizeof(float) * N);
-    memcpy(a->ewin + N, a->mt + p * N, sizeof(float) * N);
-    ao_forward(a->fc.plan, a->ewin, (float*)a->E);
+    memset(a->ewin, 0, sizeof(real) * N);
+    memcpy(a->ewin + N, a->mt + p * N, sizeof(real) * N);
+    ao_forward(a->fc.plan, a->ewin, (real*)a->E);
 #pragma omp parallel for schedule(static) if (L * Kf * bins >= AO_PAR_MIN_WORK)
     for (size_t l = 0; l < L; ++l)
       for (size_t k = 0; k < Kf; ++k) {
@@ -453,7 +460,7 @@ static void nlms_update(ao_aur* a) {
   }
 }
 
-void ao_aur_process(ao_aur* a, const float* mic, float* spk) {
+void ao_aur_process(ao_aur* a, const real* mic, real* spk) {
   const size_t N = a->N, L = a->L, bins = a->bins;
   /* auralizer.hpp:73-76: m~ = g m - f^ (mic q pairs with estimate q) */
   for (size_t q = 0; q < a->Q; ++q)
@@ -470,7 +477,7 @@ void ao_aur_process(ao_aur* a, const float* mic, float* spk) {
   for (size_t p = 0; p < a->P; ++p) {
 #pragma omp parallel for schedule(dynamic, 1) if (L * a->K_f * bins >= AO_PAR_MIN_WORK)
     for (size_t l = 0; l < L; ++l) mac_c2r(&a->fc, a->W + p * wsz, a->K_f, l, l, a->fc_l + l * N);
-    float* f = a->fhat + p * N;
+    real* f = a->fhat + p * N;
     for (size_t i = 0; i < N; ++i) f[i] = 0.0f;
     for (size_t l = 0; l < L; ++l)
       for (size_t i = 0; i < N; ++i) f[i] += a->fc_l[l * N + i];
@@ -478,7 +485,7 @@ void ao_aur_process(ao_aur* a, const float* mic, float* spk) {
   /* Appendix A step 5: smoothed loudspeaker power for the next update */
   if (a->mu != 0.0f) {
     for (size_t j = 0; j < bins; ++j) {
-      float s = 0.0f;
+      real s = 0.0f;
       for (size_t l = 0; l < L; ++l) {
         const cf x = fdl_slot(&a->fc, l, 0)[j];
         s += x.re * x.re + x.im * x.im;
@@ -491,25 +498,25 @@ void ao_aur_process(ao_aur* a, const float* mic, float* spk) {
 void ao_aur_reset(ao_aur* a) {
   ao_conv_reset(a->synth);
   upols_reset(&a->fc);
-  memset(a->fhat, 0, sizeof(float) * a->P * a->N);
-  memset(a->power, 0, sizeof(float) * a->bins);
+  memset(a->fhat, 0, sizeof(real) * a->P * a->N);
+  memset(a->power, 0, sizeof(real) * a->bins);
 }
 
-void ao_aur_set_gain(ao_aur* a, float gain) { a->gain = gain; }
+void ao_aur_set_gain(ao_aur* a, real gain) { a->gain = gain; }
 
-void ao_aur_feedback_estimate(const ao_aur* a, float* out) {
-  memcpy(out, a->fhat, sizeof(float) * a->P * a->N);
+void ao_aur_feedback_estimate(const ao_aur* a, real* out) {
+  memcpy(out, a->fhat, sizeof(real) * a->P * a->N);
 }
 
 size_t ao_aur_fc_partitions(const ao_aur* a) { return a->K_f; }
 size_t ao_aur_synth_partitions(const ao_aur* a) { return ao_conv_partitions(a->synth); }
 
-void ao_aur_coeffs(const ao_aur* a, float* out) {
+void ao_aur_coeffs(const ao_aur* a, real* out) {
   memcpy(out, a->W, sizeof(cf) * a->P * a->L * a->K_f * a->bins);
 }
 
-void ao_aur_power(const ao_aur* a, float* out) {
-  memcpy(out, a->power, sizeof(float) * a->bins);
+void ao_aur_power(const ao_aur* a, real* out) {
+  memcpy(out, a->power, sizeof(real) * a->bins);
 }
 
 /* oracle.hpp:15-27 */

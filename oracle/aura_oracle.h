@@ -32,6 +32,15 @@
 extern "C" {
 #endif
 
+/* arithmetic type: float (liboracle.so) or double (liboracle64.so, built
+ * with -DAO_F64: the float64 ground truth); every array argument below is
+ * of this type */
+#ifdef AO_F64
+typedef double ao_real;
+#else
+typedef float ao_real;
+#endif
+
 typedef struct ao_plan ao_plan;
 typedef struct ao_conv ao_conv;
 typedef struct ao_aur ao_aur;
@@ -42,38 +51,38 @@ enum { AO_BROADCAST = 0, AO_ELEMENTWISE = 1, AO_MIMO = 2 };
 ao_plan* ao_plan_new(size_t fft_size);
 void ao_plan_free(ao_plan* p);
 /* spectrum: (fft_size/2 + 1) complex as 2 floats each */
-void ao_forward(const ao_plan* p, const float* buffer, float* spectrum);
-void ao_inverse(const ao_plan* p, const float* spectrum, float* buffer);
+void ao_forward(const ao_plan* p, const ao_real* buffer, ao_real* spectrum);
+void ao_inverse(const ao_plan* p, const ao_real* spectrum, ao_real* buffer);
 
 /* filters: rows x n_h contiguous. broadcast: rows = outputs, inputs = 1;
  * elementwise: rows = outputs = inputs; mimo: rows = inputs * outputs,
  * row q * outputs + l = H_{l,q}. Returns NULL on bad arguments. */
 ao_conv* ao_conv_new(size_t block, size_t inputs, size_t outputs, int mode,
-                     const float* filters, size_t n_h);
+                     const ao_real* filters, size_t n_h);
 void ao_conv_free(ao_conv* c);
-void ao_conv_process(ao_conv* c, const float* in, float* out);
+void ao_conv_process(ao_conv* c, const ao_real* in, ao_real* out);
 void ao_conv_reset(ao_conv* c);
 size_t ao_conv_partitions(const ao_conv* c);
 /* copy spectrum of filter row r, partition k: (N+1) complex */
-void ao_conv_spectrum(const ao_conv* c, size_t row, size_t k, float* out);
+void ao_conv_spectrum(const ao_conv* c, size_t row, size_t k, ao_real* out);
 
 /* Auralizer. inputs Q = mics P. synth: Q*L rows x n_h (row q*L + l);
  * fc: P*L rows x n_hf (row p*L + l). mu == 0 -> fixed F^ (reference). */
 ao_aur* ao_aur_new(size_t block, size_t inputs, size_t outputs,
-                   const float* synth, size_t n_h, const float* fc,
-                   size_t n_hf, float gain, float mu, float lambda,
-                   float delta);
+                   const ao_real* synth, size_t n_h, const ao_real* fc,
+                   size_t n_hf, ao_real gain, ao_real mu, ao_real lambda,
+                   ao_real delta);
 void ao_aur_free(ao_aur* a);
-void ao_aur_process(ao_aur* a, const float* mic, float* speakers);
+void ao_aur_process(ao_aur* a, const ao_real* mic, ao_real* speakers);
 void ao_aur_reset(ao_aur* a);
-void ao_aur_set_gain(ao_aur* a, float gain);
-void ao_aur_feedback_estimate(const ao_aur* a, float* out /* P x N */);
+void ao_aur_set_gain(ao_aur* a, ao_real gain);
+void ao_aur_feedback_estimate(const ao_aur* a, ao_real* out /* P x N */);
 size_t ao_aur_fc_partitions(const ao_aur* a);
 size_t ao_aur_synth_partitions(const ao_aur* a);
 /* W as P x L x K_f x (N+1) complex */
-void ao_aur_coeffs(const ao_aur* a, float* out);
+void ao_aur_coeffs(const ao_aur* a, ao_real* out);
 /* NLMS power vector, N+1 floats */
-void ao_aur_power(const ao_aur* a, float* out);
+void ao_aur_power(const ao_aur* a, ao_real* out);
 
 /* y[0 .. nx+nh-2] = x * h in float64 (oracle.hpp:15-27) */
 void ao_direct_convolve(const double* x, size_t nx, const double* h,

@@ -193,6 +193,7 @@ def lib():
     L.aura_b200_afc_coeffs.argtypes = [vp, _f32p]
     L.aura_b200_fdl_slot.argtypes = [vp, C.c_int, sz, sz, _f32p]
     L.aura_b200_time_device_blocks.argtypes = [vp, C.c_void_p, sz, sz, _f32p, _f32p]
+    L.aura_b200_time_device_span.argtypes = [vp, C.c_void_p, sz, sz, C.POINTER(C.c_float)]
     L.aura_b200_synchronize.argtypes = [vp]
     L.aura_b200_time_host_blocks.argtypes = [vp, _f32p, sz, sz, C.c_double, _f32p]
     L.aura_b200_profile_phases.argtypes = [vp, sz, _f32p, C.POINTER(C.c_int)]
@@ -394,6 +395,17 @@ class _Engine:
         """Wait for every processed block's background work (next-block
         precompute, canceller update)."""
         _check(lib().aura_b200_synchronize(self._h))
+
+    def time_device_span(self, blocks: int, inputs: Optional[np.ndarray] = None) -> float:
+        """Mean device time per block (us) of `blocks` back-to-back blocks
+        timed with one event pair around all of them."""
+        v = C.c_float(0)
+        ptr, n = None, 0
+        if inputs is not None:
+            inputs = np.ascontiguousarray(inputs, np.float32)
+            ptr, n = inputs.ctypes.data, inputs.shape[0]
+        _check(lib().aura_b200_time_device_span(self._h, ptr, n, blocks, C.byref(v)))
+        return float(v.value) / blocks
 
     def time_device_blocks(self, blocks: int, inputs: Optional[np.ndarray] = None):
         """Back-to-back device-resident blocks timed with CUDA events.

@@ -1562,6 +1562,40 @@ int aura_b200_time_device_blocks(aura_b200_engine* e, const float* host_in,
   });
 }
 
+// Device-resident blocks back to back with ONE event pair around all of
+// them: the mean block time without per-block event records in the stream.
+int aura_b200_time_device_span(aura_b200_engine* e, const float* host_in, size_t n_in_blocks,
+                               size_t blocks, float* total_us) {
+  return guarded([&] {
+    CK(cudaSetDevice(e->device));
+    CK(cudaStreamSynchronize(e->stream));
+    const size_t per = (size_t)e->Qx * e->N;
+    const size_t slots = std::max<size_t>(1, std::min(n_in_blocks, e->pool_blocks));
+    if (host_in && n_in_blocks)
+      CK(cudaMemcpy(e->d_in_pool, host_in, slots * per * sizeof(float), cudaMemcpyHostToDevice));
+    std::vector<aura_b200_engine::BlockGraph> gs;
+    std::vector<BlockArgs> sa(slots, e->dev_args);
+    for (size_t s = 0; s < slots; ++s) {
+      sa[s].in = e->d_in_pool + s * per;
+      gs.push_back(e->capture_block(sa[s], nullptr));
+    }
+    cudaEvent_t t0, t1;
+    CK(cudaEventCreate(&t0));
+    CK(cudaEventCreate(&t1));
+    CK(cudaEventRecord(t0, e->stream));
+    for (size_t b = 0; b < blocks; ++b) e->enqueue_block(gs[b % slots], sa[b % slots], nullptr);
+    CK(cudaEventRecord(t1, e->stream));
+    CK(cudaStreamSynchronize(e->stream));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, t0, t1));
+    *total_us = ms * 1000.0f;
+    cudaEventDestroy(t0);
+    cudaEventDestroy(t1);
+    for (auto& g : gs) g.destroy();
+    e->blocks += blocks;
+  });
+}
+
 int aura_b200_time_host_blocks(aura_b200_engine* e, const float* host_in,
                                size_t n_in_blocks, size_t blocks, double pace_us,
                                float* block_us) {

@@ -60,3 +60,31 @@ def test_sweep_csv_keeps_the_reference_header_and_number_format():
     N, C, n_h, n_hf, fs = m.resolve("filter_length_s", 2.0)
     assert (N, C, n_h, n_hf, fs) == (128, 32, 96000, 48000, 48000)
     assert m.resolve("block_size", 64)[0] == 64 and m.resolve("channels", 8)[1] == 8
+
+
+def test_gpus_flag_relaunches_one_process_per_rank():
+    """`bench.py --gpus 2` without torchrun re-launches itself under
+    torch.distributed.run; the reference arm runs on rank 0 only and prints
+    ONE line whose n_gpus is the requested world (CPU-only: the reference arm
+    needs no GPU)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference",
+                          "--gpus", "2", "--config", "c1", "--steps", "3", "--warmup", "1"],
+                         capture_output=True, text=True, timeout=600, env=env, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["steps"] == 3
+    assert "weak scaling" in d["config"]["workload"]
+
+
+def test_l2_roofline_peak_from_the_committed_probe():
+    peak, kind = bench.l2_read_peak(64e6)
+    assert peak is not None and 5000 < peak < 20000 and "r2_l2_probe" in kind
+    assert bench.roofline_regime(65e6 / 2) == "l2" and bench.roofline_regime(323e6) == "hbm"

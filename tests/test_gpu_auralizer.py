@@ -187,26 +187,37 @@ def test_closed_loop_divergence_without_cancellation():
     assert all(energy[b + 1] > energy[b] for b in range(3, 12))
 
 
-def test_c3_config_streams_and_matches_oracle_subset():
+@pytest.mark.parametrize("delta", [None, 1e-2 * 2 * 64])
+def test_c3_config_streams_and_matches_oracle_subset(delta):
     """configs[2] shape (1 x 64, N = 64, 10 s synthesis, 1 s canceller, NLMS
-    on): 200 blocks on the GPU against the C oracle at full size; outputs,
-    f^ and the canceller spectra W within 1e-5 of their RMS."""
+    on) at the survey regulariser (None: 1e-6 N) and at -20 dB of the
+    per-bin loudspeaker power (1e-2 2N): 200 blocks on the GPU against the C
+    oracle and its float64 build. Outputs and f^ within 1e-5 of the oracle;
+    the canceller W as accurate as the fp32 oracle's (tiny regularisers
+    amplify fp32 rounding in quiet bins: the oracle itself is ~1e-5 off the
+    float64 W there) and within 1e-5 + that of the oracle."""
     N, L = 64, 64
     rng = np.random.default_rng(2024)
     synth = decaying_filters(rng, L, 480000)
     fc = decaying_filters(rng, L, 48000, t60_s=0.3, scale=0.1)
-    kw = dict(mu=0.005, lam=0.9)  # default regulariser 1e-2 * 2N
+    kw = dict(mu=0.005, lam=0.9, delta=delta)
     g = gpu_aur(synth, fc, N, 1, L, **kw)
     assert g.synth_partitions() == 7500 and g.fc_partitions() == 750
     o = O.OracleAuralizer(synth, fc, N, 1, L, **kw)
+    x = O.OracleAuralizer(synth, fc, N, 1, L, f64=True, **kw)
     ys, yo = [], []
     for _ in range(200):
         m = rng.standard_normal((1, N)).astype(np.float32)
         ys.append(g.process(m))
         yo.append(o.process(m))
+        x.process(m)
     assert rel_err(np.stack(ys), np.stack(yo)) <= TOL
     assert rel_err(g.feedback_estimate(), o.feedback_estimate()) <= TOL
-    assert rel_err(g.coeffs(), o.coeffs()) <= TOL
+    Wg, Wo, Wx = g.coeffs(), o.coeffs(), x.coeffs()
+    gx, ox, go = rel_err(Wg, Wx), rel_err(Wo, Wx), rel_err(Wg, Wo)
+    print(f"delta={delta}: W gpu-truth {gx:.3e} oracle-truth {ox:.3e} gpu-oracle {go:.3e}")
+    assert gx <= max(TOL, 1.5 * ox), (gx, ox)
+    assert go <= TOL + ox, (go, ox)
 
 
 def test_engines_of_different_shapes_coexist():

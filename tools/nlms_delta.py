@@ -46,6 +46,10 @@ def run(N, L, n_h, n_hf, delta, blocks, checkpoints, mu=0.005, lam=0.9, seed=11)
                              W_gpu_vs_oracle=rel_err(Wg, Wo),
                              y_gpu_vs_f64=rel_err(yg, yd), y_oracle_vs_f64=rel_err(yo, yd),
                              y_gpu_vs_oracle=rel_err(yg, yo)))
+            l, k, j = np.unravel_index(int(np.argmax(np.abs(Wg - Wo))), Wg.shape)
+            pw = o.power()
+            rows[-1].update(worst_lkj=[int(l), int(k), int(j)], power_at_worst=float(pw[j]),
+                            power_min=float(pw.min()), power_median=float(np.median(pw)))
             print(json.dumps(rows[-1]), flush=True)
     g.close()
     return rows
@@ -53,6 +57,10 @@ def run(N, L, n_h, n_hf, delta, blocks, checkpoints, mu=0.005, lam=0.9, seed=11)
 
 if __name__ == "__main__":
     cps = {1, 2, 5, 10, 20, 50, 100, 200}
+    if sys.argv[1:] == ["c3"]:  # BASELINE configs[2] at full size (10 s synthesis)
+        for delta in (1e-6 * 64, 1e-2 * 2 * 64, 1.0):
+            run(64, 64, 480000, 48000, delta, 200, {1, 2, 10, 50, 100, 200}, seed=2024)
+        sys.exit(0)
     for (N, L, n_h, n_hf) in [(64, 8, 64 * 40, 64 * 40), (64, 64, 64 * 40, 48000)]:
         for delta in (1e-6 * N, 1e-2 * 2 * N):
             run(N, L, n_h, n_hf, delta, 200, cps)
