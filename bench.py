@@ -630,6 +630,24 @@ def run_sharded(args, cfg, rank, world, local_rank):
     dist.barrier()
     local.close()
     dist.barrier()
+    # exchange ablation: the same sharded canceller with the
+    # partials all-reduced by NCCL (graph-captured) instead of our P2P kernel
+    nccl = None
+    if cfg["afc"] and not args.no_nccl:
+        try:
+            ne = S.ShardedAuralizer(LazyRows(Q * L, cfg["n_h"], cfg["fs"], seed=1000),
+                                    LazyRows(Q * L, cfg["n_hf"], cfg["fs"], t60_s=0.3, scale=0.1, seed=2000),
+                                    ec, device=device, afc=A.AfcParams(cfg.get("mu", 0.0), 0.9, None),
+                                    transport="nccl")
+            ne.engine.time_device_blocks(max(3, W), mic)
+            dist.barrier()
+            _, nd = ne.engine.time_device_blocks(K, mic)
+            dist.barrier()
+            ne.close()
+            nccl = {"dev": nd}
+        except A.Error as err:
+            nccl = {"error": str(err)}
+        dist.barrier()
     # BASELINE configs[4]: 512 loudspeakers split over the GPUs (strong)
     c5 = None if args.no_c5 else c5_secondary(A, device, K, W, world, rank)
     dist.barrier()
@@ -639,7 +657,7 @@ def run_sharded(args, cfg, rank, world, local_rank):
     if not args.no_max_rt and ndev >= world:
         maxrt = max_realtime(A, dict(CONFIGS[args.config]), device, budget_s=args.max_rt_s)
     dist.barrier()
-    mine = {"lat": lat_us, "dev": dev_us, "host": host_us, "mac_us": mac_us,
+    mine = {"lat": lat_us, "dev": dev_us, "host": host_us, "mac_us": mac_us, "nccl": nccl,
             "mac_bytes": mac_bytes, "launches": n_launch, "c5": c5, "maxrt": maxrt,
             "clocks": clocks, "channels": (eng.l0, eng.l1), "setup": t_setup}
     allr = [None] * world
@@ -677,6 +695,7 @@ def run_sharded(args, cfg, rank, world, local_rank):
             "gpu_launches": int(K * sum(r["launches"] for r in allr)),
             "setup_s": max(r["setup"] for r in allr),
             "c5": c5_summary([r["c5"] for r in allr], world) if allr[0]["c5"] else None,
+            "exchange_ablation": _exchange_ablation(dev, allr),
             "max_realtime": ({"channels": sum(r["maxrt"]["channels"] for r in allr),
                               "taps": cfg["n_h"],
                               "channels_x_taps": sum(r["maxrt"]["channels"] for r in allr) * cfg["n_h"],
@@ -692,6 +711,22 @@ def run_sharded(args, cfg, rank, world, local_rank):
     return 0
 
 
+def _exchange_ablation(dev_p2p, allr):
+    """Block p50/p99 (max over ranks) with the P2P exchange kernel (value)
+    and with the NCCL all-reduce, or why NCCL did not run."""
+    if not allr[0]["nccl"]:
+        return None
+    errs = [r["nccl"]["error"] for r in allr if "error" in r["nccl"]]
+    out = {"p2p": {"p50_us": pct(dev_p2p, 50), "p99_us": pct(dev_p2p, 99)},
+           "nccl_env": {k: os.environ.get(k) for k in ("NCCL_ALGO", "NCCL_PROTO")}}
+    if errs:
+        out["nccl"] = {"error": errs[0]}
+    else:
+        nd = np.max(np.stack([r["nccl"]["dev"] for r in allr]), axis=0)
+        out["nccl"] = {"p50_us": pct(nd, 50), "p99_us": pct(nd, 99)}
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -705,6 +740,7 @@ def main():
     ap.add_argument("--no-max-rt", action="store_true", help="skip the max real-time search")
     ap.add_argument("--max-rt-s", type=float, default=110.0, help="time box of the max-RT search")
     ap.add_argument("--no-c5", action="store_true", help="skip the configs[4] (c5) line")
+    ap.add_argument("--no-nccl", action="store_true", help="N > 1: skip the NCCL exchange ablation")
     ap.add_argument("--no-paced", action="store_true")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="N > 1: weak keeps the config's loudspeakers per GPU, strong splits them")

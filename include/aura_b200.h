@@ -186,6 +186,17 @@ int aura_b200_shard_connect(aura_b200_engine* e, const void* handles);
  * GPU, or several GPUs of one process through P2P); engine g is rank g. */
 int aura_b200_shard_connect_local(aura_b200_engine* const* engines, int world);
 int aura_b200_shard_info(const aura_b200_engine* e, int* world, int* rank);
+/* The same exchange through NCCL instead of our P2P kernel (SURVEY 8(e)'s
+ * north-star transport, kept as the ablation): one ncclAllReduce(sum) of
+ * the P*N + 2N partials per block, captured in the block's CUDA graph, then
+ * k_afc_apply. NCCL is loaded at first use (libnccl.so.2); the summation
+ * order is NCCL's (pin NCCL_ALGO / NCCL_PROTO for run-to-run determinism).
+ * Protocol: rank 0 calls nccl_unique_id, the 128 bytes reach every rank by
+ * the host's plumbing, every rank calls shard_connect_nccl. world = 1 is
+ * allowed (a local all-reduce; bit-identical to the unsharded engine). */
+#define AURA_B200_NCCL_ID_BYTES 128
+int aura_b200_nccl_unique_id(void* id);
+int aura_b200_shard_connect_nccl(aura_b200_engine* e, int world, int rank, const void* id);
 
 /* Measurement and diagnostics entry points (bench.py, tools/): see
  * aura_b200_diag.h -- not part of the reference-replacing API. */

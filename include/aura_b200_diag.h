@@ -71,6 +71,11 @@ int aura_b200_time_phase(aura_b200_engine* e, int phase, size_t reps, float* avg
  * slot 10 = {the next block's front start, 0}. -1 when the event did not
  * occur. Shows launch gaps and overlap. */
 int aura_b200_trace_blocks(aura_b200_engine* e, size_t blocks, double* out);
+/* The same timeline with the blocks run through process()'s own handshake
+ * (mapped input and output, output words; host_in: n_in_blocks x inputs x N,
+ * cycled), back to back: where the end-to-end path differs on the device. */
+int aura_b200_trace_host_blocks(aura_b200_engine* e, const float* host_in, size_t n_in_blocks, size_t blocks,
+                                double* out);
 /* Diagnostics (not in the reference): per-segment / per-CTA timeline of the
  * streaming kernel k_back for the last of `blocks` blocks, us from the
  * kernel's first CTA start. out_segs: n_segs x {kind, tile, begin, end,

@@ -205,6 +205,8 @@ def lib():
     L.aura_b200_launches_per_block.argtypes = [vp]
     L.aura_b200_time_phase.argtypes = [vp, C.c_int, sz, C.POINTER(C.c_float)]
     L.aura_b200_trace_blocks.argtypes = [vp, sz, np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")]
+    L.aura_b200_trace_host_blocks.argtypes = [vp, _f32p, sz, sz,
+                                              np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")]
     L.aura_b200_trace_back.argtypes = [vp, sz, vp, C.POINTER(C.c_size_t), vp, C.POINTER(C.c_size_t)]
     _lib = L
     return L
@@ -326,12 +328,16 @@ class _Engine:
                      "output", "afc_summed", "afc_c2r", "front_x")
     _TRACE_SLOTS = 11  # kTraceKernels: the last slot is the next block's front start
 
-    def trace_blocks(self, blocks: int = 32):
+    def trace_blocks(self, blocks: int = 32, host_inputs: Optional[np.ndarray] = None):
         """Per-kernel [start, end] (us from the block's front start) of
         back-to-back blocks, from %globaltimer stamps inside the kernels."""
         blocks = min(blocks, 64)
         out = np.zeros(blocks * self._TRACE_SLOTS * 2, np.float64)
-        _check(lib().aura_b200_trace_blocks(self._h, blocks, out))
+        if host_inputs is None:
+            _check(lib().aura_b200_trace_blocks(self._h, blocks, out))
+        else:  # through process()'s mapped-memory handshake
+            x = np.ascontiguousarray(host_inputs, np.float32)
+            _check(lib().aura_b200_trace_host_blocks(self._h, x, x.shape[0], blocks, out))
         out = out.reshape(blocks, self._TRACE_SLOTS, 2)
         res = {name: out[:, k, :] for k, name in enumerate(self.TRACE_KERNELS)
                if np.all(out[:, k, 0] >= 0)}

@@ -13,6 +13,8 @@
 //   aura_b200_filter_spectrum   PartitionedFilterSet::spectrum engine.hpp:210-219
 //   aura_b200_device_count      list_backends             backend.hpp:186-193
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <atomic>
 #include <thread>
@@ -123,6 +125,41 @@ T* dalloc(size_t count, std::vector<void*>& owned) {
   return static_cast<T*>(p);
 }
 
+// NCCL, loaded on first use (dlopen): only the NCCL exchange ablation needs
+// it, so the library loads and runs without NCCL installed.
+struct NcclApi {
+  ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*allreduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*destroy)(ncclComm_t) = nullptr;
+  const char* (*error_string)(ncclResult_t) = nullptr;
+  std::string why;
+};
+NcclApi& nccl_api() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      api.why = std::string("libnccl.so.2 not found: ") + dlerror();
+      return;
+    }
+    api.get_unique_id = reinterpret_cast<decltype(api.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+    api.init_rank = reinterpret_cast<decltype(api.init_rank)>(dlsym(h, "ncclCommInitRank"));
+    api.allreduce = reinterpret_cast<decltype(api.allreduce)>(dlsym(h, "ncclAllReduce"));
+    api.destroy = reinterpret_cast<decltype(api.destroy)>(dlsym(h, "ncclCommDestroy"));
+    api.error_string = reinterpret_cast<decltype(api.error_string)>(dlsym(h, "ncclGetErrorString"));
+    if (!api.get_unique_id || !api.init_rank || !api.allreduce || !api.destroy || !api.error_string)
+      api.why = "libnccl.so.2 lacks the NCCL 2 API";
+  });
+  if (!api.why.empty()) fail(AURA_B200_E_BACKEND_UNAVAILABLE, "NCCL exchange unavailable: " + api.why);
+  return api;
+}
+void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) fail(AURA_B200_E_CUDA, std::string(what) + ": " + nccl_api().error_string(r));
+}
+
 }  // namespace
 
 enum Phase { PH_FRONT = 0, PH_BACK_HEAD, PH_BACK, PH_REDUCE, PH_AFC_FINISH, PH_ADVANCE, PH_COUNT };
@@ -161,7 +198,6 @@ struct aura_b200_engine {
   size_t w_elems = 0;
   float* h_in = nullptr;    // mapped pinned
   float* h_out = nullptr;   // mapped pinned
-  float* h_fhat = nullptr;  // mapped pinned copy of f^
   float* d_in_pool = nullptr;
   size_t pool_blocks = 0;
   float* d_out = nullptr;
@@ -197,6 +233,7 @@ struct aura_b200_engine {
   char* xbuf = nullptr;
   size_t xbuf_bytes = 0;
   std::vector<void*> ipc_opened;  // peer buffers opened through CUDA IPC
+  ncclComm_t nccl = nullptr;      // NCCL exchange (xchg 2)
   unsigned* h_status = nullptr;   // mapped pinned; set by k_afc_finish on timeout
   size_t smem_front = 0, smem_head = 0;
 
@@ -209,10 +246,10 @@ struct aura_b200_engine {
     for (void* p : dmem) cudaFree(p);
     if (h_in) cudaFreeHost(h_in);
     if (h_out) cudaFreeHost(h_out);
-    if (h_fhat) cudaFreeHost(h_fhat);
     if (h_status) cudaFreeHost(h_status);
     if (h_outflag) cudaFreeHost(h_outflag);
     for (void* p : ipc_opened) cudaIpcCloseMemHandle(p);
+    if (nccl) nccl_api().destroy(nccl);
     if (ev_front) cudaEventDestroy(ev_front);
     if (ev_back) cudaEventDestroy(ev_back);
     if (stream) cudaStreamDestroy(stream);
@@ -225,7 +262,7 @@ struct aura_b200_engine {
   int front_grid(const BlockArgs& a) const {
     return (int)((L + a.cpb - 1) / a.cpb) + ((front_head && aur && a.nlms) ? (int)P : 0);
   }
-  bool sharded() const { return aur && G > 1; }
+  bool sharded() const { return aur && args.xchg != 0; }
 
   // k_back after k_back_head is a programmatic dependent launch: it starts
   // while k_back_head runs and waits for it (griddepcontrol.wait) only where
@@ -266,7 +303,12 @@ struct aura_b200_engine {
                      !pdl_off, a, s);
         break;
       case PH_AFC_FINISH:
-        if (sharded()) k_afc_finish<<<1, kTailThreads, 0, s>>>(a);
+        if (sharded() && a.xchg == 1) k_afc_finish<<<1, kTailThreads, 0, s>>>(a);
+        if (sharded() && a.xchg == 2) {
+          nccl_check(nccl_api().allreduce(a.xmine, a.xsum, (size_t)(P * N + 2 * N), ncclFloat, ncclSum, nccl, s),
+                     "ncclAllReduce");
+          k_afc_apply<<<1, kTailThreads, 0, s>>>(a);
+        }
         break;
       case PH_ADVANCE:
         if (!has_back()) k_advance<<<1, 1, 0, s>>>(a.st);
@@ -276,7 +318,7 @@ struct aura_b200_engine {
 
   // kernels launched per block
   int launches_per_block() const {
-    return 1 + (has_head() ? 1 : 0) + (has_back() ? 2 : 0) + (sharded() ? 1 : 0) +
+    return 1 + (has_head() ? 1 : 0) + (has_back() ? 2 : 0) + (sharded() ? 1 : 0) +  // (+ NCCL's own)
            (has_back() ? 0 : 1);
   }
 
@@ -704,11 +746,22 @@ void plan_back(aura_b200_engine* e, BlockArgs& a) {
     sl += cnt[t];
     (t < tiles ? max_syn : max_afc) = std::max(t < tiles ? max_syn : max_afc, cnt[t]);
   }
+  // items carry their partial's index in the partials array (tile's first
+  // partial + the item's rank in the tile), so k_back never reads tinfo
+  for (auto& ch : chunks) {
+    const int kind = ch.x & 1, tile = ch.x >> 1;
+    ch.w += tinfo[kind ? tiles + tile : tile].x;
+  }
   a.n_chunks = (int)chunks.size();
   a.plan_ctas = ctas;
-  int* doff = dalloc<int>(item_off.size(), e->dmem);
-  CK(cudaMemcpy(doff, item_off.data(), item_off.size() * sizeof(int), cudaMemcpyHostToDevice));
-  a.item_off = doff;
+  std::vector<int4> first(2 * (size_t)ctas);
+  for (int c = 0; c < ctas; ++c) {
+    first[2 * c] = make_int4(item_off[c], item_off[c + 1], 0, 0);
+    first[2 * c + 1] = item_off[c] < item_off[c + 1] ? chunks[item_off[c]] : make_int4(0, 0, 0, 0);
+  }
+  int4* dfirst = dalloc<int4>(first.size(), e->dmem);
+  CK(cudaMemcpy(dfirst, first.data(), first.size() * sizeof(int4), cudaMemcpyHostToDevice));
+  a.cta_first = dfirst;
   e->n_syn_segs = slot_syn;
   e->n_afc_segs = slot_afc;
   e->h_chunks = chunks;
@@ -798,11 +851,8 @@ void finish_init(aura_b200_engine* e) {
   CK(cudaHostGetDevicePointer((void**)&a.status_host, e->h_status, 0));
   a.G = 1;
   a.grank = 0;
-  if (e->aur) {
-    CK(cudaHostAlloc(&e->h_fhat, e->P * N * sizeof(float), cudaHostAllocMapped | cudaHostAllocPortable));
-    std::memset(e->h_fhat, 0, e->P * N * sizeof(float));
-    CK(cudaHostGetDevicePointer((void**)&a.fhat_host, e->h_fhat, 0));
-  }
+  a.xchg = 0;
+  a.xsum = nullptr;
   float* din;
   float* dout;
   CK(cudaHostGetDevicePointer((void**)&din, e->h_in, 0));
@@ -903,7 +953,6 @@ void reset_state(aura_b200_engine* e) {
     CK(cudaMemsetAsync(a.prev_spk, 0, sizeof(float) * e->L * N, s));
     CK(cudaMemsetAsync(a.XA, 0, sizeof(float4) * e->L * (e->KF + 1) * NF, s));
     CK(cudaMemsetAsync(a.fhat, 0, sizeof(float) * e->P * N, s));
-    std::memset(e->h_fhat, 0, sizeof(float) * e->P * N);
     CK(cudaMemsetAsync(a.pw, 0, sizeof(float2) * N, s));
     if (a.nlms)
       CK(cudaMemcpyAsync(a.W, e->W0, sizeof(float4) * e->w_elems, cudaMemcpyDeviceToDevice, s));
@@ -1252,7 +1301,10 @@ int aura_b200_feedback_estimate(aura_b200_engine* e, float* out) {
     if (e->blocks) wait_event(e, e->ev_back, "block background");
     CK(cudaStreamSynchronize(e->stream));
     check_shard_status(e);
-    std::memcpy(out, e->h_fhat, sizeof(float) * e->P * e->N);
+    // f^ stays in device memory (the background kernels never write mapped
+    // host memory: a system-scope write over PCIe at the end of k_reduce
+    // would stretch every block's kernel boundary); copy it out on demand
+    CK(cudaMemcpy(out, e->args.fhat, sizeof(float) * e->P * e->N, cudaMemcpyDeviceToHost));
   });
 }
 
@@ -1389,7 +1441,7 @@ void shard_alloc(aura_b200_engine* e, int world, int rank) {
          "only a feedback canceller exchanges data between shards (convolver shards are independent)");
   if (world < 2 || world > kMaxShards || rank < 0 || rank >= world)
     fail(AURA_B200_E_INVALID_ARGUMENT, "shard world must be 2..8 and 0 <= rank < world");
-  if (e->xbuf) fail(AURA_B200_E_INVALID_ARGUMENT, "engine is already sharded");
+  if (e->xbuf || e->args.xchg) fail(AURA_B200_E_INVALID_ARGUMENT, "engine is already sharded");
   if (e->blocks) fail(AURA_B200_E_INVALID_ARGUMENT, "shard before the first block");
   CK(cudaSetDevice(e->device));
   const size_t S = e->P * e->N + 2 * e->N;
@@ -1402,11 +1454,48 @@ void shard_alloc(aura_b200_engine* e, int world, int rank) {
   e->grank = rank;
 }
 
+// NCCL exchange: the exchange buffers, the communicator (one per engine,
+// ranks = shards), then the graphs with the all-reduce captured in them.
+void nccl_connect(aura_b200_engine* e, int world, int rank, const void* id) {
+  if (!e->aur)
+    fail(AURA_B200_E_INVALID_ARGUMENT,
+         "only a feedback canceller exchanges data between shards (convolver shards are independent)");
+  if (world < 1 || world > kMaxShards || rank < 0 || rank >= world)
+    fail(AURA_B200_E_INVALID_ARGUMENT, "shard world must be 1..8 and 0 <= rank < world");
+  if (e->args.xchg) fail(AURA_B200_E_INVALID_ARGUMENT, "engine is already sharded");
+  if (e->blocks) fail(AURA_B200_E_INVALID_ARGUMENT, "shard before the first block");
+  NcclApi& api = nccl_api();
+  CK(cudaSetDevice(e->device));
+  const size_t S = e->P * e->N + 2 * e->N;
+  e->args.xmine = dalloc<float>(S, e->dmem);
+  e->args.xsum = dalloc<float>(S, e->dmem);
+  CK(cudaMemset(e->args.xmine, 0, S * sizeof(float)));
+  CK(cudaMemset(e->args.xsum, 0, S * sizeof(float)));
+  ncclUniqueId uid;
+  std::memcpy(&uid, id, sizeof uid);
+  nccl_check(api.init_rank(&e->nccl, world, uid, rank), "ncclCommInitRank");
+  e->G = world;
+  e->grank = rank;
+  BlockArgs& a = e->args;
+  a.G = world;
+  a.grank = rank;
+  a.xchg = 2;
+  set_advance_total(e);
+  CK(cudaStreamSynchronize(e->stream));
+  e->rebuild_graphs();
+  BlockArgs d = a;
+  d.out = e->d_out;
+  d.in = e->d_in_pool;
+  d.out_flag = nullptr;
+  e->dev_args = d;
+}
+
 void shard_finalize(aura_b200_engine* e, char* const* peers) {
   CK(cudaSetDevice(e->device));
   BlockArgs& a = e->args;
   a.G = e->G;
   a.grank = e->grank;
+  a.xchg = 1;
   for (int g = 0; g < kMaxShards; ++g) a.xpeer[g] = g < e->G ? peers[g] : nullptr;
   set_advance_total(e);
   CK(cudaStreamSynchronize(e->stream));
@@ -1475,6 +1564,22 @@ int aura_b200_shard_connect_local(aura_b200_engine* const* engines, int world) {
     std::vector<char*> peers(world);
     for (int g = 0; g < world; ++g) peers[g] = engines[g]->xbuf;
     for (int g = 0; g < world; ++g) shard_finalize(engines[g], peers.data());
+  });
+}
+
+int aura_b200_nccl_unique_id(void* id) {
+  return guarded([&] {
+    if (!id) fail(AURA_B200_E_INVALID_ARGUMENT, "null argument");
+    ncclUniqueId uid;
+    nccl_check(nccl_api().get_unique_id(&uid), "ncclGetUniqueId");
+    std::memcpy(id, &uid, sizeof uid);
+  });
+}
+
+int aura_b200_shard_connect_nccl(aura_b200_engine* e, int world, int rank, const void* id) {
+  return guarded([&] {
+    if (!e || !id) fail(AURA_B200_E_INVALID_ARGUMENT, "null argument");
+    nccl_connect(e, world, rank, id);
   });
 }
 
@@ -1757,64 +1862,91 @@ int aura_b200_time_phase(aura_b200_engine* e, int phase, size_t reps, float* avg
     copy_all(false);
     CK(cudaStreamSynchronize(e->stream));
     CK(cudaFree(snap));
-    if (e->aur)  // the mapped host copy of f^ (k_reduce rewrote it)
-      CK(cudaMemcpy(e->h_fhat, e->args.fhat, sizeof(float) * e->P * e->N, cudaMemcpyDeviceToHost));
   });
 }
 
-int aura_b200_trace_blocks(aura_b200_engine* e, size_t blocks, double* out) {
-  return guarded([&] {
-    CK(cudaSetDevice(e->device));
-    CK(cudaStreamSynchronize(e->stream));
-    blocks = std::min<size_t>(blocks, kTraceBlocks);
-    const size_t words = (size_t)kTraceBlocks * kTraceKernels * 2;
-    std::vector<unsigned long long> init(words);
-    for (size_t i = 0; i < words; i += 2) {
-      init[i] = ~0ull;
-      init[i + 1] = 0ull;
-    }
-    unsigned long long* dtr = nullptr;
-    CK(cudaMalloc(&dtr, words * sizeof(unsigned long long)));
-    CK(cudaMemcpy(dtr, init.data(), words * sizeof(unsigned long long), cudaMemcpyHostToDevice));
-    BlockArgs a = e->dev_args;
-    a.trace = dtr;
-    unsigned long long* dflag = nullptr;  // device-side output words, so the front stamps TR_OUTPUT
+namespace {
+// Timeline of `blocks` traced blocks (see aura_b200_trace_blocks). host_in:
+// run them through process()'s own handshake (mapped input and output,
+// output words, back to back) instead of device-resident I/O.
+void trace_run(aura_b200_engine* e, size_t blocks, double* out, const float* host_in, size_t n_in) {
+  CK(cudaSetDevice(e->device));
+  CK(cudaStreamSynchronize(e->stream));
+  blocks = std::min<size_t>(blocks, kTraceBlocks);
+  const size_t words = (size_t)kTraceBlocks * kTraceKernels * 2;
+  std::vector<unsigned long long> init(words);
+  for (size_t i = 0; i < words; i += 2) {
+    init[i] = ~0ull;
+    init[i + 1] = 0ull;
+  }
+  unsigned long long* dtr = nullptr;
+  CK(cudaMalloc(&dtr, words * sizeof(unsigned long long)));
+  CK(cudaMemcpy(dtr, init.data(), words * sizeof(unsigned long long), cudaMemcpyHostToDevice));
+  BlockArgs a = host_in ? e->args : e->dev_args;
+  a.trace = dtr;
+  unsigned long long* dflag = nullptr;  // device-side output words, so the front stamps TR_OUTPUT
+  if (!host_in) {
     CK(cudaMalloc(&dflag, std::max<size_t>(1, e->n_outflags) * sizeof(unsigned long long)));
     a.out_flag = dflag;
-    auto g = e->capture_block(a, nullptr);
-    const uint64_t first = e->blocks;
-    for (size_t i = 0; i < blocks; ++i) CK(cudaGraphLaunch(g.ex, e->stream));
-    CK(cudaStreamSynchronize(e->stream));
-    std::vector<unsigned long long> tr(words);
-    CK(cudaMemcpy(tr.data(), dtr, words * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
-    cudaFree(dtr);
-    cudaFree(dflag);
-    g.destroy();
-    // out[i][k][2]: start/end in microseconds relative to block i's front
-    // start; slot kTraceKernels-1 holds {next block's front start, 0}: the
-    // back-to-back cycle time. The device block counter (not e->blocks)
-    // names the trace slots: measurement relaunches may have advanced it.
-    DevState dst{};
-    CK(cudaMemcpy(&dst, e->args.st, sizeof(dst), cudaMemcpyDeviceToHost));
-    (void)first;
-    const uint64_t dev_first = (uint64_t)dst.block - blocks;
+  }
+  auto g = e->capture_block(a, nullptr);
+  if (host_in) {
+    const size_t per = (size_t)e->Qx * e->N;
+    std::vector<float> y(e->L * e->N);
     for (size_t i = 0; i < blocks; ++i) {
-      const size_t slot = (dev_first + i) % kTraceBlocks;
-      const unsigned long long t0 = tr[(slot * kTraceKernels + TR_FRONT) * 2];
-      for (int k = 0; k < kTraceKernels - 1; ++k) {
-        const unsigned long long s0 = tr[(slot * kTraceKernels + k) * 2];
-        const unsigned long long s1 = tr[(slot * kTraceKernels + k) * 2 + 1];
-        const bool ran = s0 != ~0ull;
-        out[(i * kTraceKernels + k) * 2] = ran ? (double)(long long)(s0 - t0) * 1e-3 : -1.0;
-        out[(i * kTraceKernels + k) * 2 + 1] = ran ? (double)(long long)(s1 - t0) * 1e-3 : -1.0;
-      }
-      const size_t nslot = (dev_first + i + 1) % kTraceBlocks;
-      const unsigned long long t1 = tr[(nslot * kTraceKernels + TR_FRONT) * 2];
-      const bool nxt = i + 1 < blocks && t1 != ~0ull;
-      out[(i * kTraceKernels + kTraceKernels - 1) * 2] = nxt ? (double)(long long)(t1 - t0) * 1e-3 : -1.0;
-      out[(i * kTraceKernels + kTraceKernels - 1) * 2 + 1] = 0.0;
+      std::memcpy(e->h_in, host_in + (i % n_in) * per, per * sizeof(float));
+      std::atomic_thread_fence(std::memory_order_release);
+      const uint64_t nblk = device_block_hint(e);
+      CK(cudaGraphLaunch(g.ex, e->stream));
+      wait_flag(e, nblk + 1, "traced block output");
+      std::memcpy(y.data(), e->h_out, y.size() * sizeof(float));
+      ++e->blocks;
     }
+  } else {
+    for (size_t i = 0; i < blocks; ++i) CK(cudaGraphLaunch(g.ex, e->stream));
     e->blocks += blocks;
+  }
+  CK(cudaStreamSynchronize(e->stream));
+  std::vector<unsigned long long> tr(words);
+  CK(cudaMemcpy(tr.data(), dtr, words * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  cudaFree(dtr);
+  if (dflag) cudaFree(dflag);
+  g.destroy();
+  // out[i][k][2]: start/end in microseconds relative to block i's front
+  // start; slot kTraceKernels-1 holds {next block's front start, 0}: the
+  // back-to-back cycle time. The device block counter names the trace slots.
+  DevState dst{};
+  CK(cudaMemcpy(&dst, e->args.st, sizeof(dst), cudaMemcpyDeviceToHost));
+  const uint64_t dev_first = (uint64_t)dst.block - blocks;
+  for (size_t i = 0; i < blocks; ++i) {
+    const size_t slot = (dev_first + i) % kTraceBlocks;
+    const unsigned long long t0 = tr[(slot * kTraceKernels + TR_FRONT) * 2];
+    for (int k = 0; k < kTraceKernels - 1; ++k) {
+      const unsigned long long s0 = tr[(slot * kTraceKernels + k) * 2];
+      const unsigned long long s1 = tr[(slot * kTraceKernels + k) * 2 + 1];
+      const bool ran = s0 != ~0ull;
+      out[(i * kTraceKernels + k) * 2] = ran ? (double)(long long)(s0 - t0) * 1e-3 : -1.0;
+      out[(i * kTraceKernels + k) * 2 + 1] = ran ? (double)(long long)(s1 - t0) * 1e-3 : -1.0;
+    }
+    const size_t nslot = (dev_first + i + 1) % kTraceBlocks;
+    const unsigned long long t1 = tr[(nslot * kTraceKernels + TR_FRONT) * 2];
+    const bool nxt = i + 1 < blocks && t1 != ~0ull;
+    out[(i * kTraceKernels + kTraceKernels - 1) * 2] = nxt ? (double)(long long)(t1 - t0) * 1e-3 : -1.0;
+    out[(i * kTraceKernels + kTraceKernels - 1) * 2 + 1] = 0.0;
+  }
+}
+}  // namespace
+
+int aura_b200_trace_blocks(aura_b200_engine* e, size_t blocks, double* out) {
+  return guarded([&] { trace_run(e, blocks, out, nullptr, 0); });
+}
+
+int aura_b200_trace_host_blocks(aura_b200_engine* e, const float* host_in, size_t n_in_blocks, size_t blocks,
+                                double* out) {
+  return guarded([&] {
+    if (!host_in || !n_in_blocks) fail(AURA_B200_E_INVALID_ARGUMENT, "null argument");
+    if (e->launch_mode != 0) fail(AURA_B200_E_INVALID_ARGUMENT, "graph mode only");
+    trace_run(e, blocks, out, host_in, n_in_blocks);
   });
 }
 

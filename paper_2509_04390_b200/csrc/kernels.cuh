@@ -101,10 +101,10 @@ struct BlockArgs {
   int n_syn_tiles;   // (L/LT) * CTn
   int h_in_l2;       // spectra fit in L2: stream them with evict_normal
   int w_in_l2;       // canceller W + delay lines fit in L2: keep W there (evict_last)
-  const int4* chunks;   // work items {kind | tile << 1, b, e, partial slot in tile}:
+  const int4* chunks;   // work items {kind | tile << 1, b, e, partial index}:
                         //   [n_static] per-CTA static pieces, then [n_chunks - n_static] queue
   int n_chunks, n_static;
-  const int* item_off;  // [plan_ctas + 1] static items of each CTA
+  const int4* cta_first;  // [plan_ctas][2]: {first static item, end, 0, 0}, that item's record
   int plan_ctas;        // CTAs the static pieces were planned for (a larger grid: queue only)
   const int4* tinfo;    // per tile (synthesis, then canceller column tiles):
                         //   {first partial, partials, first group, groups}
@@ -151,10 +151,12 @@ struct BlockArgs {
   float4* part_afc;     // split-K partials [slot][P + nlms][CT] (row P: loudspeaker power)
   float4* yhat;         // [P+1][NF]  reduced canceller spectra (+ power row)
   float* fhat;          // P x N     feedback estimate for the next block
-  float* fhat_host;     // P x N     same, mapped pinned host copy
-  // sharding (G > 1): this engine is shard `grank` of G
-  int G, grank;
+  // sharding: this engine is shard `grank` of G; xchg = how the canceller
+  // partials are exchanged: 0 none (unsharded), 1 P2P stores + flags
+  // (k_afc_finish), 2 NCCL all-reduce into xsum (+ k_afc_apply)
+  int G, grank, xchg;
   float* xmine;                 // [P*N + 2N] this shard's partial f^ and power sum
+  float* xsum;                  // [P*N + 2N] the all-reduced sum (xchg 2)
   char* xpeer[kMaxShards];      // every shard's exchange buffer (xpeer[grank] = own)
   unsigned* status_host;        // mapped; nonzero when a peer missed the deadline
   // I/O (device pointers; may alias pinned mapped host memory)
@@ -706,7 +708,6 @@ __global__ void __launch_bounds__(kTailThreads) k_afc_finish(BlockArgs a) {
       float v = __ldcg(slots + i);
       for (int g = 1; g < G; ++g) v = __fadd_rn(v, __ldcg(slots + (size_t)g * S + i));
       a.fhat[i] = v;
-      a.fhat_host[i] = v;
     }
     if (a.nlms) {
       const float oml = __fsub_rn(1.0f, a.lambda);
@@ -722,6 +723,34 @@ __global__ void __launch_bounds__(kTailThreads) k_afc_finish(BlockArgs a) {
         w.y = __fadd_rn(__fmul_rn(a.lambda, w.y), __fmul_rn(oml, sum.y));
         a.pw[j] = w;
       }
+    }
+  }
+  trace_end(a, TR_AFC_FINISH, n);
+  retire_block(a, n);
+}
+
+// -------------------------------------------------------- k_afc_apply
+// NCCL exchange (xchg 2): after ncclAllReduce(xmine -> xsum) on the engine
+// stream, install the summed f^ and smooth the summed power exactly as
+// k_afc_finish does, then retire the block. Every rank receives the same
+// reduced values from NCCL (reduce-scatter + all-gather), so every shard
+// holds the same f^ and power; the summation order is NCCL's (pinned by
+// NCCL_ALGO / NCCL_PROTO), not rank order.
+__global__ void __launch_bounds__(kTailThreads) k_afc_apply(BlockArgs a) {
+  const blk_t n = a.st->block;
+  trace_begin(a, TR_AFC_FINISH, n);
+  const int N = a.N, P = a.P;
+  for (int i = threadIdx.x; i < P * N; i += blockDim.x) {
+    a.fhat[i] = __ldcg(a.xsum + i);
+  }
+  if (a.nlms) {
+    const float oml = __fsub_rn(1.0f, a.lambda);
+    for (int j = threadIdx.x; j < N; j += blockDim.x) {
+      const float2 sum = make_float2(__ldcg(a.xsum + (size_t)P * N + 2 * j), __ldcg(a.xsum + (size_t)P * N + 2 * j + 1));
+      float2 w = a.pw[j];
+      w.x = __fadd_rn(__fmul_rn(a.lambda, w.x), __fmul_rn(oml, sum.x));
+      w.y = __fadd_rn(__fmul_rn(a.lambda, w.y), __fmul_rn(oml, sum.y));
+      a.pw[j] = w;
     }
   }
   trace_end(a, TR_AFC_FINISH, n);

@@ -112,17 +112,16 @@ __device__ __forceinline__ void consumers_sync() {
 
 // Work item (host-planned, kernels.cuh): kind (0 synthesis, 1 canceller) |
 // tile << 1, item range [b, e) (synthesis: taps t = q (K-1) + j; canceller:
-// units u = l KF + k), index of its split-K partial among its tile's.
+// units u = l KF + k), index of its split-K partial in the partials array.
 // Everything the consumers need travels with the stage, so they never wait
-// on a global load: the producer prefetches the next item's record and its
-// tile's reduction geometry while it streams the current one.
+// on a global load: the producer prefetches the next item's record while it
+// streams the current one.
 struct StageMeta {
   int item;       // < 0: no more work
   int t, t1;      // item range of this stage
   int flags;      // bit 0: last stage of the item; bit 1: canceller
   int tile;       // synthesis tile, or canceller column tile
-  int slot;       // partial slot among the tile's
-  int4 ti;        // the tile's {first partial, partials, first group, groups}
+  int slot;       // partial index (synthesis or canceller partials array)
 };
 static_assert(2 * kMaxStages * 8 + kMaxStages * sizeof(StageMeta) <= kBackBarrierBytes,
               "barrier + metadata region");
@@ -169,7 +168,14 @@ __device__ __forceinline__ void back_produce(const BlockArgs& a, blk_t n, uint64
   const uint64_t pol_keep = policy_evict_last();
   unsigned* queue = a.tick + a.tick_queue;
   const bool planned = (int)blockIdx.x < a.plan_ctas;
-  const int s0 = planned ? a.item_off[blockIdx.x] : 0, s1 = planned ? a.item_off[blockIdx.x + 1] : 0;
+  // this CTA's static range and its first record in ONE round of loads (the
+  // ramp to the first bulk copy is on every launch's critical path)
+  int4 r0 = make_int4(0, 0, 0, 0), first = make_int4(0, 0, 0, 0);
+  if (planned) {
+    r0 = a.cta_first[2 * blockIdx.x];
+    first = a.cta_first[2 * blockIdx.x + 1];
+  }
+  const int s0 = r0.x, s1 = r0.y;
   // item sequence: static s0..s1-1, then queue claims
   auto claim = [&](int k) -> int {
     if (s0 + k < s1) return s0 + k;
@@ -181,13 +187,15 @@ __device__ __forceinline__ void back_produce(const BlockArgs& a, blk_t n, uint64
   int s = (int)(q % (uint32_t)S);
   uint32_t par = ((q / (uint32_t)S) & 1u) ^ 1u;
   int idx = claim(0);
-  int4 rec = idx >= 0 ? a.chunks[idx] : make_int4(0, 0, 0, 0);
+  int4 rec = idx < 0 ? make_int4(0, 0, 0, 0) : (s0 < s1 ? first : a.chunks[idx]);
   for (int k = 0; idx >= 0; ++k) {
-    // prefetch the next item (its atomic and loads overlap this item's stream)
+    // the next item: its claim (an atomic once past the static items) is
+    // issued now, its record is loaded after this item's first stage is
+    // issued -- neither round trip delays this item's first copy
     const int nidx = claim(k + 1);
-    const int4 nrec = nidx >= 0 ? a.chunks[nidx] : make_int4(0, 0, 0, 0);
+    int4 nrec = make_int4(0, 0, 0, 0);
+    bool have_next = false;
     const int kind = rec.x & 1, tile = rec.x >> 1;
-    const int4 ti = a.tinfo[kind ? a.n_syn_tiles + tile : tile];
     if (PT > 0 && kind == 1 && !waited) {
       griddep_wait();  // canceller inputs come from the head
       waited = true;
@@ -211,7 +219,7 @@ __device__ __forceinline__ void back_produce(const BlockArgs& a, blk_t n, uint64
         front_ok = true;
       }
       mbar_wait(empty + s, par);
-      meta[s] = StageMeta{idx, t, t1, (t1 == rec.z ? 1 : 0) | (kind << 1), tile, rec.w, ti};
+      meta[s] = StageMeta{idx, t, t1, (t1 == rec.z ? 1 : 0) | (kind << 1), tile, rec.w};
       float4* dst = slots + (size_t)s * a.slot_f4;
       const int nt = t1 - t;
       if (PT == 0 || kind == 0) {
@@ -252,7 +260,12 @@ __device__ __forceinline__ void back_produce(const BlockArgs& a, blk_t n, uint64
         par ^= 1u;
       }
       t = t1;
+      if (!have_next) {
+        if (nidx >= 0) nrec = a.chunks[nidx];
+        have_next = true;
+      }
     }
+    if (!have_next && nidx >= 0) nrec = a.chunks[nidx];
     idx = nidx;
     rec = nrec;
   }
@@ -339,7 +352,6 @@ __device__ __forceinline__ void back_consume(const BlockArgs& a, blk_t n, uint64
     }
     if (ctr && q == 0 && threadIdx.x == 0) ctr[1] = globaltimer();
     const int item = m.item, tile = m.tile, slot = m.slot;
-    const int4 ti = m.ti;
     if (a.seg_trace && threadIdx.x == 0) a.seg_trace[4 * (size_t)item] = globaltimer();
     if (PT == 0 || !(m.flags & 2)) {
       // ------------------------------------------------ synthesis item
@@ -377,7 +389,7 @@ __device__ __forceinline__ void back_consume(const BlockArgs& a, blk_t n, uint64
         m = meta[sl];
       }
       const int E = LT * CT;
-      team_partial<LT>(acc, LT, CT, PG, pg, f, pl, red, a.part_syn + (size_t)(ti.x + slot) * E,
+      team_partial<LT>(acc, LT, CT, PG, pg, f, pl, red, a.part_syn + (size_t)slot * E,
                        [](int r) { return r; });
       if (a.seg_trace && threadIdx.x == 0) a.seg_trace[4 * (size_t)item + 1] = globaltimer();
     } else if constexpr (PT > 0) {
@@ -484,7 +496,7 @@ __device__ __forceinline__ void back_consume(const BlockArgs& a, blk_t n, uint64
       }
       const int E = R * CT;
       // rows 0..P-1: the mics; row P: the loudspeaker power (accumulator PA)
-      team_partial<PA + 1>(aac, R, CT, PG, pg, f, pl, red, a.part_afc + (size_t)(ti.x + slot) * E,
+      team_partial<PA + 1>(aac, R, CT, PG, pg, f, pl, red, a.part_afc + (size_t)slot * E,
                            [&](int r) { return r < P ? r : (r == PA && nl) ? P : -1; });
       if (a.seg_trace && threadIdx.x == 0) a.seg_trace[4 * (size_t)item + 1] = globaltimer();
     }
@@ -690,7 +702,7 @@ __device__ void reduce_part(const BlockArgs& a, int b, blk_t n, float4* rsm, int
   stamp(TR_AFC_SUMMED);
   // the canceller of block n is complete: f^ for block n+1
   const int N = a.N, P = a.P;
-  const bool sharded = a.G > 1;
+  const bool sharded = a.xchg != 0;
   float2* z = reinterpret_cast<float2*>(rsm + kReduceThreads + afc_ys_f4(N, P));
   float2* tw = z + (N <= 1024 ? (size_t)P : 1) * N;
   float2* split = tw + N / 2;
@@ -701,11 +713,7 @@ __device__ void reduce_part(const BlockArgs& a, int b, blk_t n, float4* rsm, int
   for (int p = 0; p < P; ++p) {
     // sharded: this shard's partial f^_p (c2r is linear), summed by k_afc_finish
     float* fh = sharded ? a.xmine + (size_t)p * N : a.fhat + (size_t)p * N;
-    float* fhh = a.fhat_host + (size_t)p * N;
-    auto st = [&](int i, float x) {
-      fh[i] = x;
-      if (!sharded) fhh[i] = x;
-    };
+    auto st = [&](int i, float x) { fh[i] = x; };
     const float2* yp = reinterpret_cast<const float2*>(yh + (size_t)p * NF);
     if (!warps) {
       irfft_packed_tail(yp, z, N, a.logN, tw, split, st, tm);
@@ -770,7 +778,7 @@ __global__ void __launch_bounds__(kReduceThreads) k_reduce(const __grid_constant
     if (atomicAdd(t, 1u) == gridDim.x - 1u) {
       *t = 0u;
       if (a.front_seq) a.front_seq[n & 1u] = 0ull;  // every producer of block n is past its hold
-      if (a.G <= 1) a.st->block = n + 1;
+      if (a.xchg == 0) a.st->block = n + 1;
     }
   }
 }

@@ -26,7 +26,22 @@ from . import (AfcParams, Auralizer, ChannelMode, Convolver, EngineConfig, Error
                _check, lib, make_backend, make_config)
 
 HANDLE_BYTES = 64
+NCCL_ID_BYTES = 128
 MAX_SHARDS = 8
+TRANSPORTS = ("p2p", "nccl")
+
+
+def nccl_unique_id() -> bytes:
+    """A fresh NCCL unique id (rank 0 creates it, the host distributes it)."""
+    buf = C.create_string_buffer(NCCL_ID_BYTES)
+    _check(_lib_shard().aura_b200_nccl_unique_id(buf))
+    return buf.raw
+
+
+def connect_nccl(engine, world: int, rank: int, uid: bytes):
+    if len(uid) != NCCL_ID_BYTES:
+        raise Error(ErrorCode.invalid_argument, "NCCL unique id must be 128 bytes")
+    _check(_lib_shard().aura_b200_shard_connect_nccl(engine.handle, world, rank, uid))
 
 
 def shard_range(L: int, world: int, rank: int) -> Tuple[int, int]:
@@ -56,6 +71,8 @@ def _lib_shard():
         L.aura_b200_shard_connect.argtypes = [vp, C.c_char_p]
         L.aura_b200_shard_connect_local.argtypes = [C.POINTER(vp), C.c_int]
         L.aura_b200_shard_info.argtypes = [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]
+        L.aura_b200_nccl_unique_id.argtypes = [C.c_char_p]
+        L.aura_b200_shard_connect_nccl.argtypes = [vp, C.c_int, C.c_int, C.c_char_p]
         L._shard_bound = True
     return L
 
@@ -75,11 +92,13 @@ class ShardedAuralizer:
     torch.distributed group (one process per GPU). Each rank passes the FULL
     filter sets (or any object indexable by row) and gets back its own
     loudspeaker slice from ``process``. All ranks must call ``process`` with
-    the same microphone blocks, and ``reset`` together."""
+    the same microphone blocks, and ``reset`` together. ``transport``: "p2p"
+    (our in-graph exchange kernel, the default) or "nccl" (ncclAllReduce
+    captured in the graph; the ablation)."""
 
     def __init__(self, synth_filters: Sequence, fc_filters: Sequence, cfg: EngineConfig,
                  device: int = 0, input_gain: float = 1.0, afc: Optional[AfcParams] = None,
-                 group=None):
+                 group=None, transport: str = "p2p"):
         import torch.distributed as dist
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
@@ -100,7 +119,15 @@ class ShardedAuralizer:
         bad = [e for e in errs if e is not None]
         if bad:
             raise err if err is not None else Error(ErrorCode(bad[0][0]), "peer shard: " + bad[0][1])
-        if self.world > 1:
+        if transport not in TRANSPORTS:
+            raise Error(ErrorCode.invalid_argument, f"transport must be one of {TRANSPORTS}")
+        self.transport = transport
+        if transport == "nccl":
+            box = [nccl_unique_id() if self.rank == 0 else None]
+            dist.broadcast_object_list(box, src=0, group=group)
+            connect_nccl(self.engine, self.world, self.rank, box[0])
+            dist.barrier(group=group)
+        elif self.world > 1:
             h = C.create_string_buffer(HANDLE_BYTES)
             _check(_lib_shard().aura_b200_shard_export(self.engine.handle, self.world, self.rank, h))
             allh = exchange_handles(h.raw, group)

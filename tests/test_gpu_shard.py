@@ -70,7 +70,7 @@ def _free_port():
     return p
 
 
-def _ipc_worker(rank, world, port, q):
+def _ipc_worker(rank, world, port, q, devices=(0, 0), transport="p2p"):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -79,8 +79,8 @@ def _ipc_worker(rank, world, port, q):
         Q, L, N = 1, 12, 64
         synth, fc, mic = workload(Q, L, N, 77)
         cfg = A.make_config(48000, N, Q, L)
-        sh = S.ShardedAuralizer(list(synth), list(fc), cfg, device=0, input_gain=0.9,
-                                afc=A.AfcParams(0.02, 0.9, 1e-2))
+        sh = S.ShardedAuralizer(list(synth), list(fc), cfg, device=devices[rank], input_gain=0.9,
+                                afc=A.AfcParams(0.02, 0.9, 1e-2), transport=transport)
         ys, fs = [], []
         for b in range(mic.shape[0]):
             ys.append(sh.process(mic[b]))
@@ -93,14 +93,33 @@ def _ipc_worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
+def _device_count():
+    import torch
+    return torch.cuda.device_count()
+
+
 def test_two_processes_ipc_on_one_gpu():
     """One process per shard, exchange buffers opened through CUDA IPC
     (the multi-GPU wiring), both on cuda:0."""
+    _two_process_run((0, 0), "p2p")
+
+
+@pytest.mark.skipif(_device_count() < 2, reason="needs two GPUs (NVLink peers)")
+@pytest.mark.parametrize("transport", ["p2p", "nccl"])
+def test_two_gpus_cross_device_exchange(transport):
+    """Shards on cuda:0 and cuda:1, one process each: the canceller exchange
+    crosses NVLink (P2P stores into the peer's IPC-mapped buffer, or the
+    NCCL all-reduce); f^ bit-identical on both ranks, outputs within 1e-5
+    of the unsharded oracle."""
+    _two_process_run((0, 1), transport)
+
+
+def _two_process_run(devices, transport):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, q, devices, transport)) for r in range(2)]
     for p in procs:
         p.start()
     res = {}
@@ -140,3 +159,25 @@ def test_sharded_convolver_is_independent_slices():
     for b in range(40):
         y = np.concatenate([p.process(x[b]) for p in parts], axis=0)
         assert rel_err(y, o.process(x[b])) <= TOL
+
+
+def test_nccl_exchange_world_one_is_bit_identical():
+    """The NCCL transport with one rank (a local all-reduce captured in the
+    block graph, then k_afc_apply): bit-identical to the unsharded engine --
+    the same partial c2r, sum and power smoothing operations."""
+    synth, fc, mic = workload(1, 8, 64, 21)
+    cfg = A.make_config(48000, 64, 1, 8)
+    afc = A.AfcParams(0.02, 0.9, 1e-2)
+    plain = A.Auralizer(list(synth), list(fc), cfg, input_gain=0.9, afc=afc)
+    nc = A.Auralizer(list(synth), list(fc), cfg, input_gain=0.9, afc=afc)
+    S.connect_nccl(nc, 1, 0, S.nccl_unique_id())
+    for b in range(40):
+        assert np.array_equal(nc.process(mic[b]), plain.process(mic[b])), b
+        assert np.array_equal(nc.feedback_estimate(), plain.feedback_estimate()), b
+    assert np.array_equal(nc.coeffs(), plain.coeffs())
+    nc.reset()
+    plain.reset()
+    for b in range(5):
+        assert np.array_equal(nc.process(mic[b]), plain.process(mic[b]))
+    nc.close()
+    plain.close()

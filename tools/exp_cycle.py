@@ -28,3 +28,9 @@ tr = e.trace_blocks(32)
 res["trace_cycle_p50"] = float(np.median(tr["cycle"][:, 0])) if "cycle" in tr else None
 res["trace"] = {k: [float(np.median(v[:, 0])), float(np.median(v[:, 1]))] for k, v in tr.items()}
 print(json.dumps(res))
+
+# the same blocks through process()'s mapped-memory handshake
+trh = e.trace_blocks(32, host_inputs=mic)
+res2 = {"host_trace_cycle_p50": float(np.median(trh["cycle"][:, 0])) if "cycle" in trh else None,
+        "host_trace": {k: [float(np.median(v[:, 0])), float(np.median(v[:, 1]))] for k, v in trh.items()}}
+print(json.dumps(res2))
