@@ -192,7 +192,7 @@ struct aura_b200_engine {
   int LT = 1, PT = 0;
   uint64_t blocks = 0;
   cudaStream_t stream = nullptr;  // the engine's stream
-  cudaEvent_t ev_front = nullptr, ev_back = nullptr;  // completion, per block
+  cudaEvent_t ev_front = nullptr;  // output ready (only without output words, OUTFLAG=0)
   std::vector<void*> dmem;
   float4* W0 = nullptr;  // initial canceller spectra (reset of NLMS)
   size_t w_elems = 0;
@@ -251,7 +251,6 @@ struct aura_b200_engine {
     for (void* p : ipc_opened) cudaIpcCloseMemHandle(p);
     if (nccl) nccl_api().destroy(nccl);
     if (ev_front) cudaEventDestroy(ev_front);
-    if (ev_back) cudaEventDestroy(ev_back);
     if (stream) cudaStreamDestroy(stream);
   }
 
@@ -361,7 +360,9 @@ struct aura_b200_engine {
 
   void rebuild_graphs() {
     g_block.destroy();
-    g_block = capture_block(args, ev_front);
+    // no event node after k_front unless the host waits on it: a node
+    // between k_front and k_back would stand in their programmatic edge
+    g_block = capture_block(args, use_outflag ? nullptr : ev_front);
   }
 
   // Every device buffer a block writes (measurement calls that relaunch
@@ -389,6 +390,7 @@ struct aura_b200_engine {
       v.push_back({a.fhat, fl * P * N});
       v.push_back({a.part_afc, f4 * std::max<size_t>(1, n_afc_segs * (P + 1) * a.CT)});
       v.push_back({a.yhat, f4 * (P + 1) * NF});
+      if (a.xmine) v.push_back({a.xmine, fl * (P * N + 2 * N)});
     }
     return v;
   }
@@ -700,7 +702,10 @@ void plan_back(aura_b200_engine* e, BlockArgs& a) {
         // them in one round of loads and runs the c2r from shared memory
         // (reduce_part's single-CTA path; cpt_for below gives 1)
         // (only while the items stay short enough to balance: <= ~1.5 MB)
-        const long long cap = afc_single_cap(P + (e->args.nlms ? 1 : 0), CT);
+        // AFC_ROUNDS: load rounds the single reduce CTA may take (1: half
+        // as many, twice as long canceller items)
+        const int rounds = std::max(1, std::min(2, knob_i(e, "AFC_ROUNDS", 2)));
+        const long long cap = afc_single_cap(P + (e->args.nlms ? 1 : 0), CT) * rounds / 2;
         const double unit_b = (double)(P * (e->args.nlms ? 2 : 1) + 1) * CT * 16.0;
         const long long per1 = cap > 0 ? ((U + cap - 1) / cap + a.spa - 1) / a.spa * a.spa : 0;
         if (cap > 0 && (double)per1 * unit_b <= 1.5e6) per = std::max(per, per1);
@@ -826,7 +831,6 @@ void common_init(aura_b200_engine* e, int device) {
   CK(cudaSetDevice(device));
   CK(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&e->ev_front, cudaEventDisableTiming));
-  CK(cudaEventCreateWithFlags(&e->ev_back, cudaEventDisableTiming));
 }
 
 // CTAs that tick the block ticket in retire_block: only the sharded
@@ -1228,13 +1232,13 @@ void wait_flag(aura_b200_engine* e, unsigned long long target, const char* what)
   std::atomic_thread_fence(std::memory_order_acquire);
 }
 
-// Spin until `ev` (recorded on the engine stream) has completed; kernel
-// completion makes the block's mapped-memory writes visible to the host.
+// Spin until `ev` (recorded on the engine stream; null: the whole stream)
+// has completed; kernel completion makes the block's writes visible.
 void wait_event(aura_b200_engine* e, cudaEvent_t ev, const char* what) {
   uint64_t spins = 0;
   const auto t0 = std::chrono::steady_clock::now();
   for (;;) {
-    const cudaError_t q = cudaEventQuery(ev);
+    const cudaError_t q = ev ? cudaEventQuery(ev) : cudaStreamQuery(e->stream);
     if (q == cudaSuccess) break;
     if (q != cudaErrorNotReady) ck(q, what);
 #if defined(__x86_64__)
@@ -1265,8 +1269,9 @@ int aura_b200_process(aura_b200_engine* e, const float* in, float* out) {
     std::memcpy(e->h_in, in, n_in * sizeof(float));
     std::atomic_thread_fence(std::memory_order_release);
     const uint64_t nblk = device_block_hint(e);
-    e->enqueue_block(e->g_block, e->args, e->ev_front);  // records ev_front after k_front
-    CK(cudaEventRecord(e->ev_back, e->stream));
+    // (nothing else goes on the stream per block: an extra stream operation
+    // between two block graphs costs device time at every block boundary)
+    e->enqueue_block(e->g_block, e->args, e->use_outflag ? nullptr : e->ev_front);
     if (e->use_outflag) {
       // k_front's last CTA publishes block + 1 once every output is written
       wait_flag(e, nblk + 1, "block output");
@@ -1281,8 +1286,7 @@ int aura_b200_process(aura_b200_engine* e, const float* in, float* out) {
 int aura_b200_synchronize(aura_b200_engine* e) {
   return guarded([&] {
     CK(cudaSetDevice(e->device));
-    if (e->blocks) wait_event(e, e->ev_back, "block background");
-    CK(cudaStreamSynchronize(e->stream));
+    wait_event(e, nullptr, "block background");
     check_shard_status(e);
   });
 }
@@ -1298,8 +1302,7 @@ int aura_b200_feedback_estimate(aura_b200_engine* e, float* out) {
   return guarded([&] {
     if (!e->aur) fail(AURA_B200_E_INVALID_ARGUMENT, "not an auralizer");
     CK(cudaSetDevice(e->device));
-    if (e->blocks) wait_event(e, e->ev_back, "block background");
-    CK(cudaStreamSynchronize(e->stream));
+    wait_event(e, nullptr, "block background");
     check_shard_status(e);
     // f^ stays in device memory (the background kernels never write mapped
     // host memory: a system-scope write over PCIe at the end of k_reduce
@@ -1760,8 +1763,7 @@ int aura_b200_time_host_breakdown(aura_b200_engine* e, const float* host_in, siz
       const uint64_t nblk = device_block_hint(e);
       CK(cudaGraphLaunch(e->g_block.ex, e->stream));
       const auto t2 = clk::now();
-      CK(cudaEventRecord(e->ev_back, e->stream));
-      const auto t3 = clk::now();
+      const auto t3 = t2;  // (no background event any more)
       wait_flag(e, nblk + 1, "block output");
       const auto t4 = clk::now();
       std::memcpy(y.data(), e->h_out, y.size() * sizeof(float));
@@ -1818,7 +1820,6 @@ int aura_b200_time_phase(aura_b200_engine* e, int phase, size_t reps, float* avg
       fail(AURA_B200_E_INVALID_ARGUMENT, "only the front, k_back and k_reduce can be re-launched");
     if (phase == PH_BACK && !e->has_back())
       fail(AURA_B200_E_INVALID_ARGUMENT, "this engine has no streaming work");
-    if (e->G > 1) fail(AURA_B200_E_INVALID_ARGUMENT, "time phases on an unsharded engine");
     CK(cudaSetDevice(e->device));
     CK(cudaStreamSynchronize(e->stream));
     // The relaunches are not idempotent (k_reduce advances the block
