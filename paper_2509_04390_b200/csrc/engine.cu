@@ -517,7 +517,7 @@ BackFn back_for(bool elem, int PT) {
 
 // Canceller partials per column tile that one k_reduce CTA sums in two load
 // rounds per thread (kReduceThreads threads over E elements, 16 loads in
-// flight per round: reduce_part).
+// flight per round: reduce_part; 32 in flight measured slower at c2 and c3).
 long long afc_single_cap(int rows, int CT) {
   const int E = rows * CT;
   return E > kReduceThreads ? 0 : 2LL * 16LL * (kReduceThreads / E);
@@ -702,10 +702,9 @@ void plan_back(aura_b200_engine* e, BlockArgs& a) {
         // them in one round of loads and runs the c2r from shared memory
         // (reduce_part's single-CTA path; cpt_for below gives 1)
         // (only while the items stay short enough to balance: <= ~1.5 MB)
-        // AFC_ROUNDS: load rounds the single reduce CTA may take (1: half
-        // as many, twice as long canceller items)
-        const int rounds = std::max(1, std::min(2, knob_i(e, "AFC_ROUNDS", 2)));
-        const long long cap = afc_single_cap(P + (e->args.nlms ? 1 : 0), CT) * rounds / 2;
+        // (halving the cap -- twice as long canceller items -- made c3's
+        // k_back 11 us slower: the long items unbalance the queue)
+        const long long cap = afc_single_cap(P + (e->args.nlms ? 1 : 0), CT);
         const double unit_b = (double)(P * (e->args.nlms ? 2 : 1) + 1) * CT * 16.0;
         const long long per1 = cap > 0 ? ((U + cap - 1) / cap + a.spa - 1) / a.spa * a.spa : 0;
         if (cap > 0 && (double)per1 * unit_b <= 1.5e6) per = std::max(per, per1);
