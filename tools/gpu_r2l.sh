@@ -1,0 +1,11 @@
+#!/bin/bash
+O=gpurun_out/r2l
+mkdir -p $O
+timeout 1200 python tools/exp_knobs.py c3 '{"AURA_B200_AFC_TAIL": 0}' '{"AURA_B200_AFC_SPAN": 0.3, "AURA_B200_AFC_START": 0.1}' '{"AURA_B200_AFC_SPAN": 0.2, "AURA_B200_AFC_START": 0.0}' '{"AURA_B200_AFC_SPAN": 0.45, "AURA_B200_AFC_START": 0.15}' '{"AURA_B200_AFC_SPAN": 0.3, "AURA_B200_AFC_START": 0.1, "AURA_B200_AFC_TAIL": 0}' '{"AURA_B200_AFC_SPAN": 0.5, "AURA_B200_AFC_START": 0.0}' > $O/knobs.jsonl 2> $O/knobs.err
+python3 - <<'PY'
+import json
+for l in open('gpurun_out/r2l/knobs.jsonl'):
+    d=json.loads(l); t=d['trace']
+    print(d['env'], 'span', round(d['span_mean_us'],2), 'ev', round(d['events_p50'],2), round(d['events_p99'],2), 'e2e', round(d['e2e_p50'],2), round(d['e2e_p99'],2), 'back', t.get('k_back'), 'red', t.get('k_reduce'), 'summed', t.get('afc_summed'), 'done', t.get('afc_done'), 'cyc', t.get('cycle'))
+PY
+tail -3 $O/knobs.err
