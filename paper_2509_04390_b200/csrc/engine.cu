@@ -1,6 +1,8 @@
-// engine.cu -- host side of libaura_b200.so: the C-ABI declared in
-// include/aura_b200.h, device memory layout, filter preparation on the GPU,
-// per-block CUDA graphs and the measurement entry points.
+// engine.cu -- host side of libaura_b200.so: the reference-replacing C-ABI
+// of include/aura_b200.h, the device memory layout, filter preparation on
+// the GPU, the k_back work planner and the per-block CUDA graphs. The only
+// translation unit that contains (and launches) the kernels; sharding is in
+// shard.cu, the measurement entry points in diag.cu.
 //
 // Reference interfaces replaced (under /root/reference/proj/include/aura):
 //   aura_b200_convolver_create  Convolver::Convolver      convolver.hpp:67-94
@@ -12,412 +14,47 @@
 //   aura_b200_feedback_estimate Auralizer::feedback_estimate auralizer.hpp:56-58
 //   aura_b200_filter_spectrum   PartitionedFilterSet::spectrum engine.hpp:210-219
 //   aura_b200_device_count      list_backends             backend.hpp:186-193
-#include <cuda_runtime.h>
-#include <dlfcn.h>
-#include <nccl.h>
-
-#include <atomic>
-#include <thread>
-#include <chrono>
-#include <cmath>
-#include <cstdio>
-#include <cstdlib>
-#include <cstring>
-#include <memory>
-#include <mutex>
-#include <string>
-#include <vector>
-
-#if defined(__x86_64__)
-#include <immintrin.h>
-#endif
-
-#include "../../include/aura_b200_diag.h"
+#include "engine.hpp"
 #include "kernels.cuh"
 #include "stream.cuh"
-#include <algorithm>
-#include <tuple>
-
-using namespace aura_b200;
-
-namespace {
 
 thread_local std::string g_err;
 
-struct Fail {
-  int code;
-  std::string msg;
-};
+// ---------------------------------------------------------------- launches
 
-[[noreturn]] void fail(int code, const std::string& msg) { throw Fail{code, msg}; }
-
-void ck(cudaError_t e, const char* what) {
-  if (e == cudaSuccess) return;
-  cudaGetLastError();
-  if (e == cudaErrorMemoryAllocation)
-    fail(AURA_B200_E_OUT_OF_MEMORY, std::string(what) + ": " + cudaGetErrorString(e));
-  fail(AURA_B200_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
-}
-#define CK(x) ck((x), #x)
-
-// Raise a kernel's dynamic shared-memory limit on the current device, never
-// lower it: the attribute is per function, so engines of different shapes in
-// one process must not undo each other's (a smaller engine created after a
-// larger one would otherwise make the larger one's launches invalid).
-template <typename Fn>
-void raise_smem_limit(Fn fn, size_t bytes) {
-  static std::mutex mu;
-  std::lock_guard<std::mutex> lock(mu);
-  cudaFuncAttributes fa{};
-  CK(cudaFuncGetAttributes(&fa, (const void*)fn));
-  if ((size_t)fa.maxDynamicSharedSizeBytes < bytes)
-    CK(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-}
-
-template <class F>
-int guarded(F&& f) {
-  try {
-    f();
-    return AURA_B200_OK;
-  } catch (const Fail& e) {
-    g_err = e.msg;
-    return e.code;
-  } catch (const std::bad_alloc&) {
-    g_err = "host allocation failed";
-    return AURA_B200_E_OUT_OF_MEMORY;
-  }
-}
-
-bool is_pow2(size_t v) { return v && !(v & (v - 1)); }
-int ilog2(size_t v) {
-  int r = 0;
-  while ((size_t(1) << r) < v) ++r;
-  return r;
-}
-
-// engine.hpp:74-94 (validate_config), same codes and precedence. MIMO (an
-// extension) lifts only the C_in in {1, C_out} rule.
-void validate(const aura_b200_config* c, bool mimo) {
-  if (!c) fail(AURA_B200_E_INVALID_ARGUMENT, "config is null");
-  if (c->sample_rate_hz == 0) fail(AURA_B200_E_ZERO_SAMPLE_RATE, "sample rate must be positive");
-  if (!is_pow2(c->block_size) || c->block_size < 16 || c->block_size > 8192)
-    fail(AURA_B200_E_NON_POWER_OF_TWO_BLOCK,
-         "block size must be a power of two in [16, 8192], got " + std::to_string(c->block_size));
-  if (c->fft_size != 2 * c->block_size)
-    fail(AURA_B200_E_FFT_SIZE_MISMATCH, "fft size must be 2 * block size");
-  if (c->outputs == 0 || c->inputs == 0 ||
-      (!mimo && c->inputs != 1 && c->inputs != c->outputs))
-    fail(AURA_B200_E_BAD_CHANNEL_COMBINATION,
-         "input channels must be 1 or equal to output channels");
-}
-
-// NLMS regulariser default: SURVEY Appendix A's delta = 1e-6 N (DESIGN.md
-// section 4: at this value the GPU's W error against a float64 run is within
-// 1.5x of the fp32 C oracle's own).
-constexpr float kDefaultDeltaPerN = 1e-6f;
-
-template <class T>
-T* dalloc(size_t count, std::vector<void*>& owned) {
-  void* p = nullptr;
-  if (count == 0) count = 1;
-  CK(cudaMalloc(&p, count * sizeof(T)));
-  owned.push_back(p);
-  return static_cast<T*>(p);
-}
-
-// NCCL, loaded on first use (dlopen): only the NCCL exchange ablation needs
-// it, so the library loads and runs without NCCL installed.
-struct NcclApi {
-  ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
-  ncclResult_t (*init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
-  ncclResult_t (*allreduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
-                            cudaStream_t) = nullptr;
-  ncclResult_t (*destroy)(ncclComm_t) = nullptr;
-  const char* (*error_string)(ncclResult_t) = nullptr;
-  std::string why;
-};
-NcclApi& nccl_api() {
-  static NcclApi api;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-    if (!h) {
-      api.why = std::string("libnccl.so.2 not found: ") + dlerror();
-      return;
-    }
-    api.get_unique_id = reinterpret_cast<decltype(api.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
-    api.init_rank = reinterpret_cast<decltype(api.init_rank)>(dlsym(h, "ncclCommInitRank"));
-    api.allreduce = reinterpret_cast<decltype(api.allreduce)>(dlsym(h, "ncclAllReduce"));
-    api.destroy = reinterpret_cast<decltype(api.destroy)>(dlsym(h, "ncclCommDestroy"));
-    api.error_string = reinterpret_cast<decltype(api.error_string)>(dlsym(h, "ncclGetErrorString"));
-    if (!api.get_unique_id || !api.init_rank || !api.allreduce || !api.destroy || !api.error_string)
-      api.why = "libnccl.so.2 lacks the NCCL 2 API";
-  });
-  if (!api.why.empty()) fail(AURA_B200_E_BACKEND_UNAVAILABLE, "NCCL exchange unavailable: " + api.why);
-  return api;
-}
-void nccl_check(ncclResult_t r, const char* what) {
-  if (r != ncclSuccess) fail(AURA_B200_E_CUDA, std::string(what) + ": " + nccl_api().error_string(r));
-}
-
-}  // namespace
-
-enum Phase { PH_FRONT = 0, PH_BACK_HEAD, PH_BACK, PH_REDUCE, PH_AFC_FINISH, PH_ADVANCE, PH_COUNT };
-static const char* kPhaseNames[PH_COUNT] = {"k_front",  "k_back_head",  "k_back",
-                                            "k_reduce", "k_afc_finish", "k_advance"};
-
-using BackFn = void (*)(BlockArgs);
-
-// Poll until the stream has drained (true) or `seconds` pass (false).
-static bool wait_stream_idle(cudaStream_t s, double seconds) {
-  const auto t0 = std::chrono::steady_clock::now();
-  for (;;) {
-    const cudaError_t q = cudaStreamQuery(s);
-    if (q != cudaErrorNotReady) {
-      cudaGetLastError();
-      return true;
-    }
-    if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > seconds) return false;
-    std::this_thread::sleep_for(std::chrono::microseconds(50));
-  }
-}
-
-struct aura_b200_engine {
-  int device = 0;
-  int sms = 148;
-  bool aur = false;
-  int mode = 0;
-  size_t N = 0, Q = 1, L = 1, P = 0, K = 0, KF = 0, n_h = 0, n_hf = 0;
-  int Qx = 1;  // FDL channels
-  int LT = 1, PT = 0;
-  uint64_t blocks = 0;
-  cudaStream_t stream = nullptr;  // the engine's stream
-  cudaEvent_t ev_front = nullptr;  // output ready (only without output words, OUTFLAG=0)
-  std::vector<void*> dmem;
-  float4* W0 = nullptr;  // initial canceller spectra (reset of NLMS)
-  size_t w_elems = 0;
-  float* h_in = nullptr;    // mapped pinned
-  float* h_out = nullptr;   // mapped pinned
-  float* d_in_pool = nullptr;
-  size_t pool_blocks = 0;
-  float* d_out = nullptr;
-  BlockArgs args{};
-  BlockArgs dev_args{};
-  struct BlockGraph {
-    cudaGraph_t g = nullptr;
-    cudaGraphExec_t ex = nullptr;
-    cudaGraphNode_t out_node = nullptr;  // external event-record node (output ready)
-    void destroy() {
-      if (ex) cudaGraphExecDestroy(ex);
-      if (g) cudaGraphDestroy(g);
-      ex = nullptr;
-      g = nullptr;
-    }
-  };
-  BlockGraph g_block;
-  // streaming kernel k_back
-  BackFn back_fn = nullptr;
-  bool pdl_off = false;  // measurement: serialise k_back / k_reduce launches
-  int launch_mode = 0;   // 0: one CUDA graph per block; 1: the same kernels launched on the stream
-  unsigned long long* h_outflag = nullptr;  // mapped: k_front CTA b writes block + 1 in [b] when done
-  size_t n_outflags = 0;    // = k_front's grid (every CTA that reads the mapped input)
-  bool use_outflag = true;
-  std::string knobs;        // non-default AURA_B200_* tuning knobs in effect (describe())
-  uint64_t block_base = 0;  // device number of host block 0 (aura_b200_seek_block; else 0)
-  int back_ctas = 0;
-  size_t smem_back = 0, smem_reduce = 0;
-  size_t n_syn_segs = 0, n_afc_segs = 0;
-  std::vector<int4> h_chunks;  // host copy of the k_back work queue (diagnostics)
-  // sharding: shard grank of G; xbuf = own exchange buffer
-  int G = 1, grank = 0;
-  char* xbuf = nullptr;
-  size_t xbuf_bytes = 0;
-  std::vector<void*> ipc_opened;  // peer buffers opened through CUDA IPC
-  ncclComm_t nccl = nullptr;      // NCCL exchange (xchg 2)
-  unsigned* h_status = nullptr;   // mapped pinned; set by k_afc_finish on timeout
-  size_t smem_front = 0, smem_head = 0;
-
-  ~aura_b200_engine() {
-    cudaSetDevice(device);
-    // wedged (a shard peer that never arrives is bounded in-kernel, but be
-    // safe): leak rather than block, the frees below would synchronise
-    if (stream && !wait_stream_idle(stream, 10.0)) return;
-    g_block.destroy();
-    for (void* p : dmem) cudaFree(p);
-    if (h_in) cudaFreeHost(h_in);
-    if (h_out) cudaFreeHost(h_out);
-    if (h_status) cudaFreeHost(h_status);
-    if (h_outflag) cudaFreeHost(h_outflag);
-    for (void* p : ipc_opened) cudaIpcCloseMemHandle(p);
-    if (nccl) nccl_api().destroy(nccl);
-    if (ev_front) cudaEventDestroy(ev_front);
-    if (stream) cudaStreamDestroy(stream);
-  }
-
-  bool has_syn() const { return K > 1; }
-  bool has_back() const { return has_syn() || aur; }
-  bool front_head = true;  // k_front runs the canceller head; k_back is its PDL dependent
-  bool has_head() const { return !front_head && (aur || mode != AURA_B200_ELEMENTWISE); }
-  int front_grid(const BlockArgs& a) const {
-    return (int)((L + a.cpb - 1) / a.cpb) + ((front_head && aur && a.nlms) ? (int)P : 0);
-  }
-  bool sharded() const { return aur && args.xchg != 0; }
-
-  // k_back after k_back_head is a programmatic dependent launch: it starts
-  // while k_back_head runs and waits for it (griddepcontrol.wait) only where
-  // it reads k_back_head's outputs.
-  template <typename Kern>
-  void launch_pdl(Kern kern, unsigned grid, unsigned threads, size_t smem, bool pdl, const BlockArgs& a,
-                  cudaStream_t s) {
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(threads);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = pdl ? 1 : 0;
-    CK(cudaLaunchKernelEx(&cfg, kern, a));
-  }
-
-  void launch_phase(int ph, const BlockArgs& a, cudaStream_t s) {
-    switch (ph) {
-      case PH_FRONT:
-        k_front<<<front_grid(a), kFrontThreads, smem_front, s>>>(a);
-        break;
-      case PH_BACK_HEAD:
-        if (has_head())
-          k_back_head<<<(unsigned)(aur ? L + (a.nlms ? P : 0) : 1), kFrontThreads, smem_head, s>>>(a);
-        break;
-      case PH_BACK:
-        if (has_back())
-          launch_pdl(back_fn, (unsigned)back_ctas, kBackThreads, smem_back,
-                     (has_head() || front_head) && !pdl_off, a, s);
-        break;
-      case PH_REDUCE:
-        if (has_back())
-          launch_pdl(k_reduce, (unsigned)(a.red_syn_ctas + a.red_afc_ctas), kReduceThreads, smem_reduce,
-                     !pdl_off, a, s);
-        break;
-      case PH_AFC_FINISH:
-        if (sharded() && a.xchg == 1) k_afc_finish<<<1, kTailThreads, 0, s>>>(a);
-        if (sharded() && a.xchg == 2) {
-          nccl_check(nccl_api().allreduce(a.xmine, a.xsum, (size_t)(P * N + 2 * N), ncclFloat, ncclSum, nccl, s),
-                     "ncclAllReduce");
-          k_afc_apply<<<1, kTailThreads, 0, s>>>(a);
-        }
-        break;
-      case PH_ADVANCE:
-        if (!has_back()) k_advance<<<1, 1, 0, s>>>(a.st);
-        break;
-    }
-  }
-
-  // kernels launched per block
-  int launches_per_block() const {
-    return 1 + (has_head() ? 1 : 0) + (has_back() ? 2 : 0) + (sharded() ? 1 : 0) +  // (+ NCCL's own)
-           (has_back() ? 0 : 1);
-  }
-
-  // One graph per block: k_front, an external event node the host waits on
-  // (output ready), then k_back_head -> k_back (PDL) [-> k_afc_finish].
-  BlockGraph capture_block(const BlockArgs& a, cudaEvent_t out_event) {
-    BlockGraph bg;
-    CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
-    launch_phase(PH_FRONT, a, stream);
-    if (out_event) CK(cudaEventRecordWithFlags(out_event, stream, cudaEventRecordExternal));
-    for (int ph = PH_BACK_HEAD; ph < PH_COUNT; ++ph) launch_phase(ph, a, stream);
-    CK(cudaStreamEndCapture(stream, &bg.g));
-    if (out_event) {
-      size_t n = 0;
-      CK(cudaGraphGetNodes(bg.g, nullptr, &n));
-      std::vector<cudaGraphNode_t> nodes(n);
-      CK(cudaGraphGetNodes(bg.g, nodes.data(), &n));
-      for (auto nd : nodes) {
-        cudaGraphNodeType t;
-        CK(cudaGraphNodeGetType(nd, &t));
-        if (t == cudaGraphNodeTypeEventRecord) bg.out_node = nd;
+void aura_b200_engine::launch_phase(int ph, const BlockArgs& a, cudaStream_t s) {
+  switch (ph) {
+    case PH_FRONT:
+      k_front<<<front_grid(a), kFrontThreads, smem_front, s>>>(a);
+      break;
+    case PH_BACK_HEAD:
+      if (has_head())
+        k_back_head<<<(unsigned)(aur ? L + (a.nlms ? P : 0) : 1), kFrontThreads, smem_head, s>>>(a);
+      break;
+    case PH_BACK:
+      if (has_back())
+        launch_pdl(back_fn, (unsigned)back_ctas, kBackThreads, smem_back,
+                   (has_head() || front_head) && !pdl_off, a, s);
+      break;
+    case PH_REDUCE:
+      if (has_back())
+        launch_pdl(k_reduce, (unsigned)(a.red_syn_ctas + a.red_afc_ctas), kReduceThreads, smem_reduce,
+                   !pdl_off, a, s);
+      break;
+    case PH_AFC_FINISH:
+      if (sharded() && a.xchg == 1) k_afc_finish<<<1, kTailThreads, 0, s>>>(a);
+      if (sharded() && a.xchg == 2) {
+        nccl_check(nccl_api().allreduce(a.xmine, a.xsum, (size_t)(P * N + 2 * N), ncclFloat, ncclSum, nccl, s),
+                   "ncclAllReduce");
+        k_afc_apply<<<1, kTailThreads, 0, s>>>(a);
       }
-    }
-    CK(cudaGraphInstantiate(&bg.ex, bg.g, 0));
-    return bg;
+      break;
+    case PH_ADVANCE:
+      if (!has_back()) k_advance<<<1, 1, 0, s>>>(a.st);
+      break;
   }
+}
 
-  // Enqueue one block on the stream: the graph, or (launch_mode 1) the same
-  // kernels launched directly (PDL edges included); out_event is recorded
-  // after k_front.
-  void enqueue_block(const BlockGraph& g, const BlockArgs& a, cudaEvent_t out_event) {
-    if (launch_mode == 0) {
-      CK(cudaGraphLaunch(g.ex, stream));
-      return;
-    }
-    launch_phase(PH_FRONT, a, stream);
-    if (out_event) CK(cudaEventRecord(out_event, stream));
-    for (int ph = PH_BACK_HEAD; ph < PH_COUNT; ++ph) launch_phase(ph, a, stream);
-  }
-
-  void rebuild_graphs() {
-    g_block.destroy();
-    // no event node after k_front unless the host waits on it: a node
-    // between k_front and k_back would stand in their programmatic edge
-    g_block = capture_block(args, use_outflag ? nullptr : ev_front);
-  }
-
-  // Every device buffer a block writes (measurement calls that relaunch
-  // kernels snapshot and restore them): {pointer, bytes}
-  std::vector<std::pair<void*, size_t>> mutable_state() const {
-    const size_t NF = N / 2, f4 = sizeof(float4), fl = sizeof(float);
-    const BlockArgs& a = args;
-    std::vector<std::pair<void*, size_t>> v = {
-        {a.st, sizeof(DevState)},
-        {a.prev_in, fl * Qx * N},
-        {a.hist1, fl * Qx * N},
-        {a.cur_mt, fl * std::max<size_t>(1, Q) * N},
-        {a.X, f4 * Qx * K * NF},
-        {a.S, f4 * L * NF},
-        {a.part_syn, f4 * std::max<size_t>(1, n_syn_segs * LT * a.CT)},
-        {a.front_seq, 2 * sizeof(unsigned long long)},
-        {a.tick, 6 * sizeof(unsigned)}};
-    if (aur) {
-      v.push_back({a.prev_spk, fl * L * N});
-      v.push_back({a.spk, fl * L * N});
-      v.push_back({a.XA, f4 * L * (KF + 1) * NF});
-      v.push_back({a.W, f4 * w_elems});
-      v.push_back({a.pw, sizeof(float2) * N});
-      v.push_back({a.E, f4 * Q * NF});
-      v.push_back({a.fhat, fl * P * N});
-      v.push_back({a.part_afc, f4 * std::max<size_t>(1, n_afc_segs * (P + 1) * a.CT)});
-      v.push_back({a.yhat, f4 * (P + 1) * NF});
-      if (a.xmine) v.push_back({a.xmine, fl * (P * N + 2 * N)});
-    }
-    return v;
-  }
-
-  // algorithmic HBM bytes per block: 8N per packed partition
-  double phase_bytes(int ph) const {
-    const double row = 8.0 * (double)N;  // one packed partition
-    const double Qh = mode == AURA_B200_MIMO ? (double)Q : 1.0;
-    switch (ph) {
-      case PH_FRONT:  // inputs, X push, H[.][.][0], S, outputs
-        return 4.0 * N * Qx + row * Qx + row * (double)L * Qh + row * L + 4.0 * N * L;
-      case PH_BACK: {
-        double b = has_syn() ? row * ((double)L * Qh * (K - 1) + (double)Qx * (K - 1)) : 0.0;
-        if (aur) b += row * ((double)P * L * KF * (1.0 + (args.nlms ? 1.0 : 0.0)) + (double)L * KF);
-        return b;
-      }
-      case PH_REDUCE: {  // the split-K partials, read once
-        const double E = (double)LT * args.CT * 16.0;
-        return (double)n_syn_segs * E + (double)n_afc_segs * args.red_afc_rows * args.CT * 16.0;
-      }
-      case PH_AFC_FINISH:  // push P*N + 2N floats to G shards, read G slots
-        return sharded() ? 2.0 * G * 4.0 * (double)(P * N + 2 * N) : 0.0;
-      case PH_BACK_HEAD: return aur ? (row + 8.0 * N) * L + row * P : 4.0 * N * Qx;
-    }
-    return 0.0;
-  }
-};
 
 namespace {
 
@@ -832,9 +469,6 @@ void common_init(aura_b200_engine* e, int device) {
   CK(cudaEventCreateWithFlags(&e->ev_front, cudaEventDisableTiming));
 }
 
-// CTAs that tick the block ticket in retire_block: only the sharded
-// canceller's k_afc_finish (k_back retires a block itself).
-void set_advance_total(aura_b200_engine* e) { e->args.advance_total = e->sharded() ? 1 : 0; }
 
 void finish_init(aura_b200_engine* e) {
   BlockArgs& a = e->args;
@@ -1196,60 +830,6 @@ int aura_b200_auralizer_create(const aura_b200_config* cfg,
 
 void aura_b200_destroy(aura_b200_engine* e) { delete e; }
 
-namespace {
-// The device block number the next graph launch will process: the host
-// counts blocks; measurement calls advance host and device together.
-uint64_t device_block_hint(aura_b200_engine* e) { return e->blocks + e->block_base; }
-
-// A shard peer missed the canceller exchange deadline (k_afc_finish): the
-// engine's f^ stopped tracking the other shards', so every call fails until
-// a coordinated reset of all shards.
-void check_shard_status(aura_b200_engine* e) {
-  if (e->h_status && *reinterpret_cast<volatile unsigned*>(e->h_status))
-    fail(AURA_B200_E_TIMEOUT, "a shard peer missed the canceller exchange deadline (reset every shard)");
-}
-
-// Spin until every k_front CTA has published `target` in its mapped word.
-void wait_flag(aura_b200_engine* e, unsigned long long target, const char* what) {
-  volatile unsigned long long* f = e->h_outflag;
-  uint64_t spins = 0;
-  const auto t0 = std::chrono::steady_clock::now();
-  size_t i = 0;
-  for (;;) {
-    while (i < e->n_outflags && f[i] >= target) ++i;
-    if (i == e->n_outflags) break;
-#if defined(__x86_64__)
-    _mm_pause();
-#endif
-    if ((++spins & 0xFFFF) == 0) {
-      const cudaError_t q = cudaStreamQuery(e->stream);
-      if (q != cudaErrorNotReady && q != cudaSuccess) ck(q, what);
-      if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(20))
-        fail(AURA_B200_E_TIMEOUT, std::string(what) + ": not complete within 20 s");
-    }
-  }
-  std::atomic_thread_fence(std::memory_order_acquire);
-}
-
-// Spin until `ev` (recorded on the engine stream; null: the whole stream)
-// has completed; kernel completion makes the block's writes visible.
-void wait_event(aura_b200_engine* e, cudaEvent_t ev, const char* what) {
-  uint64_t spins = 0;
-  const auto t0 = std::chrono::steady_clock::now();
-  for (;;) {
-    const cudaError_t q = ev ? cudaEventQuery(ev) : cudaStreamQuery(e->stream);
-    if (q == cudaSuccess) break;
-    if (q != cudaErrorNotReady) ck(q, what);
-#if defined(__x86_64__)
-    _mm_pause();
-#endif
-    if ((++spins & 0xFFF) == 0 &&
-        std::chrono::steady_clock::now() - t0 > std::chrono::seconds(20))
-      fail(AURA_B200_E_TIMEOUT, std::string(what) + ": not complete within 20 s");
-  }
-  std::atomic_thread_fence(std::memory_order_acquire);
-}
-}  // namespace
 
 // One block: launch FRONT then BACK; return as soon as the front has
 // written the output. The background keeps running; the next call's front
@@ -1344,33 +924,6 @@ int aura_b200_fdl_slot(aura_b200_engine* e, int which, size_t channel, size_t ag
   });
 }
 
-int aura_b200_seek_block(aura_b200_engine* e, uint64_t n) {
-  return guarded([&] {
-    if (e->blocks) fail(AURA_B200_E_INVALID_ARGUMENT, "seek only before the first block (or after reset)");
-    if (e->G > 1) fail(AURA_B200_E_INVALID_ARGUMENT, "seek does not apply to sharded engines");
-    CK(cudaSetDevice(e->device));
-    CK(cudaStreamSynchronize(e->stream));
-    // every delay line is zero here, so starting the ring slots (block mod
-    // K) at n instead of 0 changes no value
-    DevState st{};
-    st.block = n;
-    CK(cudaMemcpy(e->args.st, &st, sizeof(st), cudaMemcpyHostToDevice));
-    e->block_base = n;
-  });
-}
-
-int aura_b200_set_launch_mode(aura_b200_engine* e, int mode) {
-  return guarded([&] {
-    if (mode < 0 || mode > 1)
-      fail(AURA_B200_E_INVALID_ARGUMENT, "launch mode is 0 (one CUDA graph per block) or 1 (kernels on the stream)");
-    CK(cudaSetDevice(e->device));
-    CK(cudaStreamSynchronize(e->stream));
-    e->launch_mode = mode;
-  });
-}
-
-int aura_b200_launch_mode(const aura_b200_engine* e) { return e->launch_mode; }
-
 int aura_b200_set_input_gain(aura_b200_engine* e, float gain) {
   return guarded([&] {
     if (!e->aur) fail(AURA_B200_E_INVALID_ARGUMENT, "not an auralizer");
@@ -1431,597 +984,6 @@ int aura_b200_afc_coeffs(aura_b200_engine* e, float* out) {
         unpack_row(reinterpret_cast<const float2*>(row.data()), e->N,
                    out + (p * U + u) * 2 * (e->N + 1));
       }
-  });
-}
-
-// ----------------------------------------------------------- sharding
-namespace {
-
-void shard_alloc(aura_b200_engine* e, int world, int rank) {
-  if (!e->aur)
-    fail(AURA_B200_E_INVALID_ARGUMENT,
-         "only a feedback canceller exchanges data between shards (convolver shards are independent)");
-  if (world < 2 || world > kMaxShards || rank < 0 || rank >= world)
-    fail(AURA_B200_E_INVALID_ARGUMENT, "shard world must be 2..8 and 0 <= rank < world");
-  if (e->xbuf || e->args.xchg) fail(AURA_B200_E_INVALID_ARGUMENT, "engine is already sharded");
-  if (e->blocks) fail(AURA_B200_E_INVALID_ARGUMENT, "shard before the first block");
-  CK(cudaSetDevice(e->device));
-  const size_t S = e->P * e->N + 2 * e->N;
-  e->xbuf_bytes = kXFlagBytes + 2 * (size_t)world * S * sizeof(float);
-  e->xbuf = reinterpret_cast<char*>(dalloc<float>(e->xbuf_bytes / sizeof(float), e->dmem));
-  CK(cudaMemset(e->xbuf, 0, e->xbuf_bytes));
-  e->args.xmine = dalloc<float>(S, e->dmem);
-  CK(cudaMemset(e->args.xmine, 0, S * sizeof(float)));
-  e->G = world;
-  e->grank = rank;
-}
-
-// NCCL exchange: the exchange buffers, the communicator (one per engine,
-// ranks = shards), then the graphs with the all-reduce captured in them.
-void nccl_connect(aura_b200_engine* e, int world, int rank, const void* id) {
-  if (!e->aur)
-    fail(AURA_B200_E_INVALID_ARGUMENT,
-         "only a feedback canceller exchanges data between shards (convolver shards are independent)");
-  if (world < 1 || world > kMaxShards || rank < 0 || rank >= world)
-    fail(AURA_B200_E_INVALID_ARGUMENT, "shard world must be 1..8 and 0 <= rank < world");
-  if (e->args.xchg) fail(AURA_B200_E_INVALID_ARGUMENT, "engine is already sharded");
-  if (e->blocks) fail(AURA_B200_E_INVALID_ARGUMENT, "shard before the first block");
-  NcclApi& api = nccl_api();
-  CK(cudaSetDevice(e->device));
-  const size_t S = e->P * e->N + 2 * e->N;
-  e->args.xmine = dalloc<float>(S, e->dmem);
-  e->args.xsum = dalloc<float>(S, e->dmem);
-  CK(cudaMemset(e->args.xmine, 0, S * sizeof(float)));
-  CK(cudaMemset(e->args.xsum, 0, S * sizeof(float)));
-  ncclUniqueId uid;
-  std::memcpy(&uid, id, sizeof uid);
-  nccl_check(api.init_rank(&e->nccl, world, uid, rank), "ncclCommInitRank");
-  e->G = world;
-  e->grank = rank;
-  BlockArgs& a = e->args;
-  a.G = world;
-  a.grank = rank;
-  a.xchg = 2;
-  set_advance_total(e);
-  CK(cudaStreamSynchronize(e->stream));
-  e->rebuild_graphs();
-  BlockArgs d = a;
-  d.out = e->d_out;
-  d.in = e->d_in_pool;
-  d.out_flag = nullptr;
-  e->dev_args = d;
-}
-
-void shard_finalize(aura_b200_engine* e, char* const* peers) {
-  CK(cudaSetDevice(e->device));
-  BlockArgs& a = e->args;
-  a.G = e->G;
-  a.grank = e->grank;
-  a.xchg = 1;
-  for (int g = 0; g < kMaxShards; ++g) a.xpeer[g] = g < e->G ? peers[g] : nullptr;
-  set_advance_total(e);
-  CK(cudaStreamSynchronize(e->stream));
-  e->rebuild_graphs();
-  BlockArgs d = a;
-  d.out = e->d_out;
-  d.in = e->d_in_pool;
-  d.out_flag = nullptr;
-  e->dev_args = d;
-}
-
-}  // namespace
-
-int aura_b200_shard_export(aura_b200_engine* e, int world, int rank, void* handle) {
-  return guarded([&] {
-    if (!e || !handle) fail(AURA_B200_E_INVALID_ARGUMENT, "null argument");
-    shard_alloc(e, world, rank);
-    cudaIpcMemHandle_t h;
-    CK(cudaIpcGetMemHandle(&h, e->xbuf));
-    static_assert(sizeof(h) == AURA_B200_SHARD_HANDLE_BYTES, "IPC handle size");
-    std::memcpy(handle, &h, sizeof h);
-  });
-}
-
-int aura_b200_shard_connect(aura_b200_engine* e, const void* handles) {
-  return guarded([&] {
-    if (!e || !handles) fail(AURA_B200_E_INVALID_ARGUMENT, "null argument");
-    if (!e->xbuf) fail(AURA_B200_E_INVALID_ARGUMENT, "call aura_b200_shard_export first");
-    CK(cudaSetDevice(e->device));
-    std::vector<char*> peers(e->G, nullptr);
-    for (int g = 0; g < e->G; ++g) {
-      if (g == e->grank) {
-        peers[g] = e->xbuf;
-        continue;
-      }
-      cudaIpcMemHandle_t h;
-      std::memcpy(&h, static_cast<const char*>(handles) + (size_t)g * sizeof h, sizeof h);
-      void* p = nullptr;
-      CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
-      e->ipc_opened.push_back(p);
-      peers[g] = static_cast<char*>(p);
-    }
-    shard_finalize(e, peers.data());
-  });
-}
-
-int aura_b200_shard_connect_local(aura_b200_engine* const* engines, int world) {
-  return guarded([&] {
-    if (!engines) fail(AURA_B200_E_INVALID_ARGUMENT, "null argument");
-    for (int g = 0; g < world; ++g)
-      if (!engines[g]) fail(AURA_B200_E_INVALID_ARGUMENT, "null engine");
-    for (int g = 0; g < world; ++g) shard_alloc(engines[g], world, g);
-    // engines on different devices of one process reach each other by P2P
-    for (int g = 0; g < world; ++g)
-      for (int h = 0; h < world; ++h) {
-        const int dg = engines[g]->device, dh = engines[h]->device;
-        if (dg == dh) continue;
-        int ok = 0;
-        CK(cudaDeviceCanAccessPeer(&ok, dg, dh));
-        if (!ok) fail(AURA_B200_E_BACKEND_UNAVAILABLE, "devices cannot access each other (no P2P)");
-        CK(cudaSetDevice(dg));
-        const cudaError_t r = cudaDeviceEnablePeerAccess(dh, 0);
-        if (r != cudaErrorPeerAccessAlreadyEnabled) ck(r, "cudaDeviceEnablePeerAccess");
-        cudaGetLastError();
-      }
-    std::vector<char*> peers(world);
-    for (int g = 0; g < world; ++g) peers[g] = engines[g]->xbuf;
-    for (int g = 0; g < world; ++g) shard_finalize(engines[g], peers.data());
-  });
-}
-
-int aura_b200_nccl_unique_id(void* id) {
-  return guarded([&] {
-    if (!id) fail(AURA_B200_E_INVALID_ARGUMENT, "null argument");
-    ncclUniqueId uid;
-    nccl_check(nccl_api().get_unique_id(&uid), "ncclGetUniqueId");
-    std::memcpy(id, &uid, sizeof uid);
-  });
-}
-
-int aura_b200_shard_connect_nccl(aura_b200_engine* e, int world, int rank, const void* id) {
-  return guarded([&] {
-    if (!e || !id) fail(AURA_B200_E_INVALID_ARGUMENT, "null argument");
-    nccl_connect(e, world, rank, id);
-  });
-}
-
-int aura_b200_shard_info(const aura_b200_engine* e, int* world, int* rank) {
-  return guarded([&] {
-    if (!e || !world || !rank) fail(AURA_B200_E_INVALID_ARGUMENT, "null argument");
-    *world = e->G;
-    *rank = e->grank;
-  });
-}
-
-// ------------------------------------------------------------ measurement
-
-// Device-resident timing. block_us[b]: back-to-back block time, CUDA events
-// recorded on the engine stream between consecutive block graphs (so a
-// block's interval spans all of its kernels and the launch of the next).
-// latency_us[b] (optional, separate pass): block start -> output written,
-// from the graph's external event node after k_front.
-int aura_b200_time_device_blocks(aura_b200_engine* e, const float* host_in,
-                                 size_t n_in_blocks, size_t blocks, float* latency_us,
-                                 float* block_us) {
-  return guarded([&] {
-    CK(cudaSetDevice(e->device));
-    CK(cudaStreamSynchronize(e->stream));
-    const size_t per = (size_t)e->Qx * e->N;
-    if (host_in && n_in_blocks) {
-      const size_t nb = std::min(n_in_blocks, e->pool_blocks);
-      CK(cudaMemcpy(e->d_in_pool, host_in, nb * per * sizeof(float), cudaMemcpyHostToDevice));
-    }
-    // one block graph per pool slot (the input pointer is baked per slot)
-    const size_t slots = std::max<size_t>(1, std::min(n_in_blocks, e->pool_blocks));
-    std::vector<aura_b200_engine::BlockGraph> gs;
-    for (size_t s = 0; s < slots; ++s) {
-      BlockArgs a = e->dev_args;
-      a.in = e->d_in_pool + s * per;
-      gs.push_back(e->capture_block(a, nullptr));
-    }
-    std::vector<cudaEvent_t> ev(blocks + 1);
-    for (auto& x : ev) CK(cudaEventCreate(&x));
-    std::vector<BlockArgs> sa(slots, e->dev_args);
-    for (size_t s = 0; s < slots; ++s) sa[s].in = e->d_in_pool + s * per;
-    for (size_t b = 0; b < blocks; ++b) {
-      CK(cudaEventRecord(ev[b], e->stream));
-      e->enqueue_block(gs[b % slots], sa[b % slots], nullptr);
-    }
-    CK(cudaEventRecord(ev[blocks], e->stream));
-    CK(cudaStreamSynchronize(e->stream));
-    for (size_t b = 0; b < blocks; ++b) {
-      float ms = 0.f;
-      CK(cudaEventElapsedTime(&ms, ev[b], ev[b + 1]));
-      block_us[b] = ms * 1000.0f;
-    }
-    for (auto& g : gs) g.destroy();
-    e->blocks += blocks;
-    if (latency_us) {
-      // separate pass: the output-ready event node is re-pointed per block
-      cudaEvent_t proto;
-      CK(cudaEventCreate(&proto));
-      std::vector<aura_b200_engine::BlockGraph> gl;
-      for (size_t s = 0; s < slots; ++s) {
-        BlockArgs a = e->dev_args;
-        a.in = e->d_in_pool + s * per;
-        gl.push_back(e->capture_block(a, proto));
-      }
-      std::vector<cudaEvent_t> ev2(2 * blocks);
-      for (auto& x : ev2) CK(cudaEventCreate(&x));
-      for (size_t b = 0; b < blocks; ++b) {
-        auto& g = gl[b % slots];
-        CK(cudaGraphExecEventRecordNodeSetEvent(g.ex, g.out_node, ev2[2 * b + 1]));
-        CK(cudaEventRecord(ev2[2 * b], e->stream));
-        CK(cudaGraphLaunch(g.ex, e->stream));
-      }
-      CK(cudaStreamSynchronize(e->stream));
-      for (size_t b = 0; b < blocks; ++b) {
-        float ms = 0.f;
-        CK(cudaEventElapsedTime(&ms, ev2[2 * b], ev2[2 * b + 1]));
-        latency_us[b] = ms * 1000.0f;
-      }
-      for (auto& x : ev2) cudaEventDestroy(x);
-      for (auto& g : gl) g.destroy();
-      cudaEventDestroy(proto);
-      e->blocks += blocks;
-    }
-    for (auto& x : ev) cudaEventDestroy(x);
-  });
-}
-
-// Device-resident blocks back to back with ONE event pair around all of
-// them: the mean block time without per-block event records in the stream.
-int aura_b200_time_device_span(aura_b200_engine* e, const float* host_in, size_t n_in_blocks,
-                               size_t blocks, float* total_us) {
-  return guarded([&] {
-    CK(cudaSetDevice(e->device));
-    CK(cudaStreamSynchronize(e->stream));
-    const size_t per = (size_t)e->Qx * e->N;
-    const size_t slots = std::max<size_t>(1, std::min(n_in_blocks, e->pool_blocks));
-    if (host_in && n_in_blocks)
-      CK(cudaMemcpy(e->d_in_pool, host_in, slots * per * sizeof(float), cudaMemcpyHostToDevice));
-    std::vector<aura_b200_engine::BlockGraph> gs;
-    std::vector<BlockArgs> sa(slots, e->dev_args);
-    for (size_t s = 0; s < slots; ++s) {
-      sa[s].in = e->d_in_pool + s * per;
-      gs.push_back(e->capture_block(sa[s], nullptr));
-    }
-    cudaEvent_t t0, t1;
-    CK(cudaEventCreate(&t0));
-    CK(cudaEventCreate(&t1));
-    CK(cudaEventRecord(t0, e->stream));
-    for (size_t b = 0; b < blocks; ++b) e->enqueue_block(gs[b % slots], sa[b % slots], nullptr);
-    CK(cudaEventRecord(t1, e->stream));
-    CK(cudaStreamSynchronize(e->stream));
-    float ms = 0.f;
-    CK(cudaEventElapsedTime(&ms, t0, t1));
-    *total_us = ms * 1000.0f;
-    cudaEventDestroy(t0);
-    cudaEventDestroy(t1);
-    for (auto& g : gs) g.destroy();
-    e->blocks += blocks;
-  });
-}
-
-int aura_b200_time_host_blocks(aura_b200_engine* e, const float* host_in,
-                               size_t n_in_blocks, size_t blocks, double pace_us,
-                               float* block_us) {
-  if (!e || !host_in || !n_in_blocks || !block_us) {
-    g_err = "null argument";
-    return AURA_B200_E_INVALID_ARGUMENT;
-  }
-  const size_t per = (size_t)e->Qx * e->N;
-  std::vector<float> out(e->L * e->N);
-  using clk = std::chrono::steady_clock;
-  auto next = clk::now();
-  for (size_t b = 0; b < blocks; ++b) {
-    if (pace_us > 0) {
-      while (clk::now() < next) {
-#if defined(__x86_64__)
-        _mm_pause();
-#endif
-      }
-      next += std::chrono::nanoseconds((long long)(pace_us * 1000.0));
-    }
-    const auto t0 = clk::now();
-    const int rc = aura_b200_process(e, host_in + (b % n_in_blocks) * per, out.data());
-    const auto t1 = clk::now();
-    if (rc) return rc;
-    block_us[b] = (float)std::chrono::duration<double, std::micro>(t1 - t0).count();
-  }
-  return AURA_B200_OK;
-}
-
-// Diagnostics: where the host-visible latency of process() goes (graph
-// mode). Per block (optionally paced), steady_clock offsets in us from the
-// call's start: {input staged, graph launched, background event recorded,
-// output flag seen, output copied}.
-int aura_b200_time_host_breakdown(aura_b200_engine* e, const float* host_in, size_t n_in_blocks,
-                                  size_t blocks, double pace_us, double* out) {
-  return guarded([&] {
-    if (e->launch_mode != 0) fail(AURA_B200_E_INVALID_ARGUMENT, "graph mode only");
-    CK(cudaSetDevice(e->device));
-    const size_t per = (size_t)e->Qx * e->N;
-    std::vector<float> y(e->L * e->N);
-    using clk = std::chrono::steady_clock;
-    auto next = clk::now();
-    for (size_t b = 0; b < blocks; ++b) {
-      if (pace_us > 0) {
-        while (clk::now() < next) {
-#if defined(__x86_64__)
-          _mm_pause();
-#endif
-        }
-        next += std::chrono::nanoseconds((long long)(pace_us * 1000.0));
-      }
-      const auto t0 = clk::now();
-      auto us = [&](clk::time_point t) { return std::chrono::duration<double, std::micro>(t - t0).count(); };
-      std::memcpy(e->h_in, host_in + (b % n_in_blocks) * per, per * sizeof(float));
-      std::atomic_thread_fence(std::memory_order_release);
-      const auto t1 = clk::now();
-      const uint64_t nblk = device_block_hint(e);
-      CK(cudaGraphLaunch(e->g_block.ex, e->stream));
-      const auto t2 = clk::now();
-      const auto t3 = t2;  // (no background event any more)
-      wait_flag(e, nblk + 1, "block output");
-      const auto t4 = clk::now();
-      std::memcpy(y.data(), e->h_out, y.size() * sizeof(float));
-      const auto t5 = clk::now();
-      ++e->blocks;
-      double* o = out + 5 * b;
-      o[0] = us(t1);
-      o[1] = us(t2);
-      o[2] = us(t3);
-      o[3] = us(t4);
-      o[4] = us(t5);
-    }
-    CK(cudaStreamSynchronize(e->stream));
-  });
-}
-
-int aura_b200_profile_phases(aura_b200_engine* e, size_t blocks, float* phase_us,
-                             int* n_phases) {
-  return guarded([&] {
-    CK(cudaSetDevice(e->device));
-    CK(cudaStreamSynchronize(e->stream));
-    const int np = PH_COUNT;
-    std::vector<cudaEvent_t> ev((size_t)(np + 1) * blocks);
-    for (auto& x : ev) CK(cudaEventCreate(&x));
-    for (size_t b = 0; b < blocks; ++b) {
-      BlockArgs a = e->dev_args;
-      a.in = e->d_in_pool + (b % e->pool_blocks) * (size_t)e->Qx * e->N;
-      for (int ph = 0; ph < np; ++ph) {
-        CK(cudaEventRecord(ev[b * (np + 1) + ph], e->stream));
-        e->launch_phase(ph, a, e->stream);
-      }
-      CK(cudaEventRecord(ev[b * (np + 1) + np], e->stream));
-    }
-    CK(cudaGetLastError());
-    CK(cudaStreamSynchronize(e->stream));
-    for (int ph = 0; ph < np; ++ph) {
-      double s = 0;
-      for (size_t b = 0; b < blocks; ++b) {
-        float ms = 0.f;
-        CK(cudaEventElapsedTime(&ms, ev[b * (np + 1) + ph], ev[b * (np + 1) + ph + 1]));
-        s += ms;
-      }
-      phase_us[ph] = (float)(1000.0 * s / (double)blocks);
-    }
-    for (auto& x : ev) cudaEventDestroy(x);
-    *n_phases = np;
-    e->blocks += blocks;
-  });
-}
-
-int aura_b200_time_phase(aura_b200_engine* e, int phase, size_t reps, float* avg_us) {
-  return guarded([&] {
-    if (phase != PH_BACK && phase != PH_FRONT && phase != PH_REDUCE)
-      fail(AURA_B200_E_INVALID_ARGUMENT, "only the front, k_back and k_reduce can be re-launched");
-    if (phase == PH_BACK && !e->has_back())
-      fail(AURA_B200_E_INVALID_ARGUMENT, "this engine has no streaming work");
-    CK(cudaSetDevice(e->device));
-    CK(cudaStreamSynchronize(e->stream));
-    // The relaunches are not idempotent (k_reduce advances the block
-    // counter, k_back updates W in place, the fused canceller head shifts
-    // the loudspeaker history): snapshot every mutable device buffer and put
-    // it back afterwards, so the engine continues as if this never ran.
-    const auto state = e->mutable_state();
-    size_t total = 0;
-    for (auto& b : state) total += (b.second + 255) & ~size_t(255);
-    char* snap = nullptr;
-    CK(cudaMalloc(&snap, std::max<size_t>(total, 1)));
-    auto copy_all = [&](bool save) {
-      size_t off = 0;
-      for (auto& b : state) {
-        char* s0 = snap + off;
-        CK(cudaMemcpyAsync(save ? s0 : b.first, save ? b.first : s0, b.second, cudaMemcpyDeviceToDevice,
-                           e->stream));
-        off += (b.second + 255) & ~size_t(255);
-      }
-    };
-    copy_all(true);
-    // single launches, back to back without programmatic overlap, so the
-    // mean is one launch's duration (ramp-up and tail included)
-    BlockArgs a = e->dev_args;
-    e->pdl_off = true;
-    e->launch_phase(phase, a, e->stream);  // warm
-    cudaEvent_t t0, t1;
-    CK(cudaEventCreate(&t0));
-    CK(cudaEventCreate(&t1));
-    CK(cudaEventRecord(t0, e->stream));
-    for (size_t r = 0; r < reps; ++r) e->launch_phase(phase, a, e->stream);
-    CK(cudaEventRecord(t1, e->stream));
-    e->pdl_off = false;
-    CK(cudaGetLastError());
-    CK(cudaStreamSynchronize(e->stream));
-    float ms = 0.f;
-    CK(cudaEventElapsedTime(&ms, t0, t1));
-    cudaEventDestroy(t0);
-    cudaEventDestroy(t1);
-    *avg_us = 1000.0f * ms / (float)reps;
-    copy_all(false);
-    CK(cudaStreamSynchronize(e->stream));
-    CK(cudaFree(snap));
-  });
-}
-
-namespace {
-// Timeline of `blocks` traced blocks (see aura_b200_trace_blocks). host_in:
-// run them through process()'s own handshake (mapped input and output,
-// output words, back to back) instead of device-resident I/O.
-void trace_run(aura_b200_engine* e, size_t blocks, double* out, const float* host_in, size_t n_in) {
-  CK(cudaSetDevice(e->device));
-  CK(cudaStreamSynchronize(e->stream));
-  blocks = std::min<size_t>(blocks, kTraceBlocks);
-  const size_t words = (size_t)kTraceBlocks * kTraceKernels * 2;
-  std::vector<unsigned long long> init(words);
-  for (size_t i = 0; i < words; i += 2) {
-    init[i] = ~0ull;
-    init[i + 1] = 0ull;
-  }
-  unsigned long long* dtr = nullptr;
-  CK(cudaMalloc(&dtr, words * sizeof(unsigned long long)));
-  CK(cudaMemcpy(dtr, init.data(), words * sizeof(unsigned long long), cudaMemcpyHostToDevice));
-  BlockArgs a = host_in ? e->args : e->dev_args;
-  a.trace = dtr;
-  unsigned long long* dflag = nullptr;  // device-side output words, so the front stamps TR_OUTPUT
-  if (!host_in) {
-    CK(cudaMalloc(&dflag, std::max<size_t>(1, e->n_outflags) * sizeof(unsigned long long)));
-    a.out_flag = dflag;
-  }
-  auto g = e->capture_block(a, nullptr);
-  if (host_in) {
-    const size_t per = (size_t)e->Qx * e->N;
-    std::vector<float> y(e->L * e->N);
-    for (size_t i = 0; i < blocks; ++i) {
-      std::memcpy(e->h_in, host_in + (i % n_in) * per, per * sizeof(float));
-      std::atomic_thread_fence(std::memory_order_release);
-      const uint64_t nblk = device_block_hint(e);
-      CK(cudaGraphLaunch(g.ex, e->stream));
-      wait_flag(e, nblk + 1, "traced block output");
-      std::memcpy(y.data(), e->h_out, y.size() * sizeof(float));
-      ++e->blocks;
-    }
-  } else {
-    for (size_t i = 0; i < blocks; ++i) CK(cudaGraphLaunch(g.ex, e->stream));
-    e->blocks += blocks;
-  }
-  CK(cudaStreamSynchronize(e->stream));
-  std::vector<unsigned long long> tr(words);
-  CK(cudaMemcpy(tr.data(), dtr, words * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
-  cudaFree(dtr);
-  if (dflag) cudaFree(dflag);
-  g.destroy();
-  // out[i][k][2]: start/end in microseconds relative to block i's front
-  // start; slot kTraceKernels-1 holds {next block's front start, 0}: the
-  // back-to-back cycle time. The device block counter names the trace slots.
-  DevState dst{};
-  CK(cudaMemcpy(&dst, e->args.st, sizeof(dst), cudaMemcpyDeviceToHost));
-  const uint64_t dev_first = (uint64_t)dst.block - blocks;
-  for (size_t i = 0; i < blocks; ++i) {
-    const size_t slot = (dev_first + i) % kTraceBlocks;
-    const unsigned long long t0 = tr[(slot * kTraceKernels + TR_FRONT) * 2];
-    for (int k = 0; k < kTraceKernels - 1; ++k) {
-      const unsigned long long s0 = tr[(slot * kTraceKernels + k) * 2];
-      const unsigned long long s1 = tr[(slot * kTraceKernels + k) * 2 + 1];
-      const bool ran = s0 != ~0ull;
-      out[(i * kTraceKernels + k) * 2] = ran ? (double)(long long)(s0 - t0) * 1e-3 : -1.0;
-      out[(i * kTraceKernels + k) * 2 + 1] = ran ? (double)(long long)(s1 - t0) * 1e-3 : -1.0;
-    }
-    const size_t nslot = (dev_first + i + 1) % kTraceBlocks;
-    const unsigned long long t1 = tr[(nslot * kTraceKernels + TR_FRONT) * 2];
-    const bool nxt = i + 1 < blocks && t1 != ~0ull;
-    out[(i * kTraceKernels + kTraceKernels - 1) * 2] = nxt ? (double)(long long)(t1 - t0) * 1e-3 : -1.0;
-    out[(i * kTraceKernels + kTraceKernels - 1) * 2 + 1] = 0.0;
-  }
-}
-}  // namespace
-
-int aura_b200_trace_blocks(aura_b200_engine* e, size_t blocks, double* out) {
-  return guarded([&] { trace_run(e, blocks, out, nullptr, 0); });
-}
-
-int aura_b200_trace_host_blocks(aura_b200_engine* e, const float* host_in, size_t n_in_blocks, size_t blocks,
-                                double* out) {
-  return guarded([&] {
-    if (!host_in || !n_in_blocks) fail(AURA_B200_E_INVALID_ARGUMENT, "null argument");
-    if (e->launch_mode != 0) fail(AURA_B200_E_INVALID_ARGUMENT, "graph mode only");
-    trace_run(e, blocks, out, host_in, n_in_blocks);
-  });
-}
-
-// Diagnostics: run `blocks` blocks with k_back's per-chunk / per-CTA
-// %globaltimer stamps on; report the last block's, in us from k_back's
-// earliest CTA start. out_segs[i] = {kind, tile, b, e, cta, start_us,
-// partial_written_us, end_us} per item; out_ctas[c] = {start_us,
-// first_data_us, exit_us}. Sizes via
-// *n_segs / *n_ctas (call with null outputs first).
-int aura_b200_trace_back(aura_b200_engine* e, size_t blocks, double* out_segs, size_t* n_segs,
-                         double* out_ctas, size_t* n_ctas) {
-  return guarded([&] {
-    const size_t ns = e->h_chunks.size(), nc = (size_t)e->back_ctas;
-    if (!out_segs || !out_ctas) {
-      *n_segs = ns;
-      *n_ctas = nc;
-      return;
-    }
-    if (!e->has_back()) fail(AURA_B200_E_INVALID_ARGUMENT, "this engine has no streaming work");
-    CK(cudaSetDevice(e->device));
-    CK(cudaStreamSynchronize(e->stream));
-    const size_t words = 4 * ns + 3 * nc;
-    unsigned long long* d = nullptr;
-    CK(cudaMalloc(&d, words * sizeof(unsigned long long)));
-    BlockArgs a = e->dev_args;
-    a.seg_trace = d;
-    auto g = e->capture_block(a, nullptr);
-    blocks = std::max<size_t>(1, blocks);
-    for (size_t i = 0; i < blocks; ++i) CK(cudaGraphLaunch(g.ex, e->stream));
-    CK(cudaStreamSynchronize(e->stream));
-    std::vector<unsigned long long> h(words);
-    CK(cudaMemcpy(h.data(), d, words * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
-    cudaFree(d);
-    g.destroy();
-    unsigned long long t0 = ~0ull;
-    for (size_t c = 0; c < nc; ++c) t0 = std::min(t0, h[4 * ns + 3 * c]);
-    auto us = [&](unsigned long long t) { return (double)(long long)(t - t0) * 1e-3; };
-    for (size_t i = 0; i < ns; ++i) {
-      const int4 s = e->h_chunks[i];
-      double* o = out_segs + 8 * i;
-      o[0] = s.x & 1;
-      o[1] = s.x >> 1;
-      o[2] = s.y;
-      o[3] = s.z;
-      o[4] = (double)h[4 * i + 3];
-      o[5] = us(h[4 * i]);
-      o[6] = us(h[4 * i + 1]);
-      o[7] = us(h[4 * i + 2]);
-    }
-    for (size_t c = 0; c < nc; ++c)
-      for (int k = 0; k < 3; ++k) out_ctas[3 * c + k] = us(h[4 * ns + 3 * c + k]);
-    e->blocks += blocks;
-  });
-}
-
-const char* aura_b200_phase_name(const aura_b200_engine*, int phase) {
-  return (phase >= 0 && phase < PH_COUNT) ? kPhaseNames[phase] : "";
-}
-
-double aura_b200_phase_bytes(const aura_b200_engine* e, int phase) { return e->phase_bytes(phase); }
-int aura_b200_launches_per_block(const aura_b200_engine* e) { return e->launches_per_block(); }
-
-int aura_b200_describe(const aura_b200_engine* e, char* buf, size_t cap) {
-  return guarded([&] {
-    const BlockArgs& a = e->args;
-    std::snprintf(buf, cap,
-                  "N=%zu Q=%zu L=%zu P=%zu K=%zu KF=%zu mode=%d LT=%d PT=%d | front: grid=%zu cpb=%d "
-                  "warps=%d smem=%zu | back: ctas=%d x %d thr, CT=%d CTn=%d sp=%d spa=%d stages=%d slot=%d B "
-                  "smem=%zu partials=%zu+%zu items=%d (static %d) w_l2=%d | reduce: %d+%d ctas l2keep=%d "
-                  "nlms=%d delta=%g knobs=%s",
-                  e->N, e->Q, e->L, e->P, e->K, e->KF, e->mode, e->LT, e->PT,
-                  (e->L + a.cpb - 1) / a.cpb, a.cpb, a.front_warps, e->smem_front, e->back_ctas, kBackThreads, a.CT,
-                  a.CTn, a.sp, a.spa, a.stages, a.slot_f4 * 16, e->smem_back, e->n_syn_segs,
-                  e->n_afc_segs, a.n_chunks, a.n_static, a.w_in_l2, a.red_syn_ctas, a.red_afc_ctas, a.h_in_l2,
-                  a.nlms, (double)a.delta, e->knobs.empty() ? "none" : e->knobs.c_str());
   });
 }
 

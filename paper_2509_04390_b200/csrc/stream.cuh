@@ -41,10 +41,6 @@
 
 namespace aura_b200 {
 
-constexpr int kConsumers = 256;                 // 8 consumer warps
-constexpr int kBackThreads = kConsumers + 32;   // + the producer warp
-constexpr int kMaxStages = 8;
-constexpr int kBackBarrierBytes = 512;          // mbarriers + stage metadata at the start of smem
 
 // ------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -586,19 +582,7 @@ __global__ void __launch_bounds__(kBackThreads, 1) k_back(const __grid_constant_
 // the reference's L, auralizer.hpp:81-86) and smooths the power (Appendix A
 // step 5). The last CTA advances the block (sharded: k_afc_finish does).
 // grid = red_syn_ctas + red_afc_ctas, kReduceThreads threads.
-constexpr int kReduceThreads = 256;
 
-// Shared-memory float4 count of k_reduce's scratch: the combine buffer, and
-// for the canceller the c2r scratch (N float2), the DftPlan tables and the
-// smoothed power (N float2).
-// Canceller sums kept in shared memory by the single-CTA path (one column
-// tile, N <= 64): (P + 1) rows of NF float4.
-__host__ __device__ inline size_t afc_ys_f4(int N, int P) { return N <= 64 ? (size_t)(P + 1) * (N / 2) : 0; }
-__host__ __device__ inline size_t reduce_smem_f4(int N, bool aur, int P = 1) {
-  // c2r scratch: one N-float2 area per mic when the mics' c2r run on separate warps
-  const size_t scratch = (N <= 1024 ? (size_t)P : 1) * N;
-  return kReduceThreads + (aur ? afc_ys_f4(N, P) + (scratch + N + table_f2(N) + 1) / 2 : 0);
-}
 
 // Canceller reduce CTAs: stage the DftPlan tables and the smoothed power --
 // they do not depend on the streaming kernel -- for whichever of them
