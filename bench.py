@@ -523,8 +523,9 @@ def run_b200_arm(args, cfg, rank, world, local_rank):
                    "parallelism": "1 GPU", "engine": describe},
         "p50_us": pct(dev_us, 50), "p99_us": pct(dev_us, 99), "max_us": float(np.max(dev_us)),
         "budget_us": 1e6 * N / cfg["fs"],
-        "value_definition": "p99 device time of ALL of a block's work (front + background "
-                            "graphs), back to back, inputs in HBM",
+        "value_definition": "p99 device time of ALL of a block's work (its whole block graph), "
+                            "back to back, inputs in HBM: CUDA events recorded by an event node "
+                            "after each block graph's last kernel (end of block b-1 -> end of b)",
         "latency_to_output_us": {"p50": pct(lat_us, 50), "p99": pct(lat_us, 99),
                                  "definition": "CUDA events: graph launch -> end of k_front (which "
                                                "also runs the canceller head after publishing the "

@@ -51,23 +51,34 @@ int aura_b200_time_device_blocks(aura_b200_engine* e, const float* host_in,
       const size_t nb = std::min(n_in_blocks, e->pool_blocks);
       CK(cudaMemcpy(e->d_in_pool, host_in, nb * per * sizeof(float), cudaMemcpyHostToDevice));
     }
-    // one block graph per pool slot (the input pointer is baked per slot)
+    // one block graph per pool slot (the input pointer is baked per slot);
+    // graph mode: block b's own graph records ev[b + 1] after its last
+    // kernel (an event node re-pointed per launch), so nothing is inserted
+    // between two block graphs; stream mode: events between the blocks
     const size_t slots = std::max<size_t>(1, std::min(n_in_blocks, e->pool_blocks));
+    const bool in_graph = e->launch_mode == 0;
+    std::vector<cudaEvent_t> ev(blocks + 1);
+    for (auto& x : ev) CK(cudaEventCreate(&x));
     std::vector<aura_b200_engine::BlockGraph> gs;
     for (size_t s = 0; s < slots; ++s) {
       BlockArgs a = e->dev_args;
       a.in = e->d_in_pool + s * per;
-      gs.push_back(e->capture_block(a, nullptr));
+      gs.push_back(e->capture_block(a, nullptr, in_graph ? ev[0] : nullptr));
     }
-    std::vector<cudaEvent_t> ev(blocks + 1);
-    for (auto& x : ev) CK(cudaEventCreate(&x));
     std::vector<BlockArgs> sa(slots, e->dev_args);
     for (size_t s = 0; s < slots; ++s) sa[s].in = e->d_in_pool + s * per;
+    CK(cudaEventRecord(ev[0], e->stream));
     for (size_t b = 0; b < blocks; ++b) {
-      CK(cudaEventRecord(ev[b], e->stream));
-      e->enqueue_block(gs[b % slots], sa[b % slots], nullptr);
+      auto& g = gs[b % slots];
+      if (in_graph) {
+        CK(cudaGraphExecEventRecordNodeSetEvent(g.ex, g.end_node, ev[b + 1]));
+        CK(cudaGraphLaunch(g.ex, e->stream));
+      } else {
+        if (b) CK(cudaEventRecord(ev[b], e->stream));
+        e->enqueue_block(g, sa[b % slots], nullptr);
+      }
     }
-    CK(cudaEventRecord(ev[blocks], e->stream));
+    if (!in_graph) CK(cudaEventRecord(ev[blocks], e->stream));
     CK(cudaStreamSynchronize(e->stream));
     for (size_t b = 0; b < blocks; ++b) {
       float ms = 0.f;

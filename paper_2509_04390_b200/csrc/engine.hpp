@@ -196,6 +196,7 @@ struct aura_b200_engine {
     cudaGraph_t g = nullptr;
     cudaGraphExec_t ex = nullptr;
     cudaGraphNode_t out_node = nullptr;  // external event-record node (output ready)
+    cudaGraphNode_t end_node = nullptr;  // event-record node after the block's last kernel
     void destroy() {
       if (ex) cudaGraphExecDestroy(ex);
       if (g) cudaGraphDestroy(g);
@@ -283,14 +284,18 @@ struct aura_b200_engine {
 
   // One graph per block: k_front, an external event node the host waits on
   // (output ready), then k_back_head -> k_back (PDL) [-> k_afc_finish].
-  BlockGraph capture_block(const BlockArgs& a, cudaEvent_t out_event) {
+  // end_event (measurement): an event-record node after the block's last
+  // kernel, re-pointed per launch -- per-block device times without an
+  // extra operation in the stream between two block graphs
+  BlockGraph capture_block(const BlockArgs& a, cudaEvent_t out_event, cudaEvent_t end_event = nullptr) {
     BlockGraph bg;
     CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
     launch_phase(PH_FRONT, a, stream);
     if (out_event) CK(cudaEventRecordWithFlags(out_event, stream, cudaEventRecordExternal));
     for (int ph = PH_BACK_HEAD; ph < PH_COUNT; ++ph) launch_phase(ph, a, stream);
+    if (end_event) CK(cudaEventRecordWithFlags(end_event, stream, cudaEventRecordExternal));
     CK(cudaStreamEndCapture(stream, &bg.g));
-    if (out_event) {
+    if (out_event || end_event) {
       size_t n = 0;
       CK(cudaGraphGetNodes(bg.g, nullptr, &n));
       std::vector<cudaGraphNode_t> nodes(n);
@@ -298,7 +303,11 @@ struct aura_b200_engine {
       for (auto nd : nodes) {
         cudaGraphNodeType t;
         CK(cudaGraphNodeGetType(nd, &t));
-        if (t == cudaGraphNodeTypeEventRecord) bg.out_node = nd;
+        if (t != cudaGraphNodeTypeEventRecord) continue;
+        cudaEvent_t ev = nullptr;
+        CK(cudaGraphEventRecordNodeGetEvent(nd, &ev));
+        if (ev == out_event) bg.out_node = nd;
+        if (ev == end_event) bg.end_node = nd;
       }
     }
     CK(cudaGraphInstantiate(&bg.ex, bg.g, 0));
