@@ -381,9 +381,15 @@ def l2_read_peak(footprint_bytes):
     return best, "measured L2-resident read at %.0f MB (profiles/r2_l2_probe.jsonl)" % mb
 
 
+L2_RESIDENT_BYTES = 80e6  # the engine's own rule (engine.cu plan_back: h_in_l2)
+
+
 def roofline_regime(eng_bytes_footprint):
-    """SURVEY 8(d) regime rule: footprint (H + W + FDLs) < L2/2 -> L2."""
-    return "l2" if eng_bytes_footprint < 126e6 / 2 else "hbm"
+    """SURVEY 8(d)'s regime rule (footprint H + W + FDLs < L2/2 -> L2),
+    with the engine's threshold: below 80 MB k_back streams the spectra with
+    evict_normal hints and they stay in the 126 MB L2 between blocks (c2's
+    65 MB included: warm ncu, profiles/r2_l2.md); above it, evict_first."""
+    return "l2" if eng_bytes_footprint < L2_RESIDENT_BYTES else "hbm"
 
 
 def c5_secondary(A, device, K, W, world=1, rank=0):

@@ -87,4 +87,4 @@ def test_gpus_flag_relaunches_one_process_per_rank():
 def test_l2_roofline_peak_from_the_committed_probe():
     peak, kind = bench.l2_read_peak(64e6)
     assert peak is not None and 5000 < peak < 20000 and "r2_l2_probe" in kind
-    assert bench.roofline_regime(65e6 / 2) == "l2" and bench.roofline_regime(323e6) == "hbm"
+    assert bench.roofline_regime(65.3e6) == "l2" and bench.roofline_regime(323e6) == "hbm"
