@@ -159,6 +159,13 @@ int aura_b200_fdl_slot(aura_b200_engine* e, int which, size_t channel,
                        size_t age, float* out);
 /* Current canceller spectra W[p][l][k][j], P x L x K_f x (N+1) complex. */
 int aura_b200_afc_coeffs(aura_b200_engine* e, float* out);
+/* Load canceller spectra in the same layout (checkpoint / warm start of the
+ * NLMS canceller, e.g. from a measured feedback path or a previous run's
+ * aura_b200_afc_coeffs). DC and Nyquist bins must be real
+ * (AURA_B200_E_NON_REAL_EDGE_BINS otherwise, as DftPlan::inverse,
+ * dft.hpp:115-117). as_initial != 0: reset() returns to these spectra too
+ * (NLMS engines; a mu = 0 canceller keeps whatever was loaded). */
+int aura_b200_afc_load_coeffs(aura_b200_engine* e, const float* in, int as_initial);
 
 /* Wait until every processed block has fully finished, including the
  * background work (next-block precompute, canceller update, f^). process()

@@ -191,6 +191,7 @@ def lib():
     L.aura_b200_mode.argtypes = [vp]
     L.aura_b200_filter_spectrum.argtypes = [vp, sz, sz, _f32p]
     L.aura_b200_afc_coeffs.argtypes = [vp, _f32p]
+    L.aura_b200_afc_load_coeffs.argtypes = [vp, _f32p, C.c_int]
     L.aura_b200_fdl_slot.argtypes = [vp, C.c_int, sz, sz, _f32p]
     L.aura_b200_time_device_blocks.argtypes = [vp, C.c_void_p, sz, sz, _f32p, _f32p]
     L.aura_b200_time_device_span.argtypes = [vp, C.c_void_p, sz, sz, C.POINTER(C.c_float)]
@@ -593,3 +594,12 @@ class Auralizer(_Engine):
         out = np.zeros(P * L * self._kf * (N + 1) * 2, np.float32)
         _check(lib().aura_b200_afc_coeffs(self._h, out))
         return out.view(np.complex64).reshape(P, L, self._kf, N + 1)
+
+    def load_coeffs(self, W: np.ndarray, as_initial: bool = False):
+        """Load canceller spectra W (P, L, K_f, N+1) complex64: checkpoint /
+        warm start; as_initial makes reset() return to them."""
+        P, L, N = self.cfg.input_channels, self.cfg.output_channels, self.cfg.block_size
+        w = np.ascontiguousarray(W, np.complex64)
+        if w.shape != (P, L, self._kf, N + 1):
+            _raise(ErrorCode.shape_mismatch, f"canceller spectra must be {(P, L, self._kf, N + 1)}")
+        _check(lib().aura_b200_afc_load_coeffs(self._h, w.view(np.float32).ravel(), 1 if as_initial else 0))

@@ -987,4 +987,31 @@ int aura_b200_afc_coeffs(aura_b200_engine* e, float* out) {
   });
 }
 
+int aura_b200_afc_load_coeffs(aura_b200_engine* e, const float* in, int as_initial) {
+  return guarded([&] {
+    if (!e || !in) fail(AURA_B200_E_INVALID_ARGUMENT, "null argument");
+    if (!e->aur) fail(AURA_B200_E_INVALID_ARGUMENT, "not an auralizer");
+    const size_t N = e->N, CT = e->args.CT, CTn = e->args.CTn, P = e->P, U = e->L * e->KF;
+    // reference rows [p][l][k] of N + 1 bins -> tiled [CTn][U][P][CT]; the
+    // DC and Nyquist bins must be real (dft.hpp:115-117's inverse() check)
+    std::vector<float4> buf(e->w_elems);
+    for (size_t p = 0; p < P; ++p)
+      for (size_t u = 0; u < U; ++u) {
+        const float* r = in + (p * U + u) * 2 * (N + 1);
+        if (r[1] != 0.0f || r[2 * N + 1] != 0.0f)
+          fail(AURA_B200_E_NON_REAL_EDGE_BINS, "DC and Nyquist bins must have zero imaginary part");
+        std::vector<float2> packed(N);
+        packed[0] = make_float2(r[0], r[2 * N]);
+        for (size_t j = 1; j < N; ++j) packed[j] = make_float2(r[2 * j], r[2 * j + 1]);
+        const float4* pk = reinterpret_cast<const float4*>(packed.data());
+        for (size_t c = 0; c < CTn; ++c)
+          std::memcpy(&buf[((c * U + u) * P + p) * CT], pk + c * CT, sizeof(float4) * CT);
+      }
+    CK(cudaSetDevice(e->device));
+    CK(cudaStreamSynchronize(e->stream));
+    CK(cudaMemcpy(e->args.W, buf.data(), sizeof(float4) * e->w_elems, cudaMemcpyHostToDevice));
+    if (as_initial && e->W0) CK(cudaMemcpy(e->W0, buf.data(), sizeof(float4) * e->w_elems, cudaMemcpyHostToDevice));
+  });
+}
+
 }  // extern "C"

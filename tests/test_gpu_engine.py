@@ -94,3 +94,33 @@ def test_shard_exchange_timeout_reports_and_reset_recovers():
     assert np.array_equal(ests[0], ests[1])
     v.close()
     ref.close()
+
+
+def test_canceller_checkpoint_resumes_bit_identically():
+    """afc_coeffs / afc_load_coeffs as a checkpoint of the NLMS canceller:
+    an engine whose W is loaded from another's is bit-identical to an engine
+    created with those spectra's filters when both start fresh (W at load =
+    the partitioned F^), and an exported W loaded back continues exactly."""
+    N, L = 64, 8
+    rng = np.random.default_rng(31)
+    synth = decaying_filters(rng, L, 9 * N, scale=0.5)
+    fc_a = decaying_filters(rng, L, 3 * N, scale=0.1)
+    fc_b = decaying_filters(rng, L, 3 * N, scale=0.1)
+    cfg = A.make_config(48000, N, 1, L)
+    afc = A.AfcParams(0.02, 0.9, 1e-2)
+    a = A.Auralizer(list(synth), list(fc_a), cfg, afc=afc)
+    b = A.Auralizer(list(synth), list(fc_b), cfg, afc=afc)
+    b.load_coeffs(a.coeffs(), as_initial=True)   # b now starts from F^_a
+    mics = rng.standard_normal((20, 1, N)).astype(np.float32)
+    for i in range(20):
+        assert np.array_equal(a.process(mics[i]), b.process(mics[i])), i
+    assert np.array_equal(a.coeffs(), b.coeffs())
+    b.reset()  # back to the loaded spectra (as_initial)
+    a.reset()
+    for i in range(5):
+        assert np.array_equal(a.process(mics[i]), b.process(mics[i]))
+    W = a.coeffs()
+    W[0, 0, 0, 0] = W[0, 0, 0, 0] + 1j  # DC must be real
+    with pytest.raises(A.Error) as ei:
+        b.load_coeffs(W)
+    assert ei.value.code == A.ErrorCode.non_real_edge_bins
