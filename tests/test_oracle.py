@@ -167,3 +167,56 @@ def test_fused_vs_manual_pin_is_bit_identity_not_accuracy():
             x = rng.standard_normal((1, N)).astype(np.float32)
             worst = max(worst, float(np.max(np.abs(r.process(x) - d.process(x)))))
     assert worst > 1e-5
+
+
+def test_c1_exact_size_fixture_is_bit_exact():
+    """BASELINE configs[0] at its exact size (96k taps, 375 partitions,
+    K + 3 = 378 blocks): the C oracle reproduces the reference-generated
+    fixture bit for bit (the fixture the GPU test also checks)."""
+    from conftest import c1_inputs
+    N, L, n_h, blocks, filt, x = c1_inputs()
+    g = golden("c1_full")
+    oc = O.OracleConvolver(filt, N, 1, L, O.BROADCAST)
+    assert oc.partitions == 375 and int(g["blocks"]) == blocks
+    y = np.stack([oc.process(x[b]) for b in range(blocks)])
+    assert bits_equal(y, g["y"])
+
+
+def test_f64_oracle_is_the_exact_linear_convolution():
+    """liboracle64.so (the ground truth of the full-length GPU tests) equals
+    the float64 linear convolution of the stream to ~1e-15, while the fp32
+    oracle (= the reference) is ~1e-6 off already at 200 partitions."""
+    rng = np.random.default_rng(12)
+    N, C = 64, 3
+    f = scaled_filters(rng, C, 200 * N)
+    x = rng.standard_normal((230, 1, N)).astype(np.float32)
+    o32 = O.OracleConvolver(f, N, 1, C, O.BROADCAST)
+    o64 = O.OracleConvolver(f, N, 1, C, O.BROADCAST, f64=True)
+    y32 = np.stack([o32.process(b) for b in x]).transpose(1, 0, 2).reshape(C, -1)
+    y64 = np.stack([o64.process(b) for b in x]).transpose(1, 0, 2).reshape(C, -1)
+    xs = x.reshape(-1).astype(np.float64)
+    exact = np.stack([np.convolve(xs, f[c].astype(np.float64))[:xs.size] for c in range(C)])
+    rms = np.sqrt(np.mean(exact ** 2))
+    assert np.max(np.abs(y64 - exact)) / rms < 1e-12
+    assert 1e-8 < np.max(np.abs(y32 - exact)) / rms < 1e-4
+
+
+def test_f64_oracle_nlms_tracks_the_f64_restatement():
+    """The float64 oracle's NLMS canceller agrees with the independent numpy
+    float64 restatement (tests/nlms_f64.py) to rounding."""
+    from nlms_f64 import NlmsF64
+    rng = np.random.default_rng(13)
+    N, L = 32, 4
+    s = scaled_filters(rng, L, 6 * N, 0.5)
+    fc = scaled_filters(rng, L, 3 * N, 0.1)
+    # parameters exactly representable in float32 (the oracle holds them as
+    # the fp32 engines do)
+    kw = dict(gain=0.75, mu=0.0625, lam=0.875, delta=2.0 ** -10)
+    o = O.OracleAuralizer(s, fc, N, 1, L, f64=True, **kw)
+    d = NlmsF64(s, fc, N, 1, L, **kw)
+    for _ in range(40):
+        m = rng.standard_normal((1, N)).astype(np.float32)
+        y, yd = o.process(m), d.process(m)
+        assert np.max(np.abs(y - yd)) <= 1e-10 * max(1.0, np.max(np.abs(yd)))
+    Wd = d.W
+    assert np.max(np.abs(o.coeffs() - Wd)) <= 1e-10 * np.max(np.abs(Wd))
