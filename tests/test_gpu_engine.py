@@ -124,3 +124,27 @@ def test_canceller_checkpoint_resumes_bit_identically():
     with pytest.raises(A.Error) as ei:
         b.load_coeffs(W)
     assert ei.value.code == A.ErrorCode.non_real_edge_bins
+
+
+def test_measurement_entry_points_run_and_leave_the_stream_consistent():
+    """The diag.cu entry points bench.py and tools/ use: device-resident and
+    host-I/O traced timelines, the span timing, per-phase timing -- and the
+    engine still streams bit-identically to an untouched twin afterwards
+    (they advance the block counter, which only moves ring slots)."""
+    mk, rng = small_aur(0.02)
+    a, b = mk(), mk()
+    mics = rng.standard_normal((8, 1, 64)).astype(np.float32)
+    tr = a.trace_blocks(6)
+    trh = a.trace_blocks(6, host_inputs=mics)
+    for t in (tr, trh):
+        assert {"k_front", "k_back", "k_reduce", "output", "cycle"} <= set(t)
+        assert np.all(t["output"][:, 0] > 0) and np.all(t["cycle"][:, 0] > t["output"][:, 0])
+    assert a.time_device_span(10, mics) > 0
+    lat, us = a.time_device_blocks(10, mics)
+    assert np.all(us > 0) and np.all(lat > 0)
+    ph = a.profile_phases(3)
+    assert ph["k_back"][1] > 0
+    a.reset()
+    b.reset()
+    for i in range(8):
+        assert np.array_equal(a.process(mics[i]), b.process(mics[i]))
