@@ -469,14 +469,6 @@ def run_b200_arm(args, cfg, rank, world, local_rank):
                  "blocks": int(paced_us.size),
                  "definition": "aura_b200_process() latency with calls on the real-time grid "
                                "(one block every N/fs), host buffers"}
-        # the armed launch mode: the next block's graph waits on the GPU for
-        # process() to ring its doorbell (launch latency off the user path)
-        eng.set_launch_mode(2)
-        eng.time_host_blocks(mic, 20, pace_us=1e6 * N / cfg["fs"])
-        armed_us = eng.time_host_blocks(mic, min(K, 2000), pace_us=1e6 * N / cfg["fs"])
-        eng.set_launch_mode(0)
-        paced["armed"] = {"p50_us": pct(armed_us, 50), "p99_us": pct(armed_us, 99),
-                          "launch_mode": "2 (armed: aura_b200_set_launch_mode)"}
 
     cpu = None
     if not args.no_cpu_baseline:
