@@ -14,16 +14,9 @@
 extern "C" {
 #endif
 
-/* How blocks run (all bit-identical): 0 = one CUDA graph per block
- * (default); 1 = the same kernels launched on the engine stream (an A/B for
- * launch overhead); 2 = armed: right after each process() the NEXT block's
- * graph is launched, its k_front resident and waiting on a doorbell in
- * mapped host memory, so the next process() only writes its input and rings
- * it -- the launch latency leaves the user-visible path. While armed the
- * engine keeps its k_front CTAs (one per 8 loudspeakers, plus one per mic)
- * resident on their SMs; every call that needs the engine idle (reset,
- * synchronize, feedback_estimate, the accessors, destroy) calls the armed
- * block off first. Unsharded engines only. */
+/* How blocks run: 0 = one CUDA graph per block (default), 1 = the same
+ * kernels launched on the engine stream (bit-identical; an A/B for launch
+ * overhead). */
 int aura_b200_set_launch_mode(aura_b200_engine* e, int mode);
 int aura_b200_launch_mode(const aura_b200_engine* e);
 /* Testing: number the device blocks from n instead of 0 (only before the

@@ -359,9 +359,7 @@ class _Engine:
 
     def set_launch_mode(self, mode: int):
         """0: one CUDA graph per block (default); 1: the same kernels
-        launched on the stream; 2: armed -- the next block's graph waits on
-        the GPU for process() to ring a doorbell (launch latency off the
-        user-visible path). All bit-identical."""
+        launched on the stream (bit-identical)."""
         _check(lib().aura_b200_set_launch_mode(self._h, mode))
 
     def launch_mode(self) -> int:

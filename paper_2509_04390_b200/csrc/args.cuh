@@ -26,11 +26,8 @@ typedef unsigned long long blk_t;
 struct DevState {
   blk_t block;
   uint32_t ticket;
-  uint32_t cancel;  // armed launch mode: the pre-launched block was called off
+  uint32_t pad;
 };
-
-// Armed launch mode: the doorbell value that calls a pre-launched block off.
-constexpr unsigned long long kDoorbellCancel = ~0ull;
 
 // Optional timeline trace (%globaltimer, ns): per traced block slot and
 // kernel, the earliest CTA start and the latest CTA end.
@@ -94,10 +91,6 @@ struct BlockArgs {
   // release store per CTA (every k_front CTA, the error-spectrum CTAs too,
   // so no CTA still reads the mapped input when process() returns)
   unsigned long long* out_flag;
-  // armed launch mode (launch mode 2): the block graph is launched ahead of
-  // its input and k_front waits, resident, for the host to ring this mapped
-  // word with block + 1 (or kDoorbellCancel); null otherwise
-  const unsigned long long* doorbell;
   // fused head: k_front also runs the canceller head (and, on P extra CTAs,
   // the NLMS error spectra) and k_back is its programmatic dependent; the
   // window history then alternates prev_in / hist1 by block parity

@@ -12,7 +12,7 @@ int aura_b200_seek_block(aura_b200_engine* e, uint64_t n) {
     if (e->blocks) fail(AURA_B200_E_INVALID_ARGUMENT, "seek only before the first block (or after reset)");
     if (e->G > 1) fail(AURA_B200_E_INVALID_ARGUMENT, "seek does not apply to sharded engines");
     CK(cudaSetDevice(e->device));
-    quiesce(e);
+    CK(cudaStreamSynchronize(e->stream));
     // every delay line is zero here, so starting the ring slots (block mod
     // K) at n instead of 0 changes no value
     DevState st{};
@@ -24,15 +24,11 @@ int aura_b200_seek_block(aura_b200_engine* e, uint64_t n) {
 
 int aura_b200_set_launch_mode(aura_b200_engine* e, int mode) {
   return guarded([&] {
-    if (mode < 0 || mode > 2)
-      fail(AURA_B200_E_INVALID_ARGUMENT,
-           "launch mode is 0 (one CUDA graph per block), 1 (kernels on the stream) or 2 (armed)");
-    if (mode == 2 && (e->G > 1 || !e->front_head || !e->use_outflag))
-      fail(AURA_B200_E_INVALID_ARGUMENT, "the armed mode needs an unsharded engine with the fused head and output words");
+    if (mode < 0 || mode > 1)
+      fail(AURA_B200_E_INVALID_ARGUMENT, "launch mode is 0 (one CUDA graph per block) or 1 (kernels on the stream)");
     CK(cudaSetDevice(e->device));
-    quiesce(e);
+    CK(cudaStreamSynchronize(e->stream));
     e->launch_mode = mode;
-    e->rebuild_graphs();
   });
 }
 
@@ -49,7 +45,7 @@ int aura_b200_time_device_blocks(aura_b200_engine* e, const float* host_in,
                                  float* block_us) {
   return guarded([&] {
     CK(cudaSetDevice(e->device));
-    quiesce(e);
+    CK(cudaStreamSynchronize(e->stream));
     const size_t per = (size_t)e->Qx * e->N;
     if (host_in && n_in_blocks) {
       const size_t nb = std::min(n_in_blocks, e->pool_blocks);
@@ -83,7 +79,7 @@ int aura_b200_time_device_blocks(aura_b200_engine* e, const float* host_in,
       }
     }
     if (!in_graph) CK(cudaEventRecord(ev[blocks], e->stream));
-    quiesce(e);
+    CK(cudaStreamSynchronize(e->stream));
     for (size_t b = 0; b < blocks; ++b) {
       float ms = 0.f;
       CK(cudaEventElapsedTime(&ms, ev[b], ev[b + 1]));
@@ -109,7 +105,7 @@ int aura_b200_time_device_blocks(aura_b200_engine* e, const float* host_in,
         CK(cudaEventRecord(ev2[2 * b], e->stream));
         CK(cudaGraphLaunch(g.ex, e->stream));
       }
-      quiesce(e);
+      CK(cudaStreamSynchronize(e->stream));
       for (size_t b = 0; b < blocks; ++b) {
         float ms = 0.f;
         CK(cudaEventElapsedTime(&ms, ev2[2 * b], ev2[2 * b + 1]));
@@ -130,7 +126,7 @@ int aura_b200_time_device_span(aura_b200_engine* e, const float* host_in, size_t
                                size_t blocks, float* total_us) {
   return guarded([&] {
     CK(cudaSetDevice(e->device));
-    quiesce(e);
+    CK(cudaStreamSynchronize(e->stream));
     const size_t per = (size_t)e->Qx * e->N;
     const size_t slots = std::max<size_t>(1, std::min(n_in_blocks, e->pool_blocks));
     if (host_in && n_in_blocks)
@@ -147,7 +143,7 @@ int aura_b200_time_device_span(aura_b200_engine* e, const float* host_in, size_t
     CK(cudaEventRecord(t0, e->stream));
     for (size_t b = 0; b < blocks; ++b) e->enqueue_block(gs[b % slots], sa[b % slots], nullptr);
     CK(cudaEventRecord(t1, e->stream));
-    quiesce(e);
+    CK(cudaStreamSynchronize(e->stream));
     float ms = 0.f;
     CK(cudaEventElapsedTime(&ms, t0, t1));
     *total_us = ms * 1000.0f;
@@ -230,7 +226,7 @@ int aura_b200_time_host_breakdown(aura_b200_engine* e, const float* host_in, siz
       o[3] = us(t4);
       o[4] = us(t5);
     }
-    quiesce(e);
+    CK(cudaStreamSynchronize(e->stream));
   });
 }
 
@@ -238,7 +234,7 @@ int aura_b200_profile_phases(aura_b200_engine* e, size_t blocks, float* phase_us
                              int* n_phases) {
   return guarded([&] {
     CK(cudaSetDevice(e->device));
-    quiesce(e);
+    CK(cudaStreamSynchronize(e->stream));
     const int np = PH_COUNT;
     std::vector<cudaEvent_t> ev((size_t)(np + 1) * blocks);
     for (auto& x : ev) CK(cudaEventCreate(&x));
@@ -252,7 +248,7 @@ int aura_b200_profile_phases(aura_b200_engine* e, size_t blocks, float* phase_us
       CK(cudaEventRecord(ev[b * (np + 1) + np], e->stream));
     }
     CK(cudaGetLastError());
-    quiesce(e);
+    CK(cudaStreamSynchronize(e->stream));
     for (int ph = 0; ph < np; ++ph) {
       double s = 0;
       for (size_t b = 0; b < blocks; ++b) {
@@ -275,7 +271,7 @@ int aura_b200_time_phase(aura_b200_engine* e, int phase, size_t reps, float* avg
     if (phase == PH_BACK && !e->has_back())
       fail(AURA_B200_E_INVALID_ARGUMENT, "this engine has no streaming work");
     CK(cudaSetDevice(e->device));
-    quiesce(e);
+    CK(cudaStreamSynchronize(e->stream));
     // The relaunches are not idempotent (k_reduce advances the block
     // counter, k_back updates W in place, the fused canceller head shifts
     // the loudspeaker history): snapshot every mutable device buffer and put
@@ -308,14 +304,14 @@ int aura_b200_time_phase(aura_b200_engine* e, int phase, size_t reps, float* avg
     CK(cudaEventRecord(t1, e->stream));
     e->pdl_off = false;
     CK(cudaGetLastError());
-    quiesce(e);
+    CK(cudaStreamSynchronize(e->stream));
     float ms = 0.f;
     CK(cudaEventElapsedTime(&ms, t0, t1));
     cudaEventDestroy(t0);
     cudaEventDestroy(t1);
     *avg_us = 1000.0f * ms / (float)reps;
     copy_all(false);
-    quiesce(e);
+    CK(cudaStreamSynchronize(e->stream));
     CK(cudaFree(snap));
   });
 }
@@ -326,7 +322,7 @@ namespace {
 // output words, back to back) instead of device-resident I/O.
 void trace_run(aura_b200_engine* e, size_t blocks, double* out, const float* host_in, size_t n_in) {
   CK(cudaSetDevice(e->device));
-  quiesce(e);
+  CK(cudaStreamSynchronize(e->stream));
   blocks = std::min<size_t>(blocks, kTraceBlocks);
   const size_t words = (size_t)kTraceBlocks * kTraceKernels * 2;
   std::vector<unsigned long long> init(words);
@@ -361,7 +357,7 @@ void trace_run(aura_b200_engine* e, size_t blocks, double* out, const float* hos
     for (size_t i = 0; i < blocks; ++i) CK(cudaGraphLaunch(g.ex, e->stream));
     e->blocks += blocks;
   }
-  quiesce(e);
+  CK(cudaStreamSynchronize(e->stream));
   std::vector<unsigned long long> tr(words);
   CK(cudaMemcpy(tr.data(), dtr, words * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
   cudaFree(dtr);
@@ -422,7 +418,7 @@ int aura_b200_trace_back(aura_b200_engine* e, size_t blocks, double* out_segs, s
     }
     if (!e->has_back()) fail(AURA_B200_E_INVALID_ARGUMENT, "this engine has no streaming work");
     CK(cudaSetDevice(e->device));
-    quiesce(e);
+    CK(cudaStreamSynchronize(e->stream));
     const size_t words = 4 * ns + 3 * nc;
     unsigned long long* d = nullptr;
     CK(cudaMalloc(&d, words * sizeof(unsigned long long)));
@@ -431,7 +427,7 @@ int aura_b200_trace_back(aura_b200_engine* e, size_t blocks, double* out_segs, s
     auto g = e->capture_block(a, nullptr);
     blocks = std::max<size_t>(1, blocks);
     for (size_t i = 0; i < blocks; ++i) CK(cudaGraphLaunch(g.ex, e->stream));
-    quiesce(e);
+    CK(cudaStreamSynchronize(e->stream));
     std::vector<unsigned long long> h(words);
     CK(cudaMemcpy(h.data(), d, words * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
     cudaFree(d);

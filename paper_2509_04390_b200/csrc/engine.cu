@@ -128,7 +128,7 @@ void partition_rows(aura_b200_engine* e, const BlockArgs& a, const float* const*
     k_partition<<<grid, 256, smem, e->stream>>>(d_taps, n_h, (int)K, (int)N, ilog2(N), a.tw, a.split, o,
                                                  d_off, d_off + nb);
     CK(cudaGetLastError());
-    quiesce(e);
+    CK(cudaStreamSynchronize(e->stream));
   }
   cudaFree(d_taps);
   cudaFree(d_off);
@@ -567,22 +567,19 @@ void finish_init(aura_b200_engine* e) {
   std::memset(e->h_outflag, 0, e->n_outflags * sizeof(unsigned long long));
   CK(cudaHostGetDevicePointer((void**)&a.out_flag, e->h_outflag, 0));
   e->use_outflag = knob_i(e, "OUTFLAG", 1) != 0;
-  CK(cudaHostAlloc(&e->h_doorbell, sizeof(unsigned long long), cudaHostAllocMapped | cudaHostAllocPortable));
-  *e->h_doorbell = 0ull;
-  a.doorbell = nullptr;  // only the armed graph (launch mode 2) waits on it
   e->rebuild_graphs();
   e->dev_args = a;
   e->dev_args.out = e->d_out;
   e->dev_args.in = e->d_in_pool;
   e->dev_args.out_flag = nullptr;  // device-resident measurement: no host handshake
-  quiesce(e);
+  CK(cudaStreamSynchronize(e->stream));
 }
 
 void reset_state(aura_b200_engine* e) {
   BlockArgs& a = e->args;
   const size_t N = e->N, NF = N / 2;
   cudaStream_t s = e->stream;
-  quiesce(e);
+  CK(cudaStreamSynchronize(s));
   CK(cudaMemsetAsync(a.st, 0, sizeof(DevState), s));
   CK(cudaMemsetAsync(a.prev_in, 0, sizeof(float) * e->Qx * N, s));
   if (a.hist1) CK(cudaMemsetAsync(a.hist1, 0, sizeof(float) * e->Qx * N, s));
@@ -851,20 +848,6 @@ int aura_b200_process(aura_b200_engine* e, const float* in, float* out) {
     std::memcpy(e->h_in, in, n_in * sizeof(float));
     std::atomic_thread_fence(std::memory_order_release);
     const uint64_t nblk = device_block_hint(e);
-    if (e->launch_mode == 2) {
-      // armed: this block's graph is already on the stream, its k_front
-      // resident and waiting; ring it, then arm the next block at once
-      if (!e->armed) {
-        CK(cudaGraphLaunch(e->g_armed.ex, e->stream));
-        e->armed = true;
-      }
-      reinterpret_cast<volatile unsigned long long*>(e->h_doorbell)[0] = nblk + 1;
-      wait_flag(e, nblk + 1, "block output");
-      std::memcpy(out, e->h_out, e->L * e->N * sizeof(float));
-      ++e->blocks;
-      CK(cudaGraphLaunch(e->g_armed.ex, e->stream));
-      return;
-    }
     // (nothing else goes on the stream per block: an extra stream operation
     // between two block graphs costs device time at every block boundary)
     e->enqueue_block(e->g_block, e->args, e->use_outflag ? nullptr : e->ev_front);
@@ -882,7 +865,6 @@ int aura_b200_process(aura_b200_engine* e, const float* in, float* out) {
 int aura_b200_synchronize(aura_b200_engine* e) {
   return guarded([&] {
     CK(cudaSetDevice(e->device));
-    disarm(e);
     wait_event(e, nullptr, "block background");
     check_shard_status(e);
   });
@@ -899,7 +881,6 @@ int aura_b200_feedback_estimate(aura_b200_engine* e, float* out) {
   return guarded([&] {
     if (!e->aur) fail(AURA_B200_E_INVALID_ARGUMENT, "not an auralizer");
     CK(cudaSetDevice(e->device));
-    disarm(e);
     wait_event(e, nullptr, "block background");
     check_shard_status(e);
     // f^ stays in device memory (the background kernels never write mapped
@@ -913,7 +894,7 @@ int aura_b200_fdl_slot(aura_b200_engine* e, int which, size_t channel, size_t ag
                        float* out) {
   return guarded([&] {
     CK(cudaSetDevice(e->device));
-    quiesce(e);
+    CK(cudaStreamSynchronize(e->stream));
     size_t cap, chans;
     const float4* base;
     if (which == 0) {
@@ -947,7 +928,7 @@ int aura_b200_set_input_gain(aura_b200_engine* e, float gain) {
   return guarded([&] {
     if (!e->aur) fail(AURA_B200_E_INVALID_ARGUMENT, "not an auralizer");
     CK(cudaSetDevice(e->device));
-    quiesce(e);
+    CK(cudaStreamSynchronize(e->stream));
     e->args.gain = gain;
     e->dev_args.gain = gain;
     e->rebuild_graphs();
@@ -990,7 +971,7 @@ int aura_b200_afc_coeffs(aura_b200_engine* e, float* out) {
   return guarded([&] {
     if (!e->aur) fail(AURA_B200_E_INVALID_ARGUMENT, "not an auralizer");
     CK(cudaSetDevice(e->device));
-    quiesce(e);
+    CK(cudaStreamSynchronize(e->stream));
     std::vector<float4> buf(e->w_elems);
     CK(cudaMemcpy(buf.data(), e->args.W, sizeof(float4) * e->w_elems, cudaMemcpyDeviceToHost));
     // tiled [CTn][U][P][CT] -> reference rows [p][l][k], N + 1 bins each
@@ -1027,7 +1008,7 @@ int aura_b200_afc_load_coeffs(aura_b200_engine* e, const float* in, int as_initi
           std::memcpy(&buf[((c * U + u) * P + p) * CT], pk + c * CT, sizeof(float4) * CT);
       }
     CK(cudaSetDevice(e->device));
-    quiesce(e);
+    CK(cudaStreamSynchronize(e->stream));
     CK(cudaMemcpy(e->args.W, buf.data(), sizeof(float4) * e->w_elems, cudaMemcpyHostToDevice));
     if (as_initial && e->W0) CK(cudaMemcpy(e->W0, buf.data(), sizeof(float4) * e->w_elems, cudaMemcpyHostToDevice));
   });

@@ -205,14 +205,10 @@ struct aura_b200_engine {
     }
   };
   BlockGraph g_block;
-  BlockGraph g_armed;  // launch mode 2: the block graph whose k_front waits for the doorbell
   // streaming kernel k_back
   BackFn back_fn = nullptr;
   bool pdl_off = false;  // measurement: serialise k_back / k_reduce launches
-  int launch_mode = 0;   // 0: one CUDA graph per block; 1: the same kernels launched on the stream;
-                         // 2: armed -- the next block's graph is launched ahead of its input
-  unsigned long long* h_doorbell = nullptr;  // mapped: the armed block's go (block + 1) or cancel
-  bool armed = false;    // a pre-launched block is waiting on the stream for the doorbell
+  int launch_mode = 0;   // 0: one CUDA graph per block; 1: the same kernels launched on the stream
   unsigned long long* h_outflag = nullptr;  // mapped: k_front CTA b writes block + 1 in [b] when done
   size_t n_outflags = 0;    // = k_front's grid (every CTA that reads the mapped input)
   bool use_outflag = true;
@@ -235,19 +231,13 @@ struct aura_b200_engine {
     cudaSetDevice(device);
     // wedged (a shard peer that never arrives is bounded in-kernel, but be
     // safe): leak rather than block, the frees below would synchronise
-    if (armed && h_doorbell) {  // call the pre-launched block off
-      reinterpret_cast<volatile unsigned long long*>(h_doorbell)[0] = kDoorbellCancel;
-      std::atomic_thread_fence(std::memory_order_seq_cst);
-    }
     if (stream && !wait_stream_idle(stream, 10.0)) return;
     g_block.destroy();
-    g_armed.destroy();
     for (void* p : dmem) cudaFree(p);
     if (h_in) cudaFreeHost(h_in);
     if (h_out) cudaFreeHost(h_out);
     if (h_status) cudaFreeHost(h_status);
     if (h_outflag) cudaFreeHost(h_outflag);
-    if (h_doorbell) cudaFreeHost(h_doorbell);
     for (void* p : ipc_opened) cudaIpcCloseMemHandle(p);
     if (nccl) nccl_api().destroy(nccl);
     if (ev_front) cudaEventDestroy(ev_front);
@@ -342,14 +332,6 @@ struct aura_b200_engine {
     // no event node after k_front unless the host waits on it: a node
     // between k_front and k_back would stand in their programmatic edge
     g_block = capture_block(args, use_outflag ? nullptr : ev_front);
-    g_armed.destroy();
-    if (launch_mode == 2) {
-      BlockArgs b = args;
-      unsigned long long* d = nullptr;
-      CK(cudaHostGetDevicePointer((void**)&d, h_doorbell, 0));
-      b.doorbell = d;
-      g_armed = capture_block(b, nullptr);
-    }
   }
 
   // Every device buffer a block writes (measurement calls that relaunch
@@ -461,23 +443,5 @@ inline void wait_event(aura_b200_engine* e, cudaEvent_t ev, const char* what) {
       fail(AURA_B200_E_TIMEOUT, std::string(what) + ": not complete within 20 s");
   }
   std::atomic_thread_fence(std::memory_order_acquire);
-}
-
-// Launch mode 2: call the pre-launched block off (its kernels then do
-// nothing and the block counter stays) and let the stream drain -- before
-// anything that needs the engine idle.
-inline void disarm(aura_b200_engine* e) {
-  if (!e->armed) return;
-  volatile unsigned long long* db = e->h_doorbell;
-  *db = kDoorbellCancel;
-  std::atomic_thread_fence(std::memory_order_seq_cst);
-  wait_event(e, nullptr, "armed block cancel");
-  *db = 0ull;
-  e->armed = false;
-}
-// The engine idle: no armed block, nothing queued on its stream.
-inline void quiesce(aura_b200_engine* e) {
-  disarm(e);
-  CK(cudaStreamSynchronize(e->stream));
 }
 

@@ -384,35 +384,10 @@ __device__ void front_warps_body(const BlockArgs& a, blk_t n, int c0, int c1, fl
   }
 }
 
-// Armed launch mode: wait (thread 0 of the CTA, resident) until the host
-// rings the doorbell for block n -- true -- or calls the block off (false:
-// the CTA records the cancel and exits; k_back / k_reduce then do nothing).
-__device__ __forceinline__ bool await_doorbell(const BlockArgs& a, blk_t n) {
-  __shared__ int s_go;
-  if (threadIdx.x == 0) {
-    unsigned long long v;
-    for (;;) {
-      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(a.doorbell) : "memory");
-      if (v >= n + 1) break;
-      __nanosleep(32);
-    }
-    s_go = v != kDoorbellCancel;
-    if (!s_go) a.st->cancel = 1u;
-  }
-  __syncthreads();
-  return s_go;
-}
-
 __global__ void __launch_bounds__(kFrontThreads) k_front(BlockArgs a) {
   extern __shared__ float4 smem4[];
-  if (a.front_head && !a.doorbell) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (a.front_head) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const blk_t n = a.st->block;
-  if (a.doorbell) {
-    // armed: k_back (our programmatic dependent) may start only once the
-    // block is real, so it is released after the doorbell
-    if (!await_doorbell(a, n)) return;
-    if (a.front_head) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  }
   trace_begin(a, TR_FRONT, n);
   const int nerr = (a.front_head && a.is_aur && a.nlms) ? a.P : 0;
   const int nfront = (int)gridDim.x - nerr;

@@ -16,7 +16,6 @@ void shard_alloc(aura_b200_engine* e, int world, int rank) {
   if (world < 2 || world > kMaxShards || rank < 0 || rank >= world)
     fail(AURA_B200_E_INVALID_ARGUMENT, "shard world must be 2..8 and 0 <= rank < world");
   if (e->xbuf || e->args.xchg) fail(AURA_B200_E_INVALID_ARGUMENT, "engine is already sharded");
-  if (e->launch_mode == 2) fail(AURA_B200_E_INVALID_ARGUMENT, "leave the armed launch mode before sharding");
   if (e->blocks) fail(AURA_B200_E_INVALID_ARGUMENT, "shard before the first block");
   CK(cudaSetDevice(e->device));
   const size_t S = e->P * e->N + 2 * e->N;
@@ -39,7 +38,6 @@ void nccl_connect(aura_b200_engine* e, int world, int rank, const void* id) {
     fail(AURA_B200_E_INVALID_ARGUMENT, "shard world must be 1..8 and 0 <= rank < world");
   if (e->args.xchg) fail(AURA_B200_E_INVALID_ARGUMENT, "engine is already sharded");
   if (e->blocks) fail(AURA_B200_E_INVALID_ARGUMENT, "shard before the first block");
-  if (e->launch_mode == 2) fail(AURA_B200_E_INVALID_ARGUMENT, "leave the armed launch mode before sharding");
   NcclApi& api = nccl_api();
   CK(cudaSetDevice(e->device));
   const size_t S = e->P * e->N + 2 * e->N;
@@ -57,7 +55,7 @@ void nccl_connect(aura_b200_engine* e, int world, int rank, const void* id) {
   a.grank = rank;
   a.xchg = 2;
   set_advance_total(e);
-  quiesce(e);
+  CK(cudaStreamSynchronize(e->stream));
   e->rebuild_graphs();
   BlockArgs d = a;
   d.out = e->d_out;
@@ -74,7 +72,7 @@ void shard_finalize(aura_b200_engine* e, char* const* peers) {
   a.xchg = 1;
   for (int g = 0; g < kMaxShards; ++g) a.xpeer[g] = g < e->G ? peers[g] : nullptr;
   set_advance_total(e);
-  quiesce(e);
+  CK(cudaStreamSynchronize(e->stream));
   e->rebuild_graphs();
   BlockArgs d = a;
   d.out = e->d_out;

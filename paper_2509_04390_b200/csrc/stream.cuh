@@ -195,7 +195,6 @@ __device__ __forceinline__ void back_produce(const BlockArgs& a, blk_t n, uint64
     if (PT > 0 && kind == 1 && !waited) {
       griddep_wait();  // canceller inputs come from the head
       waited = true;
-      if (a.doorbell && *reinterpret_cast<volatile const uint32_t*>(&a.st->cancel)) break;  // called off
     }
     // per item: the input (synthesis) or loudspeaker (canceller) block b of
     // the first stage; stages never cross a block boundary
@@ -214,7 +213,6 @@ __device__ __forceinline__ void back_produce(const BlockArgs& a, blk_t n, uint64
       if (!front_ok && kind == 0 && t == b0) {
         griddep_wait();  // this stage reads X(age 0), pushed by the front
         front_ok = true;
-        if (a.doorbell && *reinterpret_cast<volatile const uint32_t*>(&a.st->cancel)) break;  // called off
       }
       mbar_wait(empty + s, par);
       meta[s] = StageMeta{idx, t, t1, (t1 == rec.z ? 1 : 0) | (kind << 1), tile, rec.w};
@@ -263,8 +261,6 @@ __device__ __forceinline__ void back_produce(const BlockArgs& a, blk_t n, uint64
         have_next = true;
       }
     }
-    if (a.doorbell && (waited || front_ok) && *reinterpret_cast<volatile const uint32_t*>(&a.st->cancel))
-      break;  // armed block called off: no more work (partials already written are scratch)
     if (!have_next && nidx >= 0) nrec = a.chunks[nidx];
     idx = nidx;
     rec = nrec;
@@ -757,20 +753,16 @@ __global__ void __launch_bounds__(kReduceThreads) k_reduce(const __grid_constant
   const blk_t n = a.st->block;
   const int4 ti = reduce_tile_info(a, blockIdx.x);
   griddep_wait();  // k_back's partials
-  // armed launch mode: a block called off before it started does nothing
-  const bool cancelled = a.doorbell && *reinterpret_cast<volatile const uint32_t*>(&a.st->cancel);
   trace_begin(a, TR_REDUCE, n);
-  if (!cancelled) reduce_part(a, blockIdx.x, n, rsm, &s_last, Cta(), ti);
+  reduce_part(a, blockIdx.x, n, rsm, &s_last, Cta(), ti);
   trace_end(a, TR_REDUCE, n);
-  // retire: advance the block (sharded: k_afc_finish does); a cancelled
-  // block is not one -- clear the mark instead
+  // retire: advance the block (sharded: k_afc_finish does)
   if (threadIdx.x == 0) {
     unsigned* t = a.tick + 1;
     if (atomicAdd(t, 1u) == gridDim.x - 1u) {
       *t = 0u;
       if (a.front_seq) a.front_seq[n & 1u] = 0ull;  // every producer of block n is past its hold
-      if (cancelled) a.st->cancel = 0u;
-      else if (a.xchg == 0) a.st->block = n + 1;
+      if (a.xchg == 0) a.st->block = n + 1;
     }
   }
 }

@@ -148,58 +148,3 @@ def test_measurement_entry_points_run_and_leave_the_stream_consistent():
     b.reset()
     for i in range(8):
         assert np.array_equal(a.process(mics[i]), b.process(mics[i]))
-
-
-@pytest.mark.parametrize("kind", ["auralizer", "convolver"])
-def test_armed_mode_is_bit_identical_and_cancellable(kind):
-    """Launch mode 2 (the next block's graph pre-launched, its k_front
-    waiting for the doorbell): bit-identical to the graph mode through
-    process(), feedback_estimate() and reset() (which call the armed block
-    off), mode switches mid-stream, and an engine destroyed while armed."""
-    rng = np.random.default_rng(41)
-    N, L = 64, 8
-    if kind == "auralizer":
-        mk, _ = small_aur(0.02)
-        a, b, c = mk(), mk(), mk()
-    else:
-        f = decaying_filters(rng, L, 20 * N)
-        mk = lambda: A.Convolver(list(f), A.make_config(48000, N, 1, L))
-        a, b, c = mk(), mk(), mk()
-    a.set_launch_mode(2)
-    mics = rng.standard_normal((30, 1, N)).astype(np.float32)
-    for i in range(30):
-        if i == 20:
-            a.set_launch_mode(0)
-        if i == 25:
-            a.set_launch_mode(2)
-        assert np.array_equal(a.process(mics[i]), b.process(mics[i])), i
-        if kind == "auralizer" and i % 7 == 3:
-            assert np.array_equal(a.feedback_estimate(), b.feedback_estimate()), i
-    a.reset()
-    b.reset()
-    for i in range(5):
-        assert np.array_equal(a.process(mics[i]), b.process(mics[i]))
-    if kind == "auralizer":
-        assert np.array_equal(a.coeffs(), b.coeffs())
-    c.set_launch_mode(2)
-    c.process(mics[0])
-    c.close()  # armed: the pre-launched block is called off, no hang
-
-
-def test_armed_mode_paced_latency():
-    """On the real-time grid the armed mode takes the graph launch off the
-    user-visible path: report both (c3-like shape, 64 loudspeakers)."""
-    N, L = 64, 64
-    rng = np.random.default_rng(43)
-    synth = decaying_filters(rng, L, 200 * N)
-    fc = decaying_filters(rng, L, 20 * N, scale=0.1)
-    e = A.Auralizer(list(synth), list(fc), A.make_config(48000, N, 1, L), afc=A.AfcParams(0.005, 0.9, None))
-    mic = rng.standard_normal((64, 1, N)).astype(np.float32)
-    res = {}
-    for mode in (0, 2, 0, 2):
-        e.set_launch_mode(mode)
-        e.time_host_blocks(mic, 50, pace_us=1333.33)
-        us = e.time_host_blocks(mic, 400, pace_us=1333.33)
-        res.setdefault(mode, []).append(float(np.median(us)))
-    print("paced process() p50 us, graph vs armed:", res)
-    assert min(res[2]) < 1000 and min(res[0]) < 1000
