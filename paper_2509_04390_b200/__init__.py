@@ -326,8 +326,8 @@ class _Engine:
         return out.view(np.complex64)
 
     TRACE_KERNELS = ("k_front", "k_back_head", "k_back", "k_reduce", "afc_done", "k_afc_finish",
-                     "output", "afc_summed", "afc_c2r", "front_x")
-    _TRACE_SLOTS = 11  # kTraceKernels: the last slot is the next block's front start
+                     "output", "afc_summed", "afc_c2r", "front_x", "afc_wait")
+    _TRACE_SLOTS = 12  # kTraceKernels: the last slot is the next block's front start
 
     def trace_blocks(self, blocks: int = 32, host_inputs: Optional[np.ndarray] = None):
         """Per-kernel [start, end] (us from the block's front start) of

@@ -32,12 +32,13 @@ struct DevState {
 // Optional timeline trace (%globaltimer, ns): per traced block slot and
 // kernel, the earliest CTA start and the latest CTA end.
 constexpr int kTraceBlocks = 64;
-constexpr int kTraceKernels = 11;  // the last slot carries the next block's front start (cycle)
+constexpr int kTraceKernels = 12;  // the last slot carries the next block's front start (cycle)
 enum TraceId {
   TR_FRONT = 0, TR_BACK_HEAD, TR_BACK, TR_REDUCE, TR_AFC_DONE, TR_AFC_FINISH, TR_OUTPUT,
   TR_AFC_SUMMED,  // k_reduce: the canceller's split-K sums are in (the CTA that runs the c2r)
   TR_AFC_C2R,     // k_reduce: f^ written (before the power update)
-  TR_FRONT_X      // k_front: this block's input spectra computed and pushed (per front CTA)
+  TR_FRONT_X,     // k_front: this block's input spectra computed and pushed (per front CTA)
+  TR_AFC_WAIT     // k_reduce's early canceller CTA: {resident, partials published}
 };
 
 // Loudspeaker-channel sharding: at most kMaxShards engines
@@ -84,6 +85,10 @@ struct BlockArgs {
   int red_syn_ctas, red_syn_cpt;  // k_reduce: synthesis CTAs, CTAs per tile
   int red_afc_ctas, red_afc_cpt;  // canceller CTAs, CTAs per column tile
   int red_afc_rows;               // canceller partial rows: P (+1 power row with NLMS)
+  // single-CTA canceller reduction that starts before k_back ends: per
+  // canceller partial, (block + 1) once k_back has published it; k_reduce's
+  // canceller CTA (index 0) waits on these words instead of on all of k_back
+  blk_t* afc_seq;
   float* hist1;                 // second window-history buffer (the first is prev_in)
   // front CTA b publishes (block + 1) in out_flag[b] (mapped host memory)
   // once it is done with the block's input and its outputs are written --
@@ -148,7 +153,8 @@ __host__ __device__ inline size_t front_warps_f2(int N, int Qs, int W) {
 
 // ---- k_back (stream.cuh)
 constexpr int kConsumers = 256;                 // 8 consumer warps
-constexpr int kBackThreads = kConsumers + 32;   // + the producer warp
+constexpr int kBackThreads = kConsumers + 64;   // + the producer warp + the signal warp
+constexpr int kSigSlots = 4;                    // consumers -> signal warp hand-off ring
 constexpr int kMaxStages = 8;
 constexpr int kBackBarrierBytes = 512;          // mbarriers + stage metadata at the start of smem
 

@@ -294,6 +294,9 @@ int aura_b200_time_phase(aura_b200_engine* e, int phase, size_t reps, float* avg
     // single launches, back to back without programmatic overlap, so the
     // mean is one launch's duration (ramp-up and tail included)
     BlockArgs a = e->dev_args;
+    // k_reduce alone: its canceller CTA cannot wait for k_back's published
+    // partials (k_back does not run), so it takes the griddepcontrol path
+    if (phase == PH_REDUCE) a.afc_seq = nullptr;
     e->pdl_off = true;
     e->launch_phase(phase, a, e->stream);  // warm
     cudaEvent_t t0, t1;

@@ -426,6 +426,15 @@ void plan_back(aura_b200_engine* e, BlockArgs& a) {
   a.red_afc_cpt = U > 0 ? cpt_for(a.red_afc_rows * CT, max_afc) : 1;
   if (U > 0 && CTn == 1 && max_afc <= afc_single_cap(a.red_afc_rows, CT)) a.red_afc_cpt = 1;
   a.red_afc_ctas = U > 0 ? CTn * a.red_afc_cpt : 0;
+  // the single canceller CTA (reduce_part) starts as soon as k_back has
+  // published the canceller partials, off the end-of-block critical path
+  a.afc_seq = nullptr;
+  e->n_afc_seq = 0;
+  if (U > 0 && a.red_afc_ctas == 1 && afc_ys_f4((int)N, P) > 0 && knob_i(e, "AFC_EARLY", 1)) {
+    e->n_afc_seq = (size_t)std::max(slot_afc, 1);
+    a.afc_seq = dalloc<blk_t>(e->n_afc_seq, e->dmem);
+    CK(cudaMemset(a.afc_seq, 0, e->n_afc_seq * sizeof(blk_t)));
+  }
   e->smem_reduce = 16 * reduce_smem_f4(N, e->aur, P);
   raise_smem_limit(k_reduce, e->smem_reduce);
   // tickets: [0] canceller CTAs of k_reduce, [1] all k_reduce CTAs, [2] work
@@ -581,6 +590,7 @@ void reset_state(aura_b200_engine* e) {
   cudaStream_t s = e->stream;
   CK(cudaStreamSynchronize(s));
   CK(cudaMemsetAsync(a.st, 0, sizeof(DevState), s));
+  if (a.afc_seq) CK(cudaMemsetAsync(a.afc_seq, 0, e->n_afc_seq * sizeof(blk_t), s));
   CK(cudaMemsetAsync(a.prev_in, 0, sizeof(float) * e->Qx * N, s));
   if (a.hist1) CK(cudaMemsetAsync(a.hist1, 0, sizeof(float) * e->Qx * N, s));
   if (a.front_seq) CK(cudaMemsetAsync(a.front_seq, 0, 2 * sizeof(unsigned long long), s));

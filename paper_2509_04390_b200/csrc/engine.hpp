@@ -217,6 +217,7 @@ struct aura_b200_engine {
   int back_ctas = 0;
   size_t smem_back = 0, smem_reduce = 0;
   size_t n_syn_segs = 0, n_afc_segs = 0;
+  size_t n_afc_seq = 0;  // words of args.afc_seq (early canceller reduction)
   std::vector<int4> h_chunks;  // host copy of the k_back work queue (diagnostics)
   // sharding: shard grank of G; xbuf = own exchange buffer
   int G = 1, grank = 0;
@@ -349,6 +350,7 @@ struct aura_b200_engine {
         {a.part_syn, f4 * std::max<size_t>(1, n_syn_segs * LT * a.CT)},
         {a.front_seq, 2 * sizeof(unsigned long long)},
         {a.tick, 6 * sizeof(unsigned)}};
+    if (a.afc_seq) v.push_back({a.afc_seq, n_afc_seq * sizeof(blk_t)});
     if (aur) {
       v.push_back({a.prev_spk, fl * L * N});
       v.push_back({a.spk, fl * L * N});
@@ -401,7 +403,9 @@ inline uint64_t device_block_hint(aura_b200_engine* e) { return e->blocks + e->b
 // a coordinated reset of all shards.
 inline void check_shard_status(aura_b200_engine* e) {
   if (e->h_status && *reinterpret_cast<volatile unsigned*>(e->h_status))
-    fail(AURA_B200_E_TIMEOUT, "a shard peer missed the canceller exchange deadline (reset every shard)");
+    fail(AURA_B200_E_TIMEOUT, *reinterpret_cast<volatile unsigned*>(e->h_status) == 2u
+                                  ? "the canceller reduction timed out waiting for its partials (reset)"
+                                  : "a shard peer missed the canceller exchange deadline (reset every shard)");
 }
 
 // Spin until every k_front CTA has published `target` in its mapped word.

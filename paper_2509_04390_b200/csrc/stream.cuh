@@ -119,7 +119,13 @@ struct StageMeta {
   int tile;       // synthesis tile, or canceller column tile
   int slot;       // partial index (synthesis or canceller partials array)
 };
-static_assert(2 * kMaxStages * 8 + kMaxStages * sizeof(StageMeta) <= kBackBarrierBytes,
+// The consumers hand each published canceller partial to the signal warp
+// through a small ring (afc_seq mode): {full, empty} mbarriers + the slot.
+struct SigRing {
+  uint64_t full[kSigSlots], empty[kSigSlots];
+  int slot[kSigSlots];
+};
+static_assert(2 * kMaxStages * 8 + kMaxStages * sizeof(StageMeta) + sizeof(SigRing) <= kBackBarrierBytes,
               "barrier + metadata region");
 
 // Rows v = vlo..vhi (vlo may be < 0: ring wrap) of a ring of `cap` rows of
@@ -307,13 +313,28 @@ __device__ __forceinline__ void team_partial(float4 (&acc)[RM], int R, int CT, i
 // Warps 0-7: consume this CTA's stages of block n until the producer's
 // sentinel (q is the CTA's running stage count, shared with the producer's
 // by construction), leaving one split-K partial per work item.
+// Consumer thread 0 -> signal warp: the canceller partial `slot` is stored
+// (every consumer's stores precede the barrier that ended team_partial, and
+// the arrive releases them at CTA scope). The signal warp makes them visible
+// GPU-wide and publishes afc_seq[slot], so no consumer waits for that fence
+// (a fence in a consumer warp waits for its in-flight W stores: ~1 us of
+// k_back per canceller item). slot < 0: no more items.
+__device__ __forceinline__ void sig_post(SigRing* r, uint32_t& k, int slot) {
+  const int i = (int)(k % kSigSlots);
+  mbar_wait(&r->empty[i], ((k / kSigSlots) & 1u) ^ 1u);
+  r->slot[i] = slot;
+  mbar_arrive(&r->full[i]);
+  ++k;
+}
+
 template <int LT, bool ELEM, int PT>
 __device__ __forceinline__ void back_consume(const BlockArgs& a, blk_t n, uint64_t* full,
                                              uint64_t* empty, StageMeta* meta, float4* red,
-                                             float4* slots, uint32_t& q, unsigned long long* ctr) {
+                                             float4* slots, uint32_t& q, unsigned long long* ctr,
+                                             SigRing* sig) {
+  uint32_t sq = 0;  // hand-offs posted (thread 0)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int S = a.stages;
-  (void)n;
   // consumer geometry: lane = pl * 8 + cl ; warp = pg * CG + cg
   const int CT = a.CT, CTn = a.CTn, KF = a.KF;
   const int CG = CT >> 3, PG = 8 / CG, PH = PG * 4;
@@ -344,6 +365,7 @@ __device__ __forceinline__ void back_consume(const BlockArgs& a, blk_t n, uint64
     if (m.item < 0) {  // sentinel: release its slot too
       __syncwarp();
       if (lane == 0) mbar_arrive(empty + sl);
+      if (sig && threadIdx.x == 0) sig_post(sig, sq, -1);
       break;
     }
     if (ctr && q == 0 && threadIdx.x == 0) ctr[1] = globaltimer();
@@ -494,6 +516,7 @@ __device__ __forceinline__ void back_consume(const BlockArgs& a, blk_t n, uint64
       // rows 0..P-1: the mics; row P: the loudspeaker power (accumulator PA)
       team_partial<PA + 1>(aac, R, CT, PG, pg, f, pl, red, a.part_afc + (size_t)slot * E,
                            [&](int r) { return r < P ? r : (r == PA && nl) ? P : -1; });
+      if (sig && threadIdx.x == 0) sig_post(sig, sq, slot);
       if (a.seg_trace && threadIdx.x == 0) a.seg_trace[4 * (size_t)item + 1] = globaltimer();
     }
     if (a.seg_trace && threadIdx.x == 0) {
@@ -514,6 +537,8 @@ __global__ void __launch_bounds__(kBackThreads, 1) k_back(const __grid_constant_
   uint64_t* full = reinterpret_cast<uint64_t*>(bsm);
   uint64_t* empty = full + kMaxStages;
   StageMeta* meta = reinterpret_cast<StageMeta*>(empty + kMaxStages);
+  SigRing* ring = reinterpret_cast<SigRing*>(meta + kMaxStages);
+  SigRing* sig = PT > 0 && a.afc_seq ? ring : nullptr;
   float4* red = reinterpret_cast<float4*>(bsm + kBackBarrierBytes);
   float4* slots = red + a.red_f4;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -522,6 +547,10 @@ __global__ void __launch_bounds__(kBackThreads, 1) k_back(const __grid_constant_
     for (int s = 0; s < S; ++s) {
       mbar_init(full + s, 1);
       mbar_init(empty + s, kConsumers / 32);
+    }
+    for (int i = 0; i < kSigSlots; ++i) {
+      mbar_init(&ring->full[i], 1);
+      mbar_init(&ring->empty[i], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -547,13 +576,29 @@ __global__ void __launch_bounds__(kBackThreads, 1) k_back(const __grid_constant_
     }
     return;
   }
+  if (warp == kConsumers / 32 + 1) {
+    // signal warp: publish each canceller partial the consumers hand over
+    // (k_reduce's early canceller CTA waits for these words)
+    if (sig && lane == 0) {
+      for (uint32_t k = 0;; ++k) {
+        const int i = (int)(k % kSigSlots);
+        mbar_wait(&sig->full[i], (k / kSigSlots) & 1u);
+        const int slot = sig->slot[i];
+        mbar_arrive(&sig->empty[i]);
+        if (slot < 0) break;
+        __threadfence();
+        *reinterpret_cast<volatile blk_t*>(a.afc_seq + slot) = n + 1;
+      }
+    }
+    return;
+  }
   if (a.trace && threadIdx.x == 0)
     atomicMin(&a.trace[((n % kTraceBlocks) * kTraceKernels + TR_BACK) * 2], globaltimer());
   unsigned long long* ctr = a.seg_trace ? a.seg_trace + 4 * (size_t)a.n_chunks + 3 * blockIdx.x : nullptr;
   if (ctr && threadIdx.x == 0) ctr[0] = globaltimer();
 
   uint32_t q = 0;
-  back_consume<LT, ELEM, PT>(a, n, full, empty, meta, red, slots, q, ctr);
+  back_consume<LT, ELEM, PT>(a, n, full, empty, meta, red, slots, q, ctr, sig);
   if (ctr && threadIdx.x == 0) ctr[2] = globaltimer();
   if (threadIdx.x == 0) {
     if (a.trace) atomicMax(&a.trace[((n % kTraceBlocks) * kTraceKernels + TR_BACK) * 2 + 1], globaltimer());
@@ -748,14 +793,44 @@ __global__ void __launch_bounds__(kReduceThreads) k_reduce(const __grid_constant
   extern __shared__ float4 rsm[];  // reduce_smem_f4(N, aur) float4
   __shared__ int s_last;
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  reduce_prefetch(a, blockIdx.x, rsm, Cta());
+  // early canceller (afc_seq): the single canceller CTA is index 0, so it is
+  // the first to take an SM that k_back leaves, and it waits for the
+  // canceller partials themselves -- which are done well before the
+  // synthesis stream ends -- instead of for the whole of k_back
+  const bool early = a.afc_seq != nullptr;
+  const int b = !early ? (int)blockIdx.x : blockIdx.x == 0 ? a.red_syn_ctas : (int)blockIdx.x - 1;
+  reduce_prefetch(a, b, rsm, Cta());
   // neither is written by k_back: load them before waiting for it
   const blk_t n = a.st->block;
-  const int4 ti = reduce_tile_info(a, blockIdx.x);
-  griddep_wait();  // k_back's partials
+  const int4 ti = reduce_tile_info(a, b);
+  const bool afc_early = early && b == a.red_syn_ctas;
+  if (afc_early) {
+    const unsigned long long t0 = globaltimer();
+    if (a.trace && threadIdx.x == 0) a.trace[((n % kTraceBlocks) * kTraceKernels + TR_AFC_WAIT) * 2] = t0;
+    bool late = false;
+    for (int i = threadIdx.x; i < ti.y; i += kReduceThreads) {
+      const volatile blk_t* w = a.afc_seq + ti.x + i;
+      while (*w != n + 1) {
+        if (globaltimer() - t0 > 2000000000ull) {  // bounded: a lost partial fails the next call
+          late = true;
+          break;
+        }
+        __nanosleep(64);
+      }
+    }
+    if (late) *reinterpret_cast<volatile unsigned*>(a.status_host) = 2u;
+    __threadfence();
+    __syncthreads();
+    if (a.trace && threadIdx.x == 0)
+      a.trace[((n % kTraceBlocks) * kTraceKernels + TR_AFC_WAIT) * 2 + 1] = globaltimer();
+  } else {
+    griddep_wait();  // k_back's partials
+  }
   trace_begin(a, TR_REDUCE, n);
-  reduce_part(a, blockIdx.x, n, rsm, &s_last, Cta(), ti);
+  reduce_part(a, b, n, rsm, &s_last, Cta(), ti);
   trace_end(a, TR_REDUCE, n);
+  // this grid completes only after k_back (whose epilogue resets the queue)
+  if (afc_early) griddep_wait();
   // retire: advance the block (sharded: k_afc_finish does)
   if (threadIdx.x == 0) {
     unsigned* t = a.tick + 1;

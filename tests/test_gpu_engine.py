@@ -148,3 +148,37 @@ def test_measurement_entry_points_run_and_leave_the_stream_consistent():
     b.reset()
     for i in range(8):
         assert np.array_equal(a.process(mics[i]), b.process(mics[i]))
+
+
+def test_early_canceller_reduction_is_bit_identical(monkeypatch):
+    """k_reduce's single canceller CTA normally starts as soon as k_back has
+    published the canceller partials (afc_seq words) instead of after all of
+    k_back. Same partials, same summation order: the stream must be
+    bit-identical to the griddepcontrol path (AURA_B200_AFC_EARLY=0), also
+    after a reset, which must clear the published words (block numbers
+    restart, so stale words would otherwise match)."""
+    rng = np.random.default_rng(11)
+    N, L = 64, 64
+    synth = decaying_filters(rng, L, 200 * N + 7, scale=0.5)
+    fc = decaying_filters(rng, L, 750 * N, scale=0.1)  # c3's canceller: 48k taps, 120 partials
+
+    def mk():
+        return A.Auralizer(list(synth), list(fc), A.make_config(48000, N, 1, L), input_gain=0.9,
+                           afc=A.AfcParams(0.005, 0.9, None))
+
+    on = mk()
+    monkeypatch.setenv("AURA_B200_AFC_EARLY", "0")
+    off = mk()
+    monkeypatch.delenv("AURA_B200_AFC_EARLY")
+    assert "AFC_EARLY=0" in off.describe() and "AFC_EARLY" not in on.describe()
+    mics = rng.standard_normal((40, 1, N)).astype(np.float32)
+    first = []
+    for b, m in enumerate(mics):
+        y = on.process(m)
+        assert np.array_equal(y, off.process(m)), b
+        assert np.array_equal(on.feedback_estimate(), off.feedback_estimate()), b
+        first.append(y)
+    assert np.array_equal(on.coeffs(), off.coeffs())
+    on.reset()
+    for b, m in enumerate(mics):
+        assert np.array_equal(on.process(m), first[b]), b

@@ -23,12 +23,6 @@ def run(name, eng, mic, blocks=200):
     eng.set_launch_mode(MODE)
     eng.time_device_blocks(20, mic)
     lat, us = eng.time_device_blocks(blocks, mic)
-    if MODE == 2:
-        ph = eng.loop_phases(blocks)
-        print(json.dumps({"case": name, "loop_phases_p50_us": {k: round(float(np.median(v)), 2)
-                                                              for k, v in ph.items()},
-                          "block_p50": float(np.median(us)), "block_p99": float(np.percentile(us, 99)),
-                          "latency_p50": float(np.median(lat))}), flush=True)
     tr = eng.trace_blocks(16)
     back = eng.time_phase("k_back", 20)
     byts = eng.profile_phases(5)["k_back"][1]
