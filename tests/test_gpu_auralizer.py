@@ -233,3 +233,30 @@ def test_engines_of_different_shapes_coexist():
     assert rel_err(np.stack(ys), g["y"]) <= TOL
     small.close()
     aur.close()
+
+
+@pytest.mark.parametrize("N,L", [(32, 2), (64, 8)])
+def test_nlms_adapts_closed_loop_like_the_oracle(N, L):
+    """The NLMS canceller has no reference implementation (parity is pinned
+    to the C oracle and its float64 restatement), so also check that it does
+    its job on the GPU: in a closed loop with true paths F and F^_0 = 0 it
+    suppresses the feedback (ERLE > 6 dB over the last 500 blocks, mu = 0
+    gives 0 dB), and its ERLE trajectory follows the C oracle's (every
+    250-block window within 0.2 dB)."""
+    from test_nlms_oracle import erle_run
+    rng = np.random.default_rng(4)
+    blocks = 1500
+    synth = decaying_filters(rng, L, 8 * N, scale=0.5)
+    F = decaying_filters(rng, L, 2 * N, t60_s=0.002, scale=0.3 / np.sqrt(L / 2)).astype(np.float64)
+    zero = np.zeros((L, 2 * N), np.float32)
+    kw = dict(mu=0.002, lam=0.9, delta=1.0)
+    g = gpu_aur(synth, zero, N, 1, L, **kw)
+    o = O.OracleAuralizer(synth, zero, N, 1, L, **kw)
+    fg, rg = erle_run(g, synth, F, N, blocks)
+    fo, ro = erle_run(o, synth, F, N, blocks)
+    erle = 10 * np.log10(fg[-500:].sum() / rg[-500:].sum())
+    assert erle > 6.0, erle
+    for w in range(0, blocks, 250):
+        eg = 10 * np.log10(fg[w:w + 250].sum() / rg[w:w + 250].sum())
+        eo = 10 * np.log10(fo[w:w + 250].sum() / ro[w:w + 250].sum())
+        assert abs(eg - eo) < 0.2, (w, eg, eo)
