@@ -19,6 +19,7 @@ struct AfcParams {
   float mu = 0.0f;
   float lambda = 0.9f;
   float delta = 0.0f;  // 0 -> 1e-6 * block_size
+  bool constrained = false;  // Appendix A step 2: constrained gradient
 };
 
 class Auralizer {
@@ -53,7 +54,8 @@ class Auralizer {
     const auto f = b200_detail::row_pointers(fc_filters);
     const auto c = b200_detail::to_c(cfg_);
     const aura_b200_afc p{afc.mu, afc.lambda,
-                          afc.delta > 0.0f ? afc.delta : 1e-6f * static_cast<float>(cfg_.block_size)};
+                          afc.delta > 0.0f ? afc.delta : 1e-6f * static_cast<float>(cfg_.block_size),
+                          afc.constrained ? 1 : 0};
     aura_b200_engine* e = nullptr;
     b200_detail::check(aura_b200_auralizer_create(&c, s.data(), s.size(),
                                                   synth_filters.front().size(), f.data(),

@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define AURA_B200_ABI_VERSION 1
+#define AURA_B200_ABI_VERSION 2
 
 /* 1 + aura::ErrorCode (engine.hpp:15-37), then GPU codes */
 enum aura_b200_status {
@@ -84,9 +84,12 @@ typedef struct {
 /* feedback-canceller adaptation. mu = 0 -> the
  * reference's fixed-F^ canceller (auralizer.hpp:34-37). */
 typedef struct {
-  float mu;     /* NLMS step */
-  float lambda; /* power forgetting factor */
-  float delta;  /* regulariser */
+  float mu;        /* NLMS step */
+  float lambda;    /* power forgetting factor */
+  float delta;     /* regulariser */
+  int constrained; /* != 0: constrained gradient (Appendix A step 2: c2r, keep
+                      the first N samples, r2c) -- the partitions stay linear
+                      convolutions; costs a pair of transforms per unit */
 } aura_b200_afc;
 
 /* ---- library ------------------------------------------------------- */

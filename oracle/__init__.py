@@ -75,6 +75,8 @@ def olib(f64=False):
         L.ao_aur_process.argtypes = [C.c_void_p, _f32p, _f32p]
         L.ao_aur_reset.argtypes = [C.c_void_p]
         L.ao_aur_set_gain.argtypes = [C.c_void_p, C_real]
+        L.ao_aur_set_constrained.argtypes = [C.c_void_p, C.c_int]
+        L.ao_aur_set_constrained.restype = C.c_int
         L.ao_aur_feedback_estimate.argtypes = [C.c_void_p, _f32p]
         L.ao_aur_fc_partitions.restype = _sz
         L.ao_aur_fc_partitions.argtypes = [C.c_void_p]
@@ -202,7 +204,7 @@ class OracleAuralizer:
     synth: (Q*L, n_h); fc: (P*L, n_hf) with P = Q."""
 
     def __init__(self, synth, fc, block, inputs, outputs, gain=1.0, mu=0.0,
-                 lam=0.9, delta=None, f64=False):
+                 lam=0.9, delta=None, f64=False, constrained=False):
         self.f64 = f64
         self.dt = np.float64 if f64 else np.float32
         s = np.ascontiguousarray(_f32(synth), self.dt)
@@ -219,6 +221,8 @@ class OracleAuralizer:
             raise ValueError("oracle rejected the auralizer configuration")
         self.fc_partitions = self._L.ao_aur_fc_partitions(self._h)
         self.synth_partitions = self._L.ao_aur_synth_partitions(self._h)
+        if constrained and self._L.ao_aur_set_constrained(self._h, 1) != 0:
+            raise MemoryError("oracle: constrained-update scratch")
 
     def process(self, mic):
         mic = np.ascontiguousarray(_f32(mic), self.dt).reshape(self.Q, self.N)

@@ -394,6 +394,9 @@ struct ao_aur {
   real* power;        /* bins */
   real* scale;        /* bins */
   real* fc_l;         /* L x N: per-loudspeaker canceller outputs */
+  int constrained;     /* Appendix A step 2, constrained gradient */
+  real* cwork;         /* per thread: G (bins cf), 2N window, N cf FFT scratch */
+  int cwork_threads;   /* threads cwork was sized for (the update loop uses no more) */
 };
 
 ao_aur* ao_aur_new(size_t N, size_t Q, size_t L, const real* synth,
@@ -433,12 +436,36 @@ void ao_aur_free(ao_aur* a) {
   ao_conv_free(a->synth);
   upols_free(&a->fc);
   free(a->W); free(a->fhat); free(a->mt); free(a->fc_out); free(a->ewin);
-  free(a->E); free(a->power); free(a->scale); free(a->fc_l);
+  free(a->E); free(a->power); free(a->scale); free(a->fc_l); free(a->cwork);
   free(a);
 }
 
+#define AO_CWORK(N) (6 * (N) + 2)  /* reals of constrained scratch per thread */
+
+/* The constrained gradient of one (p, l, k): G = scale (.) conj(x) E, then
+ * G' = r2c([first N samples of c2r(G), 0_N]) -- DftPlan::inverse_unchecked
+ * and DftPlan::forward (dft.hpp:69-153) -- and w += G'. */
+static void constrained_step(const ao_aur* a, const cf* x, cf* w, real* work) {
+  const size_t N = a->N, bins = a->bins;
+  cf* G = (cf*)work;
+  real* buf = work + 2 * bins;
+  cf* z = (cf*)(buf + 2 * N);
+  for (size_t j = 0; j < bins; ++j) {
+    const cf g = cmul(cconj(x[j]), a->E[j]);
+    G[j].re = a->scale[j] * g.re;
+    G[j].im = a->scale[j] * g.im;
+  }
+  inverse_w(a->fc.plan, (const real*)G, buf, z);
+  for (size_t i = N; i < 2 * N; ++i) buf[i] = 0.0f;
+  forward_w(a->fc.plan, buf, (real*)G, z);
+  for (size_t j = 0; j < bins; ++j) {
+    w[j].re += G[j].re;
+    w[j].im += G[j].im;
+  }
+}
+
 /* Appendix A step 2: W[p][l][k] += mu/(P+delta) * conj(X_l(age k)) E_p,
- * on the AFC FDL *before* X(l_n) is pushed. */
+ * on the AFC FDL *before* X(l_n) is pushed (constrained: see above). */
 static void nlms_update(ao_aur* a) {
   const size_t N = a->N, bins = a->bins, L = a->L, Kf = a->K_f;
   for (size_t j = 0; j < bins; ++j) a->scale[j] = a->mu / (a->power[j] + a->delta);
@@ -446,11 +473,16 @@ static void nlms_update(ao_aur* a) {
     memset(a->ewin, 0, sizeof(real) * N);
     memcpy(a->ewin + N, a->mt + p * N, sizeof(real) * N);
     ao_forward(a->fc.plan, a->ewin, (real*)a->E);
-#pragma omp parallel for schedule(static) if (L * Kf * bins >= AO_PAR_MIN_WORK)
+#pragma omp parallel for schedule(static) if (L * Kf * bins >= AO_PAR_MIN_WORK) \
+    num_threads(a->constrained ? a->cwork_threads : n_threads())
     for (size_t l = 0; l < L; ++l)
       for (size_t k = 0; k < Kf; ++k) {
         const cf* x = fdl_slot(&a->fc, l, k);
         cf* w = a->W + ((p * L + l) * Kf + k) * bins;
+        if (a->constrained) {
+          constrained_step(a, x, w, a->cwork + (size_t)thread_id() * AO_CWORK(N));
+          continue;
+        }
         for (size_t j = 0; j < bins; ++j) {
           const cf g = cmul(cconj(x[j]), a->E[j]);
           w[j].re += a->scale[j] * g.re;
@@ -458,6 +490,16 @@ static void nlms_update(ao_aur* a) {
         }
       }
   }
+}
+
+int ao_aur_set_constrained(ao_aur* a, int constrained) {
+  if (constrained && !a->cwork) {
+    a->cwork_threads = n_threads();
+    a->cwork = (real*)calloc((size_t)a->cwork_threads * AO_CWORK(a->N), sizeof(real));
+    if (!a->cwork) return -1;
+  }
+  a->constrained = constrained != 0;
+  return 0;
 }
 
 void ao_aur_process(ao_aur* a, const real* mic, real* spk) {

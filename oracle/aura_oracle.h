@@ -76,6 +76,12 @@ void ao_aur_free(ao_aur* a);
 void ao_aur_process(ao_aur* a, const ao_real* mic, ao_real* speakers);
 void ao_aur_reset(ao_aur* a);
 void ao_aur_set_gain(ao_aur* a, ao_real gain);
+/* SURVEY Appendix A step 2, optional constrained variant: per (p, l, k) the
+ * gradient mu/(P + delta) conj(X) E is taken to the time domain (c2r),
+ * its last N samples are zeroed (a partition's taps live in the first N),
+ * and it is transformed back (r2c) before it is added to W. Returns 0, or
+ * -1 when the scratch cannot be allocated. */
+int ao_aur_set_constrained(ao_aur* a, int constrained);
 void ao_aur_feedback_estimate(const ao_aur* a, ao_real* out /* P x N */);
 size_t ao_aur_fc_partitions(const ao_aur* a);
 size_t ao_aur_synth_partitions(const ao_aur* a);

@@ -143,7 +143,8 @@ class _Cfg(C.Structure):
 
 
 class _Afc(C.Structure):
-    _fields_ = [("mu", C.c_float), ("lambda_", C.c_float), ("delta", C.c_float)]
+    _fields_ = [("mu", C.c_float), ("lambda_", C.c_float), ("delta", C.c_float),
+                ("constrained", C.c_int)]
 
 
 _lib = None
@@ -326,8 +327,8 @@ class _Engine:
         return out.view(np.complex64)
 
     TRACE_KERNELS = ("k_front", "k_back_head", "k_back", "k_reduce", "afc_done", "k_afc_finish",
-                     "output", "afc_summed", "afc_c2r", "front_x", "afc_wait")
-    _TRACE_SLOTS = 12  # kTraceKernels: the last slot is the next block's front start
+                     "output", "afc_summed", "afc_c2r", "front_x", "afc_wait", "k_afc_constrain")
+    _TRACE_SLOTS = 13  # kTraceKernels: the last slot is the next block's front start
 
     def trace_blocks(self, blocks: int = 32, host_inputs: Optional[np.ndarray] = None):
         """Per-kernel [start, end] (us from the block's front start) of
@@ -505,10 +506,13 @@ class Convolver(_Engine):
 @dataclass
 class AfcParams:
     """Feedback-canceller adaptation; mu = 0 is the
-    reference's fixed canceller. delta None -> 1e-6 * N."""
+    reference's fixed canceller. delta None -> 1e-6 * N.
+    constrained: the constrained gradient of Appendix A step 2 (each
+    partition's update keeps only its first N taps)."""
     mu: float = 0.0
     lam: float = 0.9
     delta: Optional[float] = None
+    constrained: bool = False
 
 
 def default_delta(block_size: int) -> float:
@@ -541,7 +545,7 @@ class Auralizer(_Engine):
         device = backend.device if backend is not None else 0
         a = afc or AfcParams()
         delta = a.delta if a.delta is not None else default_delta(cfg.block_size)
-        pa = _Afc(a.mu, a.lam, delta)
+        pa = _Afc(a.mu, a.lam, delta, 1 if a.constrained else 0)
         h = C.c_void_p()
         _check(lib().aura_b200_auralizer_create(
             C.byref(_cfg(cfg)), _row_ptrs(srows), len(srows), srows[0].size,

@@ -32,13 +32,14 @@ struct DevState {
 // Optional timeline trace (%globaltimer, ns): per traced block slot and
 // kernel, the earliest CTA start and the latest CTA end.
 constexpr int kTraceBlocks = 64;
-constexpr int kTraceKernels = 12;  // the last slot carries the next block's front start (cycle)
+constexpr int kTraceKernels = 13;  // the last slot carries the next block's front start (cycle)
 enum TraceId {
   TR_FRONT = 0, TR_BACK_HEAD, TR_BACK, TR_REDUCE, TR_AFC_DONE, TR_AFC_FINISH, TR_OUTPUT,
   TR_AFC_SUMMED,  // k_reduce: the canceller's split-K sums are in (the CTA that runs the c2r)
   TR_AFC_C2R,     // k_reduce: f^ written (before the power update)
   TR_FRONT_X,     // k_front: this block's input spectra computed and pushed (per front CTA)
-  TR_AFC_WAIT     // k_reduce's early canceller CTA: {resident, partials published}
+  TR_AFC_WAIT,    // k_reduce's early canceller CTA: {resident, partials published}
+  TR_AFC_CONS     // k_afc_constrain (constrained NLMS gradient)
 };
 
 // Loudspeaker-channel sharding: at most kMaxShards engines
@@ -57,6 +58,7 @@ struct BlockArgs {
   int K, KF;         // synth partitions, canceller partitions
   int mode;          // 0 broadcast, 1 elementwise, 2 mimo
   int is_aur, nlms;
+  int afc_cons;      // constrained NLMS gradient (k_afc_constrain updates W; k_back only filters)
   float gain, mu, lambda, delta;
   int cpb;           // output channels per front CTA
   int front_pre;     // k_front stages its first channel's S and H0 up front
@@ -157,6 +159,12 @@ constexpr int kBackThreads = kConsumers + 64;   // + the producer warp + the sig
 constexpr int kSigSlots = 4;                    // consumers -> signal warp hand-off ring
 constexpr int kMaxStages = 8;
 constexpr int kBackBarrierBytes = 512;          // mbarriers + stage metadata at the start of smem
+
+// ---- k_afc_constrain (kernels.cuh): one warp per canceller unit (p, l, k)
+constexpr int kConsThreads = 128;
+// Shared-memory bytes per warp: the gradient spectrum (N float2), the 2N
+// window and the FFT scratch (N float2).
+__host__ __device__ inline size_t cons_smem_per_warp(int N) { return (size_t)N * 24; }
 
 // ---- k_reduce (stream.cuh)
 constexpr int kReduceThreads = 256;

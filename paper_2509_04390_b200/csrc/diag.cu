@@ -470,12 +470,12 @@ int aura_b200_describe(const aura_b200_engine* e, char* buf, size_t cap) {
                   "N=%zu Q=%zu L=%zu P=%zu K=%zu KF=%zu mode=%d LT=%d PT=%d | front: grid=%zu cpb=%d "
                   "warps=%d smem=%zu | back: ctas=%d x %d thr, CT=%d CTn=%d sp=%d spa=%d stages=%d slot=%d B "
                   "smem=%zu partials=%zu+%zu items=%d (static %d) w_l2=%d | reduce: %d+%d ctas l2keep=%d "
-                  "nlms=%d delta=%g knobs=%s",
+                  "nlms=%d cons=%d delta=%g knobs=%s",
                   e->N, e->Q, e->L, e->P, e->K, e->KF, e->mode, e->LT, e->PT,
                   (e->L + a.cpb - 1) / a.cpb, a.cpb, a.front_warps, e->smem_front, e->back_ctas, kBackThreads, a.CT,
                   a.CTn, a.sp, a.spa, a.stages, a.slot_f4 * 16, e->smem_back, e->n_syn_segs,
                   e->n_afc_segs, a.n_chunks, a.n_static, a.w_in_l2, a.red_syn_ctas, a.red_afc_ctas, a.h_in_l2,
-                  a.nlms, (double)a.delta, e->knobs.empty() ? "none" : e->knobs.c_str());
+                  a.nlms, a.afc_cons, (double)a.delta, e->knobs.empty() ? "none" : e->knobs.c_str());
   });
 }
 

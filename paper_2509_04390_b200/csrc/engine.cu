@@ -30,11 +30,13 @@ void aura_b200_engine::launch_phase(int ph, const BlockArgs& a, cudaStream_t s) 
     case PH_BACK_HEAD:
       if (has_head())
         k_back_head<<<(unsigned)(aur ? L + (a.nlms ? P : 0) : 1), kFrontThreads, smem_head, s>>>(a);
+      if (a.afc_cons)  // after the front (or head): E_p and the pushed canceller FDL row
+        launch_pdl(k_afc_constrain, (unsigned)cons_ctas, 32u * cons_warps, smem_cons, !pdl_off, a, s);
       break;
     case PH_BACK:
       if (has_back())
         launch_pdl(back_fn, (unsigned)back_ctas, kBackThreads, smem_back,
-                   (has_head() || front_head) && !pdl_off, a, s);
+                   (has_head() || front_head || a.afc_cons) && !pdl_off, a, s);
       break;
     case PH_REDUCE:
       if (has_back())
@@ -804,6 +806,19 @@ int aura_b200_auralizer_create(const aura_b200_config* cfg,
     a.lambda = afc ? afc->lambda : 0.9f;
     a.delta = afc ? afc->delta : kDefaultDeltaPerN * (float)N;
     a.nlms = mu > 0.0f;
+    a.afc_cons = a.nlms && afc->constrained != 0;
+    if (a.afc_cons) {
+      // one warp per canceller unit, up to 4 per CTA (fewer when a warp's
+      // transform scratch is large); enough CTAs to share the SMs with k_back
+      const size_t per_warp = cons_smem_per_warp((int)N);
+      e->cons_warps = (int)std::max<size_t>(1, std::min<size_t>(kConsThreads / 32, (227 * 1024) / per_warp));
+      e->smem_cons = (size_t)e->cons_warps * per_warp;
+      if (e->smem_cons > 227 * 1024)
+        fail(AURA_B200_E_INVALID_ARGUMENT, "block size too large for the constrained canceller update");
+      raise_smem_limit(k_afc_constrain, e->smem_cons);
+      const long long units = (long long)Q * L * (long long)e->KF;
+      e->cons_ctas = (int)std::min<long long>(2LL * e->sms, (units + e->cons_warps - 1) / e->cons_warps);
+    }
     e->w_elems = Q * L * e->KF * NF;
     a.W = dalloc<float4>(e->w_elems, e->dmem);
     {  // W [CTn][L*KF][P][CT], row p*L + l

@@ -227,6 +227,8 @@ struct aura_b200_engine {
   ncclComm_t nccl = nullptr;      // NCCL exchange (xchg 2)
   unsigned* h_status = nullptr;   // mapped pinned; set by k_afc_finish on timeout
   size_t smem_front = 0, smem_head = 0;
+  size_t smem_cons = 0;  // k_afc_constrain (constrained NLMS gradient)
+  int cons_ctas = 0, cons_warps = 0;
 
   ~aura_b200_engine() {
     cudaSetDevice(device);
@@ -280,7 +282,7 @@ struct aura_b200_engine {
   // kernels launched per block
   int launches_per_block() const {
     return 1 + (has_head() ? 1 : 0) + (has_back() ? 2 : 0) + (sharded() ? 1 : 0) +  // (+ NCCL's own)
-           (has_back() ? 0 : 1);
+           (has_back() ? 0 : 1) + (args.afc_cons ? 1 : 0);
   }
 
   // One graph per block: k_front, an external event node the host waits on

@@ -136,7 +136,9 @@ __device__ void rfft_packed(const float* win, float2* z, float2* spec, int N,
 // convolver.hpp:202-205), scaled by 1/(2N): store(i, x[N + i]).
 // dft.hpp:124-153 (merge, conj -> forward FFT -> conj, scale 1/half).
 // z: N float2 shared scratch. Ends with a barrier.
-template <typename Store, typename Team = Cta>
+// kHead: the FIRST N samples instead, store(i, x[i]) (the constrained
+// canceller gradient keeps those).
+template <typename Store, typename Team = Cta, bool kHead = false>
 __device__ void irfft_packed_tail(const float2* spec, float2* z, int N,
                                   int logN, const float2* __restrict__ tw,
                                   const float2* __restrict__ split,
@@ -169,9 +171,9 @@ __device__ void irfft_packed_tail(const float2* spec, float2* z, int N,
   tm.sync();
   fft_dit_smem(z, N, tw, tm);
   const float scale = 1.0f / (float)N;
-  // samples N .. 2N-1 are z[m] for m in [N/2, N)
+  // samples N .. 2N-1 are z[m] for m in [N/2, N) (samples 0 .. N-1: m < N/2)
   for (int m = tm.tid(); m < H; m += tm.size()) {
-    const float2 v = z[H + m];
+    const float2 v = z[kHead ? m : H + m];
     store(2 * m, __fmul_rn(v.x, scale));
     store(2 * m + 1, __fmul_rn(-v.y, scale));
   }
@@ -216,7 +218,7 @@ __device__ __forceinline__ void fft_dit_warp(float2 (&v)[PER], const float2* __r
 }
 
 // irfft_packed_tail on one warp with the transform in registers (N = 32 PER).
-template <int PER, typename Store>
+template <int PER, typename Store, bool kHead = false>
 __device__ __forceinline__ void irfft_packed_tail_reg(const float2* spec, int logN, const float2* __restrict__ tw,
                                                       const float2* __restrict__ split, Store store) {
   constexpr int N = 32 * PER, H = N / 2;
@@ -257,8 +259,8 @@ __device__ __forceinline__ void irfft_packed_tail_reg(const float2* spec, int lo
   fft_dit_warp<PER>(v, tw, lane);
   const float scale = 1.0f / (float)N;
 #pragma unroll
-  for (int r = PER / 2; r < PER; ++r) {  // samples N .. 2N-1 are z[m], m in [N/2, N)
-    const int m = lane + 32 * r - H;
+  for (int r = kHead ? 0 : PER / 2; r < (kHead ? PER / 2 : PER); ++r) {  // z[m], m in [N/2, N): samples N .. 2N-1
+    const int m = lane + 32 * r - (kHead ? 0 : H);
     store(2 * m, __fmul_rn(v[r].x, scale));
     store(2 * m + 1, __fmul_rn(-v[r].y, scale));
   }
@@ -310,6 +312,15 @@ __device__ __forceinline__ void irfft_warp_any(const float2* spec, float2* z, in
   if (N == 64) irfft_packed_tail_reg<2>(spec, logN, tw, split, store);
   else if (N == 128) irfft_packed_tail_reg<4>(spec, logN, tw, split, store);
   else irfft_packed_tail(spec, z, N, logN, tw, split, store, Warp());
+}
+// The first N samples of one warp's c2r (irfft_warp_any's head).
+template <typename Store>
+__device__ __forceinline__ void irfft_warp_head(const float2* spec, float2* z, int N, int logN,
+                                                const float2* __restrict__ tw, const float2* __restrict__ split,
+                                                Store store) {
+  if (N == 64) irfft_packed_tail_reg<2, Store, true>(spec, logN, tw, split, store);
+  else if (N == 128) irfft_packed_tail_reg<4, Store, true>(spec, logN, tw, split, store);
+  else irfft_packed_tail<Store, Warp, true>(spec, z, N, logN, tw, split, store, Warp());
 }
 __device__ __forceinline__ void rfft_warp_any(const float* win, float2* z, float2* spec, int N, int logN,
                                               const float2* __restrict__ tw, const float2* __restrict__ split) {

@@ -625,6 +625,81 @@ __global__ void __launch_bounds__(kTailThreads) k_afc_apply(BlockArgs a) {
   retire_block(a, n);
 }
 
+// -------------------------------------------------- k_afc_constrain
+// SURVEY Appendix A step 2, constrained variant (AfcParams.constrained): per
+// canceller unit (p, l, k) the NLMS gradient G = mu/(P + delta) (.) conj(X_l
+// (pre-push age k)) E_p -- rounded exactly as k_back's fused update and the
+// oracle (aura_oracle.c constrained_step) -- goes to the time domain (c2r),
+// its last N samples are dropped (a partition's taps are the first N of its
+// 2N window), and the r2c of [g, 0_N] is added to W. The transforms are the
+// bit-exact DftPlan ones (fft.cuh), one warp per unit. Runs after the front
+// (E_p, the pushed canceller FDL row) and before k_back, whose canceller
+// items then only filter with the updated W: k_front -PDL-> k_afc_constrain
+// -PDL-> k_back, so the synthesis stream starts while this kernel runs.
+// grid-stride over units; up to kConsThreads threads (fewer warps for large
+// N); dynamic smem: per warp cons_smem_per_warp(N).
+__global__ void __launch_bounds__(kConsThreads) k_afc_constrain(const __grid_constant__ BlockArgs a) {
+  extern __shared__ float4 csm4[];
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const int N = a.N, NF = a.NF, CT = a.CT, CTn = a.CTn, KF = a.KF, P = a.P, L = a.L;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float2* spec = reinterpret_cast<float2*>(reinterpret_cast<char*>(csm4) + (size_t)warp * cons_smem_per_warp(N));
+  float* win = reinterpret_cast<float*>(spec + N);
+  float2* z = reinterpret_cast<float2*>(win + 2 * N);
+  float4* spec4 = reinterpret_cast<float4*>(spec);
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // E_p and this block's canceller FDL row
+  const blk_t n = a.st->block;
+  trace_begin(a, TR_AFC_CONS, n);
+  const int cap = KF + 1;
+  const int nka = (int)(n % (blk_t)cap);
+  const long long U = (long long)L * KF;
+  const long long units = (long long)P * U;
+  const float4* pw4 = reinterpret_cast<const float4*>(a.pw);
+  const int warps = (int)(blockDim.x >> 5);
+  for (long long u = (long long)blockIdx.x * warps + warp; u < units; u += (long long)gridDim.x * warps) {
+    const int p = (int)(u / U);
+    const long long ul = u - (long long)p * U;  // l KF + k
+    const int l = (int)(ul / KF), k = (int)(ul - (long long)l * KF);
+    int slot = nka - k - 1;  // pre-push age k = post-push age k + 1
+    if (slot < 0) slot += cap;
+    for (int fg = lane; fg < NF; fg += 32) {
+      const int c = fg / CT, f = fg - c * CT;
+      const bool dc = fg == 0;
+      const float4 x1 = a.XA[((size_t)(l * CTn + c) * cap + slot) * CT + f];
+      const float4 ep = a.E[(size_t)p * NF + fg];
+      const float4 pw = pw4[fg];
+      const float4 st = make_float4(__fdiv_rn(a.mu, __fadd_rn(pw.x, a.delta)), __fdiv_rn(a.mu, __fadd_rn(pw.y, a.delta)),
+                                    __fdiv_rn(a.mu, __fadd_rn(pw.z, a.delta)), __fdiv_rn(a.mu, __fadd_rn(pw.w, a.delta)));
+      const float px = __fmul_rn(x1.x, ep.x), py = __fmul_rn(x1.y, ep.y);
+      float4 gr;
+      gr.x = dc ? px : __fadd_rn(px, py);
+      gr.y = dc ? py : __fsub_rn(__fmul_rn(x1.x, ep.y), __fmul_rn(x1.y, ep.x));
+      gr.z = __fadd_rn(__fmul_rn(x1.z, ep.z), __fmul_rn(x1.w, ep.w));
+      gr.w = __fsub_rn(__fmul_rn(x1.z, ep.w), __fmul_rn(x1.w, ep.z));
+      spec4[fg] = make_float4(__fmul_rn(st.x, gr.x), __fmul_rn(st.y, gr.y), __fmul_rn(st.z, gr.z),
+                              __fmul_rn(st.w, gr.w));
+    }
+    __syncwarp();
+    irfft_warp_head(spec, z, N, a.logN, a.tw, a.split, [&](int i, float x) { win[i] = x; });
+    for (int i = lane; i < N; i += 32) win[N + i] = 0.0f;
+    __syncwarp();
+    rfft_warp_any(win, z, spec, N, a.logN, a.tw, a.split);
+    for (int fg = lane; fg < NF; fg += 32) {
+      const int c = fg / CT, f = fg - c * CT;
+      float4* wp = a.W + ((size_t)c * U + ul) * P * CT + (size_t)p * CT + f;
+      const float4 g = spec4[fg];
+      float4 w = *wp;
+      w.x = __fadd_rn(w.x, g.x);
+      w.y = __fadd_rn(w.y, g.y);
+      w.z = __fadd_rn(w.z, g.z);
+      w.w = __fadd_rn(w.w, g.w);
+      *wp = w;
+    }
+    __syncwarp();  // spec is reused by the next unit
+  }
+  trace_end(a, TR_AFC_CONS, n);
+}
+
 // ------------------------------------------------------ k_partition
 // Setup (make_partitioned_filters, convolver.hpp:19-46) on the GPU: CTA
 // (k, r) transforms taps[r][kN .. kN+N) zero-padded to 2N and scatters the

@@ -445,22 +445,23 @@ __device__ __forceinline__ void back_consume(const BlockArgs& a, blk_t n, uint64
         // rows are oldest-first: unit i (age k0 + i) reads row amax - k0 - i
         const float4* xr = xs + (size_t)(amax - k0 - i0) * CT + f;
         const float4* wr = ws + (size_t)i0 * P * CT + f;
-        if (nl) {
-          if (k0 == 0 && i0 == 0 && i1 > 0) {  // packed |X_l(age 0)|^2, rounded as the oracle
-            const float4 xv = xr[0];
-            float4& pa = aac[PA];
-            if (dc) {
-              pa.x = __fadd_rn(pa.x, __fmul_rn(xv.x, xv.x));
-              pa.y = __fadd_rn(pa.y, __fmul_rn(xv.y, xv.y));
-            } else {
-              const float mm = __fadd_rn(__fmul_rn(xv.x, xv.x), __fmul_rn(xv.y, xv.y));
-              pa.x = __fadd_rn(pa.x, mm);
-              pa.y = __fadd_rn(pa.y, mm);
-            }
-            const float m2 = __fadd_rn(__fmul_rn(xv.z, xv.z), __fmul_rn(xv.w, xv.w));
-            pa.z = __fadd_rn(pa.z, m2);
-            pa.w = __fadd_rn(pa.w, m2);
+        if (nl && k0 == 0 && i0 == 0 && i1 > 0) {  // packed |X_l(age 0)|^2, rounded as the oracle
+          const float4 xv = xr[0];
+          float4& pa = aac[PA];
+          if (dc) {
+            pa.x = __fadd_rn(pa.x, __fmul_rn(xv.x, xv.x));
+            pa.y = __fadd_rn(pa.y, __fmul_rn(xv.y, xv.y));
+          } else {
+            const float mm = __fadd_rn(__fmul_rn(xv.x, xv.x), __fmul_rn(xv.y, xv.y));
+            pa.x = __fadd_rn(pa.x, mm);
+            pa.y = __fadd_rn(pa.y, mm);
           }
+          const float m2 = __fadd_rn(__fmul_rn(xv.z, xv.z), __fmul_rn(xv.w, xv.w));
+          pa.z = __fadd_rn(pa.z, m2);
+          pa.w = __fadd_rn(pa.w, m2);
+        }
+        // constrained variant: k_afc_constrain has already updated W
+        if (nl && !a.afc_cons) {
           float4* wg = a.W + ((size_t)c * U + m.t + i0) * P * CT + f;
           float4 xa = xr[0];
 #pragma unroll 4

@@ -5,8 +5,9 @@ import numpy as np
 
 
 class NlmsF64:
-    def __init__(self, synth, fc, N, Q, L, gain=1.0, mu=0.0, lam=0.9, delta=None):
+    def __init__(self, synth, fc, N, Q, L, gain=1.0, mu=0.0, lam=0.9, delta=None, constrained=False):
         self.N, self.Q, self.L = N, Q, L
+        self.constrained = constrained
         self.gain, self.mu, self.lam = gain, mu, lam
         self.delta = 1e-6 * N if delta is None else delta
         synth = np.asarray(synth, np.float64).reshape(Q, L, -1)
@@ -36,7 +37,12 @@ class NlmsF64:
         if self.mu != 0.0:
             E = np.fft.rfft(np.concatenate([np.zeros((self.Q, N)), mt], axis=1), axis=1)
             scale = self.mu / (self.power + self.delta)
-            self.W += scale * np.conj(self.Xa)[None] * E[:, None, None, :]
+            G = scale * np.conj(self.Xa)[None] * E[:, None, None, :]
+            if self.constrained:  # App. A step 2: keep the first N taps of the gradient
+                g = np.fft.irfft(G, n=2 * N, axis=-1)
+                g[..., N:] = 0.0
+                G = np.fft.rfft(g, axis=-1)
+            self.W += G
         self.win = np.concatenate([self.win[:, N:], mt], axis=1)
         self.Xin = np.concatenate([np.fft.rfft(self.win, axis=1)[:, None], self.Xin[:, :-1]], axis=1)
         Y = np.einsum("qkj,qlkj->lj", self.Xin, self.H)

@@ -24,7 +24,7 @@ def declared_symbols(path=HEADER):
 
 def test_library_built_and_loads():
     assert os.path.exists(A.LIB_PATH), "run __graft_entry__.build()"
-    assert A.lib().aura_b200_abi_version() == 1
+    assert A.lib().aura_b200_abi_version() == 2
 
 
 def test_every_declared_symbol_is_exported():

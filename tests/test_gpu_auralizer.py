@@ -14,10 +14,10 @@ pytestmark = pytest.mark.gpu
 TOL = 1e-5
 
 
-def gpu_aur(synth, fc, N, Q, L, gain=1.0, mu=0.0, lam=0.9, delta=None):
+def gpu_aur(synth, fc, N, Q, L, gain=1.0, mu=0.0, lam=0.9, delta=None, constrained=False):
     cfg = A.make_config(48000, N, Q, L, mimo=Q > 1)
     return A.Auralizer(list(synth), list(fc), cfg, input_gain=gain,
-                       afc=A.AfcParams(mu, lam, delta))
+                       afc=A.AfcParams(mu, lam, delta, constrained))
 
 
 @pytest.mark.parametrize("name", ["aur_n64", "aur_n32_gain", "aur_n128_long"])
@@ -260,3 +260,62 @@ def test_nlms_adapts_closed_loop_like_the_oracle(N, L):
         eg = 10 * np.log10(fg[w:w + 250].sum() / rg[w:w + 250].sum())
         eo = 10 * np.log10(fo[w:w + 250].sum() / ro[w:w + 250].sum())
         assert abs(eg - eo) < 0.2, (w, eg, eo)
+
+
+def w_tail_ratio(W, N):
+    """RMS of the second half of every W partition's 2N-point time window
+    against the first: 0 for spectra of N taps + N zeros."""
+    w = np.fft.irfft(np.asarray(W, np.complex128), n=2 * N, axis=-1)
+    return float(np.sqrt(np.sum(w[..., N:] ** 2) / np.sum(w[..., :N] ** 2)))
+
+
+@pytest.mark.parametrize("Q,L,N", [(1, 4, 64), (1, 16, 32), (4, 8, 64), (2, 5, 16),
+                                   (1, 4, 256), (4, 8, 128), (2, 8, 1024), (1, 2, 8192)])
+def test_constrained_nlms_vs_oracle(Q, L, N):
+    """Appendix A step 2's constrained gradient (k_afc_constrain: c2r, keep
+    the first N samples, r2c, one warp per unit): outputs, f^ and W after 200
+    blocks match the C oracle within 1e-5 of their RMS, and W stays the
+    spectrum of N taps + N zeros in every partition (the unconstrained
+    update does not)."""
+    rng = np.random.default_rng(Q * 1000 + L * 10 + N + 5)
+    synth = decaying_filters(rng, Q * L, 12 * N + 5, scale=0.5)
+    fc = decaying_filters(rng, Q * L, 4 * N + 1, scale=0.1)
+    kw = dict(gain=0.9, mu=0.01, lam=0.9, delta=1e-2 if N <= 64 else 1e-2 * 2 * N)
+    g = gpu_aur(synth, fc, N, Q, L, constrained=True, **kw)
+    assert "cons=1" in g.describe()
+    o = O.OracleAuralizer(synth, fc, N, Q, L, constrained=True, **kw)
+    u = gpu_aur(synth, fc, N, Q, L, **kw)
+    ys, yo, fg, fo = [], [], [], []
+    for _ in range(200):
+        m = rng.standard_normal((Q, N)).astype(np.float32)
+        ys.append(g.process(m))
+        yo.append(o.process(m))
+        u.process(m)
+        fg.append(g.feedback_estimate())
+        fo.append(o.feedback_estimate())
+    assert rel_err(np.stack(ys), np.stack(yo)) <= TOL
+    assert rel_err(np.stack(fg), np.stack(fo)) <= TOL
+    assert rel_err(g.coeffs(), o.coeffs()) <= TOL
+    assert w_tail_ratio(g.coeffs(), N) < 1e-5
+    assert w_tail_ratio(u.coeffs(), N) > 1e-3
+
+
+def test_constrained_c3_shape_vs_oracle():
+    """configs[2]'s shape (1 x 64, N = 64, 10 s synthesis, 1 s canceller)
+    with the constrained update: 100 blocks against the C oracle."""
+    N, L = 64, 64
+    rng = np.random.default_rng(77)
+    synth = decaying_filters(rng, L, 480000)
+    fc = decaying_filters(rng, L, 48000, t60_s=0.3, scale=0.1)
+    kw = dict(mu=0.005, lam=0.9, delta=1e-2 * 2 * N)
+    g = gpu_aur(synth, fc, N, 1, L, constrained=True, **kw)
+    o = O.OracleAuralizer(synth, fc, N, 1, L, constrained=True, **kw)
+    ys, yo = [], []
+    for _ in range(100):
+        m = rng.standard_normal((1, N)).astype(np.float32)
+        ys.append(g.process(m))
+        yo.append(o.process(m))
+    assert rel_err(np.stack(ys), np.stack(yo)) <= TOL
+    assert rel_err(g.feedback_estimate(), o.feedback_estimate()) <= TOL
+    assert rel_err(g.coeffs(), o.coeffs()) <= TOL
+    assert w_tail_ratio(g.coeffs(), N) < 1e-5

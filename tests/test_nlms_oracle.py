@@ -76,3 +76,54 @@ def test_nlms_adapts_closed_loop():
     fixed = O.OracleAuralizer(synth, zero, N, 1, L, mu=0.0)
     fb0, rr0 = erle_run(fixed, synth, F, N, 200)
     assert np.allclose(fb0, rr0)
+
+
+@pytest.mark.parametrize("Q,L,N", [(1, 3, 32), (2, 2, 16)])
+def test_constrained_c_oracle_matches_float64_restatement(Q, L, N):
+    """Appendix A step 2's constrained variant (c2r -> zero the last N
+    samples -> r2c of each gradient) in the C oracle vs numpy float64."""
+    rng = np.random.default_rng(Q * 10 + L + 7)
+    s = scaled_filters(rng, Q * L, 5 * N + 3, 0.5)
+    fc = scaled_filters(rng, Q * L, 3 * N + 2, 0.1)
+    kw = dict(gain=0.9, mu=0.05, lam=0.8, delta=1e-3, constrained=True)
+    c = O.OracleAuralizer(s, fc, N, Q, L, **kw)
+    d = NlmsF64(s, fc, N, Q, L, **kw)
+    for b in range(60):
+        m = rng.standard_normal((Q, N)).astype(np.float32)
+        assert rel_err(c.process(m), d.process(m)) < 1e-4, b
+        assert rel_err(c.feedback_estimate(), d.feedback_estimate()) < 1e-4, b
+    assert rel_err(c.coeffs(), d.W) < 1e-4
+
+
+def test_constrained_update_keeps_partitions_causal():
+    """The point of the constraint: every W partition stays the spectrum of
+    N taps followed by N zeros (as make_partitioned_filters builds it), so
+    the canceller stays a linear convolution; the unconstrained gradient
+    fills the second half with circular-correlation terms."""
+    rng = np.random.default_rng(12)
+    N, L = 32, 2
+    s = scaled_filters(rng, L, 6 * N, 0.5)
+    fc = scaled_filters(rng, L, 3 * N, 0.1)
+    tails = {}
+    for cons in (False, True):
+        c = O.OracleAuralizer(s, fc, N, 1, L, mu=0.05, lam=0.8, delta=1e-3, constrained=cons)
+        for _ in range(80):
+            c.process(rng.standard_normal((1, N)).astype(np.float32))
+        w = np.fft.irfft(c.coeffs().astype(np.complex128), n=2 * N, axis=-1)
+        tails[cons] = np.sqrt(np.sum(w[..., N:] ** 2) / np.sum(w[..., :N] ** 2))
+    assert tails[True] < 1e-5, tails
+    assert tails[False] > 1e-2, tails
+
+
+def test_constrained_nlms_adapts_closed_loop():
+    """The constrained canceller also suppresses closed-loop feedback it
+    starts blind to (same setup as test_nlms_adapts_closed_loop)."""
+    rng = np.random.default_rng(4)
+    N, L, blocks = 32, 2, 1500
+    synth = decaying_filters(rng, L, 8 * N, scale=0.5)
+    F = decaying_filters(rng, L, 2 * N, t60_s=0.002, scale=0.3).astype(np.float64)
+    zero = np.zeros((L, 2 * N), np.float32)
+    aur = O.OracleAuralizer(synth, zero, N, 1, L, mu=0.002, lam=0.9, delta=1.0, constrained=True)
+    fb, rr = erle_run(aur, synth, F, N, blocks)
+    erle = 10 * np.log10(fb[-500:].sum() / rr[-500:].sum())
+    assert erle > 6.0, erle
