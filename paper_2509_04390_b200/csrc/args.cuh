@@ -59,6 +59,8 @@ struct BlockArgs {
   int mode;          // 0 broadcast, 1 elementwise, 2 mimo
   int is_aur, nlms;
   int afc_cons;      // constrained NLMS gradient (k_afc_constrain updates W; k_back only filters)
+  int cons_prefetch; // k_afc_constrain: register prefetch of the next unit (N = 64, 128)
+  int cons_tables;   // k_afc_constrain: DftPlan tables staged in shared memory (all but the largest N)
   float gain, mu, lambda, delta;
   int cpb;           // output channels per front CTA
   int front_pre;     // k_front stages its first channel's S and H0 up front
@@ -161,10 +163,12 @@ constexpr int kMaxStages = 8;
 constexpr int kBackBarrierBytes = 512;          // mbarriers + stage metadata at the start of smem
 
 // ---- k_afc_constrain (kernels.cuh): one warp per canceller unit (p, l, k)
-constexpr int kConsThreads = 128;
+constexpr int kConsThreads = 64;  // small CTAs: three fit beside a k_back CTA (registers)
 // Shared-memory bytes per warp: the gradient spectrum (N float2), the 2N
 // window and the FFT scratch (N float2).
 __host__ __device__ inline size_t cons_smem_per_warp(int N) { return (size_t)N * 24; }
+// ... after the CTA's copy of the DftPlan tables (16-byte aligned)
+__host__ __device__ inline size_t cons_smem_tables(int N) { return ((size_t)table_f2(N) * 8 + 15) / 16 * 16; }
 
 // ---- k_reduce (stream.cuh)
 constexpr int kReduceThreads = 256;

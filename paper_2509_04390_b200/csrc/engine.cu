@@ -808,16 +808,22 @@ int aura_b200_auralizer_create(const aura_b200_config* cfg,
     a.nlms = mu > 0.0f;
     a.afc_cons = a.nlms && afc->constrained != 0;
     if (a.afc_cons) {
-      // one warp per canceller unit, up to 4 per CTA (fewer when a warp's
-      // transform scratch is large); enough CTAs to share the SMs with k_back
+      // one warp per canceller unit, two per CTA (one when a warp's transform
+      // scratch is large), 64 registers; 12 CTAs per SM (measured: 8 / 12 /
+      // 16 give a c3 block of 120.8 / 116.8 / 116.8 us)
       const size_t per_warp = cons_smem_per_warp((int)N);
-      e->cons_warps = (int)std::max<size_t>(1, std::min<size_t>(kConsThreads / 32, (227 * 1024) / per_warp));
-      e->smem_cons = (size_t)e->cons_warps * per_warp;
+      a.cons_tables = cons_smem_tables((int)N) + per_warp <= 227 * 1024;
+      const size_t tables = a.cons_tables ? cons_smem_tables((int)N) : 0;
+      e->cons_warps = (int)std::max<size_t>(1, std::min<size_t>(kConsThreads / 32, (227 * 1024 - tables) / per_warp));
+      e->smem_cons = tables + (size_t)e->cons_warps * per_warp;
       if (e->smem_cons > 227 * 1024)
         fail(AURA_B200_E_INVALID_ARGUMENT, "block size too large for the constrained canceller update");
       raise_smem_limit(k_afc_constrain, e->smem_cons);
       const long long units = (long long)Q * L * (long long)e->KF;
-      e->cons_ctas = (int)std::min<long long>(2LL * e->sms, (units + e->cons_warps - 1) / e->cons_warps);
+      if (units >= (1LL << 30)) fail(AURA_B200_E_INVALID_ARGUMENT, "too many canceller partitions for the constrained update");
+      a.cons_prefetch = knob_i(e.get(), "CONS_PREFETCH", 1);
+      const long long per_sm = std::max(1, knob_i(e.get(), "CONS_CTAS_PER_SM", 12));
+      e->cons_ctas = (int)std::min<long long>(per_sm * e->sms, (units + e->cons_warps - 1) / e->cons_warps);
     }
     e->w_elems = Q * L * e->KF * NF;
     a.W = dalloc<float4>(e->w_elems, e->dmem);

@@ -637,66 +637,142 @@ __global__ void __launch_bounds__(kTailThreads) k_afc_apply(BlockArgs a) {
 // items then only filter with the updated W: k_front -PDL-> k_afc_constrain
 // -PDL-> k_back, so the synthesis stream starts while this kernel runs.
 // grid-stride over units; up to kConsThreads threads (fewer warps for large
-// N); dynamic smem: per warp cons_smem_per_warp(N).
-__global__ void __launch_bounds__(kConsThreads) k_afc_constrain(const __grid_constant__ BlockArgs a) {
+// N); dynamic smem: the tables (cons_smem_tables), then per warp
+// cons_smem_per_warp(N).
+// The inputs of one unit as one lane holds them (PL float4 columns: NF = 32 PL).
+template <int PL>
+struct ConsIn {
+  float4 x1[PL], ep[PL], pw[PL], w[PL];
+};
+
+// Units u, u + stride, ... of one warp. PL > 0 (N = 64, 128): the next
+// unit's loads -- W included -- are issued before this unit's transforms, so
+// a warp waits on memory once per unit at most; PL = 0: any N, no prefetch.
+template <int PL>
+__device__ __forceinline__ void cons_units(const BlockArgs& a, int u, int stride, int nka,
+                                           float2* spec, float* win, float2* z, const float2* tw,
+                                           const float2* split) {
+  const int N = a.N, NF = a.NF, CT = a.CT, CTn = a.CTn, KF = a.KF, P = a.P;
+  const int lane = threadIdx.x & 31, cap = KF + 1;
+  // 32-bit unit arithmetic (the planner keeps P L K_f < 2^30): a 64-bit
+  // division is ~100 instructions, as many as a butterfly stage
+  const int U = a.L * KF, units = P * U;
+  const float4* pw4 = reinterpret_cast<const float4*>(a.pw);
+  float4* spec4 = reinterpret_cast<float4*>(spec);
+  constexpr int PLm = PL > 0 ? PL : 1;
+  // unit u -> mic p, unit within the mic ul = l KF + k, canceller FDL slot of
+  // the pre-push age k (= post-push age k + 1)
+  auto decode = [&](int v, int& p, int& ul, int& slot) {
+    p = v / U;
+    ul = v - p * U;
+    const int l = ul / KF, k = ul - l * KF;
+    slot = nka - k - 1;
+    if (slot < 0) slot += cap;
+    return l;
+  };
+  auto xa_at = [&](int l, int slot, int fg) -> const float4* {
+    const int c = fg / CT, f = fg - c * CT;
+    return a.XA + ((size_t)(l * CTn + c) * cap + slot) * CT + f;
+  };
+  auto w_at = [&](int p, int ul, int fg) -> float4* {
+    const int c = fg / CT, f = fg - c * CT;
+    return a.W + ((size_t)c * U + ul) * P * CT + (size_t)p * CT + f;
+  };
+  auto load = [&](int v, ConsIn<PLm>& in) {
+    int p, slot, ul;
+    const int l = decode(v, p, ul, slot);
+#pragma unroll
+    for (int r = 0; r < PLm; ++r) {
+      const int fg = lane + 32 * r;
+      in.x1[r] = *xa_at(l, slot, fg);
+      in.ep[r] = a.E[(size_t)p * NF + fg];
+      in.pw[r] = pw4[fg];
+      in.w[r] = *w_at(p, ul, fg);
+    }
+  };
+  // G = mu / (P + delta) (.) conj(x1) E, rounded as k_back's fused update
+  auto grad = [&](float4 x1, float4 ep, float4 pw, int fg) {
+    const bool dc = fg == 0;
+    const float4 st = make_float4(__fdiv_rn(a.mu, __fadd_rn(pw.x, a.delta)), __fdiv_rn(a.mu, __fadd_rn(pw.y, a.delta)),
+                                  __fdiv_rn(a.mu, __fadd_rn(pw.z, a.delta)), __fdiv_rn(a.mu, __fadd_rn(pw.w, a.delta)));
+    const float px = __fmul_rn(x1.x, ep.x), py = __fmul_rn(x1.y, ep.y);
+    float4 gr;
+    gr.x = dc ? px : __fadd_rn(px, py);
+    gr.y = dc ? py : __fsub_rn(__fmul_rn(x1.x, ep.y), __fmul_rn(x1.y, ep.x));
+    gr.z = __fadd_rn(__fmul_rn(x1.z, ep.z), __fmul_rn(x1.w, ep.w));
+    gr.w = __fsub_rn(__fmul_rn(x1.z, ep.w), __fmul_rn(x1.w, ep.z));
+    spec4[fg] = make_float4(__fmul_rn(st.x, gr.x), __fmul_rn(st.y, gr.y), __fmul_rn(st.z, gr.z),
+                            __fmul_rn(st.w, gr.w));
+  };
+  auto add = [](float4 w, float4 g) {
+    return make_float4(__fadd_rn(w.x, g.x), __fadd_rn(w.y, g.y), __fadd_rn(w.z, g.z), __fadd_rn(w.w, g.w));
+  };
+  // c2r, keep the first N samples, r2c of [g, 0_N] (spec -> spec)
+  auto project = [&]() {
+    __syncwarp();
+    irfft_warp_head(spec, z, N, a.logN, tw, split, [&](int i, float x) { win[i] = x; });
+    for (int i = lane; i < N; i += 32) win[N + i] = 0.0f;
+    __syncwarp();
+    rfft_warp_any(win, z, spec, N, a.logN, tw, split);
+  };
+  if constexpr (PL > 0) {
+    ConsIn<PL> cur, nxt;
+    if (u < units) load(u, cur);
+    for (; u < units; u += stride) {
+#pragma unroll
+      for (int r = 0; r < PL; ++r) grad(cur.x1[r], cur.ep[r], cur.pw[r], lane + 32 * r);
+      if (u + stride < units) load(u + stride, nxt);
+      project();
+      int p, slot, ul;
+      decode(u, p, ul, slot);
+#pragma unroll
+      for (int r = 0; r < PL; ++r) *w_at(p, ul, lane + 32 * r) = add(cur.w[r], spec4[lane + 32 * r]);
+      __syncwarp();  // spec is reused by the next unit
+      cur = nxt;
+    }
+  } else {
+    for (; u < units; u += stride) {
+      int p, slot, ul;
+      const int l = decode(u, p, ul, slot);
+      for (int fg = lane; fg < NF; fg += 32) grad(*xa_at(l, slot, fg), a.E[(size_t)p * NF + fg], pw4[fg], fg);
+      project();
+      for (int fg = lane; fg < NF; fg += 32) {
+        float4* wp = w_at(p, ul, fg);
+        *wp = add(*wp, spec4[fg]);
+      }
+      __syncwarp();
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kConsThreads, 16) k_afc_constrain(const __grid_constant__ BlockArgs a) {
   extern __shared__ float4 csm4[];
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  const int N = a.N, NF = a.NF, CT = a.CT, CTn = a.CTn, KF = a.KF, P = a.P, L = a.L;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  float2* spec = reinterpret_cast<float2*>(reinterpret_cast<char*>(csm4) + (size_t)warp * cons_smem_per_warp(N));
+  const int N = a.N;
+  const int warp = threadIdx.x >> 5;
+  // the DftPlan tables (shared by the CTA's warps), then per warp its scratch
+  const float2* stw = a.tw;
+  const float2* ssplit = a.split;
+  float2* spec = reinterpret_cast<float2*>(reinterpret_cast<char*>(csm4) + (a.cons_tables ? cons_smem_tables(N) : 0) +
+                                           (size_t)warp * cons_smem_per_warp(N));
   float* win = reinterpret_cast<float*>(spec + N);
   float2* z = reinterpret_cast<float2*>(win + 2 * N);
-  float4* spec4 = reinterpret_cast<float4*>(spec);
+  if (a.cons_tables) {
+    float2* t = reinterpret_cast<float2*>(csm4);
+    stage_tables(t, t + N / 2, a.tw, a.split, N);
+    stw = t;
+    ssplit = t + N / 2;
+  }
+  __syncthreads();
   asm volatile("griddepcontrol.wait;" ::: "memory");  // E_p and this block's canceller FDL row
   const blk_t n = a.st->block;
   trace_begin(a, TR_AFC_CONS, n);
-  const int cap = KF + 1;
-  const int nka = (int)(n % (blk_t)cap);
-  const long long U = (long long)L * KF;
-  const long long units = (long long)P * U;
-  const float4* pw4 = reinterpret_cast<const float4*>(a.pw);
+  const int nka = (int)(n % (blk_t)(a.KF + 1));
   const int warps = (int)(blockDim.x >> 5);
-  for (long long u = (long long)blockIdx.x * warps + warp; u < units; u += (long long)gridDim.x * warps) {
-    const int p = (int)(u / U);
-    const long long ul = u - (long long)p * U;  // l KF + k
-    const int l = (int)(ul / KF), k = (int)(ul - (long long)l * KF);
-    int slot = nka - k - 1;  // pre-push age k = post-push age k + 1
-    if (slot < 0) slot += cap;
-    for (int fg = lane; fg < NF; fg += 32) {
-      const int c = fg / CT, f = fg - c * CT;
-      const bool dc = fg == 0;
-      const float4 x1 = a.XA[((size_t)(l * CTn + c) * cap + slot) * CT + f];
-      const float4 ep = a.E[(size_t)p * NF + fg];
-      const float4 pw = pw4[fg];
-      const float4 st = make_float4(__fdiv_rn(a.mu, __fadd_rn(pw.x, a.delta)), __fdiv_rn(a.mu, __fadd_rn(pw.y, a.delta)),
-                                    __fdiv_rn(a.mu, __fadd_rn(pw.z, a.delta)), __fdiv_rn(a.mu, __fadd_rn(pw.w, a.delta)));
-      const float px = __fmul_rn(x1.x, ep.x), py = __fmul_rn(x1.y, ep.y);
-      float4 gr;
-      gr.x = dc ? px : __fadd_rn(px, py);
-      gr.y = dc ? py : __fsub_rn(__fmul_rn(x1.x, ep.y), __fmul_rn(x1.y, ep.x));
-      gr.z = __fadd_rn(__fmul_rn(x1.z, ep.z), __fmul_rn(x1.w, ep.w));
-      gr.w = __fsub_rn(__fmul_rn(x1.z, ep.w), __fmul_rn(x1.w, ep.z));
-      spec4[fg] = make_float4(__fmul_rn(st.x, gr.x), __fmul_rn(st.y, gr.y), __fmul_rn(st.z, gr.z),
-                              __fmul_rn(st.w, gr.w));
-    }
-    __syncwarp();
-    irfft_warp_head(spec, z, N, a.logN, a.tw, a.split, [&](int i, float x) { win[i] = x; });
-    for (int i = lane; i < N; i += 32) win[N + i] = 0.0f;
-    __syncwarp();
-    rfft_warp_any(win, z, spec, N, a.logN, a.tw, a.split);
-    for (int fg = lane; fg < NF; fg += 32) {
-      const int c = fg / CT, f = fg - c * CT;
-      float4* wp = a.W + ((size_t)c * U + ul) * P * CT + (size_t)p * CT + f;
-      const float4 g = spec4[fg];
-      float4 w = *wp;
-      w.x = __fadd_rn(w.x, g.x);
-      w.y = __fadd_rn(w.y, g.y);
-      w.z = __fadd_rn(w.z, g.z);
-      w.w = __fadd_rn(w.w, g.w);
-      *wp = w;
-    }
-    __syncwarp();  // spec is reused by the next unit
-  }
+  const int u0 = (int)blockIdx.x * warps + warp, stride = (int)gridDim.x * warps;
+  if (a.NF == 32 && a.cons_prefetch) cons_units<1>(a, u0, stride, nka, spec, win, z, stw, ssplit);
+  else if (a.NF == 64 && a.cons_prefetch) cons_units<2>(a, u0, stride, nka, spec, win, z, stw, ssplit);
+  else cons_units<0>(a, u0, stride, nka, spec, win, z, stw, ssplit);
   trace_end(a, TR_AFC_CONS, n);
 }
 

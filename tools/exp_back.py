@@ -56,7 +56,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--L", type=int, default=64)
     ap.add_argument("--N", type=int, default=64)
-    ap.add_argument("--cases", default="nlms,mu0,synth,afc")
+    ap.add_argument("--cases", default="nlms,cons,mu0,synth,afc")
     ap.add_argument("--mode", type=int, default=0, help="0 graph per block, 1 stream launches")
     args = ap.parse_args()
     global MODE
@@ -73,6 +73,8 @@ def main():
     cases = args.cases.split(",")
     if "nlms" in cases:
         run("c3 nlms", A.Auralizer(synth, fc, cfg, afc=A.AfcParams(0.005, 0.9, None)), mic)
+    if "cons" in cases:
+        run("c3 nlms constrained", A.Auralizer(synth, fc, cfg, afc=A.AfcParams(0.005, 0.9, None, True)), mic)
     if "mu0" in cases:
         run("c3 mu=0", A.Auralizer(synth, fc, cfg, afc=A.AfcParams(0.0, 0.9, None)), mic)
     if "synth" in cases:
