@@ -47,18 +47,20 @@ def main():
         x = rng.standard_normal((4, 32)).astype(np.float32)
         check(ce.process(x), oe.process(x), "elementwise")
     ce.close()
-    # NLMS auralizer (fused head), MIMO, and k_back_head (env knob)
-    for Q, L, fused in ((1, 8, True), (2, 6, True), (1, 8, False)):
+    # NLMS auralizer (fused head), MIMO, k_back_head (env knob), and the
+    # constrained update (k_afc_constrain)
+    for Q, L, fused, cons in ((1, 8, True, False), (2, 6, True, False), (1, 8, False, False),
+                              (1, 8, True, True), (2, 6, False, True)):
         os.environ["AURA_B200_FRONT_HEAD"] = "1" if fused else "0"
         s = decaying_filters(rng, Q * L, 9 * N, scale=0.5)
         fc = decaying_filters(rng, Q * L, 3 * N, scale=0.1)
         kw = dict(gain=0.9, mu=0.02, lam=0.9, delta=1e-2)
         g = A.Auralizer(list(s), list(fc), A.make_config(48000, N, Q, L, mimo=Q > 1), input_gain=0.9,
-                        afc=A.AfcParams(0.02, 0.9, 1e-2))
-        oa = O.OracleAuralizer(s, fc, N, Q, L, **kw)
+                        afc=A.AfcParams(0.02, 0.9, 1e-2, cons))
+        oa = O.OracleAuralizer(s, fc, N, Q, L, constrained=cons, **kw)
         for _ in range(10):
             m = rng.standard_normal((Q, N)).astype(np.float32)
-            check(g.process(m), oa.process(m), f"auralizer Q={Q} fused={fused}")
+            check(g.process(m), oa.process(m), f"auralizer Q={Q} fused={fused} constrained={cons}")
         check(g.coeffs(), oa.coeffs(), "W")
         g.time_device_blocks(3)
         g.time_phase("k_front", 2)
