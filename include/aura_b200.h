@@ -133,6 +133,15 @@ void aura_b200_destroy(aura_b200_engine* e);
  * input with AURA_B200_E_NON_FINITE_INPUT (engine state untouched). */
 int aura_b200_process(aura_b200_engine* e, const float* in, float* out);
 
+/* Zero-copy variant for latency-critical hosts (SURVEY 8(b)'s io_buffers):
+ * the engine's own pinned, device-mapped input (inputs x N) and output
+ * (outputs x N) blocks, which k_front reads and writes over PCIe directly.
+ * Write the next block into *in, call aura_b200_process_io, read the result
+ * from *out before the next call -- no host copies on either side. Valid
+ * between process_io calls only: during a call the device owns both. */
+int aura_b200_io_buffers(aura_b200_engine* e, float** in, float** out);
+int aura_b200_process_io(aura_b200_engine* e);
+
 /* Convolver::reset (convolver.hpp:133-142) / Auralizer::reset
  * (auralizer.hpp:95-99); an NLMS canceller is restored to its initial F^. */
 int aura_b200_reset(aura_b200_engine* e);

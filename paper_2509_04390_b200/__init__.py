@@ -174,6 +174,8 @@ def lib():
                                              C.POINTER(vp)]
     L.aura_b200_destroy.argtypes = [vp]
     L.aura_b200_process.argtypes = [vp, _f32p, _f32p]
+    L.aura_b200_io_buffers.argtypes = [vp, C.POINTER(C.POINTER(C.c_float)), C.POINTER(C.POINTER(C.c_float))]
+    L.aura_b200_process_io.argtypes = [vp]
     L.aura_b200_reset.argtypes = [vp]
     L.aura_b200_feedback_estimate.argtypes = [vp, _f32p]
     L.aura_b200_set_input_gain.argtypes = [vp, C.c_float]
@@ -314,6 +316,21 @@ class _Engine:
 
     def partition_count(self) -> int:
         return int(lib().aura_b200_partition_count(self._h))
+
+    def io_buffers(self):
+        """Zero-copy I/O (aura_b200_io_buffers): numpy views of the engine's
+        pinned, device-mapped input (C_in, N) and output (C_out, N) blocks.
+        Write the input view, call process_io(), read the output view before
+        the next call."""
+        pi, po = C.POINTER(C.c_float)(), C.POINTER(C.c_float)()
+        _check(lib().aura_b200_io_buffers(self._h, C.byref(pi), C.byref(po)))
+        N = self.cfg.block_size
+        return (np.ctypeslib.as_array(pi, shape=(self.cfg.input_channels, N)),
+                np.ctypeslib.as_array(po, shape=(self.cfg.output_channels, N)))
+
+    def process_io(self):
+        """One block from / to the io_buffers() views (no host copies)."""
+        _check(lib().aura_b200_process_io(self._h))
 
     def reset(self):
         _check(lib().aura_b200_reset(self._h))

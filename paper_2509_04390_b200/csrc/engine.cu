@@ -866,6 +866,29 @@ void aura_b200_destroy(aura_b200_engine* e) { delete e; }
 // written the output. The background keeps running; the next call's front
 // is stream-ordered after it, and feedback_estimate()/synchronize() wait
 // for it explicitly.
+namespace {
+// One block whose input is already in the mapped staging buffer h_in: launch
+// the block graph and wait until every k_front CTA has published its output
+// word (h_out holds the block's output, and no CTA reads h_in any more).
+void run_staged_block(aura_b200_engine* e) {
+  const size_t n_in = (size_t)e->Qx * e->N;
+  for (size_t i = 0; i < n_in; ++i)
+    if (!std::isfinite(e->h_in[i])) fail(AURA_B200_E_NON_FINITE_INPUT, "input contains NaN or Inf");
+  std::atomic_thread_fence(std::memory_order_release);
+  const uint64_t nblk = device_block_hint(e);
+  // (nothing else goes on the stream per block: an extra stream operation
+  // between two block graphs costs device time at every block boundary)
+  e->enqueue_block(e->g_block, e->args, e->use_outflag ? nullptr : e->ev_front);
+  if (e->use_outflag) {
+    // k_front's last CTA publishes block + 1 once every output is written
+    wait_flag(e, nblk + 1, "block output");
+  } else {
+    wait_event(e, e->ev_front, "block output");
+  }
+  ++e->blocks;
+}
+}  // namespace
+
 int aura_b200_process(aura_b200_engine* e, const float* in, float* out) {
   return guarded([&] {
     if (!e || !in || !out) fail(AURA_B200_E_INVALID_ARGUMENT, "null argument");
@@ -877,19 +900,25 @@ int aura_b200_process(aura_b200_engine* e, const float* in, float* out) {
     // every k_front CTA of the previous block (output and error-spectrum
     // CTAs) has published its word, so none still reads the staging buffer
     std::memcpy(e->h_in, in, n_in * sizeof(float));
-    std::atomic_thread_fence(std::memory_order_release);
-    const uint64_t nblk = device_block_hint(e);
-    // (nothing else goes on the stream per block: an extra stream operation
-    // between two block graphs costs device time at every block boundary)
-    e->enqueue_block(e->g_block, e->args, e->use_outflag ? nullptr : e->ev_front);
-    if (e->use_outflag) {
-      // k_front's last CTA publishes block + 1 once every output is written
-      wait_flag(e, nblk + 1, "block output");
-    } else {
-      wait_event(e, e->ev_front, "block output");
-    }
+    run_staged_block(e);
     std::memcpy(out, e->h_out, e->L * e->N * sizeof(float));
-    ++e->blocks;
+  });
+}
+
+int aura_b200_io_buffers(aura_b200_engine* e, float** in, float** out) {
+  return guarded([&] {
+    if (!e || !in || !out) fail(AURA_B200_E_INVALID_ARGUMENT, "null argument");
+    *in = e->h_in;
+    *out = e->h_out;
+  });
+}
+
+int aura_b200_process_io(aura_b200_engine* e) {
+  return guarded([&] {
+    if (!e) fail(AURA_B200_E_INVALID_ARGUMENT, "null argument");
+    CK(cudaSetDevice(e->device));
+    check_shard_status(e);
+    run_staged_block(e);
   });
 }
 

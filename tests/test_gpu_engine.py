@@ -182,3 +182,29 @@ def test_early_canceller_reduction_is_bit_identical(monkeypatch):
     on.reset()
     for b, m in enumerate(mics):
         assert np.array_equal(on.process(m), first[b]), b
+
+
+def test_zero_copy_io_matches_process():
+    """aura_b200_io_buffers / process_io (the mapped staging blocks, no host
+    copies) stream bit-identically to process(); a non-finite input in the
+    mapped block is rejected before anything is launched."""
+    mk, rng = small_aur(0.02)
+    a, b = mk(), mk()
+    xin, xout = b.io_buffers()
+    assert xin.shape == (1, 64) and xout.shape == (8, 64)
+    for blk in range(40):
+        m = rng.standard_normal((1, 64)).astype(np.float32)
+        y = a.process(m)
+        xin[...] = m
+        b.process_io()
+        assert np.array_equal(y, xout), blk
+    assert np.array_equal(a.feedback_estimate(), b.feedback_estimate())
+    xin[0, 3] = np.nan
+    with pytest.raises(A.Error) as ei:
+        b.process_io()
+    assert ei.value.code == A.ErrorCode.non_finite_input
+    assert b.blocks_processed() == 40
+    m = rng.standard_normal((1, 64)).astype(np.float32)
+    xin[...] = m
+    b.process_io()
+    assert np.array_equal(a.process(m), xout)
