@@ -464,9 +464,11 @@ def run_b200_arm(args, cfg, rank, world, local_rank):
 
     paced = None
     if not args.no_paced:
+        eng.reset()  # the engine's deadline statistics cover this run only
         paced_us = eng.time_host_blocks(mic, min(K, 2000), pace_us=1e6 * N / cfg["fs"])
+        dl = eng.deadline_stats()
         paced = {"p50_us": pct(paced_us, 50), "p99_us": pct(paced_us, 99),
-                 "blocks": int(paced_us.size),
+                 "blocks": int(paced_us.size), "deadline_misses": dl["misses"], "max_us": dl["max_us"],
                  "definition": "aura_b200_process() latency with calls on the real-time grid "
                                "(one block every N/fs), host buffers"}
 

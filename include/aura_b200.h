@@ -142,6 +142,13 @@ int aura_b200_process(aura_b200_engine* e, const float* in, float* out);
 int aura_b200_io_buffers(aura_b200_engine* e, float** in, float** out);
 int aura_b200_process_io(aura_b200_engine* e);
 
+/* Failure detection (no reference counterpart): calls of
+ * process / process_io whose host-visible latency exceeded the real-time
+ * budget N / f_s since creation or the last reset, the largest and the last
+ * latency (us), and the budget (us). */
+int aura_b200_deadline_stats(const aura_b200_engine* e, uint64_t* misses, double* max_us, double* last_us,
+                             double* budget_us);
+
 /* Convolver::reset (convolver.hpp:133-142) / Auralizer::reset
  * (auralizer.hpp:95-99); an NLMS canceller is restored to its initial F^. */
 int aura_b200_reset(aura_b200_engine* e);

@@ -176,6 +176,7 @@ def lib():
     L.aura_b200_process.argtypes = [vp, _f32p, _f32p]
     L.aura_b200_io_buffers.argtypes = [vp, C.POINTER(C.POINTER(C.c_float)), C.POINTER(C.POINTER(C.c_float))]
     L.aura_b200_process_io.argtypes = [vp]
+    L.aura_b200_deadline_stats.argtypes = [vp, C.POINTER(C.c_uint64)] + [C.POINTER(C.c_double)] * 3
     L.aura_b200_reset.argtypes = [vp]
     L.aura_b200_feedback_estimate.argtypes = [vp, _f32p]
     L.aura_b200_set_input_gain.argtypes = [vp, C.c_float]
@@ -331,6 +332,14 @@ class _Engine:
     def process_io(self):
         """One block from / to the io_buffers() views (no host copies)."""
         _check(lib().aura_b200_process_io(self._h))
+
+    def deadline_stats(self) -> dict:
+        """Failure detection: process()/process_io() calls over the real-time
+        budget N / f_s since creation or reset, max / last latency (us)."""
+        m = C.c_uint64()
+        mx, last, bud = C.c_double(), C.c_double(), C.c_double()
+        _check(lib().aura_b200_deadline_stats(self._h, C.byref(m), C.byref(mx), C.byref(last), C.byref(bud)))
+        return {"misses": int(m.value), "max_us": mx.value, "last_us": last.value, "budget_us": bud.value}
 
     def reset(self):
         _check(lib().aura_b200_reset(self._h))

@@ -731,6 +731,7 @@ int aura_b200_convolver_create(const aura_b200_config* cfg, int mode,
     common_init(e.get(), device);
     e->mode = mode;
     e->N = cfg->block_size;
+    e->budget_us = 1e6 * (double)cfg->block_size / (double)cfg->sample_rate_hz;
     e->Q = mode == AURA_B200_ELEMENTWISE ? 1 : cfg->inputs;
     e->L = cfg->outputs;
     e->Qx = mode == AURA_B200_ELEMENTWISE ? (int)cfg->outputs : (int)cfg->inputs;
@@ -783,6 +784,7 @@ int aura_b200_auralizer_create(const aura_b200_config* cfg,
     e->aur = true;
     e->mode = Q == 1 ? AURA_B200_BROADCAST : AURA_B200_MIMO;
     e->N = cfg->block_size;
+    e->budget_us = 1e6 * (double)cfg->block_size / (double)cfg->sample_rate_hz;
     e->Q = Q;
     e->L = L;
     e->P = Q;
@@ -889,9 +891,19 @@ void run_staged_block(aura_b200_engine* e) {
 }
 }  // namespace
 
+// Failure detection: every call's host-visible latency against
+// the real-time budget N / f_s.
+static void note_latency(aura_b200_engine* e, std::chrono::steady_clock::time_point t0) {
+  const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+  e->last_us = us;
+  if (us > e->max_us) e->max_us = us;
+  if (us > e->budget_us) ++e->deadline_misses;
+}
+
 int aura_b200_process(aura_b200_engine* e, const float* in, float* out) {
   return guarded([&] {
     if (!e || !in || !out) fail(AURA_B200_E_INVALID_ARGUMENT, "null argument");
+    const auto t0 = std::chrono::steady_clock::now();
     const size_t n_in = (size_t)e->Qx * e->N;
     for (size_t i = 0; i < n_in; ++i)
       if (!std::isfinite(in[i])) fail(AURA_B200_E_NON_FINITE_INPUT, "input contains NaN or Inf");
@@ -902,6 +914,7 @@ int aura_b200_process(aura_b200_engine* e, const float* in, float* out) {
     std::memcpy(e->h_in, in, n_in * sizeof(float));
     run_staged_block(e);
     std::memcpy(out, e->h_out, e->L * e->N * sizeof(float));
+    note_latency(e, t0);
   });
 }
 
@@ -916,9 +929,22 @@ int aura_b200_io_buffers(aura_b200_engine* e, float** in, float** out) {
 int aura_b200_process_io(aura_b200_engine* e) {
   return guarded([&] {
     if (!e) fail(AURA_B200_E_INVALID_ARGUMENT, "null argument");
+    const auto t0 = std::chrono::steady_clock::now();
     CK(cudaSetDevice(e->device));
     check_shard_status(e);
     run_staged_block(e);
+    note_latency(e, t0);
+  });
+}
+
+int aura_b200_deadline_stats(const aura_b200_engine* e, uint64_t* misses, double* max_us, double* last_us,
+                             double* budget_us) {
+  return guarded([&] {
+    if (!e || !misses || !max_us || !last_us || !budget_us) fail(AURA_B200_E_INVALID_ARGUMENT, "null argument");
+    *misses = e->deadline_misses;
+    *max_us = e->max_us;
+    *last_us = e->last_us;
+    *budget_us = e->budget_us;
   });
 }
 
@@ -934,6 +960,8 @@ int aura_b200_reset(aura_b200_engine* e) {
   return guarded([&] {
     CK(cudaSetDevice(e->device));
     reset_state(e);
+    e->deadline_misses = 0;
+    e->max_us = e->last_us = 0.0;
   });
 }
 

@@ -186,6 +186,9 @@ struct aura_b200_engine {
   float4* W0 = nullptr;  // initial canceller spectra (reset of NLMS)
   size_t w_elems = 0;
   float* h_in = nullptr;    // mapped pinned
+  // failure detection: process() / process_io() latency vs the budget N / f_s
+  double budget_us = 0.0, max_us = 0.0, last_us = 0.0;
+  uint64_t deadline_misses = 0;
   float* h_out = nullptr;   // mapped pinned
   float* d_in_pool = nullptr;
   size_t pool_blocks = 0;

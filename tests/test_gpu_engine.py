@@ -208,3 +208,27 @@ def test_zero_copy_io_matches_process():
     xin[...] = m
     b.process_io()
     assert np.array_equal(a.process(m), xout)
+
+
+def test_deadline_stats_count_budget_misses():
+    """Failure detection: calls whose host-visible latency exceeds N / f_s
+    are counted. At 48 kHz the 1.33 ms budget of N = 64 is never missed; at a
+    (fictitious) 2 MHz sample rate the budget of N = 16 is 8 us, below what a
+    launch plus a PCIe round trip takes, so (nearly) every call misses.
+    reset() clears the statistics."""
+    mk, rng = small_aur(0.02)
+    a = mk()
+    for _ in range(20):
+        a.process(rng.standard_normal((1, 64)).astype(np.float32))
+    st = a.deadline_stats()
+    assert st["misses"] == 0 and 0 < st["last_us"] <= st["max_us"] < st["budget_us"]
+    assert abs(st["budget_us"] - 64 / 48000 * 1e6) < 1e-6
+    a.reset()
+    assert a.deadline_stats()["misses"] == 0 and a.deadline_stats()["max_us"] == 0.0
+    synth = [np.r_[1.0, np.zeros(200)].astype(np.float32)] * 2
+    fast = A.Convolver(synth, A.make_config(2_000_000, 16, 1, 2))
+    for _ in range(50):
+        fast.process(np.ones((1, 16), np.float32))
+    st = fast.deadline_stats()
+    assert st["budget_us"] == 8.0
+    assert st["misses"] >= 45 and st["max_us"] >= st["last_us"] > 0
