@@ -26,6 +26,7 @@ def check(y, ref, what):
 
 
 def main():
+    print("library:", A.lib()._name, flush=True)
     rng = np.random.default_rng(1)
     N = 64
     # broadcast convolver, then the stream launch mode
