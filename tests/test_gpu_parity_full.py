@@ -146,25 +146,29 @@ def test_c3_full_stream_vs_reference():
     tf.check("c3 f^")
 
 
-def test_c3_nlms_stream_vs_oracle():
+@pytest.mark.parametrize("constrained", [False, True])
+def test_c3_nlms_stream_vs_oracle(constrained):
     """configs[2] as benchmarked (NLMS mu = 0.005, lambda 0.9, the survey's
     delta = 1e-6 N): K_f + 3 = 753 blocks against the C oracle -- y every
-    block, f^ every block, W after the stream."""
+    block, f^ every block, W after the stream; also with the constrained
+    gradient (Appendix A step 2)."""
     N, L = 64, 64
     synth, fc = c3_filters()
     kw = dict(mu=0.005, lam=0.9)
-    g = A.Auralizer(list(synth), list(fc), A.make_config(48000, N, 1, L), afc=A.AfcParams(**kw))
-    o = O.OracleAuralizer(synth, fc, N, 1, L, **kw)
-    x = O.OracleAuralizer(synth, fc, N, 1, L, f64=True, **kw)
+    g = A.Auralizer(list(synth), list(fc), A.make_config(48000, N, 1, L),
+                    afc=A.AfcParams(**kw, constrained=constrained))
+    o = O.OracleAuralizer(synth, fc, N, 1, L, constrained=constrained, **kw)
+    x = O.OracleAuralizer(synth, fc, N, 1, L, f64=True, constrained=constrained, **kw)
     ty, tf = Tri(), Tri()
     src = noise_blocks(7, 1, N)
     for _ in range(753):
         m = next(src)
         ty.add(g.process(m), o.process(m), x.process(m))
         tf.add(g.feedback_estimate(), o.feedback_estimate(), x.feedback_estimate())
-    ty.check("c3 nlms y")
-    tf.check("c3 nlms f^")
-    w_tri(g.coeffs(), o.coeffs(), x.coeffs()).check("c3 nlms W")
+    tag = "c3 nlms constrained" if constrained else "c3 nlms"
+    ty.check(f"{tag} y")
+    tf.check(f"{tag} f^")
+    w_tri(g.coeffs(), o.coeffs(), x.coeffs()).check(f"{tag} W")
 
 
 @pytest.mark.parametrize("N,blocks", [(64, 753), (1024, 566)])
