@@ -183,11 +183,14 @@ void plan_back(aura_b200_engine* e, BlockArgs& a) {
   const int P = e->aur ? (int)e->P : 0;
   const long long U = e->aur ? (long long)e->L * e->KF : 0;
   if (T > INT32_MAX / 2 || U > INT32_MAX / 2) fail(AURA_B200_E_INVALID_ARGUMENT, "filters too long");
-  // stage sizes: ~32 KB per stage, a whole number of tap phases
-  // ~46 KB synthesis stages, four in the ring: the single producer lane's
-  // per-stage cost is what bounds an SM's stream (profiles/r1s5_stream.md),
-  // so fewer, larger stages (sp need not be a multiple of the 8 tap phases)
-  const int target_kb = std::max(4, knob_i(e, "STAGE_KB", 46));
+  // ~54 KB synthesis stages (three in the ring at c3): the single producer
+  // lane's per-stage cost is what bounds an SM's stream
+  // (profiles/r1s5_stream.md), so fewer, larger stages (sp need not be a
+  // multiple of the 8 tap phases). Measured against 46 KB x 4 (round 2,
+  // gpurun_out/r3ab, r3ac): mean block period c3 52.4 vs 53.2 us, c4 224.0
+  // vs 224.9, c2 20.1 vs 20.5, c5 and c1 unchanged; 64 KB (two stages) and
+  // 38 KB are slower.
+  const int target_kb = std::max(4, knob_i(e, "STAGE_KB", 54));
   const int target_f4 = target_kb * 1024 / 16;
   const int syn_row = (LT + XL) * CT;
   a.sp = std::max(PH, target_f4 / syn_row);
