@@ -204,7 +204,7 @@ void plan_back(aura_b200_engine* e, BlockArgs& a) {
   a.slot_f4 = (int)slot;
   const int rmax = std::max(LT, P + 1);
   a.red_f4 = std::max({kConsumers, 64 * rmax, NF});
-  const size_t budget = 200 * 1024;
+  const size_t budget = (size_t)std::max(64, std::min(224, knob_i(e, "BACK_SMEM_KB", 200))) * 1024;
   const size_t fixed = kBackBarrierBytes + (size_t)a.red_f4 * 16;
   const size_t per = (size_t)a.slot_f4 * 16;
   a.stages = per ? (int)std::min<size_t>(kMaxStages, (budget - fixed) / per) : 0;
