@@ -1,6 +1,6 @@
 #!/usr/bin/env python
 """Host-visible latency of process() (C-ABI, host buffers) in graph mode (0)
-and persistent-loop mode (2): back to back, and paced on the real-time grid
+and stream-launch mode (1): back to back, and paced on the real-time grid
 (one block every N/fs). c3 shape unless --L/--N."""
 import argparse
 import json
@@ -33,7 +33,7 @@ def main():
         br = e.time_host_breakdown(mic, 1000, pace_us=p)
         print(json.dumps({"breakdown_pace_us": p, "p50": {k: round(float(np.median(v)), 2) for k, v in br.items()},
                           "p99": {k: round(float(np.percentile(v, 99)), 2) for k, v in br.items()}}), flush=True)
-    for mode in (0, 1, 2):
+    for mode in (0, 1):
         e.set_launch_mode(mode)
         e.time_host_blocks(mic, 200)
         b2b = e.time_host_blocks(mic, args.blocks)

@@ -1,3 +1,6 @@
+"""Experiment (GPU box): process() latency at c3 on the real-time grid and
+back to back, block graph (launch mode 0) vs stream launches (mode 1), two
+repetitions: {mode_rep: [paced p50, p99, b2b p50, p99]} in us."""
 import json, os, sys
 import numpy as np
 sys.path.insert(0, os.getcwd())
