@@ -643,6 +643,11 @@ def run_sharded(args, cfg, rank, world, local_rank):
     # partials all-reduced by NCCL (graph-captured) instead of our P2P kernel
     nccl = None
     if cfg["afc"] and not args.no_nccl:
+        # one small (P*N + 2N floats) all-reduce per block --
+        # latency-bound; a pinned algorithm / protocol fixes the reduction
+        # order run to run (unless the caller chose otherwise)
+        os.environ.setdefault("NCCL_ALGO", "Ring")
+        os.environ.setdefault("NCCL_PROTO", "LL")
         try:
             ne = S.ShardedAuralizer(LazyRows(Q * L, cfg["n_h"], cfg["fs"], seed=1000),
                                     LazyRows(Q * L, cfg["n_hf"], cfg["fs"], t60_s=0.3, scale=0.1, seed=2000),
