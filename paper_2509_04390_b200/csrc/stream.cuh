@@ -616,19 +616,7 @@ __global__ void __launch_bounds__(kBackThreads, 1) k_back(const __grid_constant_
 }
 
 // ----------------------------------------------------------------- k_reduce
-// The split-K reduction of block n, after k_back (programmatic dependent
-// launch: its CTAs take the SMs k_back's CTAs leave and wait for k_back with
-// griddepcontrol.wait). CTA b sums, for `epc` elements of one tile, the
-// tile's partials in slot order -- `sub` threads per element over contiguous
-// slot ranges, combined in order through shared memory -- so the association
-// is fixed and results are bit-reproducible. Synthesis tiles -> S (block
-// n+1's partitions >= 1); canceller column tiles -> Yhat, after which the
-// last canceller CTA does one c2r per mic (f^ for block n+1; the sum over
-// loudspeakers is done in the frequency domain -- one c2r per mic instead of
-// the reference's L, auralizer.hpp:81-86) and smooths the power (Appendix A
-// step 5). The last CTA advances the block (sharded: k_afc_finish does).
-// grid = red_syn_ctas + red_afc_ctas, kReduceThreads threads.
-
+// Helpers of k_reduce (the kernel and its description are below).
 
 // Canceller reduce CTAs: stage the DftPlan tables and the smoothed power --
 // they do not depend on the streaming kernel -- for whichever of them
@@ -780,7 +768,8 @@ __device__ void reduce_part(const BlockArgs& a, int b, blk_t n, float4* rsm, int
 // ----------------------------------------------------------------- k_reduce
 // The split-K reduction of block n, after k_back (programmatic dependent
 // launch: its CTAs take the SMs k_back's CTAs leave and wait for k_back with
-// griddepcontrol.wait). CTA b sums, for `epc` elements of one tile, the
+// griddepcontrol.wait -- except the single canceller CTA with afc_seq, which
+// waits for the canceller partials k_back publishes). CTA b sums, for `epc` elements of one tile, the
 // tile's partials in slot order -- `sub` threads per element over contiguous
 // slot ranges, combined in order through shared memory -- so the association
 // is fixed and results are bit-reproducible. Synthesis tiles -> S (block
