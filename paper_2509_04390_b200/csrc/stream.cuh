@@ -26,16 +26,18 @@
 //    copy: H as [L/LT][NF/CT][tap][LT][CT] float4, W as [NF/CT][unit][P][CT],
 //    and the delay lines as [ch][NF/CT][slot][CT] so a run of partitions is
 //    one (or, at the ring wrap, two) copies;
-//  * work is planned on the host (plan_back): every CTA gets the same share
-//    of three phases -- a slice of the synthesis taps, a slice of the
-//    canceller units, then the rest of the synthesis -- so the canceller
-//    (whose inputs come from k_back_head, overlapped with this kernel via
-//    programmatic dependent launch) finishes mid-kernel and its c2r hides
-//    behind the synthesis stream;
-//  * split-K partials are reduced deterministically: warp shuffles over the
-//    four tap phases of a warp, a fixed-order shared-memory sum over the
-//    warps, one partial per (CTA, tile); the last CTA to finish a tile sums
-//    its partials in slot order (fixed association => bit-reproducible).
+//  * work is planned on the host (plan_back): every CTA streams a static
+//    slice of the first 30% of every synthesis tile, then claims items from
+//    one queue -- the middle of the synthesis with the canceller items spread
+//    through it, small items for the tail, the age-0 stages last -- so the
+//    canceller (whose inputs come from the front, overlapped with this
+//    kernel via programmatic dependent launch) ends well before the stream;
+//  * split-K partials are deterministic: warp shuffles over the tap phases
+//    of a warp, a fixed-order shared-memory sum over the warps, one partial
+//    per work item in a fixed slot; k_reduce sums each tile's partials in
+//    slot order (fixed association => bit-reproducible). A tenth warp (the
+//    signal warp) publishes each canceller partial for k_reduce's early
+//    canceller CTA.
 #pragma once
 #include "kernels.cuh"
 
