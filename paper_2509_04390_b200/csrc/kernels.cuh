@@ -6,15 +6,20 @@
 //   k_front       m~ = g m - f^ (auralizer.hpp:73-76), window + r2c of every
 //                 input (convolver.hpp:180-191), FDL push, then per output
 //                 channel  Y_l = S_l + sum_q X_q,n (.) H_{l,q}[0],  c2r +
-//                 overlap-save straight into the (mapped) output buffer.
-//                 --> event node: the host returns the block here.
-//   k_back_head   canceller stage 1 on l_n (r2c, FDL push) and the NLMS error
-//                 spectra; triggers its dependent launch immediately, so
+//                 overlap-save straight into the (mapped) output buffer; each
+//                 CTA publishes an output word the host polls (process()
+//                 returns here); then canceller stage 1 on l_n (r2c, FDL
+//                 push) and, on P extra CTAs, the NLMS error spectra. It
+//                 triggers its dependent launch at once, so
+//   [k_afc_constrain  the constrained NLMS gradient, optional]
 //   k_back        (stream.cuh, programmatic dependent launch) starts its
-//                 synthesis stream while k_back_head runs: S_l for block
-//                 n+1 (every partition but the first -- they depend only on
-//                 inputs <= n) and the canceller MAC + NLMS -> f^ for n+1.
+//                 synthesis stream during the front: S_l for block n+1
+//                 (every partition but the first -- they depend only on
+//                 inputs <= n) and the canceller MAC + NLMS;
+//   k_reduce      (stream.cuh) the fixed-order split-K sums -> S, f^ for n+1;
 //   k_afc_finish  only when the loudspeakers are sharded over GPUs.
+// (k_back_head, the separate canceller stage 1, remains for
+// AURA_B200_FRONT_HEAD=0.)
 //
 // So the output of block n is c2r(X_n H_0 + sum_{k>=1} X_{n-k} H_k), exactly
 // the reference's accumulator (backend.hpp:212-235) with the partition sum
