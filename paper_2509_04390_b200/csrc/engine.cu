@@ -30,7 +30,9 @@ void aura_b200_engine::launch_phase(int ph, const BlockArgs& a, cudaStream_t s) 
     case PH_BACK_HEAD:
       if (has_head())
         k_back_head<<<(unsigned)(aur ? L + (a.nlms ? P : 0) : 1), kFrontThreads, smem_head, s>>>(a);
-      if (a.afc_cons)  // after the front (or head): E_p and the pushed canceller FDL row
+      if (a.afc_cons && cons8)  // after the front (or head): E_p
+        launch_pdl(k_afc_constrain8, (unsigned)cons_ctas, kCons8Threads, smem_cons, !pdl_off, a, s);
+      else if (a.afc_cons)
         launch_pdl(k_afc_constrain, (unsigned)cons_ctas, 32u * cons_warps, smem_cons, !pdl_off, a, s);
       break;
     case PH_BACK:
@@ -829,6 +831,15 @@ int aura_b200_auralizer_create(const aura_b200_config* cfg,
       a.cons_prefetch = knob_i(e.get(), "CONS_PREFETCH", 1);
       const long long per_sm = std::max(1, knob_i(e.get(), "CONS_CTAS_PER_SM", 12));
       e->cons_ctas = (int)std::min<long long>(per_sm * e->sms, (units + e->cons_warps - 1) / e->cons_warps);
+      // N = 64: eight threads per unit, every butterfly computed once
+      // (k_afc_constrain8)
+      if (N == 64 && knob_i(e.get(), "CONS_OCT", 1)) {
+        e->cons8 = true;
+        e->smem_cons = cons8_smem((int)Q);
+        raise_smem_limit(k_afc_constrain8, e->smem_cons);
+        const long long per8 = std::max(1, knob_i(e.get(), "CONS8_CTAS_PER_SM", 4));
+        e->cons_ctas = (int)std::min<long long>(per8 * e->sms, (units + 15) / 16);
+      }
     }
     e->w_elems = Q * L * e->KF * NF;
     a.W = dalloc<float4>(e->w_elems, e->dmem);

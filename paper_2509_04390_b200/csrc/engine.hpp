@@ -232,6 +232,7 @@ struct aura_b200_engine {
   size_t smem_front = 0, smem_head = 0;
   size_t smem_cons = 0;  // k_afc_constrain (constrained NLMS gradient)
   int cons_ctas = 0, cons_warps = 0;
+  bool cons8 = false;  // k_afc_constrain8 (N = 64)
 
   ~aura_b200_engine() {
     cudaSetDevice(device);

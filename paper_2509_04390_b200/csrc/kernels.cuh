@@ -781,6 +781,211 @@ __global__ void __launch_bounds__(kConsThreads, 16) k_afc_constrain(const __grid
   trace_end(a, TR_AFC_CONS, n);
 }
 
+// ------------------------------------------------- k_afc_constrain8
+// k_afc_constrain for N = 64 (c3's block size) with eight threads per unit
+// and eight points per thread: the 64-point transforms run their first three
+// radix-2 stages inside each thread (contiguous points), a shared-memory
+// transpose, and the last three inside each thread again (strided points) --
+// every butterfly computed once, by one thread, with no shuffles -- where the
+// one-warp-per-unit kernel computes each butterfly on both lanes of a pair.
+// Same butterflies, twiddles and association as DftPlan (fft.cuh), so the
+// same bits as k_afc_constrain. Four units per warp; grid-stride over units.
+// Dynamic smem: the DftPlan tables, E_p and the power of the CTA's block,
+// then per warp four units x {spectrum, exchange buffer} (64 float2 each).
+constexpr int kCons8Threads = 128;
+__host__ __device__ inline size_t cons8_smem(int P) {
+  return 16 * (size_t)(34 + 32 * (P + 1)) + (size_t)(kCons8Threads / 32) * 4 * 2 * 64 * 8;
+}
+
+__device__ __forceinline__ int bitrev6(int m) { return (int)(__brev((unsigned)m) >> 26); }
+
+// radix-2 DIT butterfly on (u, v) with twiddle w: u + v w, u - v w (v w
+// rounded as cmul_rn), the same operations as fft_dit_smem / fft_dit_warp
+__device__ __forceinline__ void bfly(float2& u, float2& v, float2 w) {
+  const float2 wv = cmul_rn(v, w);
+  const float2 a = cadd_rn(u, wv);
+  v = csub_rn(u, wv);
+  u = a;
+}
+
+// 64-point DIT on the 8 points of thread t (of 8) held contiguously
+// (z[8t + r], bit-reversed input order); returns them strided (z[t + 8r]).
+// buf: the unit's 64-float2 exchange buffer; tw: e^{-2 pi i j / 64}, j < 32.
+__device__ __forceinline__ void fft64_oct(float2 (&z)[8], int t, float2* buf, const float2* tw) {
+#pragma unroll
+  for (int h = 1; h < 8; h <<= 1) {
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+      if ((r & h) == 0) bfly(z[r], z[r + h], tw[(r & (h - 1)) * (32 / h)]);
+  }
+#pragma unroll
+  for (int r = 0; r < 8; ++r) buf[8 * t + r] = z[r];
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < 8; ++r) z[r] = buf[t + 8 * r];
+  __syncwarp();
+#pragma unroll
+  for (int hh = 1; hh < 8; hh <<= 1) {  // h = 8 hh: pairs (r, r + hh) of the strided points
+    const int h = 8 * hh;
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+      if ((r & hh) == 0) bfly(z[r], z[r + hh], tw[(t + 8 * (r & (hh - 1))) * (32 / h)]);
+  }
+}
+
+__global__ void __launch_bounds__(kCons8Threads, 8) k_afc_constrain8(const __grid_constant__ BlockArgs a) {
+  extern __shared__ float4 c8sm[];
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  constexpr int N = 64, NF = 32, H = 32;
+  const int P = a.P, KF = a.KF, L = a.L;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int sub = lane >> 3, t = lane & 7;  // unit within the warp, thread within the unit
+  float2* stw = reinterpret_cast<float2*>(c8sm);  // 32 + 33 float2 (34 float4)
+  float2* ssplit = stw + N / 2;
+  float4* sE = c8sm + 34;                         // [P][NF]
+  float4* spw = sE + (size_t)P * NF;              // [NF]
+  float2* ubase = reinterpret_cast<float2*>(spw + NF) + (size_t)(warp * 4 + sub) * 2 * 64;
+  float2* spec = ubase;       // the unit's packed spectrum (64 float2)
+  float2* buf = ubase + 64;   // its exchange buffer
+  float4* spec4 = reinterpret_cast<float4*>(spec);
+  stage_tables(stw, ssplit, a.tw, a.split, N);
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // E_p from the front
+  for (int i = threadIdx.x; i < P * NF; i += blockDim.x) sE[i] = a.E[i];
+  for (int i = threadIdx.x; i < NF; i += blockDim.x) spw[i] = reinterpret_cast<const float4*>(a.pw)[i];
+  __syncthreads();
+  const blk_t n = a.st->block;
+  trace_begin(a, TR_AFC_CONS, n);
+  const int cap = KF + 1;
+  const int nka = (int)(n % (blk_t)cap);
+  const int U = L * KF, units = P * U;
+  const int per_pass = (int)gridDim.x * (kCons8Threads / 32) * 4;
+  const float scale = 1.0f / (float)N;
+  for (int base = ((int)blockIdx.x * (kCons8Threads / 32) + warp) * 4; base < units; base += per_pass) {
+    const int u = base + sub;
+    const bool ok = u < units;
+    int p = 0, ul = 0, slot = 0, l = 0;
+    if (ok) {
+      p = u / U;
+      ul = u - p * U;
+      l = ul / KF;
+      const int k = ul - l * KF;
+      slot = nka - k - 1;  // pre-push age k
+      if (slot < 0) slot += cap;
+    }
+    // (1) the gradient G = mu / (P + delta) (.) conj(x1) E_p -> spec, four
+    // float4 columns per thread, rounded as k_back's fused update
+    float4 wv[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int fg = t + 8 * j;
+      if (!ok) {
+        wv[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+        continue;
+      }
+      const bool dc = fg == 0;
+      const float4 x1 = a.XA[((size_t)l * cap + slot) * NF + fg];
+      wv[j] = a.W[((size_t)ul) * P * NF + (size_t)p * NF + fg];
+      const float4 ep = sE[(size_t)p * NF + fg];
+      const float4 pw = spw[fg];
+      const float4 st = make_float4(__fdiv_rn(a.mu, __fadd_rn(pw.x, a.delta)), __fdiv_rn(a.mu, __fadd_rn(pw.y, a.delta)),
+                                    __fdiv_rn(a.mu, __fadd_rn(pw.z, a.delta)), __fdiv_rn(a.mu, __fadd_rn(pw.w, a.delta)));
+      const float px = __fmul_rn(x1.x, ep.x), py = __fmul_rn(x1.y, ep.y);
+      float4 gr;
+      gr.x = dc ? px : __fadd_rn(px, py);
+      gr.y = dc ? py : __fsub_rn(__fmul_rn(x1.x, ep.y), __fmul_rn(x1.y, ep.x));
+      gr.z = __fadd_rn(__fmul_rn(x1.z, ep.z), __fmul_rn(x1.w, ep.w));
+      gr.w = __fsub_rn(__fmul_rn(x1.z, ep.w), __fmul_rn(x1.w, ep.z));
+      spec4[fg] = make_float4(__fmul_rn(st.x, gr.x), __fmul_rn(st.y, gr.y), __fmul_rn(st.z, gr.z),
+                              __fmul_rn(st.w, gr.w));
+    }
+    __syncwarp();
+    // (2) c2r: merge into the half-size spectrum (dft.hpp:130-146, as
+    // irfft_packed_tail), bit-reversed into this thread's 8 contiguous points
+    float2 z[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int k = bitrev6(8 * t + r);
+      float2 zk;
+      if (k == 0) {
+        const float2 s0 = spec[0];  // (DC, Nyquist)
+        const float xe = __fmul_rn(0.5f, __fadd_rn(s0.x, s0.y));
+        const float xo = __fmul_rn(0.5f, __fsub_rn(s0.x, s0.y));
+        zk = make_float2(xe, -xo);
+      } else {
+        const float2 av = spec[k];
+        const float2 bv = conjf2(spec[N - k]);
+        const float2 even = half_of(cadd_rn(av, bv));
+        float2 tw2;
+        if (k <= H) {
+          tw2 = ssplit[k];
+        } else {
+          const float2 q = conjf2(ssplit[N - k]);
+          tw2 = make_float2(-q.x, -q.y);
+        }
+        const float2 odd = cmul_rn(conjf2(tw2), half_of(csub_rn(av, bv)));
+        const float2 iodd = cmul_rn(make_float2(0.0f, 1.0f), odd);
+        zk = conjf2(cadd_rn(even, iodd));
+      }
+      z[r] = zk;
+    }
+    fft64_oct(z, t, buf, stw);  // now z[r] = point t + 8 r
+    // (3) the first N samples x[2m], x[2m+1] = (z[m].x, -z[m].y) / N for
+    // m < 32 (r < 4); the window's second half is zero. r2c input: point
+    // bitrev(m) = (x[2m], x[2m+1]), via the exchange buffer
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+      buf[t + 8 * r] = make_float2(__fmul_rn(z[r].x, scale), __fmul_rn(-z[r].y, scale));
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int m = bitrev6(8 * t + r);
+      z[r] = m < 32 ? buf[m] : make_float2(0.0f, 0.0f);
+    }
+    __syncwarp();
+    fft64_oct(z, t, buf, stw);
+    // (4) split (dft.hpp:88-100, as rfft_packed) -> spec, then W += spec
+#pragma unroll
+    for (int r = 0; r < 8; ++r) buf[t + 8 * r] = z[r];
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+      const int k = t + 8 * j;
+      if (k > H) break;
+      if (k == 0) {
+        const float2 z0 = buf[0];
+        spec[0] = make_float2(__fadd_rn(z0.x, z0.y), __fsub_rn(z0.x, z0.y));
+        continue;
+      }
+      const float2 av = buf[k];
+      const float2 bv = conjf2(buf[N - k]);
+      const float2 even = half_of(cadd_rn(av, bv));
+      const float2 d = csub_rn(av, bv);
+      const float2 odd = cmul_rn(make_float2(0.0f, -0.5f), d);
+      const float2 rot = cmul_rn(ssplit[k], odd);
+      const float2 lo = cadd_rn(even, rot);
+      const float2 hi = conjf2(csub_rn(even, rot));
+      if (k != H) spec[k] = lo;  // at k = N/2 the reference's second store wins
+      spec[N - k] = hi;
+    }
+    __syncwarp();
+    if (ok) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int fg = t + 8 * j;
+        const float4 g = spec4[fg];
+        float4 w = wv[j];
+        w.x = __fadd_rn(w.x, g.x);
+        w.y = __fadd_rn(w.y, g.y);
+        w.z = __fadd_rn(w.z, g.z);
+        w.w = __fadd_rn(w.w, g.w);
+        a.W[((size_t)ul) * P * NF + (size_t)p * NF + fg] = w;
+      }
+    }
+    __syncwarp();  // spec and buf are reused by the next unit
+  }
+  trace_end(a, TR_AFC_CONS, n);
+}
+
 // ------------------------------------------------------ k_partition
 // Setup (make_partitioned_filters, convolver.hpp:19-46) on the GPU: CTA
 // (k, r) transforms taps[r][kN .. kN+N) zero-padded to 2N and scatters the
