@@ -422,8 +422,9 @@ void plan_back(aura_b200_engine* e, BlockArgs& a) {
   a.tinfo = dti;
   // k_reduce geometry: ~16 partials per thread, elements split over CTAs
   a.LTr = LT;
+  const int red_loads = std::max(1, std::min(32, knob_i(e, "RED_LOADS", 16)));  // partial loads per thread
   auto cpt_for = [&](int E, int maxcnt) {
-    const int sub = std::min(16, std::max(1, (maxcnt + 15) / 16));
+    const int sub = std::min(16, std::max(1, (maxcnt + red_loads - 1) / red_loads));
     const int ne = std::max(1, kReduceThreads / sub);
     return (E + ne - 1) / ne;
   };
