@@ -235,7 +235,8 @@ void plan_back(aura_b200_engine* e, BlockArgs& a) {
   const double syn_b = (double)tiles * T * syn_row * 16.0;
   const double afc_b = (double)CTn * U * (P * (e->args.nlms ? 2 : 1) + 1) * CT * 16.0;
   const double drive = T > 0 ? syn_b : afc_b;
-  int ctas = (int)std::min<double>(e->sms, std::max(1.0, std::ceil(drive / (96.0 * 1024))));
+  const double cta_kb = std::max(1.0, knob_f(e, "CTA_KB", 96.0));  // bytes per CTA at least
+  int ctas = (int)std::min<double>(e->sms, std::max(1.0, std::ceil(drive / (cta_kb * 1024))));
   if (const int c = knob_i(e, "BACK_CTAS", 0)) ctas = std::max(1, std::min(ctas, c));
   e->back_ctas = ctas;
   // Work: every CTA first runs a static piece of the first 30% of every
